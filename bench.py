@@ -1,0 +1,353 @@
+"""Benchmark: order-p RIDC wall time & grid-point*steps/s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|c3|c4] [--order P] [--nt NT] [--points N]
+
+One bench "step" = one full RIDC-FBE solve (all Nt time steps, all levels) of
+the workload, starting from an initial state already resident in HBM.
+Default workload (N=1): BASELINE.json configs[1] -- 1-D reaction-diffusion,
+2^20 grid points, Nt = 10^4, order p = number of GPUs (1 GPU: FEBE, order 1);
+the same line also reports orders 2 and 4 with all levels on the one GPU.
+
+value = grid points * Nt * K / (device time of the K solves), max over ranks.
+Between timed solves L2 is flushed (a 512 MiB write, untimed).  `e2e` is the
+same metric through the host-buffer C-ABI call (``ridc_run``: H2D of y0,
+marching, D2H of the final state).  `cpu_baseline` times the CPU oracle port
+(oracle/ridc_oracle.c, one thread per level like the reference's workers) on
+a bounded sample of the same workload.
+
+`--impl reference` times only that CPU port (the reference is Python+numba
+with dense O(N^2) solves and cannot run N = 2^20) and prints
+the same JSON line with "impl": "reference".
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "order-p RIDC wall time & grid-point·steps/s vs 1-GPU FEBE (p=1,2,4,8 GPUs)"
+UNIT = "grid-point*steps/s"
+HBM_FALLBACK = 6650.0
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def workload(name, points=None, nt=None):
+    from paper_1209_4297_b200 import problems as P
+    if name == "c2":
+        n = points or (1 << 20)
+        sysm = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n))
+        return sysm, nt or 10000, {"workload": "c2-reaction-diffusion-1d", "points": n,
+                                    "nt": nt or 10000, "t_end": 1.0}
+    if name == "c1":
+        sysm = P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 1024, t_end=4.0))
+        return sysm, nt or 1000, {"workload": "c1-adv-diff-1d", "points": 1024, "nt": nt or 1000}
+    if name == "c3":
+        n = points or 4096
+        sysm = P.build_advection_diffusion_2d(P.AdvectionDiffusion2DSpec(nx=n, ny=n))
+        return sysm, nt or 1000, {"workload": "c3-adv-diff-2d", "points": n * n, "grid": [n, n],
+                                   "nt": nt or 1000}
+    if name == "c4":
+        n = points or 8192
+        sysm = P.build_reaction_diffusion_2d(P.ReactionDiffusion2DSpec(nx=n, ny=n))
+        return sysm, nt or 1000, {"workload": "c4-reaction-diffusion-2d", "points": n * n,
+                                   "grid": [n, n], "nt": nt or 1000}
+    raise SystemExit(f"unknown workload {name}")
+
+
+def bytes_per_point(level):
+    """Algorithmic HBM bytes per grid point of one level-step."""
+    return 16 if level == 0 else 8 * (level + 3)
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_sample(sysm, levels, nt, budget_s=12.0):
+    """Time the CPU oracle port on a bounded number of steps of the workload."""
+    from oracle import oracle as O
+    from paper_1209_4297_b200.quadrature import pack_weight_tables
+    ivp = sysm.ivp
+    dt = (ivp.t_end - ivp.t_start) / nt
+    w = pack_weight_tables(levels, dt)
+    n = ivp.dimension
+    probe = max(levels * (levels + 1) // 2 + 2, 4)
+    r = O.run(ivp.problem, ivp.initial_state, levels, nt, 1, dt, w, workers=levels, max_steps=probe)
+    per_step = r["wall_seconds"] / probe
+    steps = int(min(max(probe, budget_s / max(per_step, 1e-9)), nt))
+    r = O.run(ivp.problem, ivp.initial_state, levels, nt, 1, dt, w, workers=levels, max_steps=steps)
+    return {"value": n * steps / r["wall_seconds"], "unit": UNIT, "cores": levels,
+            "kind": "port", "wall_seconds": r["wall_seconds"],
+            "sample": f"{steps} of {nt} time steps, {n} points, order {levels}, "
+                      f"{levels} thread(s) (one per level, as the reference's workers)"}
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return 0
+    order = args.order or max(1, args.gpus)
+    sysm, nt, cfg = workload(args.workload, args.points, args.nt)
+    from oracle import oracle as O
+    from paper_1209_4297_b200.quadrature import pack_weight_tables
+    ivp = sysm.ivp
+    dt = (ivp.t_end - ivp.t_start) / nt
+    w = pack_weight_tables(order, dt)
+    n = ivp.dimension
+    fill = order * (order + 1) // 2 + 2
+    sample = max(fill, args.sample_steps)
+    for _ in range(args.warmup):
+        O.run(ivp.problem, ivp.initial_state, order, nt, 1, dt, w, workers=order, max_steps=fill)
+    total = 0.0
+    for _ in range(args.steps):
+        r = O.run(ivp.problem, ivp.initial_state, order, nt, 1, dt, w, workers=order, max_steps=sample)
+        total += r["wall_seconds"]
+    value = n * sample * args.steps / total
+    cfg.update({"order": order, "levels_per_gpu": order, "parallelism": "cpu-threads"})
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": order, "kind": "port",
+                         "sample": f"{sample} of {nt} time steps per bench step, {n} points"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "CPU oracle port of the reference path (reference itself is dense O(N^2), "
+                "infeasible at this N)",
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    from paper_1209_4297_b200 import engine as E
+    from paper_1209_4297_b200 import problems as P
+
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    sysm, nt, cfg = workload(args.workload, args.points, args.nt)
+    n = sysm.ivp.dimension
+    order = args.order or max(1, world)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    if world > 1:
+        from paper_1209_4297_b200 import distributed as PD
+        runner = PD.PipelineRank(sysm, E.RidcConfig(levels=order, steps=nt), rank, world, local)
+        y0 = torch.from_numpy(np.ascontiguousarray(sysm.ivp.initial_state)).cuda()
+        out = torch.empty_like(y0)
+
+        def solve_device():
+            return runner.run_device(y0, out)
+        launches_per_step = runner.kernel_launches
+        tick_launches = runner.tick_launches
+        lev_bytes = bytes_per_point(rank) + (8 if rank > 0 else 0)
+    else:
+        eng = E.Engine(sysm, E.RidcConfig(levels=order, steps=nt))
+        y0 = torch.from_numpy(np.ascontiguousarray(sysm.ivp.initial_state)).cuda()
+        out = torch.empty_like(y0)
+
+        def solve_device():
+            return eng.run_device(y0, out)
+        info = eng.info
+        launches_per_step = info["kernel_launches"]
+        tick_launches = launches_per_step - 1
+        lev_bytes = sum(bytes_per_point(j) for j in range(order)) * nt / max(tick_launches, 1)
+
+    for _ in range(max(args.warmup, 0)):
+        solve_device()
+    barrier()
+    times = []
+    clocks = ClockSampler(local)
+    with clocks:
+        barrier()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            times.append(solve_device())
+        barrier()
+    t_local = float(sum(times))
+    t_max = t_local
+    if dist is not None:
+        tt = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = n * nt * args.steps / t_max
+    ms_per_step = t_max / args.steps * 1e3
+
+    # roofline of the dominant kernel (the fused tick kernel): algorithmic bytes per
+    # launch / average launch duration over the timed region (events on its stream)
+    peak, peak_kind = hbm_peak()
+    per_launch_s = t_local / (args.steps * max(tick_launches, 1))
+    bytes_launch = lev_bytes * n
+    achieved = bytes_launch / per_launch_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(f"{cfg['workload']}/p{order}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "k_tick (fused level-step: stencils + factored tridiagonal solve)",
+                "bytes_per_launch": bytes_launch, "launch_us": per_launch_s * 1e6}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "gpu_launches": int(launches_per_step * args.steps)}
+    cfg.update({"order": order, "levels_per_gpu": 1 if world > 1 else order,
+                "parallelism": f"levels-over-gpus{world}" if world > 1 else "1gpu",
+                "l2": "flushed between solves (512 MiB write); state stays resident within a solve"})
+    line["config"] = cfg
+    line["roofline"] = roofline
+    line["clocks"] = clocks.summary()
+
+    # e2e: the host-buffer C-ABI call (H2D y0 + marching + D2H final)
+    if world == 1:
+        y0h = np.ascontiguousarray(sysm.ivp.initial_state)
+        import ctypes
+        from paper_1209_4297_b200 import _lib
+        fin = np.empty(n)
+        walls = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _lib.check(_lib.lib().ridc_run(eng._h, y0h.ctypes.data, fin.ctypes.data, None, None,
+                                           None), eng._h)
+            walls.append(time.perf_counter() - t0)
+        line["e2e"] = {"value": n * nt * len(walls) / sum(walls), "unit": UNIT,
+                       "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n}
+        # extra orders with all levels on this GPU (configs[1]: "RIDC order 1-4 on 1 B200")
+        extra = {}
+        if not args.no_extra:
+            for p in (2, 4):
+                if p == order:
+                    continue
+                with E.Engine(sysm, E.RidcConfig(levels=p, steps=nt)) as e2:
+                    e2.run_device(y0, out)
+                    ts = []
+                    for _ in range(2):
+                        flush.zero_()
+                        torch.cuda.synchronize()
+                        ts.append(e2.run_device(y0, out))
+                    extra[f"order{p}_1gpu"] = {"value": n * nt * len(ts) / sum(ts),
+                                               "ms_per_solve": sum(ts) / len(ts) * 1e3,
+                                               "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps)}
+        line["ridc_orders_1gpu"] = extra
+        line["cpu_baseline"] = cpu_sample(sysm, order, nt, budget_s=args.cpu_budget)
+    else:
+        line["e2e"] = None
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--order", type=int, default=0)
+    ap.add_argument("--points", type=int, default=0)
+    ap.add_argument("--nt", type=int, default=0)
+    ap.add_argument("--sample-steps", type=int, default=100)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-extra", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

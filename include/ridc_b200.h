@@ -1,0 +1,172 @@
+/*
+ * ridc_b200.h -- C-ABI of the B200-native RIDC-FBE marching engine.
+ *
+ * This is the drop-in boundary for the reference's hot path (paths relative
+ * to /root/reference, package pkg/src/ridc):
+ *
+ *   ridc_create / ridc_run   replace  engine.run_serial / engine.run_pipelined
+ *                                     (engine.py:476-522) including _prepare
+ *                                     (engine.py:465-473: dt, weight tables,
+ *                                     pre-factorisation, restart partition).
+ *   ridc_run_device          same run with device-resident state (no H2D/D2H).
+ *   ridc_op_apply            replaces ImplicitSolver.stiff_value (steppers.py:66-70)
+ *                                     and SplitIVP.eval_nonstiff (problems.py:133,164)
+ *   ridc_op_solve            replaces ImplicitSolver.solve_shifted -> qr_solve
+ *                                     (steppers.py:72-78, linalg.py:59-63)
+ *   ridc_op_step             replaces predict_step / correct_step (engine.py:193-231)
+ *                                     driven by states instead of f^S/f^N rows
+ *   ridc_pipe_*              the one-level-per-GPU lagged pipeline
+ *                                     (engine.py:349-459, LevelBuffer :284-331)
+ *
+ * Conventions.  All pointers are plain; no torch types.  "_host" buffers are
+ * caller-owned host memory; "_dev" buffers are caller-owned device memory on
+ * the context's device.  The library owns every other device allocation.
+ * Return value: 0 on success or a RIDC_E_* status; ridc_last_error() gives
+ * the message.  Status codes map onto the reference's exception classes
+ * (errors.py:4-47).  One host thread per context; a context is not
+ * reentrant; distinct contexts may run concurrently on distinct devices.
+ */
+#ifndef RIDC_B200_H
+#define RIDC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (mapped by paper_1209_4297_b200/errors.py) */
+#define RIDC_OK 0
+#define RIDC_E_CONFIG 1        /* ConfigError */
+#define RIDC_E_DIMENSION 2     /* DimensionMismatch */
+#define RIDC_E_NONFINITE 3     /* NonFiniteStateError */
+#define RIDC_E_PROTOCOL 4      /* PipelineProtocolError (watchdog / protocol) */
+#define RIDC_E_DETERMINISM 5   /* DeterminismError */
+#define RIDC_E_CUDA 6          /* CUDA runtime failure */
+
+/* problem kinds */
+#define RIDC_ADV_DIFF_1D 1            /* problems.py:109-138 (periodic) */
+#define RIDC_BURGERS_1D 2             /* problems.py:141-168 (Dirichlet) */
+#define RIDC_REACTION_DIFFUSION_1D 3  /* periodic, f^N = rho u (1-u) */
+#define RIDC_ADV_DIFF_2D 4            /* periodic, x-line implicit */
+#define RIDC_REACTION_DIFFUSION_2D 5  /* periodic, x-line implicit */
+
+/* Structured problem: replaces SplitIVP's callables + dense operator
+ * (ivp.py:31-66).  State layout: ny rows of nx points, row-major. */
+typedef struct ridc_problem {
+    int32_t kind;
+    int32_t nx;        /* points per x-line (1-D: the dimension) */
+    int32_t ny;        /* lines (1 for 1-D kinds) */
+    int32_t reserved;
+    double c_x, c_y;   /* advection speeds (adv-diff) */
+    double d_x, d_y;   /* diffusivity: x (stiff, implicit), y (explicit) */
+    double rho;        /* logistic reaction rate */
+    double h_x, h_y;   /* grid spacings */
+} ridc_problem;
+
+typedef struct ridc_ctx ridc_ctx;
+
+/* run flags */
+#define RIDC_RECORD_TRAJECTORY 1u  /* RidcConfig.record_trajectory */
+
+/* Engine geometry / accounting, for reports and tests. */
+typedef struct ridc_info {
+    int32_t levels;
+    int32_t restarts;
+    int64_t steps;
+    int64_t ticks_per_interval;   /* steps/restarts + levels(levels-1)/2 */
+    int64_t kernel_launches;      /* launches per ridc_run (graph nodes) */
+    int32_t tile;                 /* output points per work item */
+    int32_t halo;                 /* truncation halo per side (0: exact line solve) */
+    int32_t items_per_level;      /* work items per level-step */
+    int32_t threads;              /* CUDA threads per item */
+    int64_t ring_vectors;         /* device vectors held by all level rings */
+    double lambda;                /* decay factor of the shifted operator's factors */
+    double r;                     /* stiffness dt*d_x/h_x^2 */
+} ridc_info;
+
+/*
+ * Create a run context (RidcConfig validation engine.py:71-87, _prepare
+ * engine.py:465-473).  weights: packed quadrature tables (steady j=1..L-1,
+ * then startup (j, n) for j=2..L-1, n=0..j-2; j+1 doubles each) as produced
+ * by quadrature.pack_weight_tables; nweights its length.  device: CUDA
+ * ordinal.  All device memory, the factor tables and the CUDA graph of the
+ * whole run are set up here, outside any timed region.
+ */
+int ridc_create(const ridc_problem *problem, double t_start, double t_end,
+                int32_t levels, int64_t steps, int32_t restarts,
+                const double *weights, int64_t nweights,
+                int32_t device, uint32_t flags, ridc_ctx **out);
+
+/* One full run from host buffers (H2D of y0, marching, D2H of results).
+ * final_host (n); level_finals_host (levels*n) or NULL; traj_host
+ * ((steps+1)*n) or NULL (requires RIDC_RECORD_TRAJECTORY); wall_seconds:
+ * device time of the marching only (engine.py:482-488), may be NULL. */
+int ridc_run(ridc_ctx *ctx, const double *y0_host, double *final_host,
+             double *level_finals_host, double *traj_host, double *wall_seconds);
+
+/* Same with device-resident input/output (state already in HBM). */
+int ridc_run_device(ridc_ctx *ctx, const double *y0_dev, double *final_dev,
+                    double *wall_seconds);
+
+int ridc_info_get(const ridc_ctx *ctx, ridc_info *info);
+int ridc_destroy(ridc_ctx *ctx);
+const char *ridc_last_error(const ridc_ctx *ctx);   /* ctx may be NULL: thread's last error */
+
+/* ---- single operators (device buffers, synchronous on the device's default stream) ---- */
+
+#define RIDC_OP_STIFF 0     /* f^S(u) */
+#define RIDC_OP_NONSTIFF 1  /* f^N(u) */
+int ridc_op_apply(const ridc_problem *problem, int32_t op, const double *in_dev,
+                  double *out_dev, int32_t device);
+
+/* x_dev = (I - coeff * L_S)^{-1} rhs_dev */
+int ridc_op_solve(const ridc_problem *problem, double coeff, const double *rhs_dev,
+                  double *x_dev, int32_t device);
+
+/* One level step: rhs = eta + dt f^N(eta) + sum_k (cs[k] f^S(win[k]) + cn[k] f^N(win[k]))
+ * then out = (I - dt L_S)^{-1} rhs.  nwin = 0 for the predictor.  win_dev is a
+ * HOST array of nwin device pointers.  Returns RIDC_E_NONFINITE if out has
+ * non-finite entries. */
+int ridc_op_step(const ridc_problem *problem, double dt, const double *eta_dev,
+                 int32_t nwin, const double *const *win_dev, const double *cs,
+                 const double *cn, double *out_dev, int32_t device);
+
+/* Reference-form level step (LevelWindow with f^S / f^N rows, engine.py:200-231):
+ * rhs = eta + dt f^N(eta) + sum_k ca[k] rows[k]; out = (I - dt L_S)^{-1} rhs.
+ * rows_dev: HOST array of nrows (<= 24) device pointers. */
+int ridc_op_step_rows(const ridc_problem *problem, double dt, const double *eta_dev,
+                      int32_t nrows, const double *const *rows_dev, const double *ca,
+                      double *out_dev, int32_t device);
+
+/* ---- lagged level pipeline, one level per GPU (one process per GPU) ---- */
+
+typedef struct ridc_pipe ridc_pipe;
+
+/* Size of the opaque blob a rank exports for its neighbours (IPC handles). */
+int64_t ridc_pipe_handle_bytes(void);
+
+/* Create the rank owning `level` (0..levels-1) on `device`; the rank's inbox
+ * ring (window of level-1) and flags are allocated here. */
+int ridc_pipe_create(const ridc_problem *problem, double t_start, double t_end,
+                     int32_t levels, int64_t steps, int32_t restarts,
+                     const double *weights, int64_t nweights, int32_t level,
+                     int32_t device, double watchdog_seconds, ridc_pipe **out);
+/* Export this rank's handles into blob (ridc_pipe_handle_bytes() bytes). */
+int ridc_pipe_export(ridc_pipe *p, void *blob);
+/* Connect to the previous level (prev_blob, NULL for level 0) and the next
+ * level (next_blob, NULL for the top level). */
+int ridc_pipe_connect(ridc_pipe *p, const void *prev_blob, const void *next_blob);
+/* Run all intervals.  y0_dev: initial state on this device.  final_dev: this
+ * level's final state (the top level's is the solution); restarts re-seed
+ * every level from the top level's interval final, which the top rank
+ * broadcasts over the same peer links.  wall_seconds: device time. */
+int ridc_pipe_run(ridc_pipe *p, const double *y0_dev, double *final_dev, double *wall_seconds);
+int ridc_pipe_destroy(ridc_pipe *p);
+const char *ridc_pipe_last_error(const ridc_pipe *p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RIDC_B200_H */

@@ -1,0 +1,805 @@
+// ridc_engine.cu -- kernels + host runtime behind include/ridc_b200.h (sm_100a).
+//
+// Single-device engine: every tick of the lagged pipeline is ONE kernel launch
+// covering all active levels (levels are independent within a tick:
+// level j at tick k computes step k - j(j+1)/2, reading only data published
+// in earlier ticks, engine.py:363-371), and the whole run (all restart
+// intervals, all ticks) is captured once into a CUDA graph at create time
+// (the analogue of _prepare's pre-factorisation, engine.py:465-473).
+//
+// Level rings: level j < top keeps its last 2j+3 states in HBM (the greedy
+// schedule's live window for the reader j+1, which lags j+1 ticks); the top
+// level keeps 2 (or the whole trajectory when it is recorded).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ridc_b200.h"
+#include "ridc_device.cuh"
+
+using namespace ridc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct EngineParams {
+    DevProblem pb;
+    DevSolve sv;
+    long long V;
+    double dt;
+    int levels;
+    double* ring[kMaxLevels];
+    long long cap[kMaxLevels];
+    long long off[kMaxLevels];
+    const double* weights;
+    int steady_off[kMaxLevels];
+    int startup_off[kMaxLevels];
+    unsigned long long* err;
+};
+
+struct TickParams {
+    int nact;
+    int level[kMaxLevels];
+    long long target[kMaxLevels];
+};
+
+__device__ __forceinline__ double* ring_slot(const EngineParams& ep, int lev, long long s)
+{
+    return ep.ring[lev] + ((ep.off[lev] + s) % ep.cap[lev]) * ep.V;
+}
+
+// Window assembly for (level j, target t): _window_span / _orient /
+// _WeightTables.for_step (engine.py:124-157) with the lag terms of
+// _correct_core (engine.py:179-181) folded into the node coefficients.
+__device__ void build_item(const EngineParams& ep, int j, long long t, StepItem& it)
+{
+    it.level = j;
+    it.target = t;
+    it.vec[0] = ring_slot(ep, j, t - 1);
+    it.ca[0] = 1.0;
+    it.cs[0] = 0.0;
+    it.cn[0] = ep.dt;
+    int nn = 1;
+    if (j > 0) {
+        const bool steady = t >= j;
+        const double* w = steady ? ep.weights + ep.steady_off[j]
+                                 : ep.weights + ep.startup_off[j] + (t - 1) * (j + 1);
+        const int i_new = steady ? 0 : (int)t;
+        const int i_old = steady ? 1 : (int)t - 1;
+        for (int a = 0; a <= j; ++a) {
+            const long long s = steady ? t - a : a;
+            it.vec[nn] = ring_slot(ep, j - 1, s);
+            it.ca[nn] = 0.0;
+            it.cs[nn] = w[a] - (a == i_new ? ep.dt : 0.0);
+            it.cn[nn] = w[a] - (a == i_old ? ep.dt : 0.0);
+            ++nn;
+        }
+    }
+    it.nnodes = nn;
+    it.out = ring_slot(ep, j, t);
+}
+
+template <int KIND, int NT, int KMAX>
+__global__ void __launch_bounds__(NT) k_tick(EngineParams ep, TickParams tp)
+{
+    extern __shared__ double sbuf[];
+    __shared__ StepItem item;
+    __shared__ Aff swarp[NT / 32];
+    if (threadIdx.x == 0) build_item(ep, tp.level[blockIdx.y], tp.target[blockIdx.y], item);
+    __syncthreads();
+    process_item<KIND, NT, KMAX>(ep.pb, ep.sv, item, blockIdx.x, sbuf, swarp, ep.err);
+}
+
+template <int KIND, int NT, int KMAX>
+__global__ void __launch_bounds__(NT) k_item(DevProblem pb, DevSolve sv, StepItem it,
+                                             unsigned long long* err)
+{
+    extern __shared__ double sbuf[];
+    __shared__ Aff swarp[NT / 32];
+    process_item<KIND, NT, KMAX>(pb, sv, it, blockIdx.x, sbuf, swarp, err);
+}
+
+// state0 -> slot 0 of every level ring (engine.py:357-360: step 0 = initial data)
+__global__ void k_seed(const double* __restrict__ src, EngineParams ep)
+{
+    const long long V = ep.V;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < V;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double v = src[i];
+        for (int j = 0; j < ep.levels; ++j) ring_slot(ep, j, 0)[i] = v;
+    }
+}
+
+template <int KIND>
+__global__ void k_apply(DevProblem pb, int op, const double* __restrict__ in, double* __restrict__ out)
+{
+    const long long V = (long long)pb.nx * pb.ny;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < V;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(i / pb.nx), col = (int)(i - (long long)row * pb.nx);
+        const double* rp = in + (size_t)row * pb.nx;
+        const double* rn = in + (size_t)(row == 0 ? pb.ny - 1 : row - 1) * pb.nx;
+        const double* rs = in + (size_t)(row == pb.ny - 1 ? 0 : row + 1) * pb.nx;
+        double u, fs, fn;
+        eval_point<KIND>(pb, rp, rn, rs, col, op == RIDC_OP_STIFF, op == RIDC_OP_NONSTIFF, u, fs, fn);
+        out[i] = op == RIDC_OP_STIFF ? fs : fn;
+    }
+}
+
+// ---------------------------------------------------------------- dispatch
+
+struct LaunchCfg {
+    int id;       // 0: 128x8, 1: 256x16, 2: 512x16
+    int nt, kmax;
+    size_t smem;
+};
+
+constexpr int kSmax = 512 * 16;
+
+LaunchCfg pick_cfg(int S)
+{
+    LaunchCfg c;
+    if (S <= 128 * 8) { c.id = 0; c.nt = 128; c.kmax = 8; }
+    else if (S <= 256 * 16) { c.id = 1; c.nt = 256; c.kmax = 16; }
+    else { c.id = 2; c.nt = 512; c.kmax = 16; }
+    const int cap = c.nt * c.kmax;
+    c.smem = (size_t)(cap + cap / 16 + 1) * sizeof(double);
+    return c;
+}
+
+template <int KIND, int NT, int KMAX>
+cudaError_t launch_tick_t(dim3 grid, size_t smem, cudaStream_t st, const EngineParams& ep,
+                          const TickParams& tp)
+{
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k_tick<KIND, NT, KMAX>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    k_tick<KIND, NT, KMAX><<<grid, NT, smem, st>>>(ep, tp);
+    return cudaGetLastError();
+}
+
+template <int KIND, int NT, int KMAX>
+cudaError_t launch_item_t(int items, size_t smem, cudaStream_t st, const DevProblem& pb,
+                          const DevSolve& sv, const StepItem& it, unsigned long long* err)
+{
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k_item<KIND, NT, KMAX>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    k_item<KIND, NT, KMAX><<<items, NT, smem, st>>>(pb, sv, it, err);
+    return cudaGetLastError();
+}
+
+#define RIDC_DISPATCH_CFG(FN, KIND, CFG, ...)                          \
+    ((CFG).id == 0 ? FN<KIND, 128, 8>(__VA_ARGS__)                     \
+     : (CFG).id == 1 ? FN<KIND, 256, 16>(__VA_ARGS__)                  \
+                     : FN<KIND, 512, 16>(__VA_ARGS__))
+
+cudaError_t launch_tick(int kind, const LaunchCfg& c, dim3 grid, cudaStream_t st,
+                        const EngineParams& ep, const TickParams& tp)
+{
+    switch (kind) {
+    case ADV_DIFF_1D: return RIDC_DISPATCH_CFG(launch_tick_t, ADV_DIFF_1D, c, grid, c.smem, st, ep, tp);
+    case BURGERS_1D: return RIDC_DISPATCH_CFG(launch_tick_t, BURGERS_1D, c, grid, c.smem, st, ep, tp);
+    case RD_1D: return RIDC_DISPATCH_CFG(launch_tick_t, RD_1D, c, grid, c.smem, st, ep, tp);
+    case ADV_DIFF_2D: return RIDC_DISPATCH_CFG(launch_tick_t, ADV_DIFF_2D, c, grid, c.smem, st, ep, tp);
+    case RD_2D: return RIDC_DISPATCH_CFG(launch_tick_t, RD_2D, c, grid, c.smem, st, ep, tp);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_item(int kind, const LaunchCfg& c, int items, cudaStream_t st,
+                        const DevProblem& pb, const DevSolve& sv, const StepItem& it,
+                        unsigned long long* err)
+{
+    switch (kind) {
+    case ADV_DIFF_1D: return RIDC_DISPATCH_CFG(launch_item_t, ADV_DIFF_1D, c, items, c.smem, st, pb, sv, it, err);
+    case BURGERS_1D: return RIDC_DISPATCH_CFG(launch_item_t, BURGERS_1D, c, items, c.smem, st, pb, sv, it, err);
+    case RD_1D: return RIDC_DISPATCH_CFG(launch_item_t, RD_1D, c, items, c.smem, st, pb, sv, it, err);
+    case ADV_DIFF_2D: return RIDC_DISPATCH_CFG(launch_item_t, ADV_DIFF_2D, c, items, c.smem, st, pb, sv, it, err);
+    case RD_2D: return RIDC_DISPATCH_CFG(launch_item_t, RD_2D, c, items, c.smem, st, pb, sv, it, err);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_apply(const DevProblem& pb, int op, const double* in, double* out, cudaStream_t st)
+{
+    const long long V = (long long)pb.nx * pb.ny;
+    int blocks = (int)std::min<long long>((V + 255) / 256, 148 * 16);
+    switch (pb.kind) {
+    case ADV_DIFF_1D: k_apply<ADV_DIFF_1D><<<blocks, 256, 0, st>>>(pb, op, in, out); break;
+    case BURGERS_1D: k_apply<BURGERS_1D><<<blocks, 256, 0, st>>>(pb, op, in, out); break;
+    case RD_1D: k_apply<RD_1D><<<blocks, 256, 0, st>>>(pb, op, in, out); break;
+    case ADV_DIFF_2D: k_apply<ADV_DIFF_2D><<<blocks, 256, 0, st>>>(pb, op, in, out); break;
+    case RD_2D: k_apply<RD_2D><<<blocks, 256, 0, st>>>(pb, op, in, out); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- host setup
+
+int fail(std::string* dst, int code, const std::string& msg)
+{
+    g_last_error = msg;
+    if (dst) *dst = msg;
+    return code;
+}
+
+#define CUDA_TRY(dst, expr)                                                            \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess)                                                         \
+            return fail(dst, RIDC_E_CUDA, std::string(#expr " failed: ") +             \
+                                              cudaGetErrorString(_e));                 \
+    } while (0)
+
+int validate_problem(const ridc_problem* p)
+{
+    if (!p) return fail(nullptr, RIDC_E_CONFIG, "problem is NULL");
+    if (p->kind < 1 || p->kind > 5) return fail(nullptr, RIDC_E_CONFIG, "unknown problem kind");
+    if (p->nx < 3 || p->ny < 1) return fail(nullptr, RIDC_E_DIMENSION, "grid too small (nx >= 3)");
+    const bool two_d = p->kind == ADV_DIFF_2D || p->kind == RD_2D;
+    if (two_d && p->ny < 3) return fail(nullptr, RIDC_E_DIMENSION, "2-D problems need ny >= 3");
+    if (!two_d && p->ny != 1) return fail(nullptr, RIDC_E_DIMENSION, "1-D problems need ny == 1");
+    if (!(p->d_x > 0.0) || !(p->h_x > 0.0) || (two_d && !(p->h_y > 0.0)))
+        return fail(nullptr, RIDC_E_CONFIG, "need d_x > 0 and positive grid spacings");
+    return RIDC_OK;
+}
+
+DevProblem make_problem(const ridc_problem* p)
+{
+    DevProblem d;
+    d.kind = p->kind;
+    d.nx = p->nx;
+    d.ny = p->ny;
+    d.periodic = p->kind != BURGERS_1D;
+    d.cax = p->c_x / p->h_x;
+    d.cay = p->ny > 1 ? p->c_y / p->h_y : 0.0;
+    d.cdx = p->d_x / (p->h_x * p->h_x);
+    d.cdy = p->ny > 1 ? p->d_y / (p->h_y * p->h_y) : 0.0;
+    d.rho = p->rho;
+    d.bs = 1.0 / (4.0 * p->h_x);
+    return d;
+}
+
+// Host precompute of the shifted-operator factors (the analogue of
+// qr_factor(I - dt L), linalg.py:33-56, done once per run).
+struct SolveSetup {
+    DevSolve sv;
+    std::vector<double> tab;   // [m_0..m_{n-1}, g_0..g_{n-1}]
+    double r;
+    LaunchCfg cfg;
+    std::string err;
+};
+
+int make_solve(const DevProblem& pb, double coeff, SolveSetup& ss)
+{
+    const double r = coeff * pb.cdx;
+    ss.r = r;
+    DevSolve& sv = ss.sv;
+    memset(&sv, 0, sizeof sv);
+    const double b = 1.0 + 2.0 * r;
+    const double s = std::sqrt(1.0 + 4.0 * r);
+    sv.lam = 2.0 * r / (b + s);
+    sv.g = 2.0 / (b + s);
+    if (!pb.periodic) {
+        // Thomas pivots den_i = b - r^2/den_{i-1} converge geometrically;
+        // keep the exact prefix, then the fixed point.
+        std::vector<double> m, g;
+        double den = b;
+        for (int i = 0; i < pb.nx; ++i) {
+            if (i > 0) {
+                const double nd = b - r * r / den;
+                if (nd == den && i > 1) break;
+                den = nd;
+            }
+            m.push_back(r / den);
+            g.push_back(1.0 / den);
+        }
+        sv.ntab = (int)m.size();
+        sv.lam = m.back();
+        sv.g = g.back();
+        ss.tab.assign(m.begin(), m.end());
+        ss.tab.insert(ss.tab.end(), g.begin(), g.end());
+    }
+    if (pb.nx <= kSmax) {
+        sv.nseg = 1;
+        sv.tile = pb.nx;
+        sv.halo = 0;
+        ss.cfg = pick_cfg(pb.nx);
+    } else {
+        // truncated halo: lam^H <= 2^-60 relative to the recurrence magnitude
+        int H = 0;
+        if (sv.lam > 0.0) H = (int)std::ceil(60.0 * std::log(2.0) / -std::log(sv.lam)) + 1;
+        H = (H + 1) & ~1;
+        int T = ((kSmax - 2 * H) / 512) * 512;
+        if (T < 512) {
+            char buf[256];
+            snprintf(buf, sizeof buf,
+                     "stiffness r=%.4g needs a truncation halo of %d points; the segmented "
+                     "line solve supports at most %d (use fewer points or a smaller dt)",
+                     r, H, (kSmax - 512) / 2);
+            ss.err = buf;
+            return RIDC_E_CONFIG;
+        }
+        sv.halo = H;
+        sv.tile = T;
+        sv.nseg = (pb.nx + T - 1) / T;
+        ss.cfg = pick_cfg(kSmax);
+    }
+    return RIDC_OK;
+}
+
+}  // namespace
+
+// ================================================================ context
+
+struct ridc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    ridc_problem prob;
+    DevProblem pb;
+    SolveSetup ss;
+    double t_start = 0, t_end = 0, dt = 0;
+    int levels = 0, restarts = 0;
+    long long steps = 0, per = 0, ticks = 0;
+    uint32_t flags = 0;
+    long long V = 0;
+    double* d_weights = nullptr;
+    double* d_tab = nullptr;
+    double* d_ring[kMaxLevels] = {};
+    long long cap[kMaxLevels] = {};
+    double* d_y0 = nullptr;
+    unsigned long long* d_err = nullptr;
+    EngineParams ep;
+    std::vector<int> steady_off, startup_off;
+    cudaGraphExec_t gexec = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    long long launches = 0;
+    long long ring_vectors = 0;
+    std::string err;
+};
+
+namespace {
+
+long long delay(int j) { return (long long)j * (j + 1) / 2; }   // engine.py:50-54
+
+// Offsets of the packed weight tables (quadrature.pack_weight_tables).
+void weight_offsets(int L, std::vector<int>& st, std::vector<int>& su, long long& total)
+{
+    st.assign(kMaxLevels, 0);
+    su.assign(kMaxLevels, 0);
+    long long off = 0;
+    for (int j = 1; j < L; ++j) { st[j] = (int)off; off += j + 1; }
+    for (int j = 2; j < L; ++j) { su[j] = (int)off; off += (long long)(j - 1) * (j + 1); }
+    total = off;
+}
+
+EngineParams interval_params(ridc_ctx* c, int interval)
+{
+    EngineParams ep = c->ep;
+    for (int j = 0; j < c->levels; ++j) ep.off[j] = 0;
+    if (c->flags & RIDC_RECORD_TRAJECTORY) ep.off[c->levels - 1] = (long long)interval * c->per;
+    return ep;
+}
+
+// Capture the whole run: per interval one seed + one launch per tick.
+int capture_graph(ridc_ctx* c)
+{
+    const int L = c->levels;
+    const int items = c->pb.ny * c->ss.sv.nseg;
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(&c->err, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    long long launches = 0;
+    cudaError_t le = cudaSuccess;
+    for (int r = 0; r < c->restarts && le == cudaSuccess; ++r) {
+        EngineParams ep = interval_params(c, r);
+        const double* src = c->d_y0;
+        if (r > 0) {
+            EngineParams prev = interval_params(c, r - 1);
+            const int top = L - 1;
+            src = prev.ring[top] + ((prev.off[top] + c->per) % prev.cap[top]) * c->V;
+        }
+        int sb = (int)std::min<long long>((c->V + 255) / 256, 148 * 8);
+        k_seed<<<sb, 256, 0, c->stream>>>(src, ep);
+        le = cudaGetLastError();
+        ++launches;
+        for (long long k = 1; k <= c->ticks && le == cudaSuccess; ++k) {
+            TickParams tp;
+            memset(&tp, 0, sizeof tp);
+            for (int j = 0; j < L; ++j) {
+                const long long t = k - delay(j);
+                if (t >= 1 && t <= c->per) {
+                    tp.level[tp.nact] = j;
+                    tp.target[tp.nact] = t;
+                    ++tp.nact;
+                }
+            }
+            if (tp.nact == 0) continue;
+            le = launch_tick(c->pb.kind, c->ss.cfg, dim3(items, tp.nact), c->stream, ep, tp);
+            ++launches;
+        }
+    }
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+    if (le != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        return fail(&c->err, RIDC_E_CUDA, std::string("kernel launch during capture: ") +
+                                              cudaGetErrorString(le));
+    }
+    CUDA_TRY(&c->err, ce);
+    cudaError_t ie = cudaGraphInstantiate(&c->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    CUDA_TRY(&c->err, ie);
+    c->launches = launches;
+    return RIDC_OK;
+}
+
+int check_err_word(ridc_ctx* c)
+{
+    unsigned long long w = 0;
+    CUDA_TRY(&c->err, cudaMemcpyAsync(&w, c->d_err, sizeof w, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(&c->err, cudaStreamSynchronize(c->stream));
+    if (w != ULLONG_MAX) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "level %d produced non-finite entries at step %lld",
+                 (int)(w & 0xff), (long long)(w >> 8));
+        return fail(&c->err, RIDC_E_NONFINITE, buf);
+    }
+    return RIDC_OK;
+}
+
+int march(ridc_ctx* c, double* wall_seconds)
+{
+    CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+    CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
+    CUDA_TRY(&c->err, cudaEventRecord(c->ev1, c->stream));
+    CUDA_TRY(&c->err, cudaEventSynchronize(c->ev1));
+    if (wall_seconds) {
+        float ms = 0.f;
+        CUDA_TRY(&c->err, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        *wall_seconds = ms * 1e-3;
+    }
+    return check_err_word(c);
+}
+
+const double* final_slot(ridc_ctx* c, int level)
+{
+    EngineParams ep = interval_params(c, c->restarts - 1);
+    return ep.ring[level] + ((ep.off[level] + c->per) % ep.cap[level]) * c->V;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32_t levels,
+                int64_t steps, int32_t restarts, const double* weights, int64_t nweights,
+                int32_t device, uint32_t flags, ridc_ctx** out)
+{
+    if (!out) return fail(nullptr, RIDC_E_CONFIG, "out is NULL");
+    *out = nullptr;
+    int rc = validate_problem(problem);
+    if (rc) return rc;
+    // RidcConfig.__post_init__ (engine.py:71-87)
+    if (levels < 1 || levels > kMaxLevels)
+        return fail(nullptr, RIDC_E_CONFIG, "levels must be in 1..12");
+    if (steps < 1 || restarts < 1) return fail(nullptr, RIDC_E_CONFIG, "steps and restarts must be positive");
+    if (steps % restarts) return fail(nullptr, RIDC_E_CONFIG, "steps must be divisible by restarts");
+    const long long per = steps / restarts;
+    if (per < delay(levels) + 1) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "each restart interval has %lld steps; %d levels need >= %lld",
+                 per, levels, delay(levels) + 1);
+        return fail(nullptr, RIDC_E_CONFIG, buf);
+    }
+    if (!(t_start < t_end)) return fail(nullptr, RIDC_E_CONFIG, "need t_start < t_end");
+    std::vector<int> st, su;
+    long long wtotal = 0;
+    weight_offsets(levels, st, su, wtotal);
+    if (nweights < wtotal || (wtotal > 0 && !weights))
+        return fail(nullptr, RIDC_E_DIMENSION, "weight table shorter than levels require");
+
+    ridc_ctx* c = new ridc_ctx();
+    c->device = device;
+    c->prob = *problem;
+    c->pb = make_problem(problem);
+    c->t_start = t_start;
+    c->t_end = t_end;
+    c->levels = levels;
+    c->steps = steps;
+    c->restarts = restarts;
+    c->per = per;
+    c->ticks = per + delay(levels - 1);
+    c->flags = flags;
+    c->V = (long long)problem->nx * problem->ny;
+    c->dt = (t_end - t_start) / (double)steps;   // engine.py:468 global dt
+    c->steady_off = st;
+    c->startup_off = su;
+    auto bail = [&](int code) {
+        std::string m = c->err.empty() ? g_last_error : c->err;
+        ridc_destroy(c);
+        g_last_error = m;
+        return code;
+    };
+    if ((rc = make_solve(c->pb, c->dt, c->ss)) != RIDC_OK) {
+        c->err = c->ss.err;
+        return bail(rc);
+    }
+    if (cudaSetDevice(device) != cudaSuccess) {
+        c->err = "cudaSetDevice failed";
+        return bail(RIDC_E_CUDA);
+    }
+#define CTX_TRY(expr)                                                                        \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            c->err = std::string(#expr " failed: ") + cudaGetErrorString(_e);               \
+            return bail(RIDC_E_CUDA);                                                        \
+        }                                                                                    \
+    } while (0)
+    CTX_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CTX_TRY(cudaEventCreate(&c->ev0));
+    CTX_TRY(cudaEventCreate(&c->ev1));
+    const size_t vb = (size_t)c->V * sizeof(double);
+    CTX_TRY(cudaMalloc(&c->d_weights, std::max<long long>(wtotal, 1) * sizeof(double)));
+    if (wtotal > 0)
+        CTX_TRY(cudaMemcpy(c->d_weights, weights, wtotal * sizeof(double), cudaMemcpyHostToDevice));
+    if (!c->ss.tab.empty()) {
+        CTX_TRY(cudaMalloc(&c->d_tab, c->ss.tab.size() * sizeof(double)));
+        CTX_TRY(cudaMemcpy(c->d_tab, c->ss.tab.data(), c->ss.tab.size() * sizeof(double),
+                           cudaMemcpyHostToDevice));
+        c->ss.sv.tab_m = c->d_tab;
+        c->ss.sv.tab_g = c->d_tab + c->ss.sv.ntab;
+    }
+    for (int j = 0; j < levels; ++j) {
+        const bool top = j == levels - 1;
+        long long cap = top ? 2 : 2LL * j + 3;
+        if (top && (flags & RIDC_RECORD_TRAJECTORY)) cap = steps + 1;
+        c->cap[j] = cap;
+        c->ring_vectors += cap;
+        CTX_TRY(cudaMalloc(&c->d_ring[j], (size_t)cap * vb));
+    }
+    CTX_TRY(cudaMalloc(&c->d_y0, vb));
+    CTX_TRY(cudaMalloc(&c->d_err, sizeof(unsigned long long)));
+    EngineParams& ep = c->ep;
+    memset(&ep, 0, sizeof ep);
+    ep.pb = c->pb;
+    ep.sv = c->ss.sv;
+    ep.V = c->V;
+    ep.dt = c->dt;
+    ep.levels = levels;
+    for (int j = 0; j < levels; ++j) {
+        ep.ring[j] = c->d_ring[j];
+        ep.cap[j] = c->cap[j];
+    }
+    ep.weights = c->d_weights;
+    for (int j = 0; j < kMaxLevels; ++j) {
+        ep.steady_off[j] = st[j];
+        ep.startup_off[j] = su[j];
+    }
+    ep.err = c->d_err;
+    if ((rc = capture_graph(c)) != RIDC_OK) return bail(rc);
+#undef CTX_TRY
+    *out = c;
+    return RIDC_OK;
+}
+
+int ridc_run(ridc_ctx* c, const double* y0_host, double* final_host, double* level_finals_host,
+             double* traj_host, double* wall_seconds)
+{
+    if (!c || !y0_host || !final_host) return fail(c ? &c->err : nullptr, RIDC_E_CONFIG, "NULL argument");
+    if (traj_host && !(c->flags & RIDC_RECORD_TRAJECTORY))
+        return fail(&c->err, RIDC_E_CONFIG, "trajectory requested but not recorded (flags)");
+    CUDA_TRY(&c->err, cudaSetDevice(c->device));
+    const size_t vb = (size_t)c->V * sizeof(double);
+    CUDA_TRY(&c->err, cudaMemcpyAsync(c->d_y0, y0_host, vb, cudaMemcpyHostToDevice, c->stream));
+    int rc = march(c, wall_seconds);
+    if (rc) return rc;
+    CUDA_TRY(&c->err, cudaMemcpyAsync(final_host, final_slot(c, c->levels - 1), vb,
+                                      cudaMemcpyDeviceToHost, c->stream));
+    if (level_finals_host)
+        for (int j = 0; j < c->levels; ++j)
+            CUDA_TRY(&c->err, cudaMemcpyAsync(level_finals_host + (size_t)j * c->V, final_slot(c, j),
+                                              vb, cudaMemcpyDeviceToHost, c->stream));
+    if (traj_host)
+        CUDA_TRY(&c->err, cudaMemcpyAsync(traj_host, c->d_ring[c->levels - 1],
+                                          (size_t)(c->steps + 1) * vb, cudaMemcpyDeviceToHost,
+                                          c->stream));
+    CUDA_TRY(&c->err, cudaStreamSynchronize(c->stream));
+    return RIDC_OK;
+}
+
+int ridc_run_device(ridc_ctx* c, const double* y0_dev, double* final_dev, double* wall_seconds)
+{
+    if (!c || !y0_dev || !final_dev) return fail(c ? &c->err : nullptr, RIDC_E_CONFIG, "NULL argument");
+    CUDA_TRY(&c->err, cudaSetDevice(c->device));
+    const size_t vb = (size_t)c->V * sizeof(double);
+    CUDA_TRY(&c->err, cudaMemcpyAsync(c->d_y0, y0_dev, vb, cudaMemcpyDeviceToDevice, c->stream));
+    int rc = march(c, wall_seconds);
+    if (rc) return rc;
+    CUDA_TRY(&c->err, cudaMemcpyAsync(final_dev, final_slot(c, c->levels - 1), vb,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(&c->err, cudaStreamSynchronize(c->stream));
+    return RIDC_OK;
+}
+
+int ridc_info_get(const ridc_ctx* c, ridc_info* info)
+{
+    if (!c || !info) return fail(nullptr, RIDC_E_CONFIG, "NULL argument");
+    info->levels = c->levels;
+    info->restarts = c->restarts;
+    info->steps = c->steps;
+    info->ticks_per_interval = c->ticks;
+    info->kernel_launches = c->launches;
+    info->tile = c->ss.sv.tile;
+    info->halo = c->ss.sv.halo;
+    info->items_per_level = c->pb.ny * c->ss.sv.nseg;
+    info->threads = c->ss.cfg.nt;
+    info->ring_vectors = c->ring_vectors;
+    info->lambda = c->ss.sv.lam;
+    info->r = c->ss.r;
+    return RIDC_OK;
+}
+
+int ridc_destroy(ridc_ctx* c)
+{
+    if (!c) return RIDC_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (int j = 0; j < kMaxLevels; ++j)
+        if (c->d_ring[j]) cudaFree(c->d_ring[j]);
+    if (c->d_weights) cudaFree(c->d_weights);
+    if (c->d_tab) cudaFree(c->d_tab);
+    if (c->d_y0) cudaFree(c->d_y0);
+    if (c->d_err) cudaFree(c->d_err);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return RIDC_OK;
+}
+
+const char* ridc_last_error(const ridc_ctx* c)
+{
+    if (c && !c->err.empty()) return c->err.c_str();
+    return g_last_error.c_str();
+}
+
+// ---------------------------------------------------------------- single ops
+
+int ridc_op_apply(const ridc_problem* problem, int32_t op, const double* in_dev, double* out_dev,
+                  int32_t device)
+{
+    int rc = validate_problem(problem);
+    if (rc) return rc;
+    if (op != RIDC_OP_STIFF && op != RIDC_OP_NONSTIFF) return fail(nullptr, RIDC_E_CONFIG, "bad op");
+    CUDA_TRY(nullptr, cudaSetDevice(device));
+    DevProblem pb = make_problem(problem);
+    CUDA_TRY(nullptr, launch_apply(pb, op, in_dev, out_dev, 0));
+    CUDA_TRY(nullptr, cudaDeviceSynchronize());
+    return RIDC_OK;
+}
+
+static int run_single_item(const ridc_problem* problem, double coeff, StepItem& it, int32_t device)
+{
+    int rc = validate_problem(problem);
+    if (rc) return rc;
+    CUDA_TRY(nullptr, cudaSetDevice(device));
+    DevProblem pb = make_problem(problem);
+    SolveSetup ss;
+    if ((rc = make_solve(pb, coeff, ss)) != RIDC_OK) return fail(nullptr, rc, ss.err);
+    double* d_tab = nullptr;
+    unsigned long long* d_err = nullptr;
+    auto cleanup = [&]() {
+        if (d_tab) cudaFree(d_tab);
+        if (d_err) cudaFree(d_err);
+    };
+    if (!ss.tab.empty()) {
+        if (cudaMalloc(&d_tab, ss.tab.size() * sizeof(double)) != cudaSuccess ||
+            cudaMemcpy(d_tab, ss.tab.data(), ss.tab.size() * sizeof(double),
+                       cudaMemcpyHostToDevice) != cudaSuccess) {
+            cleanup();
+            return fail(nullptr, RIDC_E_CUDA, "factor table upload failed");
+        }
+        ss.sv.tab_m = d_tab;
+        ss.sv.tab_g = d_tab + ss.sv.ntab;
+    }
+    if (cudaMalloc(&d_err, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(d_err, 0xff, sizeof(unsigned long long)) != cudaSuccess) {
+        cleanup();
+        return fail(nullptr, RIDC_E_CUDA, "error word allocation failed");
+    }
+    cudaError_t e = launch_item(pb.kind, ss.cfg, pb.ny * ss.sv.nseg, 0, pb, ss.sv, it, d_err);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    unsigned long long w = ULLONG_MAX;
+    if (e == cudaSuccess) e = cudaMemcpy(&w, d_err, sizeof w, cudaMemcpyDeviceToHost);
+    cleanup();
+    if (e != cudaSuccess) return fail(nullptr, RIDC_E_CUDA, cudaGetErrorString(e));
+    if (w != ULLONG_MAX) return fail(nullptr, RIDC_E_NONFINITE, "step produced non-finite entries");
+    return RIDC_OK;
+}
+
+int ridc_op_solve(const ridc_problem* problem, double coeff, const double* rhs_dev, double* x_dev,
+                  int32_t device)
+{
+    StepItem it;
+    memset(&it, 0, sizeof it);
+    it.nnodes = 1;
+    it.vec[0] = rhs_dev;
+    it.ca[0] = 1.0;
+    it.out = x_dev;
+    it.level = 0;
+    it.target = -1;
+    return run_single_item(problem, coeff, it, device);
+}
+
+int ridc_op_step(const ridc_problem* problem, double dt, const double* eta_dev, int32_t nwin,
+                 const double* const* win_dev, const double* cs, const double* cn, double* out_dev,
+                 int32_t device)
+{
+    if (nwin < 0 || nwin > kMaxNodes - 1) return fail(nullptr, RIDC_E_PROTOCOL, "window too large");
+    if (nwin > 0 && (!win_dev || !cs || !cn)) return fail(nullptr, RIDC_E_CONFIG, "NULL window");
+    StepItem it;
+    memset(&it, 0, sizeof it);
+    it.nnodes = 1 + nwin;
+    it.vec[0] = eta_dev;
+    it.ca[0] = 1.0;
+    it.cs[0] = 0.0;
+    it.cn[0] = dt;
+    for (int a = 0; a < nwin; ++a) {
+        it.vec[1 + a] = win_dev[a];
+        it.ca[1 + a] = 0.0;
+        it.cs[1 + a] = cs[a];
+        it.cn[1 + a] = cn[a];
+    }
+    it.out = out_dev;
+    it.level = nwin > 0 ? nwin - 1 : 0;
+    it.target = -1;
+    return run_single_item(problem, dt, it, device);
+}
+
+int ridc_op_step_rows(const ridc_problem* problem, double dt, const double* eta_dev, int32_t nrows,
+                      const double* const* rows_dev, const double* ca, double* out_dev,
+                      int32_t device)
+{
+    if (nrows < 0 || nrows > kMaxNodes - 1) return fail(nullptr, RIDC_E_PROTOCOL, "window too large");
+    if (nrows > 0 && (!rows_dev || !ca)) return fail(nullptr, RIDC_E_CONFIG, "NULL window");
+    StepItem it;
+    memset(&it, 0, sizeof it);
+    it.nnodes = 1 + nrows;
+    it.vec[0] = eta_dev;
+    it.ca[0] = 1.0;
+    it.cn[0] = dt;
+    for (int a = 0; a < nrows; ++a) {
+        it.vec[1 + a] = rows_dev[a];
+        it.ca[1 + a] = ca[a];
+    }
+    it.out = out_dev;
+    it.target = -1;
+    return run_single_item(problem, dt, it, device);
+}
+
+}  // extern "C"
