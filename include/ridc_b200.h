@@ -139,6 +139,10 @@ int ridc_op_step_rows(const ridc_problem *problem, double dt, const double *eta_
                       int32_t nrows, const double *const *rows_dev, const double *ca,
                       double *out_dev, int32_t device);
 
+/* Diagnostic: clock64 phase trace of the last tick launch (CTA 0, 8 items x 16
+ * stamps); only when the context was created with RIDC_PHASE_TIMING=1. */
+int ridc_debug_phase_trace(const ridc_ctx *ctx, long long *out, int32_t n);
+
 /* ---- lagged level pipeline, one level per GPU (one process per GPU) ---- */
 
 typedef struct ridc_pipe ridc_pipe;

@@ -47,6 +47,7 @@ SIGNATURES = {
                                     ctypes.c_int32]),
     "ridc_op_step_rows": (ctypes.c_int, [_P(CProblem), _d, _vp, ctypes.c_int32, _P(_vp), _dp, _vp,
                                          ctypes.c_int32]),
+    "ridc_debug_phase_trace": (ctypes.c_int, [_vp, _P(ctypes.c_longlong), ctypes.c_int32]),
     "ridc_pipe_handle_bytes": (ctypes.c_int64, []),
     "ridc_pipe_create": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int32, ctypes.c_int64,
                                         ctypes.c_int32, _vp, ctypes.c_int64, ctypes.c_int32,

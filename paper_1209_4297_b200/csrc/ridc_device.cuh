@@ -31,6 +31,7 @@ enum Kind { ADV_DIFF_1D = 1, BURGERS_1D = 2, RD_1D = 3, ADV_DIFF_2D = 4, RD_2D =
 
 constexpr int kMaxLevels = 12;              // engine.py:47 (MAX_LEVEL + 1)
 constexpr int kMaxNodes = 2 * kMaxLevels + 1;  // own state + window (states, or f^S and f^N rows)
+constexpr int kMaxChunk = 32;               // max elements per thread in the scan phase
 
 struct DevProblem {
     int kind, nx, ny, periodic;
@@ -49,7 +50,18 @@ struct DevSolve {
     int halo;            // truncation halo per side (segment mode), 0 = whole line
     int tile;            // output points per item along x
     int nseg;            // items per x-line (1 = whole-line exact mode)
+    double pw[kMaxChunk];  // pw[e] = lam^(e+1): carry weights of a constant-coefficient chunk
+    double zf4[4], zf8[8], zf16[16];  // forward-carry response of a backward chunk pass (K = 4/8/16)
+    const struct PlanRow* plans;   // TMA staging plans [nseg][row parity] (engine only)
+    long long* dbg;                // optional phase trace (RIDC_PHASE_TIMING), CTA 0 only
 };
+
+// Phase trace: CTA 0, thread 0, first 8 items of a launch, 16 stamps each.
+#define RIDC_STAMP(sv, item_no, idx)                                                         \
+    do {                                                                                     \
+        if ((sv).dbg && blockIdx.x == 0 && threadIdx.x == 0 && (item_no) < 8)                \
+            (sv).dbg[(item_no) * 16 + (idx)] = clock64();                                    \
+    } while (0)
 
 struct StepItem {
     int nnodes;
@@ -124,13 +136,23 @@ __device__ __forceinline__ void eval_point(const DevProblem& pb, const double* r
     }
 }
 
+// Barrier over the NT compute threads only (named barrier 1); a producer
+// warp, when present, never joins it.
+template <int N>
+__device__ __forceinline__ void csync()
+{
+    asm volatile("bar.sync 1, %0;" ::"r"(N) : "memory");
+}
+
 // Block-wide exclusive scan of affine maps in thread order (reverse: from the
 // last thread down).  Returns the composition of all chunks before this
 // thread's; `total` receives the composition over the whole block.
+// swarp needs 2*NW+1 entries: warp totals, then warp prefixes + block total.
 template <int NT>
 __device__ __forceinline__ Aff block_scan(Aff mine, bool reverse, Aff* swarp, Aff& total)
 {
     constexpr int NW = NT / 32;
+    static_assert(NW <= 32, "one warp scans the warp totals");
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Aff inc = mine;
@@ -138,35 +160,35 @@ __device__ __forceinline__ Aff block_scan(Aff mine, bool reverse, Aff* swarp, Af
     for (int d = 1; d < 32; d <<= 1) {
         double A = reverse ? __shfl_down_sync(FULL, inc.A, d) : __shfl_up_sync(FULL, inc.A, d);
         double B = reverse ? __shfl_down_sync(FULL, inc.B, d) : __shfl_up_sync(FULL, inc.B, d);
-        bool ok = reverse ? (lane + d < 32) : (lane >= d);
+        const bool ok = reverse ? (lane + d < 32) : (lane >= d);
         if (ok) inc = compose(inc, Aff{A, B});
     }
     double eA = reverse ? __shfl_down_sync(FULL, inc.A, 1) : __shfl_up_sync(FULL, inc.A, 1);
     double eB = reverse ? __shfl_down_sync(FULL, inc.B, 1) : __shfl_up_sync(FULL, inc.B, 1);
     const bool first = reverse ? (lane == 31) : (lane == 0);
-    Aff exc = first ? Aff{1.0, 0.0} : Aff{eA, eB};
+    const Aff exc = first ? Aff{1.0, 0.0} : Aff{eA, eB};
     const bool last = reverse ? (lane == 0) : (lane == 31);
     if (last) swarp[warp] = inc;
-    __syncthreads();
-    Aff wp{1.0, 0.0}, tot{1.0, 0.0};
-    if (!reverse) {
+    csync<NT>();
+    if (warp == 0) {
+        // lane l holds the l-th warp total in scan order
+        const int w = reverse ? NW - 1 - lane : lane;
+        Aff t = lane < NW ? swarp[w] : Aff{1.0, 0.0};
+        Aff ti = t;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            Aff s = swarp[w];
-            if (w < warp) wp = compose(s, wp);
-            tot = compose(s, tot);
+        for (int d = 1; d < NW; d <<= 1) {
+            const double A = __shfl_up_sync(FULL, ti.A, d);
+            const double B = __shfl_up_sync(FULL, ti.B, d);
+            if (lane >= d) ti = compose(ti, Aff{A, B});
         }
-    } else {
-#pragma unroll
-        for (int w = NW - 1; w >= 0; --w) {
-            Aff s = swarp[w];
-            if (w > warp) wp = compose(s, wp);
-            tot = compose(s, tot);
-        }
+        const double pA = __shfl_up_sync(FULL, ti.A, 1);
+        const double pB = __shfl_up_sync(FULL, ti.B, 1);
+        if (lane < NW) swarp[NW + w] = lane == 0 ? Aff{1.0, 0.0} : Aff{pA, pB};
+        if (lane == NW - 1) swarp[2 * NW] = ti;
     }
-    __syncthreads();
-    total = tot;
-    return compose(exc, wp);
+    csync<NT>();
+    total = swarp[2 * NW];
+    return compose(exc, swarp[NW + warp]);
 }
 
 __device__ __forceinline__ void coef(const DevSolve& sv, int col, double& m, double& g)
@@ -186,141 +208,459 @@ __device__ __forceinline__ unsigned long long err_code(long long target, int lev
     return ((unsigned long long)target << 8) | (unsigned long long)level;
 }
 
-// One work item.  sbuf: padded shared buffer of >= pad(NT*KMAX) doubles.
+// Shared-memory layout of one item (doubles): the padded buffer used for
+// the x-stencil neighbours and then for the recurrences.
+template <int NT, int KMAX>
+struct Smem {
+    static constexpr int NW = NT / 32;
+    static constexpr int CAP = NT * KMAX;
+    static constexpr int TOTAL = CAP + CAP / 16 + 1;
+};
+
+// Geometry of one item.  Positions q = 0..Q-1 map to columns c_first + q
+// (c_first = s0 - 1): the extended range plus one stencil neighbour on each
+// side.  rhs lives on q in [1, Q-1).
+struct Geo {
+    int item_no;           // ordinal of the item within its CTA (phase trace)
+    int row, seg, c0, tlen;
+    int s0, S, out_lo;     // extended range [s0, s0+S), outputs at p in [out_lo, out_lo+tlen)
+    bool cyclic;
+    bool fast;             // truncated segment: no wrap / ghosts / coefficient tables
+};
+
+template <int KIND, int NT, int KMAX>
+__device__ __forceinline__ Geo make_geo(const DevProblem& pb, const DevSolve& sv, int tile)
+{
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr int CAP = NT * KMAX;
+    Geo g;
+    g.item_no = 0;
+    g.row = tile / sv.nseg;
+    const int seg = tile - g.row * sv.nseg;
+    g.seg = seg;
+    const int nx = pb.nx;
+    g.c0 = seg * sv.tile;
+    g.tlen = min(sv.tile, nx - g.c0);
+    if (sv.nseg == 1) {
+        g.s0 = 0; g.S = nx; g.out_lo = 0; g.cyclic = periodic;
+    } else if (periodic) {
+        g.s0 = g.c0 - sv.halo; g.S = g.tlen + 2 * sv.halo; g.out_lo = sv.halo; g.cyclic = false;
+    } else {
+        g.s0 = max(g.c0 - sv.halo, 0);
+        const int send = min(g.c0 + g.tlen + sv.halo, nx);
+        g.S = send - g.s0; g.out_lo = g.c0 - g.s0; g.cyclic = false;
+    }
+    g.fast = sv.nseg > 1 && g.S + 2 <= CAP && g.s0 - 1 >= 0 && g.s0 + g.S + 1 <= nx &&
+             (sv.ntab == 0 || g.s0 - 1 >= sv.ntab);
+    return g;
+}
+
+// Fold one node value into the pointwise accumulators (see item_body):
+//   P  += ca u + cn * (pointwise parts of f^N: reaction, y-stencil, y-advection)
+//   WS += cs u
+//   WX += cn u (x-advection) | cn u^2 (Burgers flux)
+template <int KIND>
+__device__ __forceinline__ void accumulate_point(const DevProblem& pb, double ca, double cs, double cn,
+                                                 double v, double vn, double vs, double& P,
+                                                 double& WS, double& WX)
+{
+    double p = P;
+    if (ca != 0.0) p = fma(ca, v, p);
+    if (cn != 0.0) {   // uniform; also keeps unloaded y-neighbours out of the sum
+        if (KIND == RD_1D) p = fma(cn, pb.rho * v * (1.0 - v), p);
+        if (KIND == RD_2D) p = fma(cn, fma(pb.rho * v, 1.0 - v, pb.cdy * (vn - 2.0 * v + vs)), p);
+        if (KIND == ADV_DIFF_2D) p = fma(cn, fma(pb.cay, vs - v, pb.cdy * (vn - 2.0 * v + vs)), p);
+    }
+    P = p;
+    WS = fma(cs, v, WS);
+    if (KIND == BURGERS_1D) WX = fma(cn, v * v, WX);
+    else if (KIND == ADV_DIFF_1D || KIND == ADV_DIFF_2D) WX = fma(cn, v, WX);
+}
+
+template <int KMAX>
+__device__ __forceinline__ const double* zf_of(const DevSolve& sv)
+{
+    return KMAX == 4 ? sv.zf4 : (KMAX == 8 ? sv.zf8 : sv.zf16);
+}
+
+// Constant-coefficient solve of a truncated segment held as KMAX consecutive
+// points per thread (thread t owns chunk t).  Both local recurrences run
+// first (zero carries); the chunk-to-chunk carries then need only the B
+// halves of the affine maps because every chunk multiplier is M = lam^KMAX:
+//   forward  c_t = sum_{u<t} M^{t-1-u} Bf_u,
+//   backward d_t = sum_{u>t} M^{u-t-1} (Bb_u + c_u zf_0),
+// each a warp shuffle scan plus a scan of the warp totals that every warp
+// repeats redundantly (one barrier per direction).  Finally
+//   x_e = xloc_e + c_t zf_e + d_t lam^(KMAX-e).
+template <int NT, int KMAX>
+__device__ __forceinline__ void fast_solve(const DevSolve& sv, double (&vv)[KMAX], double* sx)
+{
+    constexpr int NW = NT / 32;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double m = sv.lam, g = sv.g;
+    const double* zf = zf_of<KMAX>(sv);
+    double mp[10];   // M^(2^i)
+    mp[0] = sv.pw[KMAX - 1];
+#pragma unroll
+    for (int i = 1; i < 10; ++i) mp[i] = mp[i - 1] * mp[i - 1];
+    double y = 0.0;
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e) { y = fma(m, y, g * vv[e]); vv[e] = y; }
+    const double bf = y;
+    double x = 0.0;
+#pragma unroll
+    for (int e = KMAX - 1; e >= 0; --e) { x = fma(m, x, vv[e]); vv[e] = x; }
+    const double bb = x;
+    // M^lane and M^(31-lane)
+    double ml = 1.0, mr = 1.0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if (lane & (1 << i)) ml *= mp[i];
+        if ((31 - lane) & (1 << i)) mr *= mp[i];
+    }
+    // ---- forward carries
+    double inc = bf;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const double t = __shfl_up_sync(FULL, inc, 1 << i);
+        if (lane >= (1 << i)) inc = fma(mp[i], t, inc);
+    }
+    if (lane == 31) sx[warp] = inc;
+    double ex = __shfl_up_sync(FULL, inc, 1);
+    if (lane == 0) ex = 0.0;
+    csync<NT>();
+    double wi = lane < NW ? sx[lane] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if ((1 << i) >= NW) break;
+        const double t = __shfl_up_sync(FULL, wi, 1 << i);
+        if (lane >= (1 << i)) wi = fma(mp[5 + i], t, wi);
+    }
+    double cw = __shfl_sync(FULL, wi, warp > 0 ? warp - 1 : 0);
+    if (warp == 0) cw = 0.0;
+    const double cf = fma(ml, cw, ex);
+    // ---- backward carries
+    double rinc = fma(cf, zf[0], bb);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const double t = __shfl_down_sync(FULL, rinc, 1 << i);
+        if (lane + (1 << i) < 32) rinc = fma(mp[i], t, rinc);
+    }
+    if (lane == 0) sx[NW + warp] = rinc;
+    double exr = __shfl_down_sync(FULL, rinc, 1);
+    if (lane == 31) exr = 0.0;
+    csync<NT>();
+    // reverse warp scan: lane l holds the total of warp NW-1-l
+    double wr = lane < NW ? sx[NW + (NW - 1 - lane)] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if ((1 << i) >= NW) break;
+        const double t = __shfl_up_sync(FULL, wr, 1 << i);
+        if (lane >= (1 << i)) wr = fma(mp[5 + i], t, wr);
+    }
+    const int rl = NW - 1 - warp;   // my warp's position in reverse order
+    double dw = __shfl_sync(FULL, wr, rl > 0 ? rl - 1 : 0);
+    if (rl == 0) dw = 0.0;
+    const double dc = fma(mr, dw, exr);
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e) vv[e] = fma(dc, sv.pw[KMAX - 1 - e], fma(cf, zf[e], vv[e]));
+}
+
+// Phases 2-5 of an item, shared by the register-load and the TMA-staged paths:
+// x-stencils of the accumulators, the two recurrences, the coalesced store.
+template <int KIND, int NT, int KMAX, bool FAST>
+__device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve& sv,
+                                            const StepItem& it, const Geo& geo, const double* P,
+                                            const double* WS, const double* WX, double* sbuf,
+                                            Aff* swarp, unsigned long long* err)
+{
+    constexpr int CAP = NT * KMAX;
+    constexpr bool has_wx = KIND == ADV_DIFF_1D || KIND == BURGERS_1D || KIND == ADV_DIFF_2D;
+    const int nx = pb.nx;
+    const int tid = threadIdx.x;
+    const int cf = geo.s0 - 1;
+    const int Q = geo.S + 2;
+    const size_t rbase = (size_t)geo.row * nx;
+    auto valid = [&](int q) { return q < Q; };
+    (void)nx;
+    const int ino = geo.item_no;
+    RIDC_STAMP(sv, ino, 2);
+    // ---- phase 2: x-stencils of WS (then WX) through shared memory
+    // (FAST: every position is computed; rhs outside [1, Q-1) is zeroed below)
+    double rhs[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        const int q = tid + k * NT;
+        rhs[k] = P[k];
+        if (FAST || valid(q)) sbuf[pad(q)] = WS[k];
+    }
+    csync<NT>();
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        const int q = tid + k * NT;
+        if (FAST ? (q >= 1 && q < CAP - 1) : (q >= 1 && q < Q - 1))
+            rhs[k] = fma(pb.cdx, (sbuf[pad(q - 1)] - 2.0 * WS[k]) + sbuf[pad(q + 1)], rhs[k]);
+    }
+    csync<NT>();
+    if (has_wx) {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const int q = tid + k * NT;
+            if (FAST || valid(q)) sbuf[pad(q)] = WX[k];
+        }
+        csync<NT>();
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const int q = tid + k * NT;
+            if (FAST ? (q >= 1 && q < CAP - 1) : (q >= 1 && q < Q - 1)) {
+                if (KIND == BURGERS_1D)
+                    rhs[k] = fma(-pb.bs, sbuf[pad(q + 1)] - sbuf[pad(q - 1)], rhs[k]);
+                else
+                    rhs[k] = fma(pb.cax, sbuf[pad(q + 1)] - WX[k], rhs[k]);
+            }
+        }
+        csync<NT>();
+    }
+    // scan coordinates: FAST scans all CAP positions (rhs 0 outside [1, Q-1):
+    // those lie in the truncation halo); otherwise e = q - 1 in [0, S).
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        const int q = tid + k * NT;
+        if (FAST) sbuf[pad(q)] = (q == 0 || q >= Q - 1) ? 0.0 : rhs[k];
+        else if (q >= 1 && q < Q - 1) sbuf[pad(q - 1)] = rhs[k];
+    }
+    csync<NT>();
+    RIDC_STAMP(sv, ino, 3);
+    // ---- phases 3-4: y_i = g_i rhs_i + m_i y_{i-1}, then x_i = y_i + m_i x_{i+1}
+    const int S = FAST ? CAP : geo.S;
+    const int e0 = FAST ? cf : geo.s0;          // column of scan index 0
+    const int base = tid * KMAX;
+    const int nm = FAST ? KMAX : max(0, min(KMAX, S - base));
+    double vv[KMAX];
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e) vv[e] = (FAST || e < nm) ? sbuf[pad(base + e)] : 0.0;
+    const bool cmode = FAST || (sv.ntab == 0) || (e0 + base >= sv.ntab);
+    const double m = sv.lam, g = sv.g;
+    if constexpr (FAST) {
+        RIDC_STAMP(sv, ino, 4);
+        fast_solve<NT, KMAX>(sv, vv, reinterpret_cast<double*>(swarp));
+        RIDC_STAMP(sv, ino, 7);
+    } else {
+    {
+        double y = 0.0, A = 1.0;
+        if (cmode) {
+#pragma unroll
+            for (int e = 0; e < KMAX; ++e)
+                if (FAST || e < nm) { y = fma(m, y, g * vv[e]); vv[e] = y; }
+            A = FAST ? sv.pw[KMAX - 1] : (nm > 0 ? sv.pw[nm - 1] : 1.0);
+        } else {
+#pragma unroll
+            for (int e = 0; e < KMAX; ++e)
+                if (e < nm) {
+                    double mm, gg;
+                    coef(sv, e0 + base + e, mm, gg);
+                    y = fma(mm, y, gg * vv[e]);
+                    A *= mm;
+                    vv[e] = y;
+                }
+        }
+        Aff tot;
+        RIDC_STAMP(sv, ino, 4);
+        const Aff pre = block_scan<NT>(Aff{A, y}, false, swarp, tot);
+        RIDC_STAMP(sv, ino, 5);
+        const double yinit = (!FAST && geo.cyclic) ? tot.B / (1.0 - tot.A) : 0.0;
+        const double cin = fma(pre.A, yinit, pre.B);
+        if (cmode) {
+#pragma unroll
+            for (int e = 0; e < KMAX; ++e)
+                if (FAST || e < nm) vv[e] = fma(sv.pw[e], cin, vv[e]);
+        } else {
+            double Pm = 1.0;
+#pragma unroll
+            for (int e = 0; e < KMAX; ++e)
+                if (e < nm) {
+                    double mm, gg;
+                    coef(sv, e0 + base + e, mm, gg);
+                    Pm *= mm;
+                    vv[e] = fma(Pm, cin, vv[e]);
+                }
+        }
+    }
+    {
+        double x = 0.0, A = 1.0;
+        if (cmode) {
+#pragma unroll
+            for (int e = KMAX - 1; e >= 0; --e)
+                if (FAST || e < nm) { x = fma(m, x, vv[e]); vv[e] = x; }
+            A = FAST ? sv.pw[KMAX - 1] : (nm > 0 ? sv.pw[nm - 1] : 1.0);
+        } else {
+#pragma unroll
+            for (int e = KMAX - 1; e >= 0; --e)
+                if (e < nm) {
+                    double mm, gg;
+                    coef(sv, e0 + base + e, mm, gg);
+                    x = fma(mm, x, vv[e]);
+                    A *= mm;
+                    vv[e] = x;
+                }
+        }
+        Aff tot;
+        RIDC_STAMP(sv, ino, 6);
+        const Aff pre = block_scan<NT>(Aff{A, x}, true, swarp, tot);
+        RIDC_STAMP(sv, ino, 7);
+        const double xinit = (!FAST && geo.cyclic) ? tot.B / (1.0 - tot.A) : 0.0;
+        const double cin = fma(pre.A, xinit, pre.B);
+        if (cmode) {
+#pragma unroll
+            for (int e = 0; e < KMAX; ++e)
+                if (FAST || e < nm) vv[e] = fma(sv.pw[(FAST ? KMAX : nm) - 1 - e], cin, vv[e]);
+        } else {
+            double Pm = 1.0;
+#pragma unroll
+            for (int e = KMAX - 1; e >= 0; --e)
+                if (e < nm) {
+                    double mm, gg;
+                    coef(sv, e0 + base + e, mm, gg);
+                    Pm *= mm;
+                    vv[e] = fma(Pm, cin, vv[e]);
+                }
+        }
+    }
+    }
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e)
+        if (FAST || e < nm) sbuf[pad(base + e)] = vv[e];
+    csync<NT>();
+
+    RIDC_STAMP(sv, ino, 8);
+    // ---- phase 5: coalesced store of the tile + fused finite check
+    bool bad = false;
+    double* orow = it.out + rbase;
+    const int olo = FAST ? geo.out_lo + 1 : geo.out_lo;   // in scan coordinates
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        const int e = tid + k * NT;
+        if ((unsigned)(e - olo) < (unsigned)geo.tlen) {
+            const double xo = sbuf[pad(e)];
+            bad |= !isfinite(xo);
+            orow[e0 + e] = xo;
+        }
+    }
+    if (bad) atomicMin(err, err_code(it.target, it.level));
+    RIDC_STAMP(sv, ino, 9);
+}
+
+// One work item (FAST: interior segment, every position valid, constant
+// coefficients -- no predication anywhere).  smem: Smem<NT,KMAX>::TOTAL doubles.
+//
+// Phase 1 streams the (j+2) node states once, all loads of a node in flight
+// together (the next node's are issued before the current one is consumed).
+// The operators are linear in the window states except the pointwise
+// reaction and the Burgers flux (linear in u^2), so the window contributes
+// through three pointwise accumulators:
+//   P  = sum ca_k u_k + sum cn_k (pointwise parts of f^N: reaction, y-stencil)
+//   WS = sum cs_k u_k          (f^S applied once: cdx * second difference)
+//   WX = sum cn_k u_k | u_k^2  (x-advection / Burgers flux applied once)
+// Phase 2 applies the x-stencils through shared memory; phases 3-4 run the
+// two first-order recurrences on register chunks with block-wide affine
+// scans; phase 5 stores the tile coalesced with the fused finite check.
+template <int KIND, int NT, int KMAX, bool FAST>
+__device__ __forceinline__ void item_body(const DevProblem& pb, const DevSolve& sv,
+                                          const StepItem& it, const Geo& geo, double* sbuf,
+                                          Aff* swarp, unsigned long long* err)
+{
+    constexpr int CAP = NT * KMAX;
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr bool two_d = KIND == ADV_DIFF_2D || KIND == RD_2D;
+    constexpr bool has_wx = KIND == ADV_DIFF_1D || KIND == BURGERS_1D || KIND == ADV_DIFF_2D;
+    constexpr bool prefetch = !two_d;
+    const int nx = pb.nx, ny = pb.ny;
+    const int tid = threadIdx.x;
+    const int row = geo.row;
+    const int cf = geo.s0 - 1;              // column of q = 0
+    const int Q = geo.S + 2;
+    const size_t rbase = (size_t)row * nx;
+    const size_t rn_base = (size_t)(row == 0 ? ny - 1 : row - 1) * nx;
+    const size_t rs_base = (size_t)(row == ny - 1 ? 0 : row + 1) * nx;
+
+    auto valid = [&](int q) { return q < Q; };
+    auto col_of = [&](int q) {
+        int c = cf + q;
+        if (!FAST && periodic) c = c < 0 ? c + nx : (c >= nx ? c - nx : c);
+        return c;
+    };
+    auto ghost = [&](int q) { return !FAST && !periodic && (cf + q < 0 || cf + q >= nx); };
+
+    // ---- phase 1: pointwise accumulation over all nodes
+    double P[KMAX], WS[KMAX], WX[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) { P[k] = 0.0; WS[k] = 0.0; WX[k] = 0.0; }
+
+    double ua[KMAX], ub[KMAX], un[KMAX], us[KMAX];
+    auto load = [&](int a, double* u) {
+        const double* rp = it.vec[a] + rbase;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const int q = tid + k * NT;
+            u[k] = 0.0;
+            if (valid(q) && !ghost(q)) u[k] = ld_ro(rp + col_of(q));
+        }
+    };
+    auto load_y = [&](int a) {
+        const double* rn = it.vec[a] + rn_base;
+        const double* rs = it.vec[a] + rs_base;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const int q = tid + k * NT;
+            un[k] = 0.0;
+            us[k] = 0.0;
+            if (valid(q)) {
+                const int c = col_of(q);
+                un[k] = ld_ro(rn + c);
+                us[k] = ld_ro(rs + c);
+            }
+        }
+    };
+    auto accumulate = [&](int a, const double* u) {
+        const double ca = it.ca[a], cs = it.cs[a], cn = it.cn[a];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            accumulate_point<KIND>(pb, ca, cs, cn, u[k], two_d ? un[k] : 0.0, two_d ? us[k] : 0.0,
+                                   P[k], WS[k], WX[k]);
+    };
+    const int nn = it.nnodes;
+    if (prefetch) {
+        load(0, ua);
+        for (int a = 0; a < nn; a += 2) {
+            if (a + 1 < nn) load(a + 1, ub);
+            accumulate(a, ua);
+            if (a + 1 < nn) {
+                if (a + 2 < nn) load(a + 2, ua);
+                accumulate(a + 1, ub);
+            }
+        }
+    } else {
+        for (int a = 0; a < nn; ++a) {
+            load(a, ua);
+            if (two_d && it.cn[a] != 0.0) load_y(a);
+            accumulate(a, ua);
+        }
+    }
+
+    finish_item<KIND, NT, KMAX, FAST>(pb, sv, it, geo, P, WS, WX, sbuf, swarp, err);
+}
+
 template <int KIND, int NT, int KMAX>
 __device__ __forceinline__ void process_item(const DevProblem& pb, const DevSolve& sv,
                                              const StepItem& it, int tile, double* sbuf,
                                              Aff* swarp, unsigned long long* err)
 {
-    const int nx = pb.nx, ny = pb.ny;
-    const int tid = threadIdx.x;
-    const int row = tile / sv.nseg;
-    const int seg = tile - row * sv.nseg;
-    constexpr bool periodic = KIND != BURGERS_1D;
-    constexpr bool two_d = KIND == ADV_DIFF_2D || KIND == RD_2D;
-
-    // ---- geometry: extended range [s0, s0 + S), outputs at [out_lo, out_lo + tlen)
-    const int c0 = seg * sv.tile;
-    const int tlen = min(sv.tile, nx - c0);
-    int s0, S, out_lo;
-    bool exact_l, exact_r, cyclic;
-    if (sv.nseg == 1) {
-        s0 = 0; S = nx; out_lo = 0;
-        cyclic = periodic; exact_l = exact_r = !periodic;
-    } else if (periodic) {
-        s0 = c0 - sv.halo; S = tlen + 2 * sv.halo; out_lo = sv.halo;
-        cyclic = false; exact_l = exact_r = false;
-    } else {
-        s0 = max(c0 - sv.halo, 0);
-        const int send = min(c0 + tlen + sv.halo, nx);
-        S = send - s0; out_lo = c0 - s0;
-        cyclic = false; exact_l = (s0 == 0); exact_r = (send == nx);
-    }
-    (void)exact_l; (void)exact_r;
-
-    const size_t rbase = (size_t)row * nx;
-    const size_t rn_base = (size_t)(row == 0 ? ny - 1 : row - 1) * nx;
-    const size_t rs_base = (size_t)(row == ny - 1 ? 0 : row + 1) * nx;
-
-    // ---- phase 1: fused rhs over the extended range, registers
-    double acc[KMAX];
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) acc[k] = 0.0;
-    for (int a = 0; a < it.nnodes; ++a) {
-        const double* v = it.vec[a];
-        const double ca = it.ca[a], cs = it.cs[a], cn = it.cn[a];
-        const bool need_s = cs != 0.0, need_n = cn != 0.0;
-        const double* rp = v + rbase;
-        const double* rn = two_d ? v + rn_base : nullptr;
-        const double* rs = two_d ? v + rs_base : nullptr;
-#pragma unroll
-        for (int k = 0; k < KMAX; ++k) {
-            const int p = tid + k * NT;
-            if (p < S) {
-                double u, fs, fn;
-                eval_point<KIND>(pb, rp, rn, rs, s0 + p, need_s, need_n, u, fs, fn);
-                double t = acc[k];
-                if (ca != 0.0) t = t + ca * u;
-                if (need_s) t = t + cs * fs;
-                if (need_n) t = t + cn * fn;
-                acc[k] = t;
-            }
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-        const int p = tid + k * NT;
-        if (p < S) sbuf[pad(p)] = acc[k];
-    }
-    __syncthreads();
-
-    // ---- phase 2: forward recurrence y_i = g_i rhs_i + m_i y_{i-1}
-    const int E = (S + NT - 1) / NT;
-    const int lo = min(tid * E, S), hi = min(lo + E, S);
-    {
-        double y = 0.0, A = 1.0;
-        for (int e = lo; e < hi; ++e) {
-            double m, g;
-            coef(sv, s0 + e, m, g);
-            y = fma(m, y, g * sbuf[pad(e)]);
-            A *= m;
-            sbuf[pad(e)] = y;
-        }
-        Aff tot;
-        Aff pre = block_scan<NT>(Aff{A, y}, false, swarp, tot);
-        const double yinit = cyclic ? tot.B / (1.0 - tot.A) : 0.0;
-        const double cin = fma(pre.A, yinit, pre.B);
-        if (cin != 0.0) {
-            double P = 1.0;
-            for (int e = lo; e < hi; ++e) {
-                double m, g;
-                coef(sv, s0 + e, m, g);
-                P *= m;
-                sbuf[pad(e)] = fma(P, cin, sbuf[pad(e)]);
-            }
-        }
-    }
-    __syncthreads();
-    // ---- phase 3: backward recurrence x_i = y_i + m_i x_{i+1}
-    {
-        double x = 0.0, A = 1.0;
-        for (int e = hi - 1; e >= lo; --e) {
-            double m, g;
-            coef(sv, s0 + e, m, g);
-            x = fma(m, x, sbuf[pad(e)]);
-            A *= m;
-            sbuf[pad(e)] = x;
-        }
-        Aff tot;
-        Aff pre = block_scan<NT>(Aff{A, x}, true, swarp, tot);
-        const double xinit = cyclic ? tot.B / (1.0 - tot.A) : 0.0;
-        const double cin = fma(pre.A, xinit, pre.B);
-        if (cin != 0.0) {
-            double P = 1.0;
-            for (int e = hi - 1; e >= lo; --e) {
-                double m, g;
-                coef(sv, s0 + e, m, g);
-                P *= m;
-                sbuf[pad(e)] = fma(P, cin, sbuf[pad(e)]);
-            }
-        }
-    }
-    __syncthreads();
-
-    // ---- phase 4: coalesced store of the tile + fused finite check
-    bool bad = false;
-    double* orow = it.out + rbase;
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-        const int p = tid + k * NT;
-        if (p >= out_lo && p < out_lo + tlen) {
-            const double x = sbuf[pad(p)];
-            bad |= !isfinite(x);
-            orow[s0 + p] = x;
-        }
-    }
-    if (__syncthreads_or(bad) && tid == 0) atomicMin(err, err_code(it.target, it.level));
-    // sbuf is reused by the next item only after the caller's barrier
+    const Geo geo = make_geo<KIND, NT, KMAX>(pb, sv, tile);
+    if (geo.fast)
+        item_body<KIND, NT, KMAX, true>(pb, sv, it, geo, sbuf, swarp, err);
+    else
+        item_body<KIND, NT, KMAX, false>(pb, sv, it, geo, sbuf, swarp, err);
 }
 
 }  // namespace ridc

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -22,6 +23,7 @@
 
 #include "../../include/ridc_b200.h"
 #include "ridc_device.cuh"
+#include "ridc_tma.cuh"
 
 using namespace ridc;
 
@@ -32,7 +34,8 @@ thread_local std::string g_last_error;
 struct EngineParams {
     DevProblem pb;
     DevSolve sv;
-    long long V;
+    long long V;    // points per state
+    long long Vs;   // ring slot stride (even, >= V + 4: keeps every slot 16-byte aligned + guards)
     double dt;
     int levels;
     double* ring[kMaxLevels];
@@ -52,7 +55,7 @@ struct TickParams {
 
 __device__ __forceinline__ double* ring_slot(const EngineParams& ep, int lev, long long s)
 {
-    return ep.ring[lev] + ((ep.off[lev] + s) % ep.cap[lev]) * ep.V;
+    return ep.ring[lev] + ((ep.off[lev] + s) % ep.cap[lev]) * ep.Vs;
 }
 
 // Window assembly for (level j, target t): _window_span / _orient /
@@ -86,15 +89,62 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
     it.out = ring_slot(ep, j, t);
 }
 
-template <int KIND, int NT, int KMAX>
-__global__ void __launch_bounds__(NT) k_tick(EngineParams ep, TickParams tp)
+// The production tick kernel: persistent CTAs of NT compute threads; thread
+// 0 doubles as the TMA producer (ridc_tma.cuh).  Items of the tick are dealt
+// round-robin: item i -> level slot i % nact, tile i / nact.
+template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE>
+__global__ void __launch_bounds__(NT, 1) k_tick_tma(EngineParams ep, TickParams tp, int ipl)
 {
-    extern __shared__ double sbuf[];
-    __shared__ StepItem item;
-    __shared__ Aff swarp[NT / 32];
-    if (threadIdx.x == 0) build_item(ep, tp.level[blockIdx.y], tp.target[blockIdx.y], item);
+    using L = TmaSmem<NT, KMAX, ROWS, NSTAGE>;
+    extern __shared__ __align__(128) double sm[];
+    double* stage = sm;
+    double* sbuf = sm + L::OFF_SBUF;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+    uint64_t* empty = full + NSTAGE;
+    __shared__ StepItem items[kMaxLevels];   // one descriptor per active level (shared by all its tiles)
+    __shared__ Aff swarp[2 * (NT / 32) + 1];
+    const int total = tp.nact * ipl;
+    if (threadIdx.x < tp.nact) build_item(ep, tp.level[threadIdx.x], tp.target[threadIdx.x], items[threadIdx.x]);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NT / 32);
+        }
+        mbar_fence_init();
+    }
     __syncthreads();
-    process_item<KIND, NT, KMAX>(ep.pb, ep.sv, item, blockIdx.x, sbuf, swarp, ep.err);
+    // producer cursor (thread 0): next (item, node) to load and its load number
+    LoadCursor pc{(int)blockIdx.x, 0, 0};
+    auto issue_next = [&](int s) {
+        const int slot = pc.i % tp.nact, tile = pc.i / tp.nact;
+        const Geo g = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
+        issue_node<ROWS, L::SROW>(ep.pb, ep.sv, items[slot].vec[pc.a], g, stage + (size_t)s * L::STAGE,
+                                  &full[s]);
+        if (++pc.a == items[slot].nnodes) { pc.a = 0; pc.i += gridDim.x; }
+        ++pc.n;
+    };
+    if (threadIdx.x == 0)
+        for (int k = 0; k < NSTAGE && pc.i < total; ++k) issue_next(k);
+    // after load n was released from stage s: wait for every warp, then load n + NSTAGE into s
+    auto refill = [&](long long n, int s) {
+        if (pc.i >= total) return;
+        mbar_wait(&empty[s], (uint32_t)((n / NSTAGE) & 1));
+        issue_next(s);
+    };
+    long long n = 0;
+    int ino = 0;
+    for (int i = blockIdx.x; i < total; i += gridDim.x, ++ino) {
+        const int slot = i % tp.nact, tile = i / tp.nact;
+        Geo geo = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
+        geo.item_no = ino;
+        if (geo.fast)
+            consume_item<KIND, NT, KMAX, ROWS, NSTAGE, true>(ep.pb, ep.sv, items[slot], geo, stage, full,
+                                                            empty, n, refill, sbuf, swarp, ep.err);
+        else
+            consume_item<KIND, NT, KMAX, ROWS, NSTAGE, false>(ep.pb, ep.sv, items[slot], geo, stage,
+                                                             full, empty, n, refill, sbuf, swarp, ep.err);
+        csync<NT>();   // sbuf reuse by the next item
+    }
 }
 
 template <int KIND, int NT, int KMAX>
@@ -102,7 +152,7 @@ __global__ void __launch_bounds__(NT) k_item(DevProblem pb, DevSolve sv, StepIte
                                              unsigned long long* err)
 {
     extern __shared__ double sbuf[];
-    __shared__ Aff swarp[NT / 32];
+    __shared__ Aff swarp[2 * (NT / 32) + 1];
     process_item<KIND, NT, KMAX>(pb, sv, it, blockIdx.x, sbuf, swarp, err);
 }
 
@@ -136,40 +186,24 @@ __global__ void k_apply(DevProblem pb, int op, const double* __restrict__ in, do
 // ---------------------------------------------------------------- dispatch
 
 struct LaunchCfg {
-    int id;       // 0: 128x8, 1: 256x16, 2: 512x16
+    int id;       // 0: 128x8, 1: 256x8, 2: 512x8
     int nt, kmax;
     size_t smem;
 };
 
-constexpr int kSmax = 512 * 16;
+// Largest extended range one item handles (positions incl. the two stencil
+// neighbours): 512 threads x 8 points.
+constexpr int kCap = 512 * 8;
 
-LaunchCfg pick_cfg(int S)
+LaunchCfg pick_cfg(int Q)
 {
     LaunchCfg c;
-    if (S <= 128 * 8) { c.id = 0; c.nt = 128; c.kmax = 8; }
-    else if (S <= 256 * 16) { c.id = 1; c.nt = 256; c.kmax = 16; }
-    else { c.id = 2; c.nt = 512; c.kmax = 16; }
+    if (Q <= 128 * 8) { c.id = 0; c.nt = 128; c.kmax = 8; }
+    else if (Q <= 256 * 8) { c.id = 1; c.nt = 256; c.kmax = 8; }
+    else { c.id = 2; c.nt = 512; c.kmax = 8; }
     const int cap = c.nt * c.kmax;
     c.smem = (size_t)(cap + cap / 16 + 1) * sizeof(double);
     return c;
-}
-
-template <int KIND, int NT, int KMAX>
-cudaError_t launch_tick_t(dim3 grid, size_t smem, cudaStream_t st, const EngineParams& ep,
-                          const TickParams& tp)
-{
-    static bool attr[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    if (!attr[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k_tick<KIND, NT, KMAX>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr[dev] = true;
-    }
-    k_tick<KIND, NT, KMAX><<<grid, NT, smem, st>>>(ep, tp);
-    return cudaGetLastError();
 }
 
 template <int KIND, int NT, int KMAX>
@@ -192,18 +226,97 @@ cudaError_t launch_item_t(int items, size_t smem, cudaStream_t st, const DevProb
 
 #define RIDC_DISPATCH_CFG(FN, KIND, CFG, ...)                          \
     ((CFG).id == 0 ? FN<KIND, 128, 8>(__VA_ARGS__)                     \
-     : (CFG).id == 1 ? FN<KIND, 256, 16>(__VA_ARGS__)                  \
-                     : FN<KIND, 512, 16>(__VA_ARGS__))
+     : (CFG).id == 1 ? FN<KIND, 256, 8>(__VA_ARGS__)                   \
+                     : FN<KIND, 512, 8>(__VA_ARGS__))
 
-cudaError_t launch_tick(int kind, const LaunchCfg& c, dim3 grid, cudaStream_t st,
-                        const EngineParams& ep, const TickParams& tp)
+// ---- TMA tick kernel configurations (NT consumers x KMAX points, ROWS staged
+// rows per node, NSTAGE stages).  Many warps per SM hide the fp64 / shared
+// memory latencies of the scans; 1-D items are sized so one item per level
+// per CTA covers the line (see make_solve's balancing).
+struct TmaCfg {
+    int id;
+    int nt, kmax, rows, nstage, cap;
+    size_t smem;
+};
+
+template <int NT, int KMAX, int ROWS, int NSTAGE>
+TmaCfg tma_cfg_of(int id)
 {
+    TmaCfg c;
+    c.id = id;
+    c.nt = NT;
+    c.kmax = KMAX;
+    c.rows = ROWS;
+    c.nstage = NSTAGE;
+    c.cap = NT * KMAX;
+    c.smem = TmaSmem<NT, KMAX, ROWS, NSTAGE>::BYTES;
+    return c;
+}
+
+#define RIDC_TMA_CONFIGS(X)        \
+    X(0, 128, 8, 1, 4)             \
+    X(1, 256, 8, 1, 4)             \
+    X(2, 512, 8, 1, 3)             \
+    X(3, 1024, 8, 1, 2)            \
+    X(4, 256, 4, 3, 3)             \
+    X(5, 512, 4, 3, 3)
+
+TmaCfg pick_tma(int kind, int Q)
+{
+    const bool two_d = kind == ADV_DIFF_2D || kind == RD_2D;
+    if (two_d) return Q <= 1024 ? tma_cfg_of<256, 4, 3, 3>(4) : tma_cfg_of<512, 4, 3, 3>(5);
+    if (Q <= 1024) return tma_cfg_of<128, 8, 1, 4>(0);
+    if (Q <= 2048) return tma_cfg_of<256, 8, 1, 4>(1);
+    if (Q <= 4096) return tma_cfg_of<512, 8, 1, 3>(2);
+    return tma_cfg_of<1024, 8, 1, 2>(3);
+}
+
+int tma_cap(int kind) { return (kind == ADV_DIFF_2D || kind == RD_2D) ? 2048 : 8192; }
+
+template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE>
+cudaError_t launch_tma_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
+                         const TickParams& tp, int ipl)
+{
+    auto kfn = k_tick_tma<KIND, NT, KMAX, ROWS, NSTAGE>;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    kfn<<<grid, NT, smem, st>>>(ep, tp, ipl);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t launch_tma_k(const TmaCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
+                         const TickParams& tp, int ipl)
+{
+    constexpr bool two_d = KIND == ADV_DIFF_2D || KIND == RD_2D;
+#define RIDC_TMA_CASE(ID, NT, KMAX, ROWS, NSTAGE)                                      \
+    if (c.id == ID && two_d == (ROWS == 3)) {                                          \
+        if constexpr (two_d == (ROWS == 3))                                            \
+            return launch_tma_t<KIND, NT, KMAX, ROWS, NSTAGE>(grid, c.smem, st, ep, tp, ipl); \
+    }
+    RIDC_TMA_CONFIGS(RIDC_TMA_CASE)
+#undef RIDC_TMA_CASE
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tma(int kind, const TmaCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
+                       const TickParams& tp, int ipl)
+{
+    const bool two_d = kind == ADV_DIFF_2D || kind == RD_2D;
+    if (two_d != (c.rows == 3)) return cudaErrorInvalidValue;
     switch (kind) {
-    case ADV_DIFF_1D: return RIDC_DISPATCH_CFG(launch_tick_t, ADV_DIFF_1D, c, grid, c.smem, st, ep, tp);
-    case BURGERS_1D: return RIDC_DISPATCH_CFG(launch_tick_t, BURGERS_1D, c, grid, c.smem, st, ep, tp);
-    case RD_1D: return RIDC_DISPATCH_CFG(launch_tick_t, RD_1D, c, grid, c.smem, st, ep, tp);
-    case ADV_DIFF_2D: return RIDC_DISPATCH_CFG(launch_tick_t, ADV_DIFF_2D, c, grid, c.smem, st, ep, tp);
-    case RD_2D: return RIDC_DISPATCH_CFG(launch_tick_t, RD_2D, c, grid, c.smem, st, ep, tp);
+    case ADV_DIFF_1D: return launch_tma_k<ADV_DIFF_1D>(c, grid, st, ep, tp, ipl);
+    case BURGERS_1D: return launch_tma_k<BURGERS_1D>(c, grid, st, ep, tp, ipl);
+    case RD_1D: return launch_tma_k<RD_1D>(c, grid, st, ep, tp, ipl);
+    case ADV_DIFF_2D: return launch_tma_k<ADV_DIFF_2D>(c, grid, st, ep, tp, ipl);
+    case RD_2D: return launch_tma_k<RD_2D>(c, grid, st, ep, tp, ipl);
     }
     return cudaErrorInvalidValue;
 }
@@ -288,12 +401,116 @@ DevProblem make_problem(const ridc_problem* p)
 struct SolveSetup {
     DevSolve sv;
     std::vector<double> tab;   // [m_0..m_{n-1}, g_0..g_{n-1}]
+    std::vector<PlanRow> plans;  // TMA staging plans [nseg][row parity]
     double r;
-    LaunchCfg cfg;
+    LaunchCfg cfg;             // register-path (single-op) launch
+    TmaCfg tcfg;               // TMA tick-kernel launch (engine)
     std::string err;
 };
 
-int make_solve(const DevProblem& pb, double coeff, SolveSetup& ss)
+// Host mirror of make_geo (ridc_device.cuh) for one segment.
+void seg_range(const DevProblem& pb, const DevSolve& sv, int seg, int& cf, int& Q)
+{
+    const int nx = pb.nx;
+    const int c0 = seg * sv.tile;
+    const int tlen = std::min(sv.tile, nx - c0);
+    int s0, S;
+    if (sv.nseg == 1) { s0 = 0; S = nx; }
+    else if (pb.periodic) { s0 = c0 - sv.halo; S = tlen + 2 * sv.halo; }
+    else {
+        s0 = std::max(c0 - sv.halo, 0);
+        S = std::min(c0 + tlen + sv.halo, nx) - s0;
+    }
+    cf = s0 - 1;
+    Q = S + 2;
+}
+
+// Staging plan of one row-segment (see PlanRow in ridc_tma.cuh): aligned
+// bulk runs for the TMA engine, the rest as consumer fills.
+PlanRow make_plan_host(const DevProblem& pb, int cf, int Q, int par)
+{
+    const int nx = pb.nx;
+    struct Run { int q0, c0, n; };
+    std::vector<Run> runs;
+    std::vector<std::pair<int, int>> fills;   // [q0, q1)
+    int q = 0;
+    while (q < Q) {
+        const int c = cf + q;
+        if (!pb.periodic && (c < 0 || c >= nx)) {   // Dirichlet ghost
+            fills.push_back({q, q + 1});
+            ++q;
+            continue;
+        }
+        const int cc = pb.periodic ? ((c % nx) + nx) % nx : c;
+        const int n = std::min(Q - q, nx - cc);
+        runs.push_back({q, cc, n});
+        q += n;
+    }
+    PlanRow pl;
+    memset(&pl, 0, sizeof pl);
+    int best = 0;
+    for (int k = 1; k < (int)runs.size(); ++k)
+        if (runs[k].n > runs[best].n) best = k;
+    pl.sigma = runs.empty() ? 0 : ((par + runs[best].c0 - runs[best].q0) & 1);
+    const bool single = runs.size() == 1 && runs[0].q0 == 0 && runs[0].n == Q;
+    bool overflow = runs.size() > (size_t)kMaxBulk;
+    for (const Run& r : runs) {
+        const int dpar = (pl.sigma + r.q0) & 1, spar = (par + r.c0) & 1;
+        if (dpar != spar || overflow) { fills.push_back({r.q0, r.q0 + r.n}); continue; }
+        int q0, col, n;
+        if (single) {
+            const int h = (pl.sigma + r.q0) & 1;
+            q0 = r.q0 - h; col = r.c0 - h; n = r.n + h; n += n & 1;
+        } else {
+            const int h = (pl.sigma + r.q0) & 1;
+            q0 = r.q0 + h; col = r.c0 + h; n = r.n - h; n -= n & 1;
+            if (n <= 0) { fills.push_back({r.q0, r.q0 + r.n}); continue; }
+            if (q0 > r.q0) fills.push_back({r.q0, q0});
+            if (q0 + n < r.q0 + r.n) fills.push_back({q0 + n, r.q0 + r.n});
+        }
+        pl.bq0[pl.nb] = q0;
+        pl.bcol[pl.nb] = col;
+        pl.bn[pl.nb] = n;
+        pl.bytes += n * 8;
+        ++pl.nb;
+    }
+    std::sort(fills.begin(), fills.end());
+    std::vector<std::pair<int, int>> merged;
+    for (auto& f : fills) {
+        if (!merged.empty() && merged.back().second >= f.first)
+            merged.back().second = std::max(merged.back().second, f.second);
+        else
+            merged.push_back(f);
+    }
+    if (merged.size() > (size_t)kMaxFill) {   // degenerate: consumers stage everything
+        pl.nb = 0;
+        pl.bytes = 0;
+        merged.assign(1, {0, Q});
+    }
+    pl.nf = (int)merged.size();
+    for (int f = 0; f < pl.nf; ++f) {
+        pl.fq0[f] = merged[f].first;
+        pl.fn[f] = merged[f].second - merged[f].first;
+    }
+    return pl;
+}
+
+void build_plans(const DevProblem& pb, SolveSetup& ss)
+{
+    ss.plans.clear();
+    for (int seg = 0; seg < ss.sv.nseg; ++seg) {
+        int cf, Q;
+        seg_range(pb, ss.sv, seg, cf, Q);
+        for (int par = 0; par < 2; ++par) ss.plans.push_back(make_plan_host(pb, cf, Q, par));
+    }
+}
+
+// Factors + tiling.  cap: largest item range (positions incl. 2 stencil
+// neighbours) the chosen kernel holds; balance_items > 0 asks for the
+// segment count that best balances `balance_items` items-per-segment over
+// `nsm` persistent CTAs (engine), 0 for the minimal count (single ops).
+int make_solve(const DevProblem& pb, double coeff, int cap, int balance_items, int nsm,
+               SolveSetup& ss)
 {
     const double r = coeff * pb.cdx;
     ss.r = r;
@@ -323,31 +540,63 @@ int make_solve(const DevProblem& pb, double coeff, SolveSetup& ss)
         ss.tab.assign(m.begin(), m.end());
         ss.tab.insert(ss.tab.end(), g.begin(), g.end());
     }
-    if (pb.nx <= kSmax) {
+    double pw = 1.0;
+    for (int e = 0; e < kMaxChunk; ++e) {
+        pw *= sv.lam;
+        sv.pw[e] = pw;
+    }
+    // zf[e] = sum_{k=e}^{K-1} lam^(k-e) lam^(k+1)  (fast_solve, ridc_device.cuh)
+    auto fill_zf = [&](double* zf, int K) {
+        for (int e = 0; e < K; ++e) {
+            double acc = 0.0;
+            for (int k = K - 1; k >= e; --k) acc = acc * sv.lam + sv.pw[k];
+            zf[e] = acc;   // Horner in lam over k: sum lam^(k-e) * lam^(k+1)
+        }
+    };
+    fill_zf(sv.zf4, 4);
+    fill_zf(sv.zf8, 8);
+    fill_zf(sv.zf16, 16);
+    if (pb.nx + 2 <= cap) {
         sv.nseg = 1;
         sv.tile = pb.nx;
         sv.halo = 0;
-        ss.cfg = pick_cfg(pb.nx);
-    } else {
-        // truncated halo: lam^H <= 2^-60 relative to the recurrence magnitude
-        int H = 0;
-        if (sv.lam > 0.0) H = (int)std::ceil(60.0 * std::log(2.0) / -std::log(sv.lam)) + 1;
-        H = (H + 1) & ~1;
-        int T = ((kSmax - 2 * H) / 512) * 512;
-        if (T < 512) {
-            char buf[256];
-            snprintf(buf, sizeof buf,
-                     "stiffness r=%.4g needs a truncation halo of %d points; the segmented "
-                     "line solve supports at most %d (use fewer points or a smaller dt)",
-                     r, H, (kSmax - 512) / 2);
-            ss.err = buf;
-            return RIDC_E_CONFIG;
-        }
-        sv.halo = H;
-        sv.tile = T;
-        sv.nseg = (pb.nx + T - 1) / T;
-        ss.cfg = pick_cfg(kSmax);
+        ss.cfg = pick_cfg(pb.nx + 2);
+        ss.tcfg = pick_tma(pb.kind, pb.nx + 2);
+        build_plans(pb, ss);
+        return RIDC_OK;
     }
+    // truncated halo: lam^H <= 2^-60 relative to the recurrence magnitude
+    int H = 0;
+    if (sv.lam > 0.0) H = (int)std::ceil(60.0 * std::log(2.0) / -std::log(sv.lam)) + 1;
+    const int Tmax = cap - 2 - 2 * H;
+    if (Tmax < 256) {
+        char buf[256];
+        snprintf(buf, sizeof buf,
+                 "stiffness r=%.4g needs a truncation halo of %d points; the segmented "
+                 "line solve supports at most %d (use fewer points or a smaller dt)",
+                 r, H, (cap - 2 - 256) / 2);
+        ss.err = buf;
+        return RIDC_E_CONFIG;
+    }
+    const int n0 = (pb.nx + Tmax - 1) / Tmax;
+    int nbest = n0;
+    if (balance_items > 0 && nsm > 0) {
+        // minimise the per-CTA positions of the busiest CTA (+ a fixed per-item cost)
+        long long best = LLONG_MAX;
+        for (int n = n0; n <= 4 * n0; ++n) {
+            const int T = (pb.nx + n - 1) / n;
+            const long long items = (long long)balance_items * n;
+            const long long per = (items + nsm - 1) / nsm;
+            const long long cost = per * (T + 2LL * H + 2 + 512);
+            if (cost < best) { best = cost; nbest = n; }
+        }
+    }
+    sv.halo = H;
+    sv.tile = (pb.nx + nbest - 1) / nbest;
+    sv.nseg = (pb.nx + sv.tile - 1) / sv.tile;
+    ss.cfg = pick_cfg(cap);
+    ss.tcfg = pick_tma(pb.kind, cap);
+    build_plans(pb, ss);
     return RIDC_OK;
 }
 
@@ -368,6 +617,8 @@ struct ridc_ctx {
     long long V = 0;
     double* d_weights = nullptr;
     double* d_tab = nullptr;
+    PlanRow* d_plans = nullptr;
+    long long* d_dbg = nullptr;
     double* d_ring[kMaxLevels] = {};
     long long cap[kMaxLevels] = {};
     double* d_y0 = nullptr;
@@ -378,6 +629,9 @@ struct ridc_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
     long long ring_vectors = 0;
+    long long Vs = 0;          // ring slot stride (doubles)
+    int nsm = 148;             // persistent CTAs per tick launch
+    double* d_ring_base[kMaxLevels] = {};
     std::string err;
 };
 
@@ -419,7 +673,7 @@ int capture_graph(ridc_ctx* c)
         if (r > 0) {
             EngineParams prev = interval_params(c, r - 1);
             const int top = L - 1;
-            src = prev.ring[top] + ((prev.off[top] + c->per) % prev.cap[top]) * c->V;
+            src = prev.ring[top] + ((prev.off[top] + c->per) % prev.cap[top]) * c->Vs;
         }
         int sb = (int)std::min<long long>((c->V + 255) / 256, 148 * 8);
         k_seed<<<sb, 256, 0, c->stream>>>(src, ep);
@@ -437,7 +691,8 @@ int capture_graph(ridc_ctx* c)
                 }
             }
             if (tp.nact == 0) continue;
-            le = launch_tick(c->pb.kind, c->ss.cfg, dim3(items, tp.nact), c->stream, ep, tp);
+            le = launch_tma(c->pb.kind, c->ss.tcfg, std::min(c->nsm, tp.nact * items), c->stream, ep,
+                            tp, items);
             ++launches;
         }
     }
@@ -487,7 +742,7 @@ int march(ridc_ctx* c, double* wall_seconds)
 const double* final_slot(ridc_ctx* c, int level)
 {
     EngineParams ep = interval_params(c, c->restarts - 1);
-    return ep.ring[level] + ((ep.off[level] + c->per) % ep.cap[level]) * c->V;
+    return ep.ring[level] + ((ep.off[level] + c->per) % ep.cap[level]) * c->Vs;
 }
 
 }  // namespace
@@ -534,6 +789,7 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     c->ticks = per + delay(levels - 1);
     c->flags = flags;
     c->V = (long long)problem->nx * problem->ny;
+    c->Vs = ((c->V + 1) & ~1LL) + 4;
     c->dt = (t_end - t_start) / (double)steps;   // engine.py:468 global dt
     c->steady_off = st;
     c->startup_off = su;
@@ -543,13 +799,16 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         g_last_error = m;
         return code;
     };
-    if ((rc = make_solve(c->pb, c->dt, c->ss)) != RIDC_OK) {
-        c->err = c->ss.err;
-        return bail(rc);
-    }
     if (cudaSetDevice(device) != cudaSuccess) {
         c->err = "cudaSetDevice failed";
         return bail(RIDC_E_CUDA);
+    }
+    if (cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+        c->nsm = 148;
+    if ((rc = make_solve(c->pb, c->dt, tma_cap(c->pb.kind), levels * c->pb.ny, c->nsm, c->ss)) !=
+        RIDC_OK) {
+        c->err = c->ss.err;
+        return bail(rc);
     }
 #define CTX_TRY(expr)                                                                        \
     do {                                                                                     \
@@ -573,13 +832,25 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         c->ss.sv.tab_m = c->d_tab;
         c->ss.sv.tab_g = c->d_tab + c->ss.sv.ntab;
     }
+    CTX_TRY(cudaMalloc(&c->d_plans, c->ss.plans.size() * sizeof(PlanRow)));
+    CTX_TRY(cudaMemcpy(c->d_plans, c->ss.plans.data(), c->ss.plans.size() * sizeof(PlanRow),
+                       cudaMemcpyHostToDevice));
+    c->ss.sv.plans = c->d_plans;
+    if (getenv("RIDC_PHASE_TIMING") && atoi(getenv("RIDC_PHASE_TIMING")) > 0) {
+        CTX_TRY(cudaMalloc(&c->d_dbg, 128 * sizeof(long long)));
+        CTX_TRY(cudaMemset(c->d_dbg, 0, 128 * sizeof(long long)));
+        c->ss.sv.dbg = c->d_dbg;
+    }
     for (int j = 0; j < levels; ++j) {
         const bool top = j == levels - 1;
         long long cap = top ? 2 : 2LL * j + 3;
         if (top && (flags & RIDC_RECORD_TRAJECTORY)) cap = steps + 1;
         c->cap[j] = cap;
         c->ring_vectors += cap;
-        CTX_TRY(cudaMalloc(&c->d_ring[j], (size_t)cap * vb));
+        // slot stride Vs (even) keeps every slot 16-byte aligned for the bulk
+        // copies; 2 guard doubles before slot 0 and >= 4 after each state
+        CTX_TRY(cudaMalloc(&c->d_ring_base[j], ((size_t)cap * c->Vs + 4) * sizeof(double)));
+        c->d_ring[j] = c->d_ring_base[j] + 2;
     }
     CTX_TRY(cudaMalloc(&c->d_y0, vb));
     CTX_TRY(cudaMalloc(&c->d_err, sizeof(unsigned long long)));
@@ -588,6 +859,7 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     ep.pb = c->pb;
     ep.sv = c->ss.sv;
     ep.V = c->V;
+    ep.Vs = c->Vs;
     ep.dt = c->dt;
     ep.levels = levels;
     for (int j = 0; j < levels; ++j) {
@@ -624,9 +896,10 @@ int ridc_run(ridc_ctx* c, const double* y0_host, double* final_host, double* lev
             CUDA_TRY(&c->err, cudaMemcpyAsync(level_finals_host + (size_t)j * c->V, final_slot(c, j),
                                               vb, cudaMemcpyDeviceToHost, c->stream));
     if (traj_host)
-        CUDA_TRY(&c->err, cudaMemcpyAsync(traj_host, c->d_ring[c->levels - 1],
-                                          (size_t)(c->steps + 1) * vb, cudaMemcpyDeviceToHost,
-                                          c->stream));
+        CUDA_TRY(&c->err, cudaMemcpy2DAsync(traj_host, vb, c->d_ring[c->levels - 1],
+                                            (size_t)c->Vs * sizeof(double), vb,
+                                            (size_t)(c->steps + 1), cudaMemcpyDeviceToHost,
+                                            c->stream));
     CUDA_TRY(&c->err, cudaStreamSynchronize(c->stream));
     return RIDC_OK;
 }
@@ -656,7 +929,7 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->tile = c->ss.sv.tile;
     info->halo = c->ss.sv.halo;
     info->items_per_level = c->pb.ny * c->ss.sv.nseg;
-    info->threads = c->ss.cfg.nt;
+    info->threads = c->ss.tcfg.nt;
     info->ring_vectors = c->ring_vectors;
     info->lambda = c->ss.sv.lam;
     info->r = c->ss.r;
@@ -670,9 +943,11 @@ int ridc_destroy(ridc_ctx* c)
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (int j = 0; j < kMaxLevels; ++j)
-        if (c->d_ring[j]) cudaFree(c->d_ring[j]);
+        if (c->d_ring_base[j]) cudaFree(c->d_ring_base[j]);
     if (c->d_weights) cudaFree(c->d_weights);
     if (c->d_tab) cudaFree(c->d_tab);
+    if (c->d_plans) cudaFree(c->d_plans);
+    if (c->d_dbg) cudaFree(c->d_dbg);
     if (c->d_y0) cudaFree(c->d_y0);
     if (c->d_err) cudaFree(c->d_err);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -710,7 +985,7 @@ static int run_single_item(const ridc_problem* problem, double coeff, StepItem& 
     CUDA_TRY(nullptr, cudaSetDevice(device));
     DevProblem pb = make_problem(problem);
     SolveSetup ss;
-    if ((rc = make_solve(pb, coeff, ss)) != RIDC_OK) return fail(nullptr, rc, ss.err);
+    if ((rc = make_solve(pb, coeff, kCap, 0, 0, ss)) != RIDC_OK) return fail(nullptr, rc, ss.err);
     double* d_tab = nullptr;
     unsigned long long* d_err = nullptr;
     auto cleanup = [&]() {
@@ -800,6 +1075,16 @@ int ridc_op_step_rows(const ridc_problem* problem, double dt, const double* eta_
     it.out = out_dev;
     it.target = -1;
     return run_single_item(problem, dt, it, device);
+}
+
+// Phase trace of the last tick launch (RIDC_PHASE_TIMING=1 at create): CTA 0,
+// thread 0, up to 8 items x 16 clock64 stamps.  Diagnostic only.
+int ridc_debug_phase_trace(const ridc_ctx* c, long long* out, int n)
+{
+    if (!c || !out || n < 128) return fail(nullptr, RIDC_E_CONFIG, "need a 128-entry buffer");
+    if (!c->d_dbg) return fail(nullptr, RIDC_E_CONFIG, "create with RIDC_PHASE_TIMING=1");
+    CUDA_TRY(nullptr, cudaMemcpy(out, c->d_dbg, 128 * sizeof(long long), cudaMemcpyDeviceToHost));
+    return RIDC_OK;
 }
 
 }  // extern "C"

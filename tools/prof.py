@@ -1,0 +1,46 @@
+"""Small driver for ncu: one engine, a few device solves (no timing claims)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1209_4297_b200 import engine as E  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="c2")
+ap.add_argument("--order", type=int, default=1)
+ap.add_argument("--nt", type=int, default=200)
+ap.add_argument("--points", type=int, default=0)
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+sysm, nt, cfg = bench.workload(a.workload, a.points or None, None)
+full_nt = nt
+nt = a.nt or nt
+# keep the workload's dt (and hence the stiffness r and the solve geometry): shorten T instead
+from paper_1209_4297_b200 import problems as P  # noqa: E402
+ivp = sysm.ivp
+sysm = P.StructuredIVP(ivp.problem, ivp.t_start, ivp.t_start + (ivp.t_end - ivp.t_start) * nt / full_nt,
+                       ivp.initial_state)
+eng = E.Engine(sysm, E.RidcConfig(levels=a.order, steps=nt))
+y0 = torch.from_numpy(np.array(sysm.initial_state)).cuda()
+out = torch.empty_like(y0)
+for _ in range(a.reps):
+    t = eng.run_device(y0, out)
+print(f"{cfg['workload']} p={a.order} nt={nt}: {t*1e3:.3f} ms/solve, {t/ (nt + a.order*(a.order-1)//2)*1e6:.2f} us/tick", eng.info)
+if os.environ.get("RIDC_PHASE_TIMING"):
+    import ctypes
+    from paper_1209_4297_b200 import _lib
+    buf = (ctypes.c_longlong * 128)()
+    _lib.check(_lib.lib().ridc_debug_phase_trace(eng._h, buf, 128))
+    names = ["start", "node0", "accum", "stencil", "fwd", "scan1", "carry+bwd", "scan2", "store0", "end"]
+    for it in range(8):
+        st = [buf[it * 16 + k] for k in range(10)]
+        if st[0] == 0:
+            break
+        d = [st[k] - st[k - 1] for k in range(1, 10)]
+        print(f"item {it}: " + " ".join(f"{names[k]}:{d[k-1]}" for k in range(1, 10)),
+              f"| total {st[9] - st[0]} cyc" + (f", gap from prev {st[0] - buf[(it - 1) * 16 + 9]}" if it else ""))
