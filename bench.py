@@ -214,19 +214,30 @@ def run_ours(args):
             dist.barrier()
 
     if world > 1:
+        # one level per GPU (levels = ranks): the NVLink point-to-point pipeline
         from paper_1209_4297_b200 import distributed as PD
-        runner = PD.PipelineRank(sysm, E.RidcConfig(levels=order, steps=nt), rank, world, local)
-        y0 = torch.from_numpy(np.ascontiguousarray(sysm.ivp.initial_state)).cuda()
+        if order != world:
+            raise SystemExit("--order must equal the GPU count (one level per GPU)")
+
+        def exchange(blob):
+            out = [None] * world
+            dist.all_gather_object(out, blob)
+            return out
+        runner = PD.PipelineRank(sysm, E.RidcConfig(levels=order, steps=nt), rank, world, local,
+                                 exchange=exchange)
+        y0 = torch.from_numpy(np.array(sysm.ivp.initial_state)).cuda()
         out = torch.empty_like(y0)
 
         def solve_device():
             return runner.run_device(y0, out)
         launches_per_step = runner.kernel_launches
         tick_launches = runner.tick_launches
-        lev_bytes = bytes_per_point(rank) + (8 if rank > 0 else 0)
+        # this rank's level-step bytes per point; the producer side also writes the
+        # consumer's inbox copy (8 B/pt over NVLink, counted on the consumer)
+        lev_bytes = bytes_per_point(rank) + (8 if rank < world - 1 else 0)
     else:
         eng = E.Engine(sysm, E.RidcConfig(levels=order, steps=nt))
-        y0 = torch.from_numpy(np.ascontiguousarray(sysm.ivp.initial_state)).cuda()
+        y0 = torch.from_numpy(np.array(sysm.ivp.initial_state)).cuda()
         out = torch.empty_like(y0)
 
         def solve_device():

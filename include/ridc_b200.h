@@ -143,29 +143,48 @@ int ridc_op_step_rows(const ridc_problem *problem, double dt, const double *eta_
  * stamps); only when the context was created with RIDC_PHASE_TIMING=1. */
 int ridc_debug_phase_trace(const ridc_ctx *ctx, long long *out, int32_t n);
 
-/* ---- lagged level pipeline, one level per GPU (one process per GPU) ---- */
+/* ---- lagged level pipeline, one level per GPU (one process per GPU) ----
+ *
+ * Replaces _pipelined_interval / LevelBuffer (engine.py:284-459) with levels
+ * on different devices.  Rank j owns level j.  Its tick kernel writes each
+ * new state tile both to its own ring and -- peer stores over NVLink -- to
+ * level j+1's inbox ring; after the kernel, a device-side stream write
+ * publishes the watermark into the consumer's memory (LevelBuffer.watermark,
+ * :299).  Level j waits on its own inbox watermark and on the release counter
+ * its consumer writes back (LevelBuffer.released, :300) with device-side
+ * stream waits (cuStreamWaitValue64), so no host round trip sits between
+ * ticks.  Slots are indexed by the global step number across restarts. */
 
 typedef struct ridc_pipe ridc_pipe;
 
-/* Size of the opaque blob a rank exports for its neighbours (IPC handles). */
+/* Size of the opaque blob a rank exports for its neighbours (IPC handle of
+ * its mailbox = inbox ring + watermark + release counter). */
 int64_t ridc_pipe_handle_bytes(void);
 
-/* Create the rank owning `level` (0..levels-1) on `device`; the rank's inbox
- * ring (window of level-1) and flags are allocated here. */
+/* Create the rank owning `level` (0..levels-1) on `device`.  inbox_capacity:
+ * inbox ring slots (0: default 2*level+5; >= steps/restarts+1 makes every
+ * rank runnable to completion without its consumer, e.g. ranks driven one
+ * after another on one device).  watchdog_seconds bounds every wait
+ * (PipelineProtocolError on expiry, engine.py:432-439). */
 int ridc_pipe_create(const ridc_problem *problem, double t_start, double t_end,
                      int32_t levels, int64_t steps, int32_t restarts,
                      const double *weights, int64_t nweights, int32_t level,
-                     int32_t device, double watchdog_seconds, ridc_pipe **out);
+                     int32_t device, int32_t inbox_capacity, double watchdog_seconds,
+                     ridc_pipe **out);
 /* Export this rank's handles into blob (ridc_pipe_handle_bytes() bytes). */
 int ridc_pipe_export(ridc_pipe *p, void *blob);
-/* Connect to the previous level (prev_blob, NULL for level 0) and the next
- * level (next_blob, NULL for the top level). */
+/* Connect to the previous level (prev_blob; NULL for level 0) and the next
+ * level (next_blob; NULL for the top level).  Blobs from the same process
+ * are used as direct device pointers, others through cudaIpcOpenMemHandle. */
 int ridc_pipe_connect(ridc_pipe *p, const void *prev_blob, const void *next_blob);
-/* Run all intervals.  y0_dev: initial state on this device.  final_dev: this
- * level's final state (the top level's is the solution); restarts re-seed
- * every level from the top level's interval final, which the top rank
- * broadcasts over the same peer links.  wall_seconds: device time. */
-int ridc_pipe_run(ridc_pipe *p, const double *y0_dev, double *final_dev, double *wall_seconds);
+/* Run restart interval `interval` (0..restarts-1) of this rank's level from
+ * state0_dev (the interval's initial state, on this device); final_dev
+ * receives this level's state at the interval end (the top rank's is the
+ * solution and the next interval's state0).  Blocks until the level is done
+ * (bounded by the watchdog).  wall_seconds: device time of this rank. */
+int ridc_pipe_run_interval(ridc_pipe *p, int32_t interval, const double *state0_dev,
+                           double *final_dev, double *wall_seconds);
+int ridc_pipe_info(const ridc_pipe *p, ridc_info *info);
 int ridc_pipe_destroy(ridc_pipe *p);
 const char *ridc_pipe_last_error(const ridc_pipe *p);
 

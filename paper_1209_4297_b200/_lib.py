@@ -51,10 +51,11 @@ SIGNATURES = {
     "ridc_pipe_handle_bytes": (ctypes.c_int64, []),
     "ridc_pipe_create": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int32, ctypes.c_int64,
                                         ctypes.c_int32, _vp, ctypes.c_int64, ctypes.c_int32,
-                                        ctypes.c_int32, _d, _P(_vp)]),
+                                        ctypes.c_int32, ctypes.c_int32, _d, _P(_vp)]),
     "ridc_pipe_export": (ctypes.c_int, [_vp, _vp]),
     "ridc_pipe_connect": (ctypes.c_int, [_vp, _vp, _vp]),
-    "ridc_pipe_run": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
+    "ridc_pipe_run_interval": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, _dp]),
+    "ridc_pipe_info": (ctypes.c_int, [_vp, _P(RidcInfo)]),
     "ridc_pipe_destroy": (ctypes.c_int, [_vp]),
     "ridc_pipe_last_error": (ctypes.c_char_p, [_vp]),
 }

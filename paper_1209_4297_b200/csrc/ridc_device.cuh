@@ -70,6 +70,7 @@ struct StepItem {
     const double* vec[kMaxNodes];
     double ca[kMaxNodes], cs[kMaxNodes], cn[kMaxNodes];
     double* out;
+    double* out2;   // optional mirror (the consumer GPU's inbox slot, written over NVLink)
 };
 
 struct Aff { double A, B; };   // y -> A*y + B
@@ -537,6 +538,7 @@ __device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve
     // ---- phase 5: coalesced store of the tile + fused finite check
     bool bad = false;
     double* orow = it.out + rbase;
+    double* orow2 = it.out2 ? it.out2 + rbase : nullptr;
     const int olo = FAST ? geo.out_lo + 1 : geo.out_lo;   // in scan coordinates
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {
@@ -545,6 +547,7 @@ __device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve
             const double xo = sbuf[pad(e)];
             bad |= !isfinite(xo);
             orow[e0 + e] = xo;
+            if (orow2) orow2[e0 + e] = xo;   // peer store into the next level's inbox
         }
     }
     if (bad) atomicMin(err, err_code(it.target, it.level));

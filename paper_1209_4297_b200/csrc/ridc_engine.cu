@@ -10,9 +10,14 @@
 // Level rings: level j < top keeps its last 2j+3 states in HBM (the greedy
 // schedule's live window for the reader j+1, which lags j+1 ticks); the top
 // level keeps 2 (or the whole trajectory when it is recorded).
+#include <cuda.h>   // driver-API types only; entry points come from cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
+#include <map>
+#include <thread>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -45,6 +50,8 @@ struct EngineParams {
     int steady_off[kMaxLevels];
     int startup_off[kMaxLevels];
     unsigned long long* err;
+    double* mirror;            // pipeline: consumer's inbox ring (peer memory), or null
+    long long mirror_cap, mirror_off;
 };
 
 struct TickParams {
@@ -87,6 +94,7 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
     }
     it.nnodes = nn;
     it.out = ring_slot(ep, j, t);
+    it.out2 = ep.mirror ? ep.mirror + ((ep.mirror_off + t) % ep.mirror_cap) * ep.Vs : nullptr;
 }
 
 // The production tick kernel: persistent CTAs of NT compute threads; thread
@@ -805,7 +813,9 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     }
     if (cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
         c->nsm = 148;
-    if ((rc = make_solve(c->pb, c->dt, tma_cap(c->pb.kind), levels * c->pb.ny, c->nsm, c->ss)) !=
+    // tiling depends only on the problem and dt (not on levels or devices): the
+    // one-level-per-GPU pipeline then reproduces these states bitwise
+    if ((rc = make_solve(c->pb, c->dt, tma_cap(c->pb.kind), c->pb.ny, c->nsm, c->ss)) !=
         RIDC_OK) {
         c->err = c->ss.err;
         return bail(rc);
@@ -1085,6 +1095,469 @@ int ridc_debug_phase_trace(const ridc_ctx* c, long long* out, int n)
     if (!c->d_dbg) return fail(nullptr, RIDC_E_CONFIG, "create with RIDC_PHASE_TIMING=1");
     CUDA_TRY(nullptr, cudaMemcpy(out, c->d_dbg, 128 * sizeof(long long), cudaMemcpyDeviceToHost));
     return RIDC_OK;
+}
+
+}  // extern "C"
+
+// ================================================================ level pipeline
+
+namespace {
+
+typedef CUresult (*PfnWaitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PfnWriteValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+struct DriverOps {
+    PfnWaitValue64 wait = nullptr;
+    PfnWriteValue64 write = nullptr;
+};
+
+// Stream memory operations, resolved at run time (no link-time libcuda
+// dependency, so the library also loads on hosts without a driver).
+const DriverOps& driver_ops()
+{
+    static DriverOps ops = [] {
+        DriverOps o;
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            o.wait = reinterpret_cast<PfnWaitValue64>(f);
+        f = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            o.write = reinterpret_cast<PfnWriteValue64>(f);
+        return o;
+    }();
+    return ops;
+}
+
+constexpr uint32_t kBlobMagic = 0x52494443u;   // "RIDC"
+constexpr size_t kFlagBytes = 256;             // wm (+0), rel (+8), then the inbox ring
+
+struct PipeBlob {
+    uint32_t magic;
+    int32_t pid, device, level;
+    cudaIpcMemHandle_t handle;
+    uint64_t direct;       // mailbox base (valid inside the exporting process)
+    int64_t inbox_cap;
+    int64_t vs;
+};
+
+}  // namespace
+
+struct ridc_pipe {
+    int device = 0, level = 0, levels = 0, restarts = 0;
+    long long steps = 0, per = 0, V = 0, Vs = 0;
+    double t_start = 0, t_end = 0, dt = 0, watchdog = 30.0;
+    DevProblem pb;
+    SolveSetup ss;
+    int nsm = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    char* mailbox = nullptr;
+    long long inbox_cap = 0;
+    unsigned long long* wm = nullptr;    // my inbox watermark (written by level-1)
+    unsigned long long* rel = nullptr;   // released-below counter (written by level+1)
+    double* inbox = nullptr;             // slot 0 of my inbox ring
+    double* own_base = nullptr;
+    double* own = nullptr;               // my 2-slot state ring
+    double* next_inbox = nullptr;        // peer: level+1's inbox ring
+    long long next_cap = 0;
+    unsigned long long* next_wm = nullptr;
+    unsigned long long* prev_rel = nullptr;
+    void* opened[2] = {nullptr, nullptr};
+    double* d_weights = nullptr;
+    double* d_tab = nullptr;
+    PlanRow* d_plans = nullptr;
+    unsigned long long* d_err = nullptr;
+    std::vector<int> st, su;
+    std::map<int, cudaGraphExec_t> graphs;
+    long long launches = 0;
+    std::string err;
+};
+
+namespace {
+
+int pipe_fail(ridc_pipe* p, int code, const std::string& m)
+{
+    g_last_error = m;
+    if (p) p->err = m;
+    return code;
+}
+
+#define PIPE_TRY(p, expr)                                                                    \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return pipe_fail(p, RIDC_E_CUDA, std::string(#expr " failed: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+EngineParams pipe_params(ridc_pipe* p, long long g0)
+{
+    EngineParams ep;
+    memset(&ep, 0, sizeof ep);
+    ep.pb = p->pb;
+    ep.sv = p->ss.sv;
+    ep.V = p->V;
+    ep.Vs = p->Vs;
+    ep.dt = p->dt;
+    ep.levels = p->levels;
+    const int j = p->level;
+    ep.ring[j] = p->own;
+    ep.cap[j] = 2;
+    ep.off[j] = g0;
+    if (j > 0) {
+        ep.ring[j - 1] = p->inbox;
+        ep.cap[j - 1] = p->inbox_cap;
+        ep.off[j - 1] = g0;
+    }
+    ep.weights = p->d_weights;
+    for (int k = 0; k < kMaxLevels; ++k) {
+        ep.steady_off[k] = p->st[k];
+        ep.startup_off[k] = p->su[k];
+    }
+    ep.err = p->d_err;
+    if (j < p->levels - 1 && p->next_inbox) {
+        ep.mirror = p->next_inbox;
+        ep.mirror_cap = p->next_cap;
+        ep.mirror_off = g0;
+    }
+    return ep;
+}
+
+// Enqueue one interval: per step t, wait for the window (inbox watermark)
+// and for ring space at the consumer (its release counter), run the level's
+// tick kernel (which also stores into the consumer's inbox), publish the
+// watermark to the consumer and the release to the producer.
+int pipe_enqueue(ridc_pipe* p, int interval, long long* launches)
+{
+    const DriverOps& ops = driver_ops();
+    const int j = p->level, top = p->levels - 1;
+    const long long g0 = (long long)interval * p->per;
+    const EngineParams ep = pipe_params(p, g0);
+    const int items = p->pb.ny * p->ss.sv.nseg;
+    CUstream cs = reinterpret_cast<CUstream>(p->stream);
+    long long n = 0;
+    for (long long t = 1; t <= p->per; ++t) {
+        if (j > 0) {
+            const long long need = g0 + (t < j ? j : t);
+            if (ops.wait(cs, (CUdeviceptr)p->wm, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return pipe_fail(p, RIDC_E_CUDA, "cuStreamWaitValue64 (watermark) failed");
+        }
+        if (j < top) {
+            const long long need_rel = g0 + t - p->next_cap + 1;
+            if (need_rel > 0 &&
+                ops.wait(cs, (CUdeviceptr)p->rel, (cuuint64_t)need_rel, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return pipe_fail(p, RIDC_E_CUDA, "cuStreamWaitValue64 (release) failed");
+        }
+        TickParams tp;
+        memset(&tp, 0, sizeof tp);
+        tp.nact = 1;
+        tp.level[0] = j;
+        tp.target[0] = t;
+        cudaError_t le = launch_tma(p->pb.kind, p->ss.tcfg, std::min(p->nsm, items), p->stream, ep, tp, items);
+        if (le != cudaSuccess) return pipe_fail(p, RIDC_E_CUDA, std::string("tick launch: ") + cudaGetErrorString(le));
+        ++n;
+        if (j < top &&
+            ops.write(cs, (CUdeviceptr)p->next_wm, (cuuint64_t)(g0 + t), CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return pipe_fail(p, RIDC_E_CUDA, "cuStreamWriteValue64 (watermark) failed");
+        if (j > 0) {
+            const long long below = g0 + std::max(0LL, t + 1 - j);
+            if (ops.write(cs, (CUdeviceptr)p->prev_rel, (cuuint64_t)below, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+                return pipe_fail(p, RIDC_E_CUDA, "cuStreamWriteValue64 (release) failed");
+        }
+    }
+    *launches = n;
+    return RIDC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t ridc_pipe_handle_bytes(void) { return (int64_t)sizeof(PipeBlob); }
+
+int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, int32_t levels,
+                     int64_t steps, int32_t restarts, const double* weights, int64_t nweights,
+                     int32_t level, int32_t device, int32_t inbox_capacity, double watchdog_seconds,
+                     ridc_pipe** out)
+{
+    if (!out) return pipe_fail(nullptr, RIDC_E_CONFIG, "out is NULL");
+    *out = nullptr;
+    int rc = validate_problem(problem);
+    if (rc) return rc;
+    if (levels < 1 || levels > kMaxLevels) return pipe_fail(nullptr, RIDC_E_CONFIG, "levels must be in 1..12");
+    if (level < 0 || level >= levels) return pipe_fail(nullptr, RIDC_E_CONFIG, "level out of range");
+    if (steps < 1 || restarts < 1 || steps % restarts)
+        return pipe_fail(nullptr, RIDC_E_CONFIG, "steps must be a positive multiple of restarts");
+    const long long per = steps / restarts;
+    if (per < delay(levels) + 1) return pipe_fail(nullptr, RIDC_E_CONFIG, "restart interval shorter than the pipeline fill");
+    if (!(t_start < t_end)) return pipe_fail(nullptr, RIDC_E_CONFIG, "need t_start < t_end");
+    const DriverOps& ops = driver_ops();
+    if (!ops.wait || !ops.write) return pipe_fail(nullptr, RIDC_E_CUDA, "driver stream memory operations unavailable");
+    std::vector<int> st, su;
+    long long wtotal = 0;
+    weight_offsets(levels, st, su, wtotal);
+    if (nweights < wtotal || (wtotal > 0 && !weights))
+        return pipe_fail(nullptr, RIDC_E_DIMENSION, "weight table shorter than levels require");
+    ridc_pipe* p = new ridc_pipe();
+    p->device = device;
+    p->level = level;
+    p->levels = levels;
+    p->restarts = restarts;
+    p->steps = steps;
+    p->per = per;
+    p->t_start = t_start;
+    p->t_end = t_end;
+    p->dt = (t_end - t_start) / (double)steps;
+    p->watchdog = watchdog_seconds > 0 ? watchdog_seconds : 30.0;
+    p->pb = make_problem(problem);
+    p->V = (long long)problem->nx * problem->ny;
+    p->Vs = ((p->V + 1) & ~1LL) + 4;
+    p->st = st;
+    p->su = su;
+    p->inbox_cap = inbox_capacity > 0 ? inbox_capacity : 2LL * level + 5;
+    auto bail = [&](int code) {
+        std::string m = p->err.empty() ? g_last_error : p->err;
+        ridc_pipe_destroy(p);
+        g_last_error = m;
+        return code;
+    };
+#define P_TRY(expr)                                                                          \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            p->err = std::string(#expr " failed: ") + cudaGetErrorString(_e);               \
+            return bail(RIDC_E_CUDA);                                                        \
+        }                                                                                    \
+    } while (0)
+    P_TRY(cudaSetDevice(device));
+    if (cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) p->nsm = 148;
+    // tiling depends only on the problem and dt (not on levels or devices), so a
+    // level computes bitwise the same states here as in the single-device engine
+    if ((rc = make_solve(p->pb, p->dt, tma_cap(p->pb.kind), p->pb.ny, p->nsm, p->ss)) != RIDC_OK) {
+        p->err = p->ss.err;
+        return bail(rc);
+    }
+    P_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    P_TRY(cudaEventCreate(&p->ev0));
+    P_TRY(cudaEventCreate(&p->ev1));
+    P_TRY(cudaMalloc(&p->d_weights, std::max<long long>(wtotal, 1) * sizeof(double)));
+    if (wtotal > 0) P_TRY(cudaMemcpy(p->d_weights, weights, wtotal * sizeof(double), cudaMemcpyHostToDevice));
+    if (!p->ss.tab.empty()) {
+        P_TRY(cudaMalloc(&p->d_tab, p->ss.tab.size() * sizeof(double)));
+        P_TRY(cudaMemcpy(p->d_tab, p->ss.tab.data(), p->ss.tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+        p->ss.sv.tab_m = p->d_tab;
+        p->ss.sv.tab_g = p->d_tab + p->ss.sv.ntab;
+    }
+    P_TRY(cudaMalloc(&p->d_plans, p->ss.plans.size() * sizeof(PlanRow)));
+    P_TRY(cudaMemcpy(p->d_plans, p->ss.plans.data(), p->ss.plans.size() * sizeof(PlanRow), cudaMemcpyHostToDevice));
+    p->ss.sv.plans = p->d_plans;
+    P_TRY(cudaMalloc(&p->d_err, sizeof(unsigned long long)));
+    // mailbox: flags, then the inbox ring (2 guard doubles + cap slots of Vs)
+    const size_t ring_bytes = ((size_t)p->inbox_cap * p->Vs + 4) * sizeof(double);
+    P_TRY(cudaMalloc(&p->mailbox, kFlagBytes + ring_bytes));
+    P_TRY(cudaMemset(p->mailbox, 0, kFlagBytes));
+    p->wm = reinterpret_cast<unsigned long long*>(p->mailbox);
+    p->rel = reinterpret_cast<unsigned long long*>(p->mailbox + 8);
+    p->inbox = reinterpret_cast<double*>(p->mailbox + kFlagBytes) + 2;
+    P_TRY(cudaMalloc(&p->own_base, ((size_t)2 * p->Vs + 4) * sizeof(double)));
+    p->own = p->own_base + 2;
+#undef P_TRY
+    *out = p;
+    return RIDC_OK;
+}
+
+int ridc_pipe_export(ridc_pipe* p, void* blob)
+{
+    if (!p || !blob) return pipe_fail(p, RIDC_E_CONFIG, "NULL argument");
+    PipeBlob b;
+    memset(&b, 0, sizeof b);
+    b.magic = kBlobMagic;
+    b.pid = (int32_t)getpid();
+    b.device = p->device;
+    b.level = p->level;
+    b.direct = (uint64_t)(uintptr_t)p->mailbox;
+    b.inbox_cap = p->inbox_cap;
+    b.vs = p->Vs;
+    PIPE_TRY(p, cudaSetDevice(p->device));
+    PIPE_TRY(p, cudaIpcGetMemHandle(&b.handle, p->mailbox));
+    memcpy(blob, &b, sizeof b);
+    return RIDC_OK;
+}
+
+static int open_blob(ridc_pipe* p, const void* blob, int want_level, char** base, int slot, long long* cap)
+{
+    PipeBlob b;
+    memcpy(&b, blob, sizeof b);
+    if (b.magic != kBlobMagic || b.level != want_level || b.vs != p->Vs)
+        return pipe_fail(p, RIDC_E_PROTOCOL, "pipeline handle from an incompatible rank");
+    if (b.pid == (int32_t)getpid()) {
+        *base = reinterpret_cast<char*>((uintptr_t)b.direct);
+        if (b.device != p->device) {
+            cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return pipe_fail(p, RIDC_E_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+            cudaGetLastError();
+        }
+    } else {
+        void* ptr = nullptr;
+        PIPE_TRY(p, cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
+        p->opened[slot] = ptr;
+        *base = reinterpret_cast<char*>(ptr);
+    }
+    *cap = b.inbox_cap;
+    return RIDC_OK;
+}
+
+int ridc_pipe_connect(ridc_pipe* p, const void* prev_blob, const void* next_blob)
+{
+    if (!p) return pipe_fail(nullptr, RIDC_E_CONFIG, "NULL pipe");
+    PIPE_TRY(p, cudaSetDevice(p->device));
+    const int j = p->level, top = p->levels - 1;
+    if ((j > 0) != (prev_blob != nullptr) || (j < top) != (next_blob != nullptr))
+        return pipe_fail(p, RIDC_E_CONFIG, "level needs exactly its existing neighbours");
+    int rc;
+    long long cap = 0;
+    char* base = nullptr;
+    if (prev_blob) {
+        if ((rc = open_blob(p, prev_blob, j - 1, &base, 0, &cap)) != RIDC_OK) return rc;
+        p->prev_rel = reinterpret_cast<unsigned long long*>(base + 8);
+    }
+    if (next_blob) {
+        if ((rc = open_blob(p, next_blob, j + 1, &base, 1, &cap)) != RIDC_OK) return rc;
+        p->next_wm = reinterpret_cast<unsigned long long*>(base);
+        p->next_inbox = reinterpret_cast<double*>(base + kFlagBytes) + 2;
+        p->next_cap = cap;
+    }
+    return RIDC_OK;
+}
+
+int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_dev, double* final_dev,
+                           double* wall_seconds)
+{
+    if (!p || !state0_dev || !final_dev) return pipe_fail(p, RIDC_E_CONFIG, "NULL argument");
+    if (interval < 0 || interval >= p->restarts) return pipe_fail(p, RIDC_E_CONFIG, "interval out of range");
+    const int j = p->level, top = p->levels - 1;
+    if ((j > 0 && !p->prev_rel) || (j < top && !p->next_inbox))
+        return pipe_fail(p, RIDC_E_CONFIG, "pipeline rank not connected");
+    PIPE_TRY(p, cudaSetDevice(p->device));
+    const long long g0 = (long long)interval * p->per;
+    const size_t vb = (size_t)p->V * sizeof(double);
+    // seed: step g0 of my own ring and of my inbox is the interval's state0
+    EngineParams ep = pipe_params(p, g0);
+    PIPE_TRY(p, cudaMemcpyAsync(ep.ring[j] + ((ep.off[j]) % 2) * p->Vs, state0_dev, vb,
+                                cudaMemcpyDeviceToDevice, p->stream));
+    if (j > 0)
+        PIPE_TRY(p, cudaMemcpyAsync(p->inbox + (g0 % p->inbox_cap) * p->Vs, state0_dev, vb,
+                                    cudaMemcpyDeviceToDevice, p->stream));
+    PIPE_TRY(p, cudaMemsetAsync(p->d_err, 0xff, sizeof(unsigned long long), p->stream));
+    PIPE_TRY(p, cudaEventRecord(p->ev0, p->stream));
+    // the interval's ops: captured into a graph on first use (memops included)
+    auto it = p->graphs.find(interval);
+    long long launches = 0;
+    if (it == p->graphs.end()) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        bool captured = false;
+        if (cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            int rc = pipe_enqueue(p, interval, &launches);
+            cudaError_t ce = cudaStreamEndCapture(p->stream, &graph);
+            if (rc == RIDC_OK && ce == cudaSuccess && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess)
+                captured = true;
+            if (graph) cudaGraphDestroy(graph);
+        }
+        cudaGetLastError();
+        if (captured) {
+            p->graphs[interval] = exec;
+            PIPE_TRY(p, cudaGraphLaunch(exec, p->stream));
+        } else {
+            int rc = pipe_enqueue(p, interval, &launches);   // direct enqueue fallback
+            if (rc) return rc;
+        }
+    } else {
+        PIPE_TRY(p, cudaGraphLaunch(it->second, p->stream));
+        launches = p->per;
+    }
+    p->launches = launches;
+    PIPE_TRY(p, cudaMemcpyAsync(final_dev, ep.ring[j] + ((ep.off[j] + p->per) % 2) * p->Vs, vb,
+                                cudaMemcpyDeviceToDevice, p->stream));
+    PIPE_TRY(p, cudaEventRecord(p->ev1, p->stream));
+    // watchdog (engine.py:432-439): neighbours that never publish turn into an error
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t q = cudaEventQuery(p->ev1);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) return pipe_fail(p, RIDC_E_CUDA, cudaGetErrorString(q));
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > p->watchdog) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "pipeline made no progress within %gs; waiting levels: %d@interval%d",
+                     p->watchdog, j, interval);
+            return pipe_fail(p, RIDC_E_PROTOCOL, buf);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+    if (wall_seconds) {
+        float ms = 0.f;
+        PIPE_TRY(p, cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+        *wall_seconds = ms * 1e-3;
+    }
+    unsigned long long w = 0;
+    PIPE_TRY(p, cudaMemcpy(&w, p->d_err, sizeof w, cudaMemcpyDeviceToHost));
+    if (w != ULLONG_MAX) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "level %d produced non-finite entries at step %lld", (int)(w & 0xff),
+                 (long long)(w >> 8));
+        return pipe_fail(p, RIDC_E_NONFINITE, buf);
+    }
+    return RIDC_OK;
+}
+
+int ridc_pipe_info(const ridc_pipe* p, ridc_info* info)
+{
+    if (!p || !info) return pipe_fail(nullptr, RIDC_E_CONFIG, "NULL argument");
+    memset(info, 0, sizeof *info);
+    info->levels = p->levels;
+    info->restarts = p->restarts;
+    info->steps = p->steps;
+    info->ticks_per_interval = p->per;
+    info->kernel_launches = p->per;
+    info->tile = p->ss.sv.tile;
+    info->halo = p->ss.sv.halo;
+    info->items_per_level = p->pb.ny * p->ss.sv.nseg;
+    info->threads = p->ss.tcfg.nt;
+    info->ring_vectors = 2 + (p->level > 0 ? p->inbox_cap : 0);
+    info->lambda = p->ss.sv.lam;
+    info->r = p->ss.r;
+    return RIDC_OK;
+}
+
+int ridc_pipe_destroy(ridc_pipe* p)
+{
+    if (!p) return RIDC_OK;
+    cudaSetDevice(p->device);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+    for (void* o : p->opened)
+        if (o) cudaIpcCloseMemHandle(o);
+    if (p->mailbox) cudaFree(p->mailbox);
+    if (p->own_base) cudaFree(p->own_base);
+    if (p->d_weights) cudaFree(p->d_weights);
+    if (p->d_tab) cudaFree(p->d_tab);
+    if (p->d_plans) cudaFree(p->d_plans);
+    if (p->d_err) cudaFree(p->d_err);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+    return RIDC_OK;
+}
+
+const char* ridc_pipe_last_error(const ridc_pipe* p)
+{
+    if (p && !p->err.empty()) return p->err.c_str();
+    return g_last_error.c_str();
 }
 
 }  // extern "C"

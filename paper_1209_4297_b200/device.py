@@ -26,7 +26,7 @@ def require_cuda(device: int = 0):
 
 def to_device(a, device: int = 0):
     t = torch()
-    arr = np.ascontiguousarray(a, dtype=np.float64)
+    arr = np.array(a, dtype=np.float64, copy=True)
     return t.from_numpy(arr).to(require_cuda(device))
 
 

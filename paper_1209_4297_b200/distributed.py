@@ -1,0 +1,192 @@
+"""One RIDC level per GPU: the lagged pipeline across devices and processes.
+
+The reference runs levels as threads sharing ``LevelBuffer`` rings
+(engine.py:284-459); here level j runs on GPU j in its own process
+(``torchrun``, one rank per GPU).  ``PipelineRank`` wraps the native rank
+(``ridc_pipe_*`` in include/ridc_b200.h): each tick kernel stores its new
+state tile into the next level's inbox over NVLink (peer stores through an
+IPC-mapped mailbox), and device-side stream waits/writes carry the
+watermark / release counters -- the levels form a point-to-point chain, so
+there is no collective on the data path.  The only collective is the restart
+re-seed (engine.py:511-514): the top level's interval final is broadcast to
+every level.
+
+``run_levels`` is the driver both backends share: the GPU ranks below and
+the CPU oracle ranks of tests/_oracle_pipeline.py (gloo), so the interval /
+re-seed protocol is tested on CPU with world_size > 1.
+"""
+
+import ctypes
+import os
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib, device as D
+from .errors import ConfigError
+from .problems import as_descriptor
+from .quadrature import pack_weight_tables
+
+__all__ = ["PipelineRank", "SequentialPipeline", "run_levels", "run_pipelined_distributed"]
+
+
+def run_levels(runner, restarts: int, state0, broadcast: Callable, is_top: bool):
+    """Interval loop of run_pipelined (engine.py:509-515) for ONE level.
+
+    runner.run_interval(r, state0) -> (final_of_this_level, seconds);
+    broadcast(x, is_top) returns the top level's x on every rank.
+    Returns (this level's final state of the last interval, the solution on
+    every rank, total seconds).
+    """
+    s0 = state0
+    total = 0.0
+    fin = None
+    for r in range(restarts):
+        fin, sec = runner.run_interval(r, s0)
+        total += sec
+        s0 = broadcast(fin, is_top)   # next interval's state0 = top level's final
+    return fin, s0, total
+
+
+class PipelineRank:
+    """The level this process owns, on its GPU.
+
+    ``exchange(blob) -> list of blobs`` gathers every rank's mailbox handle
+    (default: torch.distributed.all_gather_object).
+    """
+
+    def __init__(self, ivp, config, rank: int, world: int, device: int = 0,
+                 inbox_capacity: int = 0, exchange: Optional[Callable] = None):
+        if config.levels != world:
+            raise ConfigError(f"one level per GPU: levels ({config.levels}) must equal ranks ({world})")
+        self.ivp = as_descriptor(ivp)
+        self.config = config
+        self.rank, self.world, self.device = rank, world, device
+        self.problem = self.ivp.problem
+        self.dt = (self.ivp.t_end - self.ivp.t_start) / config.steps
+        self.weights = pack_weight_tables(config.levels, self.dt)
+        D.require_cuda(device)
+        cp = self.problem.to_c()
+        h = ctypes.c_void_p()
+        _lib.check_pipe(_lib.lib().ridc_pipe_create(
+            ctypes.byref(cp), float(self.ivp.t_start), float(self.ivp.t_end), config.levels,
+            config.steps, config.restarts, self.weights.ctypes.data, self.weights.shape[0],
+            rank, device, int(inbox_capacity), float(config.watchdog_seconds), ctypes.byref(h)))
+        self._h = h
+        nb = _lib.lib().ridc_pipe_handle_bytes()
+        blob = ctypes.create_string_buffer(nb)
+        _lib.check_pipe(_lib.lib().ridc_pipe_export(self._h, blob), self._h)
+        self.blob = bytes(blob.raw)
+        if exchange is not None:
+            blobs = exchange(self.blob)
+            self.connect(blobs)
+
+    def connect(self, blobs):
+        prev = blobs[self.rank - 1] if self.rank > 0 else None
+        nxt = blobs[self.rank + 1] if self.rank < self.world - 1 else None
+        _lib.check_pipe(_lib.lib().ridc_pipe_connect(self._h, prev, nxt), self._h)
+
+    @property
+    def info(self) -> dict:
+        inf = _lib.RidcInfo()
+        _lib.check_pipe(_lib.lib().ridc_pipe_info(self._h, ctypes.byref(inf)), self._h)
+        return {f: getattr(inf, f) for f, _ in inf._fields_}
+
+    @property
+    def kernel_launches(self) -> int:
+        return self.config.steps      # one tick kernel per step of this level
+
+    @property
+    def tick_launches(self) -> int:
+        return self.config.steps
+
+    def run_interval(self, r: int, state0_dev):
+        out = D.torch().empty_like(state0_dev)
+        sec = ctypes.c_double(0.0)
+        _lib.check_pipe(_lib.lib().ridc_pipe_run_interval(
+            self._h, r, state0_dev.data_ptr(), out.data_ptr(), ctypes.byref(sec)), self._h)
+        return out, sec.value
+
+    def run_device(self, y0_dev, out_dev, broadcast=None) -> float:
+        """All intervals; out_dev receives the solution on every rank."""
+        if broadcast is None:
+            broadcast = _nccl_broadcast(self.world)
+        _fin, sol, sec = run_levels(self, self.config.restarts, y0_dev, broadcast,
+                                    self.rank == self.world - 1)
+        out_dev.copy_(sol)
+        return sec
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().ridc_pipe_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _nccl_broadcast(world):
+    import torch.distributed as dist
+
+    def bcast(x, is_top):
+        y = x.clone()
+        dist.broadcast(y, src=world - 1)
+        return y
+    return bcast
+
+
+class SequentialPipeline:
+    """All levels' pipeline ranks in ONE process on ONE device, run one after
+    another per interval (inbox rings sized for the whole run, so no rank ever
+    waits on a rank that has not started).  Exercises the pipeline's data path
+    -- peer-store mirrors, inbox watermarks, stream waits, re-seeding -- on a
+    single GPU; its output must equal the single-device engine bitwise."""
+
+    def __init__(self, ivp, config, device: int = 0):
+        self.config = config
+        L = config.levels
+        self.ranks = [PipelineRank(ivp, config, j, L, device, inbox_capacity=config.steps + 1)
+                      for j in range(L)]
+        blobs = [r.blob for r in self.ranks]
+        for r in self.ranks:
+            r.connect(blobs)
+        self.ivp = self.ranks[0].ivp
+
+    def run(self, y0=None):
+        y0 = self.ivp.initial_state if y0 is None else y0
+        s0 = D.to_device(y0, self.ranks[0].device)
+        finals = [None] * len(self.ranks)
+        for r in range(self.config.restarts):
+            for j, rk in enumerate(self.ranks):
+                finals[j], _ = rk.run_interval(r, s0)
+            s0 = finals[-1]
+        return D.to_host(finals[-1]), [D.to_host(f) for f in finals]
+
+    def close(self):
+        for r in self.ranks:
+            r.close()
+
+
+def run_pipelined_distributed(ivp, config, device: Optional[int] = None):
+    """run_pipelined with one level per GPU; call on every rank (torchrun).
+
+    Returns the RidcSolution-like tuple (final_state on every rank, this
+    rank's device seconds)."""
+    import torch.distributed as dist
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    dev = int(os.environ.get("LOCAL_RANK", rank)) if device is None else device
+
+    def exchange(blob):
+        out = [None] * world
+        dist.all_gather_object(out, blob)
+        return out
+    pr = PipelineRank(ivp, config, rank, world, dev, exchange=exchange)
+    y0 = D.to_device(pr.ivp.initial_state, dev)
+    out = D.torch().empty_like(y0)
+    sec = pr.run_device(y0, out)
+    pr.close()
+    return D.to_host(out), sec

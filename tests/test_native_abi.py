@@ -18,7 +18,7 @@ def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ("ridc_create", "ridc_run", "ridc_run_device", "ridc_destroy", "ridc_last_error",
               "ridc_op_apply", "ridc_op_solve", "ridc_op_step", "ridc_pipe_create",
-              "ridc_pipe_run"):
+              "ridc_pipe_run_interval"):
         assert s in syms
 
 
