@@ -389,36 +389,47 @@ __device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve
     RIDC_STAMP(sv, ino, 2);
     // ---- phase 2: x-stencils of WS (then WX) through shared memory
     // (FAST: every position is computed; rhs outside [1, Q-1) is zeroed below)
+    // Strided position q = tid + k*NT has padded index pq + k*SK (NT is a multiple
+    // of 16); its neighbours sit at pq + k*SK + dm / + dp.
+    constexpr int SK = NT + NT / 16;
+    const int pq = pad(tid);
+    const int dm = pad(tid + NT - 1) - NT - NT / 16 - pq;   // pad(q-1) - pad(q)  (tid-1, wrapped into the row above)
+    const int dp = pad(tid + 1) - pq;                       // pad(q+1) - pad(q)
+    bool need_ws = false, need_wx = false;
+    for (int a = 0; a < it.nnodes; ++a) {
+        need_ws |= it.cs[a] != 0.0;
+        need_wx |= it.cn[a] != 0.0;
+    }
+    need_wx = need_wx && has_wx;
     double rhs[KMAX];
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-        const int q = tid + k * NT;
-        rhs[k] = P[k];
-        if (FAST || valid(q)) sbuf[pad(q)] = WS[k];
-    }
-    csync<NT>();
+    for (int k = 0; k < KMAX; ++k) rhs[k] = P[k];
+    if (need_ws) {
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-        const int q = tid + k * NT;
-        if (FAST ? (q >= 1 && q < CAP - 1) : (q >= 1 && q < Q - 1))
-            rhs[k] = fma(pb.cdx, (sbuf[pad(q - 1)] - 2.0 * WS[k]) + sbuf[pad(q + 1)], rhs[k]);
-    }
-    csync<NT>();
-    if (has_wx) {
+        for (int k = 0; k < KMAX; ++k)
+            if (FAST || valid(tid + k * NT)) sbuf[pq + k * SK] = WS[k];
+        csync<NT>();
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) {
             const int q = tid + k * NT;
-            if (FAST || valid(q)) sbuf[pad(q)] = WX[k];
+            if (FAST ? (q >= 1 && q < CAP - 1) : (q >= 1 && q < Q - 1))
+                rhs[k] = fma(pb.cdx, (sbuf[pq + k * SK + dm] - 2.0 * WS[k]) + sbuf[pq + k * SK + dp], rhs[k]);
         }
+        csync<NT>();
+    }
+    if (need_wx) {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (FAST || valid(tid + k * NT)) sbuf[pq + k * SK] = WX[k];
         csync<NT>();
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) {
             const int q = tid + k * NT;
             if (FAST ? (q >= 1 && q < CAP - 1) : (q >= 1 && q < Q - 1)) {
                 if (KIND == BURGERS_1D)
-                    rhs[k] = fma(-pb.bs, sbuf[pad(q + 1)] - sbuf[pad(q - 1)], rhs[k]);
+                    rhs[k] = fma(-pb.bs, sbuf[pq + k * SK + dp] - sbuf[pq + k * SK + dm], rhs[k]);
                 else
-                    rhs[k] = fma(pb.cax, sbuf[pad(q + 1)] - WX[k], rhs[k]);
+                    rhs[k] = fma(pb.cax, sbuf[pq + k * SK + dp] - WX[k], rhs[k]);
             }
         }
         csync<NT>();
@@ -428,7 +439,7 @@ __device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {
         const int q = tid + k * NT;
-        if (FAST) sbuf[pad(q)] = (q == 0 || q >= Q - 1) ? 0.0 : rhs[k];
+        if (FAST) sbuf[pq + k * SK] = (q == 0 || q >= Q - 1) ? 0.0 : rhs[k];
         else if (q >= 1 && q < Q - 1) sbuf[pad(q - 1)] = rhs[k];
     }
     csync<NT>();
@@ -439,8 +450,10 @@ __device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve
     const int base = tid * KMAX;
     const int nm = FAST ? KMAX : max(0, min(KMAX, S - base));
     double vv[KMAX];
+    static_assert(16 % KMAX == 0 || KMAX % 16 == 0, "chunk padding assumes KMAX | 16 or 16 | KMAX");
+    const int pc = pad(base);   // pad(base + e) == pc + e for e < KMAX
 #pragma unroll
-    for (int e = 0; e < KMAX; ++e) vv[e] = (FAST || e < nm) ? sbuf[pad(base + e)] : 0.0;
+    for (int e = 0; e < KMAX; ++e) vv[e] = (FAST || e < nm) ? sbuf[pc + e] : 0.0;
     const bool cmode = FAST || (sv.ntab == 0) || (e0 + base >= sv.ntab);
     const double m = sv.lam, g = sv.g;
     if constexpr (FAST) {
@@ -531,25 +544,27 @@ __device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve
     }
 #pragma unroll
     for (int e = 0; e < KMAX; ++e)
-        if (FAST || e < nm) sbuf[pad(base + e)] = vv[e];
+        if (FAST || e < nm) sbuf[pc + e] = vv[e];
     csync<NT>();
 
     RIDC_STAMP(sv, ino, 8);
     // ---- phase 5: coalesced store of the tile + fused finite check
-    bool bad = false;
-    double* orow = it.out + rbase;
-    double* orow2 = it.out2 ? it.out2 + rbase : nullptr;
+    // finite check folded into one FMA per point: x*0 is NaN iff x is Inf/NaN
+    double chk = 0.0;
+    double* orow = it.out + rbase + e0;
+    double* orow2 = it.out2 ? it.out2 + rbase + e0 : nullptr;
     const int olo = FAST ? geo.out_lo + 1 : geo.out_lo;   // in scan coordinates
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {
         const int e = tid + k * NT;
         if ((unsigned)(e - olo) < (unsigned)geo.tlen) {
-            const double xo = sbuf[pad(e)];
-            bad |= !isfinite(xo);
-            orow[e0 + e] = xo;
-            if (orow2) orow2[e0 + e] = xo;   // peer store into the next level's inbox
+            const double xo = sbuf[pq + k * SK];
+            chk = fma(xo, 0.0, chk);
+            orow[e] = xo;
+            if (orow2) orow2[e] = xo;   // peer store into the next level's inbox
         }
     }
+    const bool bad = chk != chk;
     if (bad) atomicMin(err, err_code(it.target, it.level));
     RIDC_STAMP(sv, ino, 9);
 }

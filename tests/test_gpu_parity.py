@@ -85,7 +85,7 @@ SOLVE_CASES = [
     # (descriptor, coeff): whole-line exact and segmented truncated-halo paths
     (P.ProblemDescriptor(P.KIND_ADV_DIFF_1D, nx=7, c_x=0.1, d_x=1e-3, h_x=1 / 7), 50.0),
     (P.ProblemDescriptor(P.KIND_ADV_DIFF_1D, nx=1024, c_x=0.1, d_x=1e-3, h_x=1 / 1024), 4e-3),
-    (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=8192, d_x=1.0, rho=1.0, h_x=1 / 8192), 1e-3),
+    (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=8190, d_x=1.0, rho=1.0, h_x=1 / 8190), 1e-3),
     (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=8193, d_x=1e-6, rho=1.0, h_x=1 / 8193), 1e-2),
     (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=1 << 20, d_x=1e-6, rho=1.0, h_x=2.0 ** -20), 1e-4),
     (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=100003, d_x=1.0, rho=1.0, h_x=1e-5), 2e-8),
@@ -110,6 +110,15 @@ def test_solve_matches_oracle(pd, coeff):
     # residual of the structured system
     res = x - coeff * O.stiff(pd, x) - rhs
     assert np.abs(res).max() <= 1e-12 * np.abs(rhs).max() * (1 + 4 * coeff * pd.d_x / pd.h_x ** 2)
+
+
+def test_segmented_solve_beyond_halo_limit_raises():
+    """r ~ 6.7e4 on a line longer than one CTA needs a >1919-point truncation halo:
+    documented limit, reported as ConfigError, never a silent fallback."""
+    from paper_1209_4297_b200.errors import ConfigError
+    pd = P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=8192, d_x=1.0, rho=1.0, h_x=1 / 8192)
+    with pytest.raises(ConfigError):
+        ops.solve_shifted(pd, 1e-3, np.ones(8192))
 
 
 def test_predict_correct_kats(golden):
