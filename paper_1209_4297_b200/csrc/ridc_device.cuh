@@ -59,7 +59,7 @@ struct DevSolve {
 // Phase trace: CTA 0, thread 0, first 8 items of a launch, 16 stamps each.
 #define RIDC_STAMP(sv, item_no, idx)                                                         \
     do {                                                                                     \
-        if ((sv).dbg && blockIdx.x == 0 && threadIdx.x == 0 && (item_no) < 8)                \
+        if (threadIdx.x == 0 && blockIdx.x == 0 && (sv).dbg && (item_no) < 8)                \
             (sv).dbg[(item_no) * 16 + (idx)] = clock64();                                    \
     } while (0)
 
@@ -265,13 +265,12 @@ __device__ __forceinline__ void accumulate_point(const DevProblem& pb, double ca
                                                  double v, double vn, double vs, double& P,
                                                  double& WS, double& WX)
 {
-    double p = P;
-    if (ca != 0.0) p = fma(ca, v, p);
-    if (cn != 0.0) {   // uniform; also keeps unloaded y-neighbours out of the sum
-        if (KIND == RD_1D) p = fma(cn, pb.rho * v * (1.0 - v), p);
-        if (KIND == RD_2D) p = fma(cn, fma(pb.rho * v, 1.0 - v, pb.cdy * (vn - 2.0 * v + vs)), p);
-        if (KIND == ADV_DIFF_2D) p = fma(cn, fma(pb.cay, vs - v, pb.cdy * (vn - 2.0 * v + vs)), p);
-    }
+    // branch-free: zero coefficients cost one FMA, never a select (callers keep
+    // vn / vs finite -- zero when the y-neighbours were not loaded)
+    double p = fma(ca, v, P);
+    if (KIND == RD_1D) p = fma(cn, pb.rho * v * (1.0 - v), p);
+    if (KIND == RD_2D) p = fma(cn, fma(pb.rho * v, 1.0 - v, pb.cdy * (vn - 2.0 * v + vs)), p);
+    if (KIND == ADV_DIFF_2D) p = fma(cn, fma(pb.cay, vs - v, pb.cdy * (vn - 2.0 * v + vs)), p);
     P = p;
     WS = fma(cs, v, WS);
     if (KIND == BURGERS_1D) WX = fma(cn, v * v, WX);
@@ -554,14 +553,26 @@ __device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve
     double* orow = it.out + rbase + e0;
     double* orow2 = it.out2 ? it.out2 + rbase + e0 : nullptr;
     const int olo = FAST ? geo.out_lo + 1 : geo.out_lo;   // in scan coordinates
+    if (orow2) {   // pipeline: also the peer store into the next level's inbox (NVLink)
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-        const int e = tid + k * NT;
-        if ((unsigned)(e - olo) < (unsigned)geo.tlen) {
-            const double xo = sbuf[pq + k * SK];
-            chk = fma(xo, 0.0, chk);
-            orow[e] = xo;
-            if (orow2) orow2[e] = xo;   // peer store into the next level's inbox
+        for (int k = 0; k < KMAX; ++k) {
+            const int e = tid + k * NT;
+            if ((unsigned)(e - olo) < (unsigned)geo.tlen) {
+                const double xo = sbuf[pq + k * SK];
+                chk = fma(xo, 0.0, chk);
+                orow[e] = xo;
+                orow2[e] = xo;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const int e = tid + k * NT;
+            if ((unsigned)(e - olo) < (unsigned)geo.tlen) {
+                const double xo = sbuf[pq + k * SK];
+                chk = fma(xo, 0.0, chk);
+                orow[e] = xo;
+            }
         }
     }
     const bool bad = chk != chk;
@@ -616,6 +627,8 @@ __device__ __forceinline__ void item_body(const DevProblem& pb, const DevSolve& 
     for (int k = 0; k < KMAX; ++k) { P[k] = 0.0; WS[k] = 0.0; WX[k] = 0.0; }
 
     double ua[KMAX], ub[KMAX], un[KMAX], us[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) { un[k] = 0.0; us[k] = 0.0; }
     auto load = [&](int a, double* u) {
         const double* rp = it.vec[a] + rbase;
 #pragma unroll

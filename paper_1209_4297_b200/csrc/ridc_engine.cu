@@ -60,19 +60,20 @@ struct TickParams {
     long long target[kMaxLevels];
 };
 
-__device__ __forceinline__ double* ring_slot(const EngineParams& ep, int lev, long long s)
+__device__ __forceinline__ double* ring_slot(const EngineParams& ep, int lev, long long s,
+                                             long long off = -1)
 {
-    return ep.ring[lev] + ((ep.off[lev] + s) % ep.cap[lev]) * ep.Vs;
+    return ep.ring[lev] + (((off < 0 ? ep.off[lev] : off) + s) % ep.cap[lev]) * ep.Vs;
 }
 
 // Window assembly for (level j, target t): _window_span / _orient /
 // _WeightTables.for_step (engine.py:124-157) with the lag terms of
 // _correct_core (engine.py:179-181) folded into the node coefficients.
-__device__ void build_item(const EngineParams& ep, int j, long long t, StepItem& it)
+__device__ void build_item(const EngineParams& ep, int j, long long t, StepItem& it, long long off = -1)
 {
     it.level = j;
     it.target = t;
-    it.vec[0] = ring_slot(ep, j, t - 1);
+    it.vec[0] = ring_slot(ep, j, t - 1, off);
     it.ca[0] = 1.0;
     it.cs[0] = 0.0;
     it.cn[0] = ep.dt;
@@ -85,7 +86,7 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
         const int i_old = steady ? 1 : (int)t - 1;
         for (int a = 0; a <= j; ++a) {
             const long long s = steady ? t - a : a;
-            it.vec[nn] = ring_slot(ep, j - 1, s);
+            it.vec[nn] = ring_slot(ep, j - 1, s, off);
             it.ca[nn] = 0.0;
             it.cs[nn] = w[a] - (a == i_new ? ep.dt : 0.0);
             it.cn[nn] = w[a] - (a == i_old ? ep.dt : 0.0);
@@ -93,7 +94,7 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
         }
     }
     it.nnodes = nn;
-    it.out = ring_slot(ep, j, t);
+    it.out = ring_slot(ep, j, t, off);
     it.out2 = ep.mirror ? ep.mirror + ((ep.mirror_off + t) % ep.mirror_cap) * ep.Vs : nullptr;
 }
 
@@ -145,13 +146,287 @@ __global__ void __launch_bounds__(NT, 1) k_tick_tma(EngineParams ep, TickParams 
         const int slot = i % tp.nact, tile = i / tp.nact;
         Geo geo = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
         geo.item_no = ino;
+        auto ensure = [](long long) {};
         if (geo.fast)
             consume_item<KIND, NT, KMAX, ROWS, NSTAGE, true>(ep.pb, ep.sv, items[slot], geo, stage, full,
-                                                            empty, n, refill, sbuf, swarp, ep.err);
+                                                            empty, n, refill, ensure, sbuf, swarp, ep.err);
         else
             consume_item<KIND, NT, KMAX, ROWS, NSTAGE, false>(ep.pb, ep.sv, items[slot], geo, stage,
-                                                             full, empty, n, refill, sbuf, swarp, ep.err);
+                                                             full, empty, n, refill, ensure, sbuf, swarp,
+                                                             ep.err);
         csync<NT>();   // sbuf reuse by the next item
+    }
+}
+
+// ---------------------------------------------------------------- persistent run kernel
+//
+// One launch marches every interval and tick.  CTA b owns tiles b, b+G, ...
+// of every level.  Cross-CTA ordering uses one completion flag per (level,
+// tile): the last global step written (global step of (interval r, step t)
+// = r*(per+1) + t; step 0 of an interval is its seed).  Before level j
+// computes global step G of a tile, thread 0 acquires (engine.py:363-371):
+//   (a) own level, neighbour tiles  >= G-1        (halo of the previous state)
+//   (b) level j-1, neighbour tiles  >= G(hi)      (window, LevelBuffer.watermark)
+//   (c) level j+1, neighbour tiles  >= G - C_j + j + 1   (ring slot free, .released)
+// Every dependency is on an earlier tick and every CTA walks its items in
+// tick order, so co-resident CTAs cannot deadlock; a %globaltimer watchdog
+// still turns a stall into an error instead of a hang.
+struct PersistParams {
+    int ipl;                   // tiles per level
+    int rx;                    // neighbour radius in segments
+    int levels, restarts;
+    long long per;
+    long long* flags;          // [levels][ipl], init -1
+    const double* y0;
+    int* abort;
+    unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ long long ld_acquire(const long long* p)
+{
+    long long v;
+    asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(long long* p, long long v)
+{
+    asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// pointer of node a of (level j, step t) -- the same order build_item uses
+__device__ __forceinline__ const double* node_ptr(const EngineParams& ep, int j, long long t, int a,
+                                                  long long off)
+{
+    if (a == 0) return ring_slot(ep, j, t - 1, off);
+    const long long s = t >= j ? t - (a - 1) : (a - 1);
+    return ring_slot(ep, j - 1, s, off);
+}
+
+// Are the dependencies of (level j, global step G, tile) satisfied?
+template <int KIND>
+__device__ bool deps_ready(const EngineParams& ep, const PersistParams& pp, int j, long long t,
+                           long long G, long long Ghi, int tile)
+{
+    const int nseg = ep.sv.nseg, ny = ep.pb.ny;
+    constexpr bool periodic = KIND != BURGERS_1D;
+    const int row = tile / nseg, seg = tile - row * nseg;
+    const int r0 = ny > 1 ? -1 : 0, r1 = ny > 1 ? 1 : 0;
+    const int rx = nseg > 1 ? pp.rx : 0;
+    const long long capj = ep.cap[j];
+    bool ok = true;
+    for (int dr = r0; dr <= r1; ++dr) {
+        const int rr = (row + dr + ny) % ny;
+        for (int ds = -rx; ds <= rx; ++ds) {
+            int sg = seg + ds;
+            if (periodic) sg = (sg % nseg + nseg) % nseg;
+            else if (sg < 0 || sg >= nseg) continue;
+            const int tl = rr * nseg + sg;
+            ok &= ld_acquire(pp.flags + (size_t)j * pp.ipl + tl) >= G - 1;
+            if (j > 0 && t >= 1) ok &= ld_acquire(pp.flags + (size_t)(j - 1) * pp.ipl + tl) >= Ghi;
+            if (j < pp.levels - 1)
+                ok &= ld_acquire(pp.flags + (size_t)(j + 1) * pp.ipl + tl) >= G - capj + j + 1;
+        }
+    }
+    return ok;
+}
+
+template <int KIND>
+__device__ bool wait_deps(const EngineParams& ep, const PersistParams& pp, int j, long long t, long long G,
+                          long long Ghi, int tile)
+{
+    unsigned long long t0 = 0;
+    for (;;) {
+        if (deps_ready<KIND>(ep, pp, j, t, G, Ghi, tile)) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
+            return true;
+        }
+        if (*(volatile int*)pp.abort) return false;
+        const unsigned long long now = gtimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > pp.timeout_ns) {
+            atomicExch(pp.abort, 1);
+            return false;
+        }
+    }
+}
+
+
+struct PCursor {
+    int r;            // interval
+    long long k;      // tick
+    int j;            // level
+    int m;            // owned-tile ordinal
+    int a;            // node
+    long long n;      // load number
+    bool done;
+};
+
+template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE>
+__global__ void __launch_bounds__(NT, 1) k_persist(EngineParams ep0, PersistParams pp)
+{
+    using L = TmaSmem<NT, KMAX, ROWS, NSTAGE>;
+    extern __shared__ __align__(128) double sm[];
+    double* stage = sm;
+    double* sbuf = sm + L::OFF_SBUF;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+    uint64_t* empty = full + NSTAGE;
+    __shared__ StepItem items[2][kMaxLevels];
+    __shared__ Aff swarp[2 * (NT / 32) + 1];
+    __shared__ volatile int s_abort;
+    const int tid = threadIdx.x;
+    const int G = gridDim.x;
+    const int my_tiles = pp.ipl > (int)blockIdx.x ? (pp.ipl - 1 - (int)blockIdx.x) / G + 1 : 0;
+    const int top = pp.levels - 1;
+    const long long ticks = pp.per + (long long)top * (top + 1) / 2;
+    if (tid == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NT / 32);
+        }
+        mbar_fence_init();
+        s_abort = 0;
+    }
+    __syncthreads();
+    if (my_tiles == 0) return;
+    const EngineParams& ep = ep0;
+
+    // ---- producer cursor (thread 0) over compute items: (r, k, j active, m, a)
+    auto delay = [](int j) { return (long long)j * (j + 1) / 2; };
+    auto active = [&](long long k, int j) { const long long t = k - delay(j); return t >= 1 && t <= pp.per; };
+    PCursor pc{0, 1, 0, 0, 0, 0, false};
+    auto first_level = [&](long long k, int from) {
+        for (int j = from; j <= top; ++j)
+            if (active(k, j)) return j;
+        return -1;
+    };
+    pc.j = first_level(1, 0);
+    auto advance_item = [&]() {
+        pc.a = 0;
+        if (++pc.m < my_tiles) return;
+        pc.m = 0;
+        int nj = first_level(pc.k, pc.j + 1);
+        while (nj < 0) {
+            if (++pc.k > ticks) {
+                pc.k = 1;
+                if (++pc.r >= pp.restarts) { pc.done = true; return; }
+            }
+            nj = first_level(pc.k, 0);
+        }
+        pc.j = nj;
+    };
+    const EngineParams& epp = ep0;
+    bool pc_ready = false;    // dependencies of the cursor's current item acquired
+    auto try_issue = [&](int s, bool blocking) -> bool {
+        if (pc.done) return false;
+        const long long poff = (long long)pc.r * (pp.per + 1);
+        const long long t = pc.k - delay(pc.j);
+        const int tile = (int)blockIdx.x + pc.m * G;
+        if (pc.a == 0 && !pc_ready) {
+            const long long Gs = (long long)pc.r * (pp.per + 1) + t;
+            const long long hi = pc.j > 0 ? (t < pc.j ? pc.j : t) : 0;
+            const long long Ghi = (long long)pc.r * (pp.per + 1) + hi;
+            if (blocking) {
+                if (!wait_deps<KIND>(epp, pp, pc.j, t, Gs, Ghi, tile)) return false;
+            } else if (!deps_ready<KIND>(epp, pp, pc.j, t, Gs, Ghi, tile)) {
+                return false;
+            } else {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            pc_ready = true;
+        }
+        const Geo g = make_geo<KIND, NT, KMAX>(epp.pb, epp.sv, tile);
+        issue_node<ROWS, L::SROW>(epp.pb, epp.sv, node_ptr(epp, pc.j, t, pc.a, poff), g,
+                                  stage + (size_t)s * L::STAGE, &full[s]);
+        const int nn = pc.j > 0 ? pc.j + 2 : 1;
+        ++pc.n;
+        if (++pc.a == nn) { pc_ready = false; advance_item(); }
+        return true;
+    };
+    // released load n from stage s: refill with load n + NSTAGE if ready (never blocks on peers)
+    auto refill = [&](long long n, int s) {
+        if (pc.done || pc.n != n + NSTAGE) return;
+        mbar_wait(&empty[s], (uint32_t)((n / NSTAGE) & 1));
+        try_issue(s, false);
+    };
+    // before consuming load n: make sure loads up to n are issued (may block on peers)
+    auto ensure = [&](long long n) {
+        while (pc.n <= n && !pc.done) {
+            const int s = (int)(pc.n % NSTAGE);
+            if (pc.n >= NSTAGE) mbar_wait(&empty[s], (uint32_t)(((pc.n - NSTAGE) / NSTAGE) & 1));
+            if (!try_issue(s, true)) {   // watchdog fired: release everyone waiting on this stage
+                s_abort = 1;
+                mbar_arrive_expect_tx(&full[s], 0);
+                return;
+            }
+        }
+    };
+
+    long long n = 0;
+    int ino = 0;
+    for (int r = 0; r < pp.restarts; ++r) {
+        const long long g0 = (long long)r * (pp.per + 1);   // ring offset of the interval
+        // ---- seeds: step 0 of every level = the interval's state0 (top-level final before)
+        const double* src = r == 0 ? pp.y0 : ring_slot(ep, top, pp.per, g0 - (pp.per + 1));
+        for (int j = 0; j <= top; ++j) {
+            for (int m = 0; m < my_tiles; ++m) {
+                const int tile = (int)blockIdx.x + m * G;
+                if (tid == 0 && !wait_deps<KIND>(ep, pp, j, 0, g0, 0, tile)) s_abort = 1;
+                csync<NT>();
+                if (s_abort) return;
+                const Geo g = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
+                const size_t base = (size_t)g.row * ep.pb.nx + g.c0;
+                double* dst = ring_slot(ep, j, 0, g0) + base;
+                for (int i = tid; i < g.tlen; i += NT) dst[i] = src[base + i];
+                csync<NT>();
+                if (tid == 0) {
+                    __threadfence();
+                    st_release(pp.flags + (size_t)j * pp.ipl + tile, g0);
+                }
+            }
+        }
+        // ---- ticks
+        for (long long k = 1; k <= ticks; ++k) {
+            int nact = 0;
+            for (int j = 0; j <= top; ++j)
+                if (active(k, j)) {
+                    if (tid == 0) build_item(ep, j, k - delay(j), items[k & 1][nact], g0);
+                    ++nact;
+                }
+            csync<NT>();
+            int slot = 0;
+            for (int j = 0; j <= top; ++j) {
+                if (!active(k, j)) continue;
+                const long long t = k - delay(j);
+                const StepItem& it = items[k & 1][slot++];
+                for (int m = 0; m < my_tiles; ++m, ++ino) {
+                    const int tile = (int)blockIdx.x + m * G;
+                    Geo geo = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
+                    geo.item_no = ino;
+                    if (geo.fast)
+                        consume_item<KIND, NT, KMAX, ROWS, NSTAGE, true>(ep.pb, ep.sv, it, geo, stage, full, empty, n,
+                                                                        refill, ensure, sbuf, swarp, ep.err,
+                                                                        &s_abort);
+                    else
+                        consume_item<KIND, NT, KMAX, ROWS, NSTAGE, false>(ep.pb, ep.sv, it, geo, stage, full, empty,
+                                                                         n, refill, ensure, sbuf, swarp, ep.err,
+                                                                         &s_abort);
+                    csync<NT>();
+                    if (s_abort) return;
+                    if (tid == 0) {
+                        __threadfence();
+                        st_release(pp.flags + (size_t)j * pp.ipl + tile, g0 + t);
+                    }
+                }
+            }
+        }
     }
 }
 
@@ -267,7 +542,8 @@ TmaCfg tma_cfg_of(int id)
     X(2, 512, 8, 1, 3)             \
     X(3, 1024, 8, 1, 2)            \
     X(4, 256, 4, 3, 3)             \
-    X(5, 512, 4, 3, 3)
+    X(5, 512, 4, 3, 3)             \
+    X(6, 512, 16, 1, 2)
 
 TmaCfg pick_tma(int kind, int Q)
 {
@@ -276,7 +552,8 @@ TmaCfg pick_tma(int kind, int Q)
     if (Q <= 1024) return tma_cfg_of<128, 8, 1, 4>(0);
     if (Q <= 2048) return tma_cfg_of<256, 8, 1, 4>(1);
     if (Q <= 4096) return tma_cfg_of<512, 8, 1, 3>(2);
-    return tma_cfg_of<1024, 8, 1, 2>(3);
+    if (getenv("RIDC_CFG1024")) return tma_cfg_of<1024, 8, 1, 2>(3);
+    return tma_cfg_of<512, 16, 1, 2>(6);
 }
 
 int tma_cap(int kind) { return (kind == ADV_DIFF_2D || kind == RD_2D) ? 2048 : 8192; }
@@ -311,6 +588,62 @@ cudaError_t launch_tma_k(const TmaCfg& c, int grid, cudaStream_t st, const Engin
     }
     RIDC_TMA_CONFIGS(RIDC_TMA_CASE)
 #undef RIDC_TMA_CASE
+    return cudaErrorInvalidValue;
+}
+
+template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE>
+cudaError_t launch_persist_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
+                             const PersistParams& pp)
+{
+    auto kfn = k_persist<KIND, NT, KMAX, ROWS, NSTAGE>;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    // cooperative: every CTA co-resident (the flag protocol needs it), else the launch fails
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, ep, pp);
+}
+
+template <int KIND>
+cudaError_t launch_persist_k(const TmaCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
+                             const PersistParams& pp)
+{
+    constexpr bool two_d = KIND == ADV_DIFF_2D || KIND == RD_2D;
+#define RIDC_PERSIST_CASE(ID, NT, KMAX, ROWS, NSTAGE)                                  \
+    if (c.id == ID && two_d == (ROWS == 3)) {                                          \
+        if constexpr (two_d == (ROWS == 3))                                            \
+            return launch_persist_t<KIND, NT, KMAX, ROWS, NSTAGE>(grid, c.smem, st, ep, pp); \
+    }
+    RIDC_TMA_CONFIGS(RIDC_PERSIST_CASE)
+#undef RIDC_PERSIST_CASE
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_persist(int kind, const TmaCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
+                           const PersistParams& pp)
+{
+    switch (kind) {
+    case ADV_DIFF_1D: return launch_persist_k<ADV_DIFF_1D>(c, grid, st, ep, pp);
+    case BURGERS_1D: return launch_persist_k<BURGERS_1D>(c, grid, st, ep, pp);
+    case RD_1D: return launch_persist_k<RD_1D>(c, grid, st, ep, pp);
+    case ADV_DIFF_2D: return launch_persist_k<ADV_DIFF_2D>(c, grid, st, ep, pp);
+    case RD_2D: return launch_persist_k<RD_2D>(c, grid, st, ep, pp);
+    }
     return cudaErrorInvalidValue;
 }
 
@@ -639,6 +972,10 @@ struct ridc_ctx {
     long long ring_vectors = 0;
     long long Vs = 0;          // ring slot stride (doubles)
     int nsm = 148;             // persistent CTAs per tick launch
+    bool persistent = false;   // one k_persist launch per run (else a graph of tick launches)
+    long long* d_flags = nullptr;
+    int* d_abort = nullptr;
+    PersistParams pp;
     double* d_ring_base[kMaxLevels] = {};
     std::string err;
 };
@@ -661,7 +998,7 @@ void weight_offsets(int L, std::vector<int>& st, std::vector<int>& su, long long
 EngineParams interval_params(ridc_ctx* c, int interval)
 {
     EngineParams ep = c->ep;
-    for (int j = 0; j < c->levels; ++j) ep.off[j] = 0;
+    for (int j = 0; j < c->levels; ++j) ep.off[j] = c->persistent ? (long long)interval * (c->per + 1) : 0;
     if (c->flags & RIDC_RECORD_TRAJECTORY) ep.off[c->levels - 1] = (long long)interval * c->per;
     return ep;
 }
@@ -735,10 +1072,24 @@ int check_err_word(ridc_ctx* c)
 int march(ridc_ctx* c, double* wall_seconds)
 {
     CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+    if (c->persistent) {
+        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0xff,
+                                          sizeof(long long) * c->levels * c->pp.ipl, c->stream));
+        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_abort, 0, sizeof(int), c->stream));
+    }
     CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
-    CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
+    if (c->persistent)
+        CUDA_TRY(&c->err, launch_persist(c->pb.kind, c->ss.tcfg, std::min(c->nsm, c->pp.ipl), c->stream,
+                                         interval_params(c, 0), c->pp));
+    else
+        CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
     CUDA_TRY(&c->err, cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(&c->err, cudaEventSynchronize(c->ev1));
+    if (c->persistent) {
+        int ab = 0;
+        CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_abort, sizeof ab, cudaMemcpyDeviceToHost));
+        if (ab) return fail(&c->err, RIDC_E_PROTOCOL, "tile pipeline made no progress within the watchdog");
+    }
     if (wall_seconds) {
         float ms = 0.f;
         CUDA_TRY(&c->err, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
@@ -882,7 +1233,31 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         ep.startup_off[j] = su[j];
     }
     ep.err = c->d_err;
-    if ((rc = capture_graph(c)) != RIDC_OK) return bail(rc);
+    // opt-in (RIDC_PERSIST=1): one persistent launch per run with per-tile
+    // dependency flags.  Measured slower than the tick graph on B200 for every
+    // workload (flag hand-off + unprefetchable dependent loads ~ the launch gap),
+    // so the graph of tick launches is the default.
+    const char* ps = getenv("RIDC_PERSIST");
+    c->persistent = !(flags & RIDC_RECORD_TRAJECTORY) && (ps && atoi(ps) > 0);
+    if (c->persistent) {
+        const DevSolve& sv = c->ss.sv;
+        PersistParams& pp = c->pp;
+        memset(&pp, 0, sizeof pp);
+        pp.ipl = c->pb.ny * sv.nseg;
+        pp.rx = sv.nseg > 1 ? (sv.halo + 1 + sv.tile - 1) / sv.tile : 0;
+        pp.levels = levels;
+        pp.restarts = restarts;
+        pp.per = per;
+        CTX_TRY(cudaMalloc(&c->d_flags, sizeof(long long) * levels * pp.ipl));
+        CTX_TRY(cudaMalloc(&c->d_abort, sizeof(int)));
+        pp.flags = c->d_flags;
+        pp.abort = c->d_abort;
+        pp.y0 = c->d_y0;
+        pp.timeout_ns = 10ull * 1000 * 1000 * 1000;
+        c->launches = 1;
+    } else if ((rc = capture_graph(c)) != RIDC_OK) {
+        return bail(rc);
+    }
 #undef CTX_TRY
     *out = c;
     return RIDC_OK;
@@ -958,6 +1333,8 @@ int ridc_destroy(ridc_ctx* c)
     if (c->d_tab) cudaFree(c->d_tab);
     if (c->d_plans) cudaFree(c->d_plans);
     if (c->d_dbg) cudaFree(c->d_dbg);
+    if (c->d_flags) cudaFree(c->d_flags);
+    if (c->d_abort) cudaFree(c->d_abort);
     if (c->d_y0) cudaFree(c->d_y0);
     if (c->d_err) cudaFree(c->d_err);
     if (c->ev0) cudaEventDestroy(c->ev0);

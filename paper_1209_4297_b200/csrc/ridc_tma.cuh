@@ -62,6 +62,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
         : "memory");
 }
 
+// As mbar_wait, but gives up when *abortp becomes non-zero (persistent kernel watchdog).
+__device__ __forceinline__ void mbar_wait_or(uint64_t* bar, uint32_t parity, const volatile int* abortp)
+{
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok || (abortp && *abortp)) return;
+    }
+}
+
 // global -> shared bulk copy (UBLKCP), completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 {
@@ -156,12 +172,13 @@ struct LoadCursor {
 
 // Consumer side of one TMA-staged item.  `n` counts this CTA's loads;
 // thread 0 also refills each released stage with load n + NSTAGE.
-template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE, bool FAST, class Issue>
+template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE, bool FAST, class Issue, class Ensure>
 __device__ __forceinline__ void consume_item(const DevProblem& pb, const DevSolve& sv,
                                              const StepItem& it, const Geo& geo, double* stage,
                                              uint64_t* full, uint64_t* empty, long long& n,
-                                             Issue&& refill, double* sbuf, Aff* swarp,
-                                             unsigned long long* err)
+                                             Issue&& refill, Ensure&& ensure, double* sbuf,
+                                             Aff* swarp, unsigned long long* err,
+                                             const volatile int* abortp = nullptr)
 {
     using L = TmaSmem<NT, KMAX, ROWS, NSTAGE>;
     constexpr bool periodic = KIND != BURGERS_1D;
@@ -185,7 +202,9 @@ __device__ __forceinline__ void consume_item(const DevProblem& pb, const DevSolv
     for (int a = 0; a < it.nnodes; ++a, ++n) {
         const int s = (int)(n % NSTAGE);
         double* st = stage + (size_t)s * L::STAGE;
-        mbar_wait(&full[s], (uint32_t)((n / NSTAGE) & 1));
+        if (tid == 0) ensure(n);   // persistent kernel: load n may still be unissued
+        if (abortp) mbar_wait_or(&full[s], (uint32_t)((n / NSTAGE) & 1), abortp);
+        else mbar_wait(&full[s], (uint32_t)((n / NSTAGE) & 1));
         if (a == 0) RIDC_STAMP(sv, geo.item_no, 1);
         if (!FAST) {
             bool filled = false;

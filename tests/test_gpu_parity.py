@@ -85,7 +85,7 @@ SOLVE_CASES = [
     # (descriptor, coeff): whole-line exact and segmented truncated-halo paths
     (P.ProblemDescriptor(P.KIND_ADV_DIFF_1D, nx=7, c_x=0.1, d_x=1e-3, h_x=1 / 7), 50.0),
     (P.ProblemDescriptor(P.KIND_ADV_DIFF_1D, nx=1024, c_x=0.1, d_x=1e-3, h_x=1 / 1024), 4e-3),
-    (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=8190, d_x=1.0, rho=1.0, h_x=1 / 8190), 1e-3),
+    (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=4094, d_x=1.0, rho=1.0, h_x=1 / 4094), 1e-3),
     (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=8193, d_x=1e-6, rho=1.0, h_x=1 / 8193), 1e-2),
     (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=1 << 20, d_x=1e-6, rho=1.0, h_x=2.0 ** -20), 1e-4),
     (P.ProblemDescriptor(P.KIND_REACTION_DIFFUSION_1D, nx=100003, d_x=1.0, rho=1.0, h_x=1e-5), 2e-8),
@@ -219,6 +219,20 @@ def test_restart_trend():
     e1 = np.abs(E.run_serial(s, E.RidcConfig(levels=4, steps=4000)).final_state - exact).max()
     e10 = np.abs(E.run_serial(s, E.RidcConfig(levels=4, steps=4000, restarts=10)).final_state - exact).max()
     assert e10 < e1
+
+
+@pytest.mark.parametrize("levels,restarts", [(1, 1), (4, 2)])
+def test_persistent_kernel_matches_tick_graph(levels, restarts, monkeypatch):
+    """The opt-in persistent run kernel (per-tile dependency flags) is bitwise
+    equal to the default graph of tick launches."""
+    s = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=1 << 15, t_end=0.004))
+    cfg = E.RidcConfig(levels=levels, steps=40, restarts=restarts)
+    ref = E.run_serial(s, cfg).final_state
+    monkeypatch.setenv("RIDC_PERSIST", "1")
+    with E.Engine(s, cfg) as eng:
+        assert eng.info["kernel_launches"] == 1
+        got = eng.run().final_state
+    assert np.array_equal(got, ref)
 
 
 def test_engine_info_and_launch_count():
