@@ -71,6 +71,8 @@ struct StepItem {
     double ca[kMaxNodes], cs[kMaxNodes], cn[kMaxNodes];
     double* out;
     double* out2;   // optional mirror (the consumer GPU's inbox slot, written over NVLink)
+    int vlev[kMaxNodes];          // ring (level) of node a   (tensor-map staging)
+    long long vslot[kMaxNodes];   // slot of node a in that ring
 };
 
 struct Aff { double A, B; };   // y -> A*y + B

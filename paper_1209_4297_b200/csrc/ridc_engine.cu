@@ -29,6 +29,7 @@
 #include "../../include/ridc_b200.h"
 #include "ridc_device.cuh"
 #include "ridc_tma.cuh"
+#include "ridc_chunk.cuh"
 
 using namespace ridc;
 
@@ -52,6 +53,8 @@ struct EngineParams {
     unsigned long long* err;
     double* mirror;            // pipeline: consumer's inbox ring (peer memory), or null
     long long mirror_cap, mirror_off;
+    ChunkLayout lay;           // padded row layout (ghost columns)
+    const ChunkGeo* cgeo;      // per-segment item geometry
 };
 
 struct TickParams {
@@ -60,10 +63,15 @@ struct TickParams {
     long long target[kMaxLevels];
 };
 
+__device__ __forceinline__ long long slot_index(const EngineParams& ep, int lev, long long s, long long off = -1)
+{
+    return ((off < 0 ? ep.off[lev] : off) + s) % ep.cap[lev];
+}
+
 __device__ __forceinline__ double* ring_slot(const EngineParams& ep, int lev, long long s,
                                              long long off = -1)
 {
-    return ep.ring[lev] + (((off < 0 ? ep.off[lev] : off) + s) % ep.cap[lev]) * ep.Vs;
+    return ep.ring[lev] + slot_index(ep, lev, s, off) * ep.Vs;
 }
 
 // Window assembly for (level j, target t): _window_span / _orient /
@@ -74,6 +82,8 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
     it.level = j;
     it.target = t;
     it.vec[0] = ring_slot(ep, j, t - 1, off);
+    it.vlev[0] = j;
+    it.vslot[0] = slot_index(ep, j, t - 1, off);
     it.ca[0] = 1.0;
     it.cs[0] = 0.0;
     it.cn[0] = ep.dt;
@@ -87,6 +97,8 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
         for (int a = 0; a <= j; ++a) {
             const long long s = steady ? t - a : a;
             it.vec[nn] = ring_slot(ep, j - 1, s, off);
+            it.vlev[nn] = j - 1;
+            it.vslot[nn] = slot_index(ep, j - 1, s, off);
             it.ca[nn] = 0.0;
             it.cs[nn] = w[a] - (a == i_new ? ep.dt : 0.0);
             it.cn[nn] = w[a] - (a == i_old ? ep.dt : 0.0);
@@ -99,20 +111,25 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
 }
 
 // The production tick kernel: persistent CTAs of NT compute threads; thread
-// 0 doubles as the TMA producer (ridc_tma.cuh).  Items of the tick are dealt
-// round-robin: item i -> level slot i % nact, tile i / nact.
-template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE>
-__global__ void __launch_bounds__(NT, 1) k_tick_tma(EngineParams ep, TickParams tp, int ipl)
+// 0 doubles as the TMA producer (ridc_chunk.cuh).  Items of the tick are
+// dealt round-robin: item i -> level slot i % nact, tile i / nact.
+template <int KIND, int NT, int ROWS, int NSTAGE>
+__global__ void __launch_bounds__(NT, 1)
+    k_tick_chunk(EngineParams ep, TickParams tp, int ipl, const __grid_constant__ TmapSet tm)
 {
-    using L = TmaSmem<NT, KMAX, ROWS, NSTAGE>;
-    extern __shared__ __align__(128) double sm[];
-    double* stage = sm;
-    double* sbuf = sm + L::OFF_SBUF;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+    using L = ChunkSmem<NT, ROWS, NSTAGE>;
+    extern __shared__ __align__(1024) char smraw[];
+    char* stage = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    double* edge = reinterpret_cast<double*>(stage + L::OFF_EDGE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(stage + L::OFF_BAR);
     uint64_t* empty = full + NSTAGE;
     __shared__ StepItem items[kMaxLevels];   // one descriptor per active level (shared by all its tiles)
     __shared__ Aff swarp[2 * (NT / 32) + 1];
     const int total = tp.nact * ipl;
+    const int nseg = ep.sv.nseg, ny = ep.pb.ny;
+    // programmatic dependent launch: let the next tick's grid get scheduled now;
+    // its CTAs run this prologue as SMs free up and wait (below) before reading
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x < tp.nact) build_item(ep, tp.level[threadIdx.x], tp.target[threadIdx.x], items[threadIdx.x]);
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
@@ -126,14 +143,21 @@ __global__ void __launch_bounds__(NT, 1) k_tick_tma(EngineParams ep, TickParams 
     LoadCursor pc{(int)blockIdx.x, 0, 0};
     auto issue_next = [&](int s) {
         const int slot = pc.i % tp.nact, tile = pc.i / tp.nact;
-        const Geo g = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
-        issue_node<ROWS, L::SROW>(ep.pb, ep.sv, items[slot].vec[pc.a], g, stage + (size_t)s * L::STAGE,
-                                  &full[s]);
-        if (++pc.a == items[slot].nnodes) { pc.a = 0; pc.i += gridDim.x; }
+        const int row = tile / nseg, seg = tile - row * nseg;
+        const StepItem& it = items[slot];
+        issue_chunk_node<NT, ROWS, NSTAGE>(tm, it.vlev[pc.a], it.vslot[pc.a], row, ny, ep.lay.gpr,
+                                           ep.lay.gdata, ep.cgeo[seg], stage + (size_t)s * L::STAGE,
+                                           &full[s]);
+        if (++pc.a == it.nnodes) { pc.a = 0; pc.i += gridDim.x; }
         ++pc.n;
     };
-    if (threadIdx.x == 0)
+    // every global read of ring data and every global write happens after the
+    // previous tick's grid completed: thread 0 waits before its first load,
+    // everyone else reads / writes only after that load's barrier
+    if (threadIdx.x == 0) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int k = 0; k < NSTAGE && pc.i < total; ++k) issue_next(k);
+    }
     // after load n was released from stage s: wait for every warp, then load n + NSTAGE into s
     auto refill = [&](long long n, int s) {
         if (pc.i >= total) return;
@@ -144,289 +168,39 @@ __global__ void __launch_bounds__(NT, 1) k_tick_tma(EngineParams ep, TickParams 
     int ino = 0;
     for (int i = blockIdx.x; i < total; i += gridDim.x, ++ino) {
         const int slot = i % tp.nact, tile = i / tp.nact;
-        Geo geo = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
-        geo.item_no = ino;
-        auto ensure = [](long long) {};
-        if (geo.fast)
-            consume_item<KIND, NT, KMAX, ROWS, NSTAGE, true>(ep.pb, ep.sv, items[slot], geo, stage, full,
-                                                            empty, n, refill, ensure, sbuf, swarp, ep.err);
-        else
-            consume_item<KIND, NT, KMAX, ROWS, NSTAGE, false>(ep.pb, ep.sv, items[slot], geo, stage,
-                                                             full, empty, n, refill, ensure, sbuf, swarp,
-                                                             ep.err);
-        csync<NT>();   // sbuf reuse by the next item
+        const int row = tile / nseg, seg = tile - row * nseg;
+        const ChunkGeo cg = ep.cgeo[seg];
+        switch (cg.mode) {
+        case 0:
+            chunk_item<KIND, NT, ROWS, NSTAGE, 0>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+                                                  full, empty, n, refill, swarp, ep.err, ino);
+            break;
+        case 1:
+            chunk_item<KIND, NT, ROWS, NSTAGE, 1>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+                                                  full, empty, n, refill, swarp, ep.err, ino);
+            break;
+        default:
+            chunk_item<KIND, NT, ROWS, NSTAGE, 2>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+                                                  full, empty, n, refill, swarp, ep.err, ino);
+        }
+        csync<NT>();   // edge / scan scratch reuse by the next item
     }
 }
 
-// ---------------------------------------------------------------- persistent run kernel
-//
-// One launch marches every interval and tick.  CTA b owns tiles b, b+G, ...
-// of every level.  Cross-CTA ordering uses one completion flag per (level,
-// tile): the last global step written (global step of (interval r, step t)
-// = r*(per+1) + t; step 0 of an interval is its seed).  Before level j
-// computes global step G of a tile, thread 0 acquires (engine.py:363-371):
-//   (a) own level, neighbour tiles  >= G-1        (halo of the previous state)
-//   (b) level j-1, neighbour tiles  >= G(hi)      (window, LevelBuffer.watermark)
-//   (c) level j+1, neighbour tiles  >= G - C_j + j + 1   (ring slot free, .released)
-// Every dependency is on an earlier tick and every CTA walks its items in
-// tick order, so co-resident CTAs cannot deadlock; a %globaltimer watchdog
-// still turns a stall into an error instead of a hang.
-struct PersistParams {
-    int ipl;                   // tiles per level
-    int rx;                    // neighbour radius in segments
-    int levels, restarts;
-    long long per;
-    long long* flags;          // [levels][ipl], init -1
-    const double* y0;
-    int* abort;
-    unsigned long long timeout_ns;
-};
-
-__device__ __forceinline__ long long ld_acquire(const long long* p)
+// state (plain [ny][nx]) -> slot 0 of every level ring, padded layout with ghosts
+// (engine.py:357-360: step 0 = initial data on every level)
+__global__ void k_seed_chunk(const double* __restrict__ src, EngineParams ep, long long off)
 {
-    long long v;
-    asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release(long long* p, long long v)
-{
-    asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned long long gtimer()
-{
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-// pointer of node a of (level j, step t) -- the same order build_item uses
-__device__ __forceinline__ const double* node_ptr(const EngineParams& ep, int j, long long t, int a,
-                                                  long long off)
-{
-    if (a == 0) return ring_slot(ep, j, t - 1, off);
-    const long long s = t >= j ? t - (a - 1) : (a - 1);
-    return ring_slot(ep, j - 1, s, off);
-}
-
-// Are the dependencies of (level j, global step G, tile) satisfied?
-template <int KIND>
-__device__ bool deps_ready(const EngineParams& ep, const PersistParams& pp, int j, long long t,
-                           long long G, long long Ghi, int tile)
-{
-    const int nseg = ep.sv.nseg, ny = ep.pb.ny;
-    constexpr bool periodic = KIND != BURGERS_1D;
-    const int row = tile / nseg, seg = tile - row * nseg;
-    const int r0 = ny > 1 ? -1 : 0, r1 = ny > 1 ? 1 : 0;
-    const int rx = nseg > 1 ? pp.rx : 0;
-    const long long capj = ep.cap[j];
-    bool ok = true;
-    for (int dr = r0; dr <= r1; ++dr) {
-        const int rr = (row + dr + ny) % ny;
-        for (int ds = -rx; ds <= rx; ++ds) {
-            int sg = seg + ds;
-            if (periodic) sg = (sg % nseg + nseg) % nseg;
-            else if (sg < 0 || sg >= nseg) continue;
-            const int tl = rr * nseg + sg;
-            ok &= ld_acquire(pp.flags + (size_t)j * pp.ipl + tl) >= G - 1;
-            if (j > 0 && t >= 1) ok &= ld_acquire(pp.flags + (size_t)(j - 1) * pp.ipl + tl) >= Ghi;
-            if (j < pp.levels - 1)
-                ok &= ld_acquire(pp.flags + (size_t)(j + 1) * pp.ipl + tl) >= G - capj + j + 1;
-        }
-    }
-    return ok;
-}
-
-template <int KIND>
-__device__ bool wait_deps(const EngineParams& ep, const PersistParams& pp, int j, long long t, long long G,
-                          long long Ghi, int tile)
-{
-    unsigned long long t0 = 0;
-    for (;;) {
-        if (deps_ready<KIND>(ep, pp, j, t, G, Ghi, tile)) {
-            asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
-            return true;
-        }
-        if (*(volatile int*)pp.abort) return false;
-        const unsigned long long now = gtimer();
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > pp.timeout_ns) {
-            atomicExch(pp.abort, 1);
-            return false;
-        }
-    }
-}
-
-
-struct PCursor {
-    int r;            // interval
-    long long k;      // tick
-    int j;            // level
-    int m;            // owned-tile ordinal
-    int a;            // node
-    long long n;      // load number
-    bool done;
-};
-
-template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE>
-__global__ void __launch_bounds__(NT, 1) k_persist(EngineParams ep0, PersistParams pp)
-{
-    using L = TmaSmem<NT, KMAX, ROWS, NSTAGE>;
-    extern __shared__ __align__(128) double sm[];
-    double* stage = sm;
-    double* sbuf = sm + L::OFF_SBUF;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-    uint64_t* empty = full + NSTAGE;
-    __shared__ StepItem items[2][kMaxLevels];
-    __shared__ Aff swarp[2 * (NT / 32) + 1];
-    __shared__ volatile int s_abort;
-    const int tid = threadIdx.x;
-    const int G = gridDim.x;
-    const int my_tiles = pp.ipl > (int)blockIdx.x ? (pp.ipl - 1 - (int)blockIdx.x) / G + 1 : 0;
-    const int top = pp.levels - 1;
-    const long long ticks = pp.per + (long long)top * (top + 1) / 2;
-    if (tid == 0) {
-        for (int i = 0; i < NSTAGE; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], NT / 32);
-        }
-        mbar_fence_init();
-        s_abort = 0;
-    }
-    __syncthreads();
-    if (my_tiles == 0) return;
-    const EngineParams& ep = ep0;
-
-    // ---- producer cursor (thread 0) over compute items: (r, k, j active, m, a)
-    auto delay = [](int j) { return (long long)j * (j + 1) / 2; };
-    auto active = [&](long long k, int j) { const long long t = k - delay(j); return t >= 1 && t <= pp.per; };
-    PCursor pc{0, 1, 0, 0, 0, 0, false};
-    auto first_level = [&](long long k, int from) {
-        for (int j = from; j <= top; ++j)
-            if (active(k, j)) return j;
-        return -1;
-    };
-    pc.j = first_level(1, 0);
-    auto advance_item = [&]() {
-        pc.a = 0;
-        if (++pc.m < my_tiles) return;
-        pc.m = 0;
-        int nj = first_level(pc.k, pc.j + 1);
-        while (nj < 0) {
-            if (++pc.k > ticks) {
-                pc.k = 1;
-                if (++pc.r >= pp.restarts) { pc.done = true; return; }
-            }
-            nj = first_level(pc.k, 0);
-        }
-        pc.j = nj;
-    };
-    const EngineParams& epp = ep0;
-    bool pc_ready = false;    // dependencies of the cursor's current item acquired
-    auto try_issue = [&](int s, bool blocking) -> bool {
-        if (pc.done) return false;
-        const long long poff = (long long)pc.r * (pp.per + 1);
-        const long long t = pc.k - delay(pc.j);
-        const int tile = (int)blockIdx.x + pc.m * G;
-        if (pc.a == 0 && !pc_ready) {
-            const long long Gs = (long long)pc.r * (pp.per + 1) + t;
-            const long long hi = pc.j > 0 ? (t < pc.j ? pc.j : t) : 0;
-            const long long Ghi = (long long)pc.r * (pp.per + 1) + hi;
-            if (blocking) {
-                if (!wait_deps<KIND>(epp, pp, pc.j, t, Gs, Ghi, tile)) return false;
-            } else if (!deps_ready<KIND>(epp, pp, pc.j, t, Gs, Ghi, tile)) {
-                return false;
-            } else {
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-            }
-            pc_ready = true;
-        }
-        const Geo g = make_geo<KIND, NT, KMAX>(epp.pb, epp.sv, tile);
-        issue_node<ROWS, L::SROW>(epp.pb, epp.sv, node_ptr(epp, pc.j, t, pc.a, poff), g,
-                                  stage + (size_t)s * L::STAGE, &full[s]);
-        const int nn = pc.j > 0 ? pc.j + 2 : 1;
-        ++pc.n;
-        if (++pc.a == nn) { pc_ready = false; advance_item(); }
-        return true;
-    };
-    // released load n from stage s: refill with load n + NSTAGE if ready (never blocks on peers)
-    auto refill = [&](long long n, int s) {
-        if (pc.done || pc.n != n + NSTAGE) return;
-        mbar_wait(&empty[s], (uint32_t)((n / NSTAGE) & 1));
-        try_issue(s, false);
-    };
-    // before consuming load n: make sure loads up to n are issued (may block on peers)
-    auto ensure = [&](long long n) {
-        while (pc.n <= n && !pc.done) {
-            const int s = (int)(pc.n % NSTAGE);
-            if (pc.n >= NSTAGE) mbar_wait(&empty[s], (uint32_t)(((pc.n - NSTAGE) / NSTAGE) & 1));
-            if (!try_issue(s, true)) {   // watchdog fired: release everyone waiting on this stage
-                s_abort = 1;
-                mbar_arrive_expect_tx(&full[s], 0);
-                return;
-            }
-        }
-    };
-
-    long long n = 0;
-    int ino = 0;
-    for (int r = 0; r < pp.restarts; ++r) {
-        const long long g0 = (long long)r * (pp.per + 1);   // ring offset of the interval
-        // ---- seeds: step 0 of every level = the interval's state0 (top-level final before)
-        const double* src = r == 0 ? pp.y0 : ring_slot(ep, top, pp.per, g0 - (pp.per + 1));
-        for (int j = 0; j <= top; ++j) {
-            for (int m = 0; m < my_tiles; ++m) {
-                const int tile = (int)blockIdx.x + m * G;
-                if (tid == 0 && !wait_deps<KIND>(ep, pp, j, 0, g0, 0, tile)) s_abort = 1;
-                csync<NT>();
-                if (s_abort) return;
-                const Geo g = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
-                const size_t base = (size_t)g.row * ep.pb.nx + g.c0;
-                double* dst = ring_slot(ep, j, 0, g0) + base;
-                for (int i = tid; i < g.tlen; i += NT) dst[i] = src[base + i];
-                csync<NT>();
-                if (tid == 0) {
-                    __threadfence();
-                    st_release(pp.flags + (size_t)j * pp.ipl + tile, g0);
-                }
-            }
-        }
-        // ---- ticks
-        for (long long k = 1; k <= ticks; ++k) {
-            int nact = 0;
-            for (int j = 0; j <= top; ++j)
-                if (active(k, j)) {
-                    if (tid == 0) build_item(ep, j, k - delay(j), items[k & 1][nact], g0);
-                    ++nact;
-                }
-            csync<NT>();
-            int slot = 0;
-            for (int j = 0; j <= top; ++j) {
-                if (!active(k, j)) continue;
-                const long long t = k - delay(j);
-                const StepItem& it = items[k & 1][slot++];
-                for (int m = 0; m < my_tiles; ++m, ++ino) {
-                    const int tile = (int)blockIdx.x + m * G;
-                    Geo geo = make_geo<KIND, NT, KMAX>(ep.pb, ep.sv, tile);
-                    geo.item_no = ino;
-                    if (geo.fast)
-                        consume_item<KIND, NT, KMAX, ROWS, NSTAGE, true>(ep.pb, ep.sv, it, geo, stage, full, empty, n,
-                                                                        refill, ensure, sbuf, swarp, ep.err,
-                                                                        &s_abort);
-                    else
-                        consume_item<KIND, NT, KMAX, ROWS, NSTAGE, false>(ep.pb, ep.sv, it, geo, stage, full, empty,
-                                                                         n, refill, ensure, sbuf, swarp, ep.err,
-                                                                         &s_abort);
-                    csync<NT>();
-                    if (s_abort) return;
-                    if (tid == 0) {
-                        __threadfence();
-                        st_release(pp.flags + (size_t)j * pp.ipl + tile, g0 + t);
-                    }
-                }
-            }
-        }
+    const int nx = ep.pb.nx, ny = ep.pb.ny, GW = ep.lay.GW, P = ep.lay.P;
+    const long long tot = (long long)ny * P;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / P), c = (int)(i - (long long)r * P) - GW;
+        double v = 0.0;
+        if (c >= 0 && c < nx) v = src[(size_t)r * nx + c];
+        else if (ep.pb.periodic && c >= -GW && c < nx + GW) v = src[(size_t)r * nx + ((c + nx) % nx)];
+        for (int j = 0; j < ep.levels; ++j)
+            if (ep.ring[j]) ring_slot(ep, j, 0, off)[i] = v;
     }
 }
 
@@ -437,17 +211,6 @@ __global__ void __launch_bounds__(NT) k_item(DevProblem pb, DevSolve sv, StepIte
     extern __shared__ double sbuf[];
     __shared__ Aff swarp[2 * (NT / 32) + 1];
     process_item<KIND, NT, KMAX>(pb, sv, it, blockIdx.x, sbuf, swarp, err);
-}
-
-// state0 -> slot 0 of every level ring (engine.py:357-360: step 0 = initial data)
-__global__ void k_seed(const double* __restrict__ src, EngineParams ep)
-{
-    const long long V = ep.V;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < V;
-         i += (long long)gridDim.x * blockDim.x) {
-        const double v = src[i];
-        for (int j = 0; j < ep.levels; ++j) ring_slot(ep, j, 0)[i] = v;
-    }
 }
 
 template <int KIND>
@@ -512,57 +275,58 @@ cudaError_t launch_item_t(int items, size_t smem, cudaStream_t st, const DevProb
      : (CFG).id == 1 ? FN<KIND, 256, 8>(__VA_ARGS__)                   \
                      : FN<KIND, 512, 8>(__VA_ARGS__))
 
-// ---- TMA tick kernel configurations (NT consumers x KMAX points, ROWS staged
-// rows per node, NSTAGE stages).  Many warps per SM hide the fp64 / shared
-// memory latencies of the scans; 1-D items are sized so one item per level
-// per CTA covers the line (see make_solve's balancing).
-struct TmaCfg {
+// ---- chunk tick kernel configurations (NT threads x 16 points, ROWS staged
+// rows per node, NSTAGE stages); many warps per SM hide the fp64 / shared
+// memory latencies of the scans.
+struct ChunkCfg {
     int id;
-    int nt, kmax, rows, nstage, cap;
+    int nt, rows, nstage;
     size_t smem;
 };
 
-template <int NT, int KMAX, int ROWS, int NSTAGE>
-TmaCfg tma_cfg_of(int id)
+#define RIDC_CHUNK_CONFIGS(X) \
+    X(0, 64, 1, 4)            \
+    X(1, 128, 1, 4)           \
+    X(2, 256, 1, 4)           \
+    X(3, 512, 1, 3)           \
+    X(4, 64, 3, 3)            \
+    X(5, 128, 3, 3)           \
+    X(6, 256, 3, 2)
+
+template <int NT, int ROWS, int NSTAGE>
+ChunkCfg chunk_cfg_of(int id)
 {
-    TmaCfg c;
+    ChunkCfg c;
     c.id = id;
     c.nt = NT;
-    c.kmax = KMAX;
     c.rows = ROWS;
     c.nstage = NSTAGE;
-    c.cap = NT * KMAX;
-    c.smem = TmaSmem<NT, KMAX, ROWS, NSTAGE>::BYTES;
+    c.smem = ChunkSmem<NT, ROWS, NSTAGE>::BYTES + 1024;   // + 1 KiB for the 1024-B alignment
     return c;
 }
 
-#define RIDC_TMA_CONFIGS(X)        \
-    X(0, 128, 8, 1, 4)             \
-    X(1, 256, 8, 1, 4)             \
-    X(2, 512, 8, 1, 3)             \
-    X(3, 1024, 8, 1, 2)            \
-    X(4, 256, 4, 3, 3)             \
-    X(5, 512, 4, 3, 3)             \
-    X(6, 512, 16, 1, 2)
-
-TmaCfg pick_tma(int kind, int Q)
+// smallest config whose NT*16 points cover `points` (the item's staged range)
+ChunkCfg pick_chunk(int kind, int points)
 {
     const bool two_d = kind == ADV_DIFF_2D || kind == RD_2D;
-    if (two_d) return Q <= 1024 ? tma_cfg_of<256, 4, 3, 3>(4) : tma_cfg_of<512, 4, 3, 3>(5);
-    if (Q <= 1024) return tma_cfg_of<128, 8, 1, 4>(0);
-    if (Q <= 2048) return tma_cfg_of<256, 8, 1, 4>(1);
-    if (Q <= 4096) return tma_cfg_of<512, 8, 1, 3>(2);
-    if (getenv("RIDC_CFG1024")) return tma_cfg_of<1024, 8, 1, 2>(3);
-    return tma_cfg_of<512, 16, 1, 2>(6);
+    if (two_d) {
+        if (points <= 64 * 16) return chunk_cfg_of<64, 3, 3>(4);
+        if (points <= 128 * 16) return chunk_cfg_of<128, 3, 3>(5);
+        return chunk_cfg_of<256, 3, 2>(6);
+    }
+    if (points <= 64 * 16) return chunk_cfg_of<64, 1, 4>(0);
+    if (points <= 128 * 16) return chunk_cfg_of<128, 1, 4>(1);
+    if (points <= 256 * 16) return chunk_cfg_of<256, 1, 4>(2);
+    return chunk_cfg_of<512, 1, 3>(3);
 }
 
-int tma_cap(int kind) { return (kind == ADV_DIFF_2D || kind == RD_2D) ? 2048 : 8192; }
+int chunk_points_max(int kind) { return (kind == ADV_DIFF_2D || kind == RD_2D) ? 256 * 16 : 512 * 16; }
 
-template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE>
-cudaError_t launch_tma_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
-                         const TickParams& tp, int ipl)
+template <int KIND, int NT, int ROWS, int NSTAGE>
+cudaError_t launch_chunk_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
+                           const TickParams& tp, int ipl, const TmapSet& tm)
 {
-    auto kfn = k_tick_tma<KIND, NT, KMAX, ROWS, NSTAGE>;
+    auto kfn = k_tick_chunk<KIND, NT, ROWS, NSTAGE>;
     static bool attr[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -572,92 +336,43 @@ cudaError_t launch_tma_t(int grid, size_t smem, cudaStream_t st, const EnginePar
         if (e != cudaSuccess) return e;
         attr[dev] = true;
     }
-    kfn<<<grid, NT, smem, st>>>(ep, tp, ipl);
-    return cudaGetLastError();
-}
-
-template <int KIND>
-cudaError_t launch_tma_k(const TmaCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
-                         const TickParams& tp, int ipl)
-{
-    constexpr bool two_d = KIND == ADV_DIFF_2D || KIND == RD_2D;
-#define RIDC_TMA_CASE(ID, NT, KMAX, ROWS, NSTAGE)                                      \
-    if (c.id == ID && two_d == (ROWS == 3)) {                                          \
-        if constexpr (two_d == (ROWS == 3))                                            \
-            return launch_tma_t<KIND, NT, KMAX, ROWS, NSTAGE>(grid, c.smem, st, ep, tp, ipl); \
-    }
-    RIDC_TMA_CONFIGS(RIDC_TMA_CASE)
-#undef RIDC_TMA_CASE
-    return cudaErrorInvalidValue;
-}
-
-template <int KIND, int NT, int KMAX, int ROWS, int NSTAGE>
-cudaError_t launch_persist_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
-                             const PersistParams& pp)
-{
-    auto kfn = k_persist<KIND, NT, KMAX, ROWS, NSTAGE>;
-    static bool attr[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    if (!attr[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr[dev] = true;
-    }
-    // cooperative: every CTA co-resident (the flag protocol needs it), else the launch fails
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kfn, ep, pp);
+    return cudaLaunchKernelEx(&cfg, kfn, ep, tp, ipl, tm);
 }
 
 template <int KIND>
-cudaError_t launch_persist_k(const TmaCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
-                             const PersistParams& pp)
+cudaError_t launch_chunk_k(const ChunkCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
+                           const TickParams& tp, int ipl, const TmapSet& tm)
 {
     constexpr bool two_d = KIND == ADV_DIFF_2D || KIND == RD_2D;
-#define RIDC_PERSIST_CASE(ID, NT, KMAX, ROWS, NSTAGE)                                  \
-    if (c.id == ID && two_d == (ROWS == 3)) {                                          \
-        if constexpr (two_d == (ROWS == 3))                                            \
-            return launch_persist_t<KIND, NT, KMAX, ROWS, NSTAGE>(grid, c.smem, st, ep, pp); \
+#define RIDC_CHUNK_CASE(ID, NT, ROWS, NSTAGE)                                                  \
+    if (c.id == ID && two_d == (ROWS == 3)) {                                                  \
+        if constexpr (two_d == (ROWS == 3))                                                    \
+            return launch_chunk_t<KIND, NT, ROWS, NSTAGE>(grid, c.smem, st, ep, tp, ipl, tm);  \
     }
-    RIDC_TMA_CONFIGS(RIDC_PERSIST_CASE)
-#undef RIDC_PERSIST_CASE
+    RIDC_CHUNK_CONFIGS(RIDC_CHUNK_CASE)
+#undef RIDC_CHUNK_CASE
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_persist(int kind, const TmaCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
-                           const PersistParams& pp)
+cudaError_t launch_chunk(int kind, const ChunkCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
+                         const TickParams& tp, int ipl, const TmapSet& tm)
 {
     switch (kind) {
-    case ADV_DIFF_1D: return launch_persist_k<ADV_DIFF_1D>(c, grid, st, ep, pp);
-    case BURGERS_1D: return launch_persist_k<BURGERS_1D>(c, grid, st, ep, pp);
-    case RD_1D: return launch_persist_k<RD_1D>(c, grid, st, ep, pp);
-    case ADV_DIFF_2D: return launch_persist_k<ADV_DIFF_2D>(c, grid, st, ep, pp);
-    case RD_2D: return launch_persist_k<RD_2D>(c, grid, st, ep, pp);
-    }
-    return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_tma(int kind, const TmaCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
-                       const TickParams& tp, int ipl)
-{
-    const bool two_d = kind == ADV_DIFF_2D || kind == RD_2D;
-    if (two_d != (c.rows == 3)) return cudaErrorInvalidValue;
-    switch (kind) {
-    case ADV_DIFF_1D: return launch_tma_k<ADV_DIFF_1D>(c, grid, st, ep, tp, ipl);
-    case BURGERS_1D: return launch_tma_k<BURGERS_1D>(c, grid, st, ep, tp, ipl);
-    case RD_1D: return launch_tma_k<RD_1D>(c, grid, st, ep, tp, ipl);
-    case ADV_DIFF_2D: return launch_tma_k<ADV_DIFF_2D>(c, grid, st, ep, tp, ipl);
-    case RD_2D: return launch_tma_k<RD_2D>(c, grid, st, ep, tp, ipl);
+    case ADV_DIFF_1D: return launch_chunk_k<ADV_DIFF_1D>(c, grid, st, ep, tp, ipl, tm);
+    case BURGERS_1D: return launch_chunk_k<BURGERS_1D>(c, grid, st, ep, tp, ipl, tm);
+    case RD_1D: return launch_chunk_k<RD_1D>(c, grid, st, ep, tp, ipl, tm);
+    case ADV_DIFF_2D: return launch_chunk_k<ADV_DIFF_2D>(c, grid, st, ep, tp, ipl, tm);
+    case RD_2D: return launch_chunk_k<RD_2D>(c, grid, st, ep, tp, ipl, tm);
     }
     return cudaErrorInvalidValue;
 }
@@ -742,116 +457,17 @@ DevProblem make_problem(const ridc_problem* p)
 struct SolveSetup {
     DevSolve sv;
     std::vector<double> tab;   // [m_0..m_{n-1}, g_0..g_{n-1}]
-    std::vector<PlanRow> plans;  // TMA staging plans [nseg][row parity]
-    double r;
+    double r = 0;
     LaunchCfg cfg;             // register-path (single-op) launch
-    TmaCfg tcfg;               // TMA tick-kernel launch (engine)
+    // engine (chunk layout)
+    ChunkCfg ccfg;
+    ChunkLayout lay;
+    std::vector<ChunkGeo> cgeo;
     std::string err;
 };
 
-// Host mirror of make_geo (ridc_device.cuh) for one segment.
-void seg_range(const DevProblem& pb, const DevSolve& sv, int seg, int& cf, int& Q)
-{
-    const int nx = pb.nx;
-    const int c0 = seg * sv.tile;
-    const int tlen = std::min(sv.tile, nx - c0);
-    int s0, S;
-    if (sv.nseg == 1) { s0 = 0; S = nx; }
-    else if (pb.periodic) { s0 = c0 - sv.halo; S = tlen + 2 * sv.halo; }
-    else {
-        s0 = std::max(c0 - sv.halo, 0);
-        S = std::min(c0 + tlen + sv.halo, nx) - s0;
-    }
-    cf = s0 - 1;
-    Q = S + 2;
-}
-
-// Staging plan of one row-segment (see PlanRow in ridc_tma.cuh): aligned
-// bulk runs for the TMA engine, the rest as consumer fills.
-PlanRow make_plan_host(const DevProblem& pb, int cf, int Q, int par)
-{
-    const int nx = pb.nx;
-    struct Run { int q0, c0, n; };
-    std::vector<Run> runs;
-    std::vector<std::pair<int, int>> fills;   // [q0, q1)
-    int q = 0;
-    while (q < Q) {
-        const int c = cf + q;
-        if (!pb.periodic && (c < 0 || c >= nx)) {   // Dirichlet ghost
-            fills.push_back({q, q + 1});
-            ++q;
-            continue;
-        }
-        const int cc = pb.periodic ? ((c % nx) + nx) % nx : c;
-        const int n = std::min(Q - q, nx - cc);
-        runs.push_back({q, cc, n});
-        q += n;
-    }
-    PlanRow pl;
-    memset(&pl, 0, sizeof pl);
-    int best = 0;
-    for (int k = 1; k < (int)runs.size(); ++k)
-        if (runs[k].n > runs[best].n) best = k;
-    pl.sigma = runs.empty() ? 0 : ((par + runs[best].c0 - runs[best].q0) & 1);
-    const bool single = runs.size() == 1 && runs[0].q0 == 0 && runs[0].n == Q;
-    bool overflow = runs.size() > (size_t)kMaxBulk;
-    for (const Run& r : runs) {
-        const int dpar = (pl.sigma + r.q0) & 1, spar = (par + r.c0) & 1;
-        if (dpar != spar || overflow) { fills.push_back({r.q0, r.q0 + r.n}); continue; }
-        int q0, col, n;
-        if (single) {
-            const int h = (pl.sigma + r.q0) & 1;
-            q0 = r.q0 - h; col = r.c0 - h; n = r.n + h; n += n & 1;
-        } else {
-            const int h = (pl.sigma + r.q0) & 1;
-            q0 = r.q0 + h; col = r.c0 + h; n = r.n - h; n -= n & 1;
-            if (n <= 0) { fills.push_back({r.q0, r.q0 + r.n}); continue; }
-            if (q0 > r.q0) fills.push_back({r.q0, q0});
-            if (q0 + n < r.q0 + r.n) fills.push_back({q0 + n, r.q0 + r.n});
-        }
-        pl.bq0[pl.nb] = q0;
-        pl.bcol[pl.nb] = col;
-        pl.bn[pl.nb] = n;
-        pl.bytes += n * 8;
-        ++pl.nb;
-    }
-    std::sort(fills.begin(), fills.end());
-    std::vector<std::pair<int, int>> merged;
-    for (auto& f : fills) {
-        if (!merged.empty() && merged.back().second >= f.first)
-            merged.back().second = std::max(merged.back().second, f.second);
-        else
-            merged.push_back(f);
-    }
-    if (merged.size() > (size_t)kMaxFill) {   // degenerate: consumers stage everything
-        pl.nb = 0;
-        pl.bytes = 0;
-        merged.assign(1, {0, Q});
-    }
-    pl.nf = (int)merged.size();
-    for (int f = 0; f < pl.nf; ++f) {
-        pl.fq0[f] = merged[f].first;
-        pl.fn[f] = merged[f].second - merged[f].first;
-    }
-    return pl;
-}
-
-void build_plans(const DevProblem& pb, SolveSetup& ss)
-{
-    ss.plans.clear();
-    for (int seg = 0; seg < ss.sv.nseg; ++seg) {
-        int cf, Q;
-        seg_range(pb, ss.sv, seg, cf, Q);
-        for (int par = 0; par < 2; ++par) ss.plans.push_back(make_plan_host(pb, cf, Q, par));
-    }
-}
-
-// Factors + tiling.  cap: largest item range (positions incl. 2 stencil
-// neighbours) the chosen kernel holds; balance_items > 0 asks for the
-// segment count that best balances `balance_items` items-per-segment over
-// `nsm` persistent CTAs (engine), 0 for the minimal count (single ops).
-int make_solve(const DevProblem& pb, double coeff, int cap, int balance_items, int nsm,
-               SolveSetup& ss)
+// Factors of (I - coeff * cdx * D_xx): limits, Dirichlet pivot tables, carry powers.
+void make_factors(const DevProblem& pb, double coeff, SolveSetup& ss)
 {
     const double r = coeff * pb.cdx;
     ss.r = r;
@@ -861,6 +477,7 @@ int make_solve(const DevProblem& pb, double coeff, int cap, int balance_items, i
     const double s = std::sqrt(1.0 + 4.0 * r);
     sv.lam = 2.0 * r / (b + s);
     sv.g = 2.0 / (b + s);
+    ss.tab.clear();
     if (!pb.periodic) {
         // Thomas pivots den_i = b - r^2/den_{i-1} converge geometrically;
         // keep the exact prefix, then the fixed point.
@@ -891,53 +508,138 @@ int make_solve(const DevProblem& pb, double coeff, int cap, int balance_items, i
         for (int e = 0; e < K; ++e) {
             double acc = 0.0;
             for (int k = K - 1; k >= e; --k) acc = acc * sv.lam + sv.pw[k];
-            zf[e] = acc;   // Horner in lam over k: sum lam^(k-e) * lam^(k+1)
+            zf[e] = acc;
         }
     };
     fill_zf(sv.zf4, 4);
     fill_zf(sv.zf8, 8);
     fill_zf(sv.zf16, 16);
+}
+
+// truncation halo: lam^H <= 2^-60 relative to the recurrence magnitude
+int halo_of(double lam)
+{
+    return lam > 0.0 ? (int)std::ceil(60.0 * std::log(2.0) / -std::log(lam)) + 1 : 0;
+}
+
+// Register-path tiling for the single operators (ridc_op_*): whole lines up
+// to kCap-2 points, else truncated segments.
+int make_solve(const DevProblem& pb, double coeff, int cap, int /*balance_items*/, int /*nsm*/,
+               SolveSetup& ss)
+{
+    make_factors(pb, coeff, ss);
+    DevSolve& sv = ss.sv;
     if (pb.nx + 2 <= cap) {
         sv.nseg = 1;
         sv.tile = pb.nx;
         sv.halo = 0;
         ss.cfg = pick_cfg(pb.nx + 2);
-        ss.tcfg = pick_tma(pb.kind, pb.nx + 2);
-        build_plans(pb, ss);
         return RIDC_OK;
     }
-    // truncated halo: lam^H <= 2^-60 relative to the recurrence magnitude
-    int H = 0;
-    if (sv.lam > 0.0) H = (int)std::ceil(60.0 * std::log(2.0) / -std::log(sv.lam)) + 1;
+    const int H = halo_of(sv.lam);
     const int Tmax = cap - 2 - 2 * H;
     if (Tmax < 256) {
         char buf[256];
         snprintf(buf, sizeof buf,
                  "stiffness r=%.4g needs a truncation halo of %d points; the segmented "
                  "line solve supports at most %d (use fewer points or a smaller dt)",
-                 r, H, (cap - 2 - 256) / 2);
+                 ss.r, H, (cap - 2 - 256) / 2);
         ss.err = buf;
         return RIDC_E_CONFIG;
     }
-    const int n0 = (pb.nx + Tmax - 1) / Tmax;
-    int nbest = n0;
-    if (balance_items > 0 && nsm > 0) {
-        // minimise the per-CTA positions of the busiest CTA (+ a fixed per-item cost)
+    sv.halo = H;
+    sv.tile = Tmax;
+    sv.nseg = (pb.nx + Tmax - 1) / Tmax;
+    sv.tile = (pb.nx + sv.nseg - 1) / sv.nseg;
+    ss.cfg = pick_cfg(cap);
+    return RIDC_OK;
+}
+
+int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// Engine tiling in chunk layout (ridc_chunk.cuh).  Tiling depends only on
+// the problem and dt (never on levels or devices), so every level computes
+// bitwise the same states on one GPU and in the multi-GPU pipeline.
+// Segment count balances `items_per_row_set` x nseg items over nsm CTAs.
+int make_chunk_solve(const DevProblem& pb, double coeff, int nsm, SolveSetup& ss)
+{
+    make_factors(pb, coeff, ss);
+    DevSolve& sv = ss.sv;
+    const int nx = pb.nx;
+    const int pmax = chunk_points_max(pb.kind);
+    const bool whole = ((nx + 15) / 16) * 16 <= pmax;
+    int H = 0, nseg = 1, T = nx;
+    if (!whole) {
+        H = halo_of(sv.lam);
+        const int Tmax = pmax - 2 * H - 2 - 32;   // group alignment slack
+        if (Tmax < 256) {
+            char buf[256];
+            snprintf(buf, sizeof buf,
+                     "stiffness r=%.4g needs a truncation halo of %d points; the segmented "
+                     "line solve supports at most %d (use fewer points or a smaller dt)",
+                     ss.r, H, (pmax - 2 - 32 - 256) / 2);
+            ss.err = buf;
+            return RIDC_E_CONFIG;
+        }
+        const int n0 = (nx + Tmax - 1) / Tmax;
+        int nbest = n0;
         long long best = LLONG_MAX;
         for (int n = n0; n <= 4 * n0; ++n) {
-            const int T = (pb.nx + n - 1) / n;
-            const long long items = (long long)balance_items * n;
+            const int Tn = (nx + n - 1) / n;
+            const long long items = (long long)pb.ny * n;
             const long long per = (items + nsm - 1) / nsm;
-            const long long cost = per * (T + 2LL * H + 2 + 512);
+            const long long cost = per * (Tn + 2LL * H + 2 + 512);
             if (cost < best) { best = cost; nbest = n; }
         }
+        T = (nx + nbest - 1) / nbest;
+        nseg = (nx + T - 1) / T;
     }
     sv.halo = H;
-    sv.tile = (pb.nx + nbest - 1) / nbest;
-    sv.nseg = (pb.nx + sv.tile - 1) / sv.tile;
-    ss.cfg = pick_cfg(cap);
-    ss.tcfg = pick_tma(pb.kind, cap);
-    build_plans(pb, ss);
+    sv.tile = T;
+    sv.nseg = nseg;
+    // ghost columns: periodic segments read up to H+1 (+15 alignment) beyond the line
+    const int GW = whole ? 16 : 16 * ((H + 1 + 15 + 15) / 16);
+    if (!whole && GW > nx) {
+        ss.err = "truncation halo longer than the line";
+        return RIDC_E_CONFIG;
+    }
+    ss.lay.GW = GW;
+    ss.lay.P = 16 * ((nx + 2 * GW + 15) / 16);
+    ss.lay.gpr = ss.lay.P / 16;
+    ss.lay.gdata = GW / 16;
+    ss.cgeo.clear();
+    int maxng = 0;
+    for (int seg = 0; seg < nseg; ++seg) {
+        ChunkGeo cg;
+        cg.c0 = seg * T;
+        cg.tlen = std::min(T, nx - cg.c0);
+        if (whole) {
+            cg.g0 = 0;
+            cg.ng = (nx + 15) / 16;
+            cg.s_end = nx;
+            cg.mode = pb.periodic ? 1 : 2;
+        } else {
+            int lo = cg.c0 - H - 1, hi = cg.c0 + cg.tlen + H + 1;
+            bool exact_l = false, exact_r = false;
+            if (!pb.periodic) {
+                if (lo <= 0) { lo = 0; exact_l = true; }
+                if (hi >= nx) { hi = nx; exact_r = true; }
+            }
+            cg.g0 = floor_div(lo, 16);
+            const int g1 = floor_div(hi + 15, 16);
+            cg.ng = g1 - cg.g0;
+            cg.s_end = exact_r ? nx - 16 * cg.g0 : 16 * cg.ng;
+            const bool in_tab = sv.ntab > 0 && 16 * cg.g0 < sv.ntab;
+            cg.mode = (exact_l || exact_r || in_tab) ? 2 : 0;
+        }
+        maxng = std::max(maxng, cg.ng);
+        ss.cgeo.push_back(cg);
+    }
+    ss.ccfg = pick_chunk(pb.kind, 16 * maxng);
+    if (maxng > ss.ccfg.nt) {
+        ss.err = "internal: item larger than the chunk kernel";
+        return RIDC_E_CONFIG;
+    }
     return RIDC_OK;
 }
 
@@ -955,28 +657,24 @@ struct ridc_ctx {
     int levels = 0, restarts = 0;
     long long steps = 0, per = 0, ticks = 0;
     uint32_t flags = 0;
-    long long V = 0;
+    long long V = 0;           // points per state
+    long long Vs = 0;          // ring slot stride: ny padded rows of P doubles
+    int nsm = 148;             // CTAs per tick launch
     double* d_weights = nullptr;
     double* d_tab = nullptr;
-    PlanRow* d_plans = nullptr;
+    ChunkGeo* d_cgeo = nullptr;
     long long* d_dbg = nullptr;
     double* d_ring[kMaxLevels] = {};
     long long cap[kMaxLevels] = {};
     double* d_y0 = nullptr;
     unsigned long long* d_err = nullptr;
     EngineParams ep;
+    TmapSet tm;
     std::vector<int> steady_off, startup_off;
     cudaGraphExec_t gexec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
     long long ring_vectors = 0;
-    long long Vs = 0;          // ring slot stride (doubles)
-    int nsm = 148;             // persistent CTAs per tick launch
-    bool persistent = false;   // one k_persist launch per run (else a graph of tick launches)
-    long long* d_flags = nullptr;
-    int* d_abort = nullptr;
-    PersistParams pp;
-    double* d_ring_base[kMaxLevels] = {};
     std::string err;
 };
 
@@ -995,12 +693,67 @@ void weight_offsets(int L, std::vector<int>& st, std::vector<int>& su, long long
     total = off;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*PfnEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+PfnEncodeTiled encode_tiled()
+{
+    static PfnEncodeTiled f = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (PfnEncodeTiled) nullptr;
+        return reinterpret_cast<PfnEncodeTiled>(p);
+    }();
+    return f;
+}
+
+// A ring of `cap` slots as a 3-D tensor {16 doubles, Vs/16 groups, cap slots},
+// boxes of BR groups, 128-byte swizzle (ridc_chunk.cuh).
+int make_ring_map(CUtensorMap* map, double* base, long long Vs, long long cap, int nt, std::string* err)
+{
+    PfnEncodeTiled enc = encode_tiled();
+    if (!enc) return fail(err, RIDC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const int BR = nt < 256 ? nt : 256;
+    cuuint64_t dims[3] = {16, (cuuint64_t)(Vs / 16), (cuuint64_t)cap};
+    cuuint64_t strides[2] = {128, (cuuint64_t)Vs * 8};
+    cuuint32_t box[3] = {16, (cuuint32_t)BR, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[96];
+        snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return fail(err, RIDC_E_CUDA, buf);
+    }
+    return RIDC_OK;
+}
+
 EngineParams interval_params(ridc_ctx* c, int interval)
 {
     EngineParams ep = c->ep;
-    for (int j = 0; j < c->levels; ++j) ep.off[j] = c->persistent ? (long long)interval * (c->per + 1) : 0;
+    for (int j = 0; j < c->levels; ++j) ep.off[j] = 0;
     if (c->flags & RIDC_RECORD_TRAJECTORY) ep.off[c->levels - 1] = (long long)interval * c->per;
     return ep;
+}
+
+const double* final_slot(ridc_ctx* c, int level)
+{
+    EngineParams ep = interval_params(c, c->restarts - 1);
+    return ep.ring[level] + ((ep.off[level] + c->per) % ep.cap[level]) * c->Vs;
+}
+
+// padded ring slot -> plain [ny][nx]
+cudaError_t copy_out(ridc_ctx* c, double* dst, const double* slot, cudaMemcpyKind kind, long long nslots = 1)
+{
+    const ChunkLayout& L = c->ss.lay;
+    return cudaMemcpy2DAsync(dst, (size_t)c->pb.nx * sizeof(double), slot + L.GW, (size_t)L.P * sizeof(double),
+                             (size_t)c->pb.nx * sizeof(double), (size_t)c->pb.ny * nslots, kind, c->stream);
 }
 
 // Capture the whole run: per interval one seed + one launch per tick.
@@ -1014,16 +767,24 @@ int capture_graph(ridc_ctx* c)
     cudaError_t le = cudaSuccess;
     for (int r = 0; r < c->restarts && le == cudaSuccess; ++r) {
         EngineParams ep = interval_params(c, r);
-        const double* src = c->d_y0;
-        if (r > 0) {
+        if (r == 0) {
+            const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
+            k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
+            le = cudaGetLastError();
+            ++launches;
+        } else {
+            // next interval's state0 = the top level's final: plain copy through d_y0
             EngineParams prev = interval_params(c, r - 1);
             const int top = L - 1;
-            src = prev.ring[top] + ((prev.off[top] + c->per) % prev.cap[top]) * c->Vs;
+            const double* src = prev.ring[top] + ((prev.off[top] + c->per) % prev.cap[top]) * c->Vs;
+            le = copy_out(c, c->d_y0 + c->V, src, cudaMemcpyDeviceToDevice);
+            const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
+            if (le == cudaSuccess) {
+                k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0 + c->V, ep, -1);
+                le = cudaGetLastError();
+            }
+            ++launches;
         }
-        int sb = (int)std::min<long long>((c->V + 255) / 256, 148 * 8);
-        k_seed<<<sb, 256, 0, c->stream>>>(src, ep);
-        le = cudaGetLastError();
-        ++launches;
         for (long long k = 1; k <= c->ticks && le == cudaSuccess; ++k) {
             TickParams tp;
             memset(&tp, 0, sizeof tp);
@@ -1036,8 +797,8 @@ int capture_graph(ridc_ctx* c)
                 }
             }
             if (tp.nact == 0) continue;
-            le = launch_tma(c->pb.kind, c->ss.tcfg, std::min(c->nsm, tp.nact * items), c->stream, ep,
-                            tp, items);
+            le = launch_chunk(c->pb.kind, c->ss.ccfg, std::min(c->nsm, tp.nact * items), c->stream, ep, tp,
+                              items, c->tm);
             ++launches;
         }
     }
@@ -1072,36 +833,16 @@ int check_err_word(ridc_ctx* c)
 int march(ridc_ctx* c, double* wall_seconds)
 {
     CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
-    if (c->persistent) {
-        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0xff,
-                                          sizeof(long long) * c->levels * c->pp.ipl, c->stream));
-        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_abort, 0, sizeof(int), c->stream));
-    }
     CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
-    if (c->persistent)
-        CUDA_TRY(&c->err, launch_persist(c->pb.kind, c->ss.tcfg, std::min(c->nsm, c->pp.ipl), c->stream,
-                                         interval_params(c, 0), c->pp));
-    else
-        CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
+    CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
     CUDA_TRY(&c->err, cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(&c->err, cudaEventSynchronize(c->ev1));
-    if (c->persistent) {
-        int ab = 0;
-        CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_abort, sizeof ab, cudaMemcpyDeviceToHost));
-        if (ab) return fail(&c->err, RIDC_E_PROTOCOL, "tile pipeline made no progress within the watchdog");
-    }
     if (wall_seconds) {
         float ms = 0.f;
         CUDA_TRY(&c->err, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         *wall_seconds = ms * 1e-3;
     }
     return check_err_word(c);
-}
-
-const double* final_slot(ridc_ctx* c, int level)
-{
-    EngineParams ep = interval_params(c, c->restarts - 1);
-    return ep.ring[level] + ((ep.off[level] + c->per) % ep.cap[level]) * c->Vs;
 }
 
 }  // namespace
@@ -1148,7 +889,6 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     c->ticks = per + delay(levels - 1);
     c->flags = flags;
     c->V = (long long)problem->nx * problem->ny;
-    c->Vs = ((c->V + 1) & ~1LL) + 4;
     c->dt = (t_end - t_start) / (double)steps;   // engine.py:468 global dt
     c->steady_off = st;
     c->startup_off = su;
@@ -1164,13 +904,11 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     }
     if (cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
         c->nsm = 148;
-    // tiling depends only on the problem and dt (not on levels or devices): the
-    // one-level-per-GPU pipeline then reproduces these states bitwise
-    if ((rc = make_solve(c->pb, c->dt, tma_cap(c->pb.kind), c->pb.ny, c->nsm, c->ss)) !=
-        RIDC_OK) {
+    if ((rc = make_chunk_solve(c->pb, c->dt, c->nsm, c->ss)) != RIDC_OK) {
         c->err = c->ss.err;
         return bail(rc);
     }
+    c->Vs = (long long)c->pb.ny * c->ss.lay.P;
 #define CTX_TRY(expr)                                                                        \
     do {                                                                                     \
         cudaError_t _e = (expr);                                                             \
@@ -1182,7 +920,6 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     CTX_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CTX_TRY(cudaEventCreate(&c->ev0));
     CTX_TRY(cudaEventCreate(&c->ev1));
-    const size_t vb = (size_t)c->V * sizeof(double);
     CTX_TRY(cudaMalloc(&c->d_weights, std::max<long long>(wtotal, 1) * sizeof(double)));
     if (wtotal > 0)
         CTX_TRY(cudaMemcpy(c->d_weights, weights, wtotal * sizeof(double), cudaMemcpyHostToDevice));
@@ -1193,27 +930,28 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         c->ss.sv.tab_m = c->d_tab;
         c->ss.sv.tab_g = c->d_tab + c->ss.sv.ntab;
     }
-    CTX_TRY(cudaMalloc(&c->d_plans, c->ss.plans.size() * sizeof(PlanRow)));
-    CTX_TRY(cudaMemcpy(c->d_plans, c->ss.plans.data(), c->ss.plans.size() * sizeof(PlanRow),
+    CTX_TRY(cudaMalloc(&c->d_cgeo, c->ss.cgeo.size() * sizeof(ChunkGeo)));
+    CTX_TRY(cudaMemcpy(c->d_cgeo, c->ss.cgeo.data(), c->ss.cgeo.size() * sizeof(ChunkGeo),
                        cudaMemcpyHostToDevice));
-    c->ss.sv.plans = c->d_plans;
     if (getenv("RIDC_PHASE_TIMING") && atoi(getenv("RIDC_PHASE_TIMING")) > 0) {
         CTX_TRY(cudaMalloc(&c->d_dbg, 128 * sizeof(long long)));
         CTX_TRY(cudaMemset(c->d_dbg, 0, 128 * sizeof(long long)));
         c->ss.sv.dbg = c->d_dbg;
     }
+    memset(&c->tm, 0, sizeof c->tm);
     for (int j = 0; j < levels; ++j) {
         const bool top = j == levels - 1;
         long long cap = top ? 2 : 2LL * j + 3;
         if (top && (flags & RIDC_RECORD_TRAJECTORY)) cap = steps + 1;
         c->cap[j] = cap;
         c->ring_vectors += cap;
-        // slot stride Vs (even) keeps every slot 16-byte aligned for the bulk
-        // copies; 2 guard doubles before slot 0 and >= 4 after each state
-        CTX_TRY(cudaMalloc(&c->d_ring_base[j], ((size_t)cap * c->Vs + 4) * sizeof(double)));
-        c->d_ring[j] = c->d_ring_base[j] + 2;
+        // ny padded rows per slot; zeroed once: Dirichlet ghosts stay 0 forever
+        CTX_TRY(cudaMalloc(&c->d_ring[j], (size_t)cap * c->Vs * sizeof(double)));
+        CTX_TRY(cudaMemset(c->d_ring[j], 0, (size_t)cap * c->Vs * sizeof(double)));
+        if ((rc = make_ring_map(&c->tm.map[j], c->d_ring[j], c->Vs, cap, c->ss.ccfg.nt, &c->err)) != RIDC_OK)
+            return bail(rc);
     }
-    CTX_TRY(cudaMalloc(&c->d_y0, vb));
+    CTX_TRY(cudaMalloc(&c->d_y0, 2 * (size_t)c->V * sizeof(double)));
     CTX_TRY(cudaMalloc(&c->d_err, sizeof(unsigned long long)));
     EngineParams& ep = c->ep;
     memset(&ep, 0, sizeof ep);
@@ -1233,31 +971,9 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         ep.startup_off[j] = su[j];
     }
     ep.err = c->d_err;
-    // opt-in (RIDC_PERSIST=1): one persistent launch per run with per-tile
-    // dependency flags.  Measured slower than the tick graph on B200 for every
-    // workload (flag hand-off + unprefetchable dependent loads ~ the launch gap),
-    // so the graph of tick launches is the default.
-    const char* ps = getenv("RIDC_PERSIST");
-    c->persistent = !(flags & RIDC_RECORD_TRAJECTORY) && (ps && atoi(ps) > 0);
-    if (c->persistent) {
-        const DevSolve& sv = c->ss.sv;
-        PersistParams& pp = c->pp;
-        memset(&pp, 0, sizeof pp);
-        pp.ipl = c->pb.ny * sv.nseg;
-        pp.rx = sv.nseg > 1 ? (sv.halo + 1 + sv.tile - 1) / sv.tile : 0;
-        pp.levels = levels;
-        pp.restarts = restarts;
-        pp.per = per;
-        CTX_TRY(cudaMalloc(&c->d_flags, sizeof(long long) * levels * pp.ipl));
-        CTX_TRY(cudaMalloc(&c->d_abort, sizeof(int)));
-        pp.flags = c->d_flags;
-        pp.abort = c->d_abort;
-        pp.y0 = c->d_y0;
-        pp.timeout_ns = 10ull * 1000 * 1000 * 1000;
-        c->launches = 1;
-    } else if ((rc = capture_graph(c)) != RIDC_OK) {
-        return bail(rc);
-    }
+    ep.lay = c->ss.lay;
+    ep.cgeo = c->d_cgeo;
+    if ((rc = capture_graph(c)) != RIDC_OK) return bail(rc);
 #undef CTX_TRY
     *out = c;
     return RIDC_OK;
@@ -1274,17 +990,14 @@ int ridc_run(ridc_ctx* c, const double* y0_host, double* final_host, double* lev
     CUDA_TRY(&c->err, cudaMemcpyAsync(c->d_y0, y0_host, vb, cudaMemcpyHostToDevice, c->stream));
     int rc = march(c, wall_seconds);
     if (rc) return rc;
-    CUDA_TRY(&c->err, cudaMemcpyAsync(final_host, final_slot(c, c->levels - 1), vb,
-                                      cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(&c->err, copy_out(c, final_host, final_slot(c, c->levels - 1), cudaMemcpyDeviceToHost));
     if (level_finals_host)
         for (int j = 0; j < c->levels; ++j)
-            CUDA_TRY(&c->err, cudaMemcpyAsync(level_finals_host + (size_t)j * c->V, final_slot(c, j),
-                                              vb, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(&c->err, copy_out(c, level_finals_host + (size_t)j * c->V, final_slot(c, j),
+                                       cudaMemcpyDeviceToHost));
     if (traj_host)
-        CUDA_TRY(&c->err, cudaMemcpy2DAsync(traj_host, vb, c->d_ring[c->levels - 1],
-                                            (size_t)c->Vs * sizeof(double), vb,
-                                            (size_t)(c->steps + 1), cudaMemcpyDeviceToHost,
-                                            c->stream));
+        CUDA_TRY(&c->err, copy_out(c, traj_host, c->d_ring[c->levels - 1], cudaMemcpyDeviceToHost,
+                                   c->steps + 1));
     CUDA_TRY(&c->err, cudaStreamSynchronize(c->stream));
     return RIDC_OK;
 }
@@ -1297,8 +1010,7 @@ int ridc_run_device(ridc_ctx* c, const double* y0_dev, double* final_dev, double
     CUDA_TRY(&c->err, cudaMemcpyAsync(c->d_y0, y0_dev, vb, cudaMemcpyDeviceToDevice, c->stream));
     int rc = march(c, wall_seconds);
     if (rc) return rc;
-    CUDA_TRY(&c->err, cudaMemcpyAsync(final_dev, final_slot(c, c->levels - 1), vb,
-                                      cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(&c->err, copy_out(c, final_dev, final_slot(c, c->levels - 1), cudaMemcpyDeviceToDevice));
     CUDA_TRY(&c->err, cudaStreamSynchronize(c->stream));
     return RIDC_OK;
 }
@@ -1314,7 +1026,7 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->tile = c->ss.sv.tile;
     info->halo = c->ss.sv.halo;
     info->items_per_level = c->pb.ny * c->ss.sv.nseg;
-    info->threads = c->ss.tcfg.nt;
+    info->threads = c->ss.ccfg.nt;
     info->ring_vectors = c->ring_vectors;
     info->lambda = c->ss.sv.lam;
     info->r = c->ss.r;
@@ -1328,13 +1040,11 @@ int ridc_destroy(ridc_ctx* c)
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (int j = 0; j < kMaxLevels; ++j)
-        if (c->d_ring_base[j]) cudaFree(c->d_ring_base[j]);
+        if (c->d_ring[j]) cudaFree(c->d_ring[j]);
     if (c->d_weights) cudaFree(c->d_weights);
     if (c->d_tab) cudaFree(c->d_tab);
-    if (c->d_plans) cudaFree(c->d_plans);
+    if (c->d_cgeo) cudaFree(c->d_cgeo);
     if (c->d_dbg) cudaFree(c->d_dbg);
-    if (c->d_flags) cudaFree(c->d_flags);
-    if (c->d_abort) cudaFree(c->d_abort);
     if (c->d_y0) cudaFree(c->d_y0);
     if (c->d_err) cudaFree(c->d_err);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1545,8 +1255,9 @@ struct ridc_pipe {
     void* opened[2] = {nullptr, nullptr};
     double* d_weights = nullptr;
     double* d_tab = nullptr;
-    PlanRow* d_plans = nullptr;
+    ChunkGeo* d_cgeo = nullptr;
     unsigned long long* d_err = nullptr;
+    TmapSet tm;
     std::vector<int> st, su;
     std::map<int, cudaGraphExec_t> graphs;
     long long launches = 0;
@@ -1599,6 +1310,8 @@ EngineParams pipe_params(ridc_pipe* p, long long g0)
         ep.mirror_cap = p->next_cap;
         ep.mirror_off = g0;
     }
+    ep.lay = p->ss.lay;
+    ep.cgeo = p->d_cgeo;
     return ep;
 }
 
@@ -1632,7 +1345,8 @@ int pipe_enqueue(ridc_pipe* p, int interval, long long* launches)
         tp.nact = 1;
         tp.level[0] = j;
         tp.target[0] = t;
-        cudaError_t le = launch_tma(p->pb.kind, p->ss.tcfg, std::min(p->nsm, items), p->stream, ep, tp, items);
+        cudaError_t le = launch_chunk(p->pb.kind, p->ss.ccfg, std::min(p->nsm, items), p->stream, ep, tp, items,
+                                      p->tm);
         if (le != cudaSuccess) return pipe_fail(p, RIDC_E_CUDA, std::string("tick launch: ") + cudaGetErrorString(le));
         ++n;
         if (j < top &&
@@ -1712,10 +1426,11 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     if (cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) p->nsm = 148;
     // tiling depends only on the problem and dt (not on levels or devices), so a
     // level computes bitwise the same states here as in the single-device engine
-    if ((rc = make_solve(p->pb, p->dt, tma_cap(p->pb.kind), p->pb.ny, p->nsm, p->ss)) != RIDC_OK) {
+    if ((rc = make_chunk_solve(p->pb, p->dt, p->nsm, p->ss)) != RIDC_OK) {
         p->err = p->ss.err;
         return bail(rc);
     }
+    p->Vs = (long long)p->pb.ny * p->ss.lay.P;
     P_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     P_TRY(cudaEventCreate(&p->ev0));
     P_TRY(cudaEventCreate(&p->ev1));
@@ -1727,19 +1442,25 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
         p->ss.sv.tab_m = p->d_tab;
         p->ss.sv.tab_g = p->d_tab + p->ss.sv.ntab;
     }
-    P_TRY(cudaMalloc(&p->d_plans, p->ss.plans.size() * sizeof(PlanRow)));
-    P_TRY(cudaMemcpy(p->d_plans, p->ss.plans.data(), p->ss.plans.size() * sizeof(PlanRow), cudaMemcpyHostToDevice));
-    p->ss.sv.plans = p->d_plans;
+    P_TRY(cudaMalloc(&p->d_cgeo, p->ss.cgeo.size() * sizeof(ChunkGeo)));
+    P_TRY(cudaMemcpy(p->d_cgeo, p->ss.cgeo.data(), p->ss.cgeo.size() * sizeof(ChunkGeo), cudaMemcpyHostToDevice));
     P_TRY(cudaMalloc(&p->d_err, sizeof(unsigned long long)));
-    // mailbox: flags, then the inbox ring (2 guard doubles + cap slots of Vs)
-    const size_t ring_bytes = ((size_t)p->inbox_cap * p->Vs + 4) * sizeof(double);
+    // mailbox: flags, then the inbox ring (cap slots of ny padded rows); zeroed: Dirichlet ghosts
+    const size_t ring_bytes = (size_t)p->inbox_cap * p->Vs * sizeof(double);
     P_TRY(cudaMalloc(&p->mailbox, kFlagBytes + ring_bytes));
-    P_TRY(cudaMemset(p->mailbox, 0, kFlagBytes));
+    P_TRY(cudaMemset(p->mailbox, 0, kFlagBytes + ring_bytes));
     p->wm = reinterpret_cast<unsigned long long*>(p->mailbox);
     p->rel = reinterpret_cast<unsigned long long*>(p->mailbox + 8);
-    p->inbox = reinterpret_cast<double*>(p->mailbox + kFlagBytes) + 2;
-    P_TRY(cudaMalloc(&p->own_base, ((size_t)2 * p->Vs + 4) * sizeof(double)));
-    p->own = p->own_base + 2;
+    p->inbox = reinterpret_cast<double*>(p->mailbox + kFlagBytes);
+    P_TRY(cudaMalloc(&p->own_base, ((size_t)2 * p->Vs + 2 * p->V) * sizeof(double)));
+    P_TRY(cudaMemset(p->own_base, 0, (size_t)2 * p->Vs * sizeof(double)));
+    p->own = p->own_base;
+    memset(&p->tm, 0, sizeof p->tm);
+    if ((rc = make_ring_map(&p->tm.map[level], p->own, p->Vs, 2, p->ss.ccfg.nt, &p->err)) != RIDC_OK)
+        return bail(rc);
+    if (level > 0 &&
+        (rc = make_ring_map(&p->tm.map[level - 1], p->inbox, p->Vs, p->inbox_cap, p->ss.ccfg.nt, &p->err)) != RIDC_OK)
+        return bail(rc);
 #undef P_TRY
     *out = p;
     return RIDC_OK;
@@ -1804,7 +1525,7 @@ int ridc_pipe_connect(ridc_pipe* p, const void* prev_blob, const void* next_blob
     if (next_blob) {
         if ((rc = open_blob(p, next_blob, j + 1, &base, 1, &cap)) != RIDC_OK) return rc;
         p->next_wm = reinterpret_cast<unsigned long long*>(base);
-        p->next_inbox = reinterpret_cast<double*>(base + kFlagBytes) + 2;
+        p->next_inbox = reinterpret_cast<double*>(base + kFlagBytes);
         p->next_cap = cap;
     }
     return RIDC_OK;
@@ -1822,12 +1543,17 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
     const long long g0 = (long long)interval * p->per;
     const size_t vb = (size_t)p->V * sizeof(double);
     // seed: step g0 of my own ring and of my inbox is the interval's state0
+    // (plain state -> padded rows with periodic ghosts)
     EngineParams ep = pipe_params(p, g0);
-    PIPE_TRY(p, cudaMemcpyAsync(ep.ring[j] + ((ep.off[j]) % 2) * p->Vs, state0_dev, vb,
-                                cudaMemcpyDeviceToDevice, p->stream));
-    if (j > 0)
-        PIPE_TRY(p, cudaMemcpyAsync(p->inbox + (g0 % p->inbox_cap) * p->Vs, state0_dev, vb,
-                                    cudaMemcpyDeviceToDevice, p->stream));
+    {
+        EngineParams sp = ep;
+        for (int k = 0; k < kMaxLevels; ++k) sp.ring[k] = nullptr;
+        sp.ring[j] = ep.ring[j];
+        if (j > 0) sp.ring[j - 1] = ep.ring[j - 1];
+        const int sb = (int)std::min<long long>((p->Vs + 255) / 256, 148 * 8);
+        k_seed_chunk<<<sb, 256, 0, p->stream>>>(state0_dev, sp, g0);
+        PIPE_TRY(p, cudaGetLastError());
+    }
     PIPE_TRY(p, cudaMemsetAsync(p->d_err, 0xff, sizeof(unsigned long long), p->stream));
     PIPE_TRY(p, cudaEventRecord(p->ev0, p->stream));
     // the interval's ops: captured into a graph on first use (memops included)
@@ -1857,8 +1583,13 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
         launches = p->per;
     }
     p->launches = launches;
-    PIPE_TRY(p, cudaMemcpyAsync(final_dev, ep.ring[j] + ((ep.off[j] + p->per) % 2) * p->Vs, vb,
-                                cudaMemcpyDeviceToDevice, p->stream));
+    {
+        const ChunkLayout& Ly = p->ss.lay;
+        const double* fin = ep.ring[j] + ((ep.off[j] + p->per) % 2) * p->Vs;
+        PIPE_TRY(p, cudaMemcpy2DAsync(final_dev, (size_t)p->pb.nx * sizeof(double), fin + Ly.GW,
+                                      (size_t)Ly.P * sizeof(double), (size_t)p->pb.nx * sizeof(double),
+                                      (size_t)p->pb.ny, cudaMemcpyDeviceToDevice, p->stream));
+    }
     PIPE_TRY(p, cudaEventRecord(p->ev1, p->stream));
     // watchdog (engine.py:432-439): neighbours that never publish turn into an error
     const auto t0 = std::chrono::steady_clock::now();
@@ -1903,7 +1634,7 @@ int ridc_pipe_info(const ridc_pipe* p, ridc_info* info)
     info->tile = p->ss.sv.tile;
     info->halo = p->ss.sv.halo;
     info->items_per_level = p->pb.ny * p->ss.sv.nseg;
-    info->threads = p->ss.tcfg.nt;
+    info->threads = p->ss.ccfg.nt;
     info->ring_vectors = 2 + (p->level > 0 ? p->inbox_cap : 0);
     info->lambda = p->ss.sv.lam;
     info->r = p->ss.r;
@@ -1922,7 +1653,7 @@ int ridc_pipe_destroy(ridc_pipe* p)
     if (p->own_base) cudaFree(p->own_base);
     if (p->d_weights) cudaFree(p->d_weights);
     if (p->d_tab) cudaFree(p->d_tab);
-    if (p->d_plans) cudaFree(p->d_plans);
+    if (p->d_cgeo) cudaFree(p->d_cgeo);
     if (p->d_err) cudaFree(p->d_err);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);

@@ -221,20 +221,6 @@ def test_restart_trend():
     assert e10 < e1
 
 
-@pytest.mark.parametrize("levels,restarts", [(1, 1), (4, 2)])
-def test_persistent_kernel_matches_tick_graph(levels, restarts, monkeypatch):
-    """The opt-in persistent run kernel (per-tile dependency flags) is bitwise
-    equal to the default graph of tick launches."""
-    s = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=1 << 15, t_end=0.004))
-    cfg = E.RidcConfig(levels=levels, steps=40, restarts=restarts)
-    ref = E.run_serial(s, cfg).final_state
-    monkeypatch.setenv("RIDC_PERSIST", "1")
-    with E.Engine(s, cfg) as eng:
-        assert eng.info["kernel_launches"] == 1
-        got = eng.run().final_state
-    assert np.array_equal(got, ref)
-
-
 def test_engine_info_and_launch_count():
     s = P.reaction_diffusion_c2(n=1 << 16)
     with E.Engine(s, E.RidcConfig(levels=4, steps=100)) as eng:
