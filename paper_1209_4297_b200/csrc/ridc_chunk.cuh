@@ -221,6 +221,9 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         RIDC_STAMP(sv, item_no, 4);
         fast_solve<NT, K>(sv, rhs, reinterpret_cast<double*>(swarp));
         RIDC_STAMP(sv, item_no, 7);
+    } else if (MODE == 1 && periodic && (NT & (NT - 1)) == 0 && cg.s_end == NT * K) {
+        // whole periodic line filling every chunk: constant-multiplier scans + cyclic closure
+        fast_solve<NT, K, true>(sv, rhs, reinterpret_cast<double*>(swarp));
     } else {
         const int nm = max(0, min(K, cg.s_end - tid * K));
         const bool cyclic = MODE == 1 && periodic;
@@ -278,6 +281,8 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
     if (mine)
 #pragma unroll
         for (int i = 0; i < K / 2; ++i) sts128(const_cast<char*>(swz(sbufc, tid, i)), rhs[2 * i], rhs[2 * i + 1]);
+    // order these generic shared writes before the TMA that will refill this stage
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     csync<NT>();
     {
         double chk = 0.0;
@@ -317,7 +322,6 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         if (chk != chk) atomicMin(err, err_code(it.target, it.level));
     }
     // release the last node's stage (used as scratch) to the producer
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s_last]);
     if (tid == 0) refill(n_last, s_last);

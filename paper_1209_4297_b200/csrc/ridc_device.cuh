@@ -294,9 +294,10 @@ __device__ __forceinline__ const double* zf_of(const DevSolve& sv)
 // each a warp shuffle scan plus a scan of the warp totals that every warp
 // repeats redundantly (one barrier per direction).  Finally
 //   x_e = xloc_e + c_t zf_e + d_t lam^(KMAX-e).
-template <int NT, int KMAX>
+template <int NT, int KMAX, bool CYCLIC = false>
 __device__ __forceinline__ void fast_solve(const DevSolve& sv, double (&vv)[KMAX], double* sx)
 {
+    static_assert(!CYCLIC || (NT & (NT - 1)) == 0, "cyclic closure needs a power-of-two thread count");
     constexpr int NW = NT / 32;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -341,7 +342,23 @@ __device__ __forceinline__ void fast_solve(const DevSolve& sv, double (&vv)[KMAX
     }
     double cw = __shfl_sync(FULL, wi, warp > 0 ? warp - 1 : 0);
     if (warp == 0) cw = 0.0;
-    const double cf = fma(ml, cw, ex);
+    double cf = fma(ml, cw, ex);
+    // cyclic whole line of NT full chunks: y_{-1} = y_{S-1} = T_f / (1 - lam^S),
+    // entering chunk t as M^t y_{-1}  (M^t = M^lane * (M^32)^warp)
+    double mwf = 1.0, mwb = 1.0, mS = 1.0;
+    if (CYCLIC) {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            if ((1 << (5 + i)) >= NT) break;
+            if (warp & (1 << i)) mwf *= mp[5 + i];
+            if ((NW - 1 - warp) & (1 << i)) mwb *= mp[5 + i];
+        }
+#pragma unroll
+        for (int i = 0; i < 10; ++i)
+            if ((1 << i) == NT) mS = mp[i];
+        const double tf = __shfl_sync(FULL, wi, NW - 1);
+        cf = fma(ml * mwf, tf / (1.0 - mS), cf);
+    }
     // ---- backward carries
     double rinc = fma(cf, zf[0], bb);
 #pragma unroll
@@ -364,7 +381,11 @@ __device__ __forceinline__ void fast_solve(const DevSolve& sv, double (&vv)[KMAX
     const int rl = NW - 1 - warp;   // my warp's position in reverse order
     double dw = __shfl_sync(FULL, wr, rl > 0 ? rl - 1 : 0);
     if (rl == 0) dw = 0.0;
-    const double dc = fma(mr, dw, exr);
+    double dc = fma(mr, dw, exr);
+    if (CYCLIC) {   // x_S = x_0 = T_b / (1 - lam^S), entering chunk t as M^(NT-1-t) x_S
+        const double tb = __shfl_sync(FULL, wr, NW - 1);
+        dc = fma(mr * mwb, tb / (1.0 - mS), dc);
+    }
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) vv[e] = fma(dc, sv.pw[KMAX - 1 - e], fma(cf, zf[e], vv[e]));
 }
