@@ -68,6 +68,8 @@ typedef struct ridc_ctx ridc_ctx;
 
 /* run flags */
 #define RIDC_RECORD_TRAJECTORY 1u  /* RidcConfig.record_trajectory */
+#define RIDC_TICK_ONLY 2u          /* never use the resident single-level march (testing:
+                                      it must agree bitwise with the tick kernel) */
 
 /* Engine geometry / accounting, for reports and tests. */
 typedef struct ridc_info {

@@ -103,77 +103,26 @@ __device__ __forceinline__ void issue_chunk_node(const TmapSet& tm, int lev, lon
 
 namespace ridc {
 
-struct ChunkLayout {
-    int P;       // row pitch (doubles, multiple of 16)
-    int GW;      // ghost columns per side (multiple of 16)
-    int gpr;     // groups per row = P / 16
-    int gdata;   // group of data column 0 within a row = GW / 16
-};
-
-// One chunk-layout item.  MODE: 0 truncated (fast_solve), 1 cyclic whole
-// line, 2 exact Dirichlet start/end with coefficient tables.
-template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, class Refill>
-__device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve& sv, const ChunkLayout& lay,
-                                           const TmapSet& tm, const StepItem& it, const ChunkGeo& cg,
-                                           int row, char* stage, double* edge, uint64_t* full,
-                                           uint64_t* empty, long long& n, Refill&& refill, Aff* swarp,
-                                           unsigned long long* err, int item_no)
+// Phases 2-4 of a chunk item (x-stencils, then the two recurrences) on the
+// pointwise accumulators of thread t's chunk; rhs receives the new state.
+// Shared by the tick kernel (TMA-staged nodes) and the resident FEBE kernel
+// (register-held state), so both produce bitwise the same states.
+template <int KIND, int NT, int MODE>
+__device__ __forceinline__ void chunk_rhs_solve(const DevProblem& pb, const DevSolve& sv, const ChunkGeo& cg,
+                                                bool need_ws, bool need_wx, bool mine,
+                                                const double (&P)[kChunk], const double (&WS)[kChunk],
+                                                const double (&WX)[kChunk], double (&rhs)[kChunk],
+                                                double* edge, Aff* swarp, int item_no)
 {
-    using L = ChunkSmem<NT, ROWS, NSTAGE>;
     constexpr int K = kChunk;
     constexpr bool periodic = KIND != BURGERS_1D;
-    constexpr bool two_d = ROWS == 3;
     constexpr bool has_wx = KIND == ADV_DIFF_1D || KIND == BURGERS_1D || KIND == ADV_DIFF_2D;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const bool mine = tid < cg.ng;            // owns a staged group
-
-    double P[K], WS[K], WX[K];
-#pragma unroll
-    for (int e = 0; e < K; ++e) { P[e] = 0.0; WS[e] = 0.0; WX[e] = 0.0; }
-
-    RIDC_STAMP(sv, item_no, 0);
-    // ---- phase 1: stream the nodes (thread t reads its group as 8 x 128-bit)
-    for (int a = 0; a < it.nnodes; ++a, ++n) {
-        const int s = (int)(n % NSTAGE);
-        const char* st = stage + (size_t)s * L::STAGE;
-        mbar_wait(&full[s], (uint32_t)((n / NSTAGE) & 1));
-        if (a == 0) RIDC_STAMP(sv, item_no, 1);
-        const double ca = it.ca[a], cs = it.cs[a], cn = it.cn[a];
-        if (mine) {
-#pragma unroll
-            for (int i = 0; i < K / 2; ++i) {
-                const double2 v = lds128(swz(st, tid, i));
-                double2 vn = make_double2(0.0, 0.0), vs = make_double2(0.0, 0.0);
-                if (two_d) {
-                    vn = lds128(swz(st + L::ROWB, tid, i));
-                    vs = lds128(swz(st + 2 * L::ROWB, tid, i));
-                }
-                accumulate_point<KIND>(pb, ca, cs, cn, v.x, vn.x, vs.x, P[2 * i], WS[2 * i], WX[2 * i]);
-                accumulate_point<KIND>(pb, ca, cs, cn, v.y, vn.y, vs.y, P[2 * i + 1], WS[2 * i + 1],
-                                       WX[2 * i + 1]);
-            }
-        }
-        if (a + 1 < it.nnodes) {   // the last node's stage is released after the store (scratch)
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            if (tid == 0) refill(n, s);
-        }
-    }
-    const long long n_last = n - 1;
-    const int s_last = (int)(n_last % NSTAGE);
-    char* sbufc = stage + (size_t)s_last * L::STAGE;   // store transpose scratch (NT x 128 B)
-    RIDC_STAMP(sv, item_no, 2);
-
+    const int tid = threadIdx.x;
     // ---- phase 2: x-stencils; the neighbour chunks' edge values via shared memory
     const int gbase = cg.g0 + tid;                  // my group (data-relative)
     const int col0 = gbase * K;                     // data column of my first point
     int nlast = K - 1;                              // my last valid point (whole lines: partial chunk)
     if (MODE == 1 || MODE == 2) nlast = min(K, cg.s_end - tid * K) - 1;
-    bool need_ws = false, need_wx = false;
-    for (int a = 0; a < it.nnodes; ++a) {
-        need_ws |= it.cs[a] != 0.0;
-        need_wx |= it.cn[a] != 0.0;
-    }
     need_wx = need_wx && has_wx;
     double wsl = 0.0, wsr = 0.0, wxl = 0.0, wxr = 0.0;   // left / right neighbour values
     if (need_ws || need_wx) {
@@ -195,7 +144,6 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         // MODE 2: zero Dirichlet ghosts; MODE 0: ends lie in the truncation halo
         csync<NT>();
     }
-    double rhs[K];
 #pragma unroll
     for (int e = 0; e < K; ++e) {
         double r = P[e];
@@ -273,6 +221,75 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
                 rhs[e] = fma(Pm, cin, rhs[e]);
             }
     }
+}
+
+struct ChunkLayout {
+    int P;       // row pitch (doubles, multiple of 16)
+    int GW;      // ghost columns per side (multiple of 16)
+    int gpr;     // groups per row = P / 16
+    int gdata;   // group of data column 0 within a row = GW / 16
+};
+
+// One chunk-layout item.  MODE: 0 truncated (fast_solve), 1 cyclic whole
+// line, 2 exact Dirichlet start/end with coefficient tables.
+template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, class Refill>
+__device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve& sv, const ChunkLayout& lay,
+                                           const TmapSet& tm, const StepItem& it, const ChunkGeo& cg,
+                                           int row, char* stage, double* edge, uint64_t* full,
+                                           uint64_t* empty, long long& n, Refill&& refill, Aff* swarp,
+                                           unsigned long long* err, int item_no)
+{
+    using L = ChunkSmem<NT, ROWS, NSTAGE>;
+    constexpr int K = kChunk;
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr bool two_d = ROWS == 3;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const bool mine = tid < cg.ng;            // owns a staged group
+
+    double P[K], WS[K], WX[K];
+#pragma unroll
+    for (int e = 0; e < K; ++e) { P[e] = 0.0; WS[e] = 0.0; WX[e] = 0.0; }
+
+    RIDC_STAMP(sv, item_no, 0);
+    // ---- phase 1: stream the nodes (thread t reads its group as 8 x 128-bit)
+    for (int a = 0; a < it.nnodes; ++a, ++n) {
+        const int s = (int)(n % NSTAGE);
+        const char* st = stage + (size_t)s * L::STAGE;
+        mbar_wait(&full[s], (uint32_t)((n / NSTAGE) & 1));
+        if (a == 0) RIDC_STAMP(sv, item_no, 1);
+        const double ca = it.ca[a], cs = it.cs[a], cn = it.cn[a];
+        if (mine) {
+#pragma unroll
+            for (int i = 0; i < K / 2; ++i) {
+                const double2 v = lds128(swz(st, tid, i));
+                double2 vn = make_double2(0.0, 0.0), vs = make_double2(0.0, 0.0);
+                if (two_d) {
+                    vn = lds128(swz(st + L::ROWB, tid, i));
+                    vs = lds128(swz(st + 2 * L::ROWB, tid, i));
+                }
+                accumulate_point<KIND>(pb, ca, cs, cn, v.x, vn.x, vs.x, P[2 * i], WS[2 * i], WX[2 * i]);
+                accumulate_point<KIND>(pb, ca, cs, cn, v.y, vn.y, vs.y, P[2 * i + 1], WS[2 * i + 1],
+                                       WX[2 * i + 1]);
+            }
+        }
+        if (a + 1 < it.nnodes) {   // the last node's stage is released after the store (scratch)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (tid == 0) refill(n, s);
+        }
+    }
+    const long long n_last = n - 1;
+    const int s_last = (int)(n_last % NSTAGE);
+    char* sbufc = stage + (size_t)s_last * L::STAGE;   // store transpose scratch (NT x 128 B)
+    RIDC_STAMP(sv, item_no, 2);
+
+    bool need_ws = false, need_wx = false;
+    for (int a = 0; a < it.nnodes; ++a) {
+        need_ws |= it.cs[a] != 0.0;
+        need_wx |= it.cn[a] != 0.0;
+    }
+    double rhs[K];
+    chunk_rhs_solve<KIND, NT, MODE>(pb, sv, cg, need_ws, need_wx, mine, P, WS, WX, rhs, edge, swarp, item_no);
     RIDC_STAMP(sv, item_no, 8);
 
     // ---- phase 5: store.  Chunks go to shared memory swizzled (conflict-free),

@@ -7,6 +7,10 @@
 // intervals, all ticks) is captured once into a CUDA graph at create time
 // (the analogue of _prepare's pre-factorisation, engine.py:465-473).
 //
+// Single level (RIDC order 1, FEBE) on 1-D lines whose segments fit one CTA
+// each: one cooperative launch marches every step with the state held in
+// registers (ridc_resident.cuh); only segment edges go through L2.
+//
 // Level rings: level j < top keeps its last 2j+3 states in HBM (the greedy
 // schedule's live window for the reader j+1, which lags j+1 ticks); the top
 // level keeps 2 (or the whole trajectory when it is recorded).
@@ -30,6 +34,7 @@
 #include "ridc_device.cuh"
 #include "ridc_tma.cuh"
 #include "ridc_chunk.cuh"
+#include "ridc_resident.cuh"
 
 using namespace ridc;
 
@@ -377,6 +382,50 @@ cudaError_t launch_chunk(int kind, const ChunkCfg& c, int grid, cudaStream_t st,
     return cudaErrorInvalidValue;
 }
 
+// ---- resident FEBE kernel (ridc_resident.cuh): same NT as the tick config
+// (the block scans' association, hence the rounding, depends on NT)
+template <int KIND, int NT>
+cudaError_t resident_t(bool launch, int grid, cudaStream_t st, const ResidentParams& rp, int* per_sm)
+{
+    auto kfn = k_resident_febe<KIND, NT>;
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, NT, 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // all segments co-resident (neighbour waits)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, rp);
+}
+
+template <int KIND>
+cudaError_t resident_k(int nt, bool launch, int grid, cudaStream_t st, const ResidentParams& rp, int* per_sm)
+{
+    switch (nt) {
+    case 64: return resident_t<KIND, 64>(launch, grid, st, rp, per_sm);
+    case 128: return resident_t<KIND, 128>(launch, grid, st, rp, per_sm);
+    case 256: return resident_t<KIND, 256>(launch, grid, st, rp, per_sm);
+    case 512: return resident_t<KIND, 512>(launch, grid, st, rp, per_sm);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+// launch == false: occupancy query into *per_sm (blocks per SM)
+cudaError_t resident_dispatch(int kind, int nt, bool launch, int grid, cudaStream_t st, const ResidentParams& rp,
+                              int* per_sm)
+{
+    switch (kind) {
+    case ADV_DIFF_1D: return resident_k<ADV_DIFF_1D>(nt, launch, grid, st, rp, per_sm);
+    case BURGERS_1D: return resident_k<BURGERS_1D>(nt, launch, grid, st, rp, per_sm);
+    case RD_1D: return resident_k<RD_1D>(nt, launch, grid, st, rp, per_sm);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
 cudaError_t launch_item(int kind, const LaunchCfg& c, int items, cudaStream_t st,
                         const DevProblem& pb, const DevSolve& sv, const StepItem& it,
                         unsigned long long* err)
@@ -675,6 +724,10 @@ struct ridc_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
     long long ring_vectors = 0;
+    // resident single-level march (ridc_resident.cuh)
+    bool resident = false;
+    unsigned* d_flags = nullptr;   // per segment published step, then the abort word
+    ResidentParams rp;
     std::string err;
 };
 
@@ -744,6 +797,7 @@ EngineParams interval_params(ridc_ctx* c, int interval)
 
 const double* final_slot(ridc_ctx* c, int level)
 {
+    if (c->resident) return c->d_ring[0] + (c->steps % c->cap[0]) * c->Vs;   // one launch, global steps
     EngineParams ep = interval_params(c, c->restarts - 1);
     return ep.ring[level] + ((ep.off[level] + c->per) % ep.cap[level]) * c->Vs;
 }
@@ -833,8 +887,19 @@ int check_err_word(ridc_ctx* c)
 int march(ridc_ctx* c, double* wall_seconds)
 {
     CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
-    CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
-    CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
+    if (c->resident) {
+        const int nseg = c->ss.sv.nseg;
+        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, (nseg + 1) * sizeof(unsigned), c->stream));
+        CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
+        EngineParams ep = interval_params(c, 0);
+        const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
+        k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
+        CUDA_TRY(&c->err, cudaGetLastError());
+        CUDA_TRY(&c->err, resident_dispatch(c->pb.kind, c->ss.ccfg.nt, true, nseg, c->stream, c->rp, nullptr));
+    } else {
+        CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
+        CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
+    }
     CUDA_TRY(&c->err, cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(&c->err, cudaEventSynchronize(c->ev1));
     if (wall_seconds) {
@@ -842,7 +907,62 @@ int march(ridc_ctx* c, double* wall_seconds)
         CUDA_TRY(&c->err, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         *wall_seconds = ms * 1e-3;
     }
+    if (c->resident) {
+        unsigned ab = 0;
+        CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_flags + c->ss.sv.nseg, sizeof ab, cudaMemcpyDeviceToHost));
+        if (ab) return fail(&c->err, RIDC_E_PROTOCOL, "resident march: a neighbour segment wait timed out");
+    }
     return check_err_word(c);
+}
+
+// Resident single-level march: RIDC order 1 on a 1-D line whose segments fit
+// one co-resident CTA each, and whose halos reach only the adjacent segments.
+int setup_resident(ridc_ctx* c)
+{
+    const SolveSetup& ss = c->ss;
+    const int nseg = ss.sv.nseg;
+    const bool one_d = c->pb.kind == ADV_DIFF_1D || c->pb.kind == BURGERS_1D || c->pb.kind == RD_1D;
+    if (c->levels != 1 || !one_d || c->pb.ny != 1 || (c->flags & RIDC_TICK_ONLY) || nseg > c->nsm) return RIDC_OK;
+    // farthest reach of a staged range beyond its tile; every column that close
+    // to a tile end is published each step (and at least the periodic ghosts)
+    int ext = 0;
+    for (const ChunkGeo& g : ss.cgeo) {
+        ext = std::max(ext, g.c0 - 16 * g.g0);
+        ext = std::max(ext, 16 * (g.g0 + g.ng) - (g.c0 + g.tlen));
+    }
+    const int W = std::max(ext, ss.lay.GW);
+    for (const ChunkGeo& g : ss.cgeo)
+        if (nseg > 1 && (ext >= g.tlen || W >= g.tlen)) return RIDC_OK;   // halo spans past a neighbour
+    int per_sm = 0;
+    ResidentParams& rp = c->rp;
+    memset(&rp, 0, sizeof rp);
+    if (resident_dispatch(c->pb.kind, ss.ccfg.nt, false, 0, c->stream, rp, &per_sm) != cudaSuccess ||
+        per_sm * c->nsm < nseg) {
+        cudaGetLastError();
+        return RIDC_OK;
+    }
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, (nseg + 1) * sizeof(unsigned)));
+    rp.pb = c->pb;
+    rp.sv = ss.sv;
+    rp.lay = ss.lay;
+    rp.cgeo = c->d_cgeo;
+    rp.ring = c->d_ring[0];
+    rp.cap = c->cap[0];
+    rp.Vs = c->Vs;
+    rp.dt = c->dt;
+    rp.steps = c->steps;
+    rp.per = c->per;
+    rp.edge_w = W;
+    rp.full_every = (c->flags & RIDC_RECORD_TRAJECTORY) ? 1 : 0;
+    rp.flags = c->d_flags;
+    rp.abort = c->d_flags + nseg;
+    rp.err = c->d_err;
+    rp.spin_limit = 4000000000LL;   // ~2 s at 1.9 GHz per neighbour wait
+    rp.dbg = c->d_dbg;
+    rp.nowait = getenv("RIDC_RESIDENT_NOWAIT") ? 1 : 0;
+    c->resident = true;
+    c->launches = 2;
+    return RIDC_OK;
 }
 
 }  // namespace
@@ -973,7 +1093,8 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     ep.err = c->d_err;
     ep.lay = c->ss.lay;
     ep.cgeo = c->d_cgeo;
-    if ((rc = capture_graph(c)) != RIDC_OK) return bail(rc);
+    if ((rc = setup_resident(c)) != RIDC_OK) return bail(rc);
+    if (!c->resident && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
 #undef CTX_TRY
     *out = c;
     return RIDC_OK;
@@ -1047,6 +1168,7 @@ int ridc_destroy(ridc_ctx* c)
     if (c->d_dbg) cudaFree(c->d_dbg);
     if (c->d_y0) cudaFree(c->d_y0);
     if (c->d_err) cudaFree(c->d_err);
+    if (c->d_flags) cudaFree(c->d_flags);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);

@@ -40,6 +40,7 @@ __all__ = ["RidcConfig", "RidcSolution", "LevelWindow", "Engine", "startup_delay
 
 MAX_LEVELS = MAX_LEVEL + 1
 RECORD_TRAJECTORY = 1
+TICK_ONLY = 2   # include/ridc_b200.h RIDC_TICK_ONLY (testing: disable the resident march)
 
 
 def startup_delay(j: int) -> int:
@@ -148,7 +149,7 @@ class Engine:
     ``run`` / ``run_device`` then only march.
     """
 
-    def __init__(self, ivp, config: RidcConfig):
+    def __init__(self, ivp, config: RidcConfig, tick_only: bool = False):
         self.ivp = as_descriptor(ivp)
         self.config = config
         self.problem = self.ivp.problem
@@ -156,6 +157,8 @@ class Engine:
         self.weights = pack_weight_tables(config.levels, self.dt)
         D.require_cuda(config.device)
         flags = RECORD_TRAJECTORY if config.record_trajectory else 0
+        if tick_only:
+            flags |= TICK_ONLY
         cp = self.problem.to_c()
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().ridc_create(

@@ -1,0 +1,74 @@
+"""The resident single-level march (csrc/ridc_resident.cuh) against the tick
+kernel: RIDC order 1 (FEBE, engine.py:167-175) on 1-D lines must give
+bitwise the same final state, level finals and trajectory whichever device
+path runs it -- both call the same per-chunk stencil/solve code, only the
+data movement differs (registers + published segment edges vs TMA-staged
+ring slots)."""
+
+import numpy as np
+import pytest
+
+import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle import oracle as O  # noqa: E402
+from paper_1209_4297_b200 import engine as E, problems as P  # noqa: E402
+from paper_1209_4297_b200.quadrature import pack_weight_tables  # noqa: E402
+
+
+def _short(system, t_end):
+    ivp = system.ivp
+    return P.StructuredIVP(ivp.problem, 0.0, t_end, ivp.initial_state)
+
+
+CASES = [
+    # (id, ivp builder, steps, restarts, trajectory)
+    ("c1-whole-cyclic", lambda: _short(P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 1024)), 4.0),
+     1000, 1, False),
+    ("c1-restarts-traj", lambda: _short(P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 1024)), 0.4),
+     120, 3, True),
+    ("burgers-whole-dirichlet", lambda: _short(P.burgers_paper(), 0.1), 200, 1, False),
+    ("burgers-segments", lambda: _short(P.build_burgers(P.BurgersSpec(dx=1 / (1 << 15))), 0.002), 100, 1, False),
+    ("rd-few-segments", lambda: _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=12000, d=1e-4)), 0.01),
+     100, 1, False),
+    ("rd-seg-2^16", lambda: _short(P.reaction_diffusion_c2(n=1 << 16), 0.02), 200, 2, False),
+    ("rd-c2-2^20", lambda: _short(P.reaction_diffusion_c2(), 0.02), 200, 1, False),
+    ("rd-c2-traj", lambda: _short(P.reaction_diffusion_c2(n=1 << 18), 0.002), 20, 2, True),
+]
+
+
+@pytest.mark.parametrize("name,builder,steps,restarts,traj", CASES, ids=[c[0] for c in CASES])
+def test_resident_equals_tick_kernel_bitwise(name, builder, steps, restarts, traj):
+    ivp = builder()
+    cfg = E.RidcConfig(levels=1, steps=steps, restarts=restarts, record_trajectory=traj)
+    with E.Engine(ivp, cfg) as res, E.Engine(ivp, cfg, tick_only=True) as tick:
+        assert res.info["kernel_launches"] == 2, res.info          # seed + one cooperative march
+        assert tick.info["kernel_launches"] == restarts + restarts * steps // restarts
+        a, b = res.run(), tick.run()
+        a2 = res.run()
+    assert np.array_equal(a.final_state, b.final_state)
+    assert np.array_equal(a.level_finals[0], b.level_finals[0])
+    assert np.array_equal(a.final_state, a2.final_state)
+    if traj:
+        assert np.array_equal(a.trajectory, b.trajectory)
+    # and the oracle (the reference's algebra restated on the CPU)
+    dt = (ivp.t_end - ivp.t_start) / steps
+    ref = O.run(ivp.problem, ivp.initial_state, 1, steps, restarts, dt, pack_weight_tables(1, dt))
+    assert G.normwise(a.final_state, ref["final_state"]) <= 1e-10
+
+
+def test_resident_device_run_and_wall():
+    ivp = _short(P.reaction_diffusion_c2(n=1 << 16), 0.02)
+    cfg = E.RidcConfig(levels=1, steps=200)
+    y0 = torch.from_numpy(np.array(ivp.initial_state)).cuda()
+    out = torch.empty_like(y0)
+    with E.Engine(ivp, cfg) as eng:
+        t = eng.run_device(y0, out)
+        host = eng.run().final_state
+    assert t > 0
+    assert np.array_equal(out.cpu().numpy(), host)
