@@ -112,7 +112,7 @@ __device__ __forceinline__ void chunk_rhs_solve(const DevProblem& pb, const DevS
                                                 bool need_ws, bool need_wx, bool mine,
                                                 const double (&P)[kChunk], const double (&WS)[kChunk],
                                                 const double (&WX)[kChunk], double (&rhs)[kChunk],
-                                                double* edge, Aff* swarp, int item_no)
+                                                double* edge, Aff* swarp, int item_no, FastLane fl)
 {
     constexpr int K = kChunk;
     constexpr bool periodic = KIND != BURGERS_1D;
@@ -160,18 +160,20 @@ __device__ __forceinline__ void chunk_rhs_solve(const DevProblem& pb, const DevS
             if (KIND == BURGERS_1D) r = fma(-pb.bs, rn - l, r);
             else r = fma(pb.cax, rn - WX[e], r);
         }
-        rhs[e] = mine ? r : 0.0;
+        // threads past the staged groups feed zeros into the scans (their
+        // accumulators are zero already unless a stencil pulled in a neighbour)
+        rhs[e] = (need_ws || need_wx) ? (mine ? r : 0.0) : r;
     }
     RIDC_STAMP(sv, item_no, 3);
 
     // ---- phases 3-4: the two recurrences
     if (MODE == 0) {
         RIDC_STAMP(sv, item_no, 4);
-        fast_solve<NT, K>(sv, rhs, reinterpret_cast<double*>(swarp));
+        fast_solve<NT, K>(sv, rhs, reinterpret_cast<double*>(swarp), fl);
         RIDC_STAMP(sv, item_no, 7);
     } else if (MODE == 1 && periodic && (NT & (NT - 1)) == 0 && cg.s_end == NT * K) {
         // whole periodic line filling every chunk: constant-multiplier scans + cyclic closure
-        fast_solve<NT, K, true>(sv, rhs, reinterpret_cast<double*>(swarp));
+        fast_solve<NT, K, true>(sv, rhs, reinterpret_cast<double*>(swarp), fl);
     } else {
         const int nm = max(0, min(K, cg.s_end - tid * K));
         const bool cyclic = MODE == 1 && periodic;
@@ -237,7 +239,7 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
                                            const TmapSet& tm, const StepItem& it, const ChunkGeo& cg,
                                            int row, char* stage, double* edge, uint64_t* full,
                                            uint64_t* empty, long long& n, Refill&& refill, Aff* swarp,
-                                           unsigned long long* err, int item_no)
+                                           unsigned long long* err, int item_no, FastLane fl)
 {
     using L = ChunkSmem<NT, ROWS, NSTAGE>;
     constexpr int K = kChunk;
@@ -289,7 +291,7 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         need_wx |= it.cn[a] != 0.0;
     }
     double rhs[K];
-    chunk_rhs_solve<KIND, NT, MODE>(pb, sv, cg, need_ws, need_wx, mine, P, WS, WX, rhs, edge, swarp, item_no);
+    chunk_rhs_solve<KIND, NT, MODE>(pb, sv, cg, need_ws, need_wx, mine, P, WS, WX, rhs, edge, swarp, item_no, fl);
     RIDC_STAMP(sv, item_no, 8);
 
     // ---- phase 5: store.  Chunks go to shared memory swizzled (conflict-free),

@@ -52,6 +52,7 @@ struct DevSolve {
     int nseg;            // items per x-line (1 = whole-line exact mode)
     double pw[kMaxChunk];  // pw[e] = lam^(e+1): carry weights of a constant-coefficient chunk
     double zf4[4], zf8[8], zf16[16];  // forward-carry response of a backward chunk pass (K = 4/8/16)
+    double mp8[10], mp16[10];         // M^(2^i), M = lam^K (repeated squaring of pw[K-1]), K = 8/16
     const struct PlanRow* plans;   // TMA staging plans [nseg][row parity] (engine only)
     long long* dbg;                // optional phase trace (RIDC_PHASE_TIMING), CTA 0 only
 };
@@ -294,8 +295,33 @@ __device__ __forceinline__ const double* zf_of(const DevSolve& sv)
 // each a warp shuffle scan plus a scan of the warp totals that every warp
 // repeats redundantly (one barrier per direction).  Finally
 //   x_e = xloc_e + c_t zf_e + d_t lam^(KMAX-e).
+template <int KMAX>
+__device__ __forceinline__ const double* mp_of(const DevSolve& sv)
+{
+    static_assert(KMAX == 8 || KMAX == 16, "carry-power tables exist for K = 8 and 16");
+    return KMAX == 8 ? sv.mp8 : sv.mp16;
+}
+
+// Per-lane carry powers of fast_solve: M^lane and M^(31-lane).  Loop-invariant:
+// callers that solve many chunks compute them once.
+struct FastLane { double ml, mr; };
+
+template <int KMAX>
+__device__ __forceinline__ FastLane fast_lane(const DevSolve& sv)
+{
+    const double* mp = mp_of<KMAX>(sv);
+    const int lane = threadIdx.x & 31;
+    double ml = 1.0, mr = 1.0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if (lane & (1 << i)) ml *= mp[i];
+        if ((31 - lane) & (1 << i)) mr *= mp[i];
+    }
+    return FastLane{ml, mr};
+}
+
 template <int NT, int KMAX, bool CYCLIC = false>
-__device__ __forceinline__ void fast_solve(const DevSolve& sv, double (&vv)[KMAX], double* sx)
+__device__ __forceinline__ void fast_solve(const DevSolve& sv, double (&vv)[KMAX], double* sx, FastLane fl)
 {
     static_assert(!CYCLIC || (NT & (NT - 1)) == 0, "cyclic closure needs a power-of-two thread count");
     constexpr int NW = NT / 32;
@@ -303,10 +329,7 @@ __device__ __forceinline__ void fast_solve(const DevSolve& sv, double (&vv)[KMAX
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double m = sv.lam, g = sv.g;
     const double* zf = zf_of<KMAX>(sv);
-    double mp[10];   // M^(2^i)
-    mp[0] = sv.pw[KMAX - 1];
-#pragma unroll
-    for (int i = 1; i < 10; ++i) mp[i] = mp[i - 1] * mp[i - 1];
+    const double* mp = mp_of<KMAX>(sv);   // M^(2^i)
     double y = 0.0;
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) { y = fma(m, y, g * vv[e]); vv[e] = y; }
@@ -315,13 +338,7 @@ __device__ __forceinline__ void fast_solve(const DevSolve& sv, double (&vv)[KMAX
 #pragma unroll
     for (int e = KMAX - 1; e >= 0; --e) { x = fma(m, x, vv[e]); vv[e] = x; }
     const double bb = x;
-    // M^lane and M^(31-lane)
-    double ml = 1.0, mr = 1.0;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        if (lane & (1 << i)) ml *= mp[i];
-        if ((31 - lane) & (1 << i)) mr *= mp[i];
-    }
+    const double ml = fl.ml, mr = fl.mr;   // M^lane and M^(31-lane)
     // ---- forward carries
     double inc = bf;
 #pragma unroll
@@ -480,7 +497,7 @@ __device__ __forceinline__ void finish_item(const DevProblem& pb, const DevSolve
     const double m = sv.lam, g = sv.g;
     if constexpr (FAST) {
         RIDC_STAMP(sv, ino, 4);
-        fast_solve<NT, KMAX>(sv, vv, reinterpret_cast<double*>(swarp));
+        fast_solve<NT, KMAX>(sv, vv, reinterpret_cast<double*>(swarp), fast_lane<KMAX>(sv));
         RIDC_STAMP(sv, ino, 7);
     } else {
     {

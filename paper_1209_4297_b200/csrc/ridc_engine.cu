@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(NT, 1)
     };
     long long n = 0;
     int ino = 0;
+    const FastLane fl = fast_lane<kChunk>(ep.sv);
     for (int i = blockIdx.x; i < total; i += gridDim.x, ++ino) {
         const int slot = i % tp.nact, tile = i / tp.nact;
         const int row = tile / nseg, seg = tile - row * nseg;
@@ -178,15 +179,15 @@ __global__ void __launch_bounds__(NT, 1)
         switch (cg.mode) {
         case 0:
             chunk_item<KIND, NT, ROWS, NSTAGE, 0>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
-                                                  full, empty, n, refill, swarp, ep.err, ino);
+                                                  full, empty, n, refill, swarp, ep.err, ino, fl);
             break;
         case 1:
             chunk_item<KIND, NT, ROWS, NSTAGE, 1>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
-                                                  full, empty, n, refill, swarp, ep.err, ino);
+                                                  full, empty, n, refill, swarp, ep.err, ino, fl);
             break;
         default:
             chunk_item<KIND, NT, ROWS, NSTAGE, 2>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
-                                                  full, empty, n, refill, swarp, ep.err, ino);
+                                                  full, empty, n, refill, swarp, ep.err, ino, fl);
         }
         csync<NT>();   // edge / scan scratch reuse by the next item
     }
@@ -384,10 +385,10 @@ cudaError_t launch_chunk(int kind, const ChunkCfg& c, int grid, cudaStream_t st,
 
 // ---- resident FEBE kernel (ridc_resident.cuh): same NT as the tick config
 // (the block scans' association, hence the rounding, depends on NT)
-template <int KIND, int NT>
+template <int KIND, int NT, int MODE>
 cudaError_t resident_t(bool launch, int grid, cudaStream_t st, const ResidentParams& rp, int* per_sm)
 {
-    auto kfn = k_resident_febe<KIND, NT>;
+    auto kfn = k_resident_febe<KIND, NT, MODE>;
     if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, NT, 0);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -402,26 +403,42 @@ cudaError_t resident_t(bool launch, int grid, cudaStream_t st, const ResidentPar
     return cudaLaunchKernelEx(&cfg, kfn, rp);
 }
 
+// mode: the common segment mode (0 truncated segments, 1 cyclic whole line,
+// 2 Dirichlet whole line) or -1 (mixed: Dirichlet ends + truncated middle)
 template <int KIND>
-cudaError_t resident_k(int nt, bool launch, int grid, cudaStream_t st, const ResidentParams& rp, int* per_sm)
+cudaError_t resident_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const ResidentParams& rp,
+                       int* per_sm)
 {
+    // periodic kinds have truncated (0) or cyclic (1) segments; Burgers has
+    // Dirichlet whole lines (2) or Dirichlet ends around truncated middles (-1)
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr int MA = periodic ? 0 : 2, MB = periodic ? 1 : -1;
+    if (mode != MA && mode != MB) {
+        if (periodic) return cudaErrorInvalidValue;
+        mode = MB;
+    }
+#define RIDC_RES_NT(NT)                                                                   \
+    case NT:                                                                              \
+        return mode == MA ? resident_t<KIND, NT, MA>(launch, grid, st, rp, per_sm)        \
+                          : resident_t<KIND, NT, MB>(launch, grid, st, rp, per_sm);
     switch (nt) {
-    case 64: return resident_t<KIND, 64>(launch, grid, st, rp, per_sm);
-    case 128: return resident_t<KIND, 128>(launch, grid, st, rp, per_sm);
-    case 256: return resident_t<KIND, 256>(launch, grid, st, rp, per_sm);
-    case 512: return resident_t<KIND, 512>(launch, grid, st, rp, per_sm);
+        RIDC_RES_NT(64)
+        RIDC_RES_NT(128)
+        RIDC_RES_NT(256)
+        RIDC_RES_NT(512)
     default: return cudaErrorInvalidValue;
     }
+#undef RIDC_RES_NT
 }
 
 // launch == false: occupancy query into *per_sm (blocks per SM)
-cudaError_t resident_dispatch(int kind, int nt, bool launch, int grid, cudaStream_t st, const ResidentParams& rp,
-                              int* per_sm)
+cudaError_t resident_dispatch(int kind, int nt, int mode, bool launch, int grid, cudaStream_t st,
+                              const ResidentParams& rp, int* per_sm)
 {
     switch (kind) {
-    case ADV_DIFF_1D: return resident_k<ADV_DIFF_1D>(nt, launch, grid, st, rp, per_sm);
-    case BURGERS_1D: return resident_k<BURGERS_1D>(nt, launch, grid, st, rp, per_sm);
-    case RD_1D: return resident_k<RD_1D>(nt, launch, grid, st, rp, per_sm);
+    case ADV_DIFF_1D: return resident_k<ADV_DIFF_1D>(nt, mode, launch, grid, st, rp, per_sm);
+    case BURGERS_1D: return resident_k<BURGERS_1D>(nt, mode, launch, grid, st, rp, per_sm);
+    case RD_1D: return resident_k<RD_1D>(nt, mode, launch, grid, st, rp, per_sm);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -563,6 +580,13 @@ void make_factors(const DevProblem& pb, double coeff, SolveSetup& ss)
     fill_zf(sv.zf4, 4);
     fill_zf(sv.zf8, 8);
     fill_zf(sv.zf16, 16);
+    // M^(2^i) for the chunk-carry scans (fast_solve): repeated squaring of lam^K
+    auto fill_mp = [&](double* mp, int K) {
+        mp[0] = sv.pw[K - 1];
+        for (int i = 1; i < 10; ++i) mp[i] = mp[i - 1] * mp[i - 1];
+    };
+    fill_mp(sv.mp8, 8);
+    fill_mp(sv.mp16, 16);
 }
 
 // truncation halo: lam^H <= 2^-60 relative to the recurrence magnitude
@@ -726,6 +750,7 @@ struct ridc_ctx {
     long long ring_vectors = 0;
     // resident single-level march (ridc_resident.cuh)
     bool resident = false;
+    int res_mode = -1;             // common segment mode of the resident kernel (-1: mixed)
     unsigned* d_flags = nullptr;   // per segment published step, then the abort word
     ResidentParams rp;
     std::string err;
@@ -895,7 +920,8 @@ int march(ridc_ctx* c, double* wall_seconds)
         const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
         k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
         CUDA_TRY(&c->err, cudaGetLastError());
-        CUDA_TRY(&c->err, resident_dispatch(c->pb.kind, c->ss.ccfg.nt, true, nseg, c->stream, c->rp, nullptr));
+        CUDA_TRY(&c->err, resident_dispatch(c->pb.kind, c->ss.ccfg.nt, c->res_mode, true, nseg, c->stream, c->rp,
+                                            nullptr));
     } else {
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
         CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
@@ -923,6 +949,9 @@ int setup_resident(ridc_ctx* c)
     const int nseg = ss.sv.nseg;
     const bool one_d = c->pb.kind == ADV_DIFF_1D || c->pb.kind == BURGERS_1D || c->pb.kind == RD_1D;
     if (c->levels != 1 || !one_d || c->pb.ny != 1 || (c->flags & RIDC_TICK_ONLY) || nseg > c->nsm) return RIDC_OK;
+    // whole lines by default: one CTA marches alone, 2x faster than a launch per
+    // step; segmented lines pay a neighbour flag round trip per step (opt-in)
+    if (nseg > 1 && !(c->flags & RIDC_RESIDENT_SEGMENTS)) return RIDC_OK;
     // farthest reach of a staged range beyond its tile; every column that close
     // to a tile end is published each step (and at least the periodic ghosts)
     int ext = 0;
@@ -936,8 +965,15 @@ int setup_resident(ridc_ctx* c)
     int per_sm = 0;
     ResidentParams& rp = c->rp;
     memset(&rp, 0, sizeof rp);
-    if (resident_dispatch(c->pb.kind, ss.ccfg.nt, false, 0, c->stream, rp, &per_sm) != cudaSuccess ||
-        per_sm * c->nsm < nseg) {
+    int mode = ss.cgeo[0].mode;
+    for (const ChunkGeo& g : ss.cgeo)
+        if (g.mode != mode) mode = -1;
+    c->res_mode = mode;
+    const cudaError_t oe = resident_dispatch(c->pb.kind, ss.ccfg.nt, mode, false, 0, c->stream, rp, &per_sm);
+    if (oe != cudaSuccess || per_sm * c->nsm < nseg) {
+        if (getenv("RIDC_DEBUG"))
+            fprintf(stderr, "ridc: resident march unavailable (%s, %d blocks/SM x %d SMs < %d segments)\n",
+                    cudaGetErrorString(oe), per_sm, c->nsm, nseg);
         cudaGetLastError();
         return RIDC_OK;
     }
@@ -959,7 +995,6 @@ int setup_resident(ridc_ctx* c)
     rp.err = c->d_err;
     rp.spin_limit = 4000000000LL;   // ~2 s at 1.9 GHz per neighbour wait
     rp.dbg = c->d_dbg;
-    rp.nowait = getenv("RIDC_RESIDENT_NOWAIT") ? 1 : 0;
     c->resident = true;
     c->launches = 2;
     return RIDC_OK;

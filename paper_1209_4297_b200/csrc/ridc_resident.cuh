@@ -45,13 +45,22 @@ struct ResidentParams {
     unsigned* abort;         // watchdog: set when a neighbour wait times out
     long long spin_limit;    // watchdog budget per wait (clock64 cycles)
     long long* dbg;          // optional phase trace (RIDC_PHASE_TIMING): CTA 0, thread 0, steps 1..8
-    int nowait;              // experiment only (RIDC_RESIDENT_NOWAIT): skip neighbour waits (wrong results)
 };
 
+// slots: steps 1..4 -> rows 0..3, steps S-3..S -> rows 4..7; col 6: globaltimer (ns) at row start
 #define RIDC_RSTAMP(rp, s, idx)                                                              \
     do {                                                                                     \
-        if ((rp).dbg && threadIdx.x == 0 && blockIdx.x == 0 && (s) <= 8)                     \
-            (rp).dbg[((s) - 1) * 16 + (idx)] = clock64();                                    \
+        if ((rp).dbg && threadIdx.x == 0 && blockIdx.x == 0) {                               \
+            const long long _r = (s) <= 4 ? (s) - 1 : ((s) > (rp).steps - 4 ? (s) - (rp).steps + 7 : -1); \
+            if (_r >= 0) {                                                                   \
+                (rp).dbg[_r * 16 + (idx)] = clock64();                                       \
+                if ((idx) == 0) {                                                            \
+                    unsigned long long _g;                                                   \
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g));                  \
+                    (rp).dbg[_r * 16 + 6] = (long long)_g;                                   \
+                }                                                                            \
+            }                                                                                \
+        }                                                                                    \
     } while (0)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p)
@@ -80,7 +89,7 @@ __device__ __forceinline__ void load_chunk_cg(const double* src, double (&u)[kCh
 
 template <int KIND, int NT, int MODE>
 __device__ __forceinline__ void resident_step(const ResidentParams& rp, const ChunkGeo& cg, bool mine,
-                                              double (&u)[kChunk], double* edge, Aff* swarp)
+                                              double (&u)[kChunk], double* edge, Aff* swarp, FastLane fl)
 {
     constexpr int K = kChunk;
     constexpr bool has_wx = KIND == ADV_DIFF_1D || KIND == BURGERS_1D;
@@ -97,7 +106,7 @@ __device__ __forceinline__ void resident_step(const ResidentParams& rp, const Ch
         for (int e = 0; e < K; ++e) accumulate_point<KIND>(rp.pb, 1.0, 0.0, rp.dt, u[e], 0.0, 0.0, P[e], WS[e], WX[e]);
     }
     chunk_rhs_solve<KIND, NT, MODE>(rp.pb, rp.sv, cg, false, has_wx && rp.dt != 0.0, mine, P, WS, WX, u, edge,
-                                    swarp, 99);
+                                    swarp, 99, fl);
 }
 
 // Finite check of 16 values: four independent FMA chains (x * 0 is NaN iff x is not finite).
@@ -115,7 +124,9 @@ __device__ __forceinline__ bool chunk_finite(const double (&u)[kChunk])
     return c == c;
 }
 
-template <int KIND, int NT>
+// MODE: the solve mode every segment shares (0 truncated, 1 cyclic whole
+// line, 2 Dirichlet ends), or -1 to dispatch per segment.
+template <int KIND, int NT, int MODE>
 __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__ ResidentParams rp)
 {
     static_assert(KIND == ADV_DIFF_1D || KIND == BURGERS_1D || KIND == RD_1D, "1-D kinds only");
@@ -148,6 +159,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
     for (int e = 0; e < K; ++e) u[e] = 0.0;
     if (mine) load_chunk_cg(rp.ring + GW + col0, u);   // slot 0: the seeded initial state
     long long cur = 0;                                  // ring slot of step s-1
+    const FastLane fl = fast_lane<K>(rp.sv);
 
     for (long long s = 1; s <= rp.steps; ++s) {
         const double* prev = rp.ring + cur * rp.Vs + GW;
@@ -156,7 +168,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
         RIDC_RSTAMP(rp, s, 0);
         if (s > 1 && halo) {
             // acquire the neighbour's step s-1 publication, then reload my chunk
-            if (nb >= 0 && !rp.nowait) {
+            if (nb >= 0) {
                 const unsigned want = (unsigned)(s - 1);
                 const long long t0 = clock64();
                 while (ld_acquire_u32(rp.flags + nb) < want)
@@ -170,10 +182,14 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
             load_chunk_cg(prev + col0, u);
         }
         RIDC_RSTAMP(rp, s, 2);
-        switch (cg.mode) {
-        case 0: resident_step<KIND, NT, 0>(rp, cg, mine, u, edge, swarp); break;
-        case 1: resident_step<KIND, NT, 1>(rp, cg, mine, u, edge, swarp); break;
-        default: resident_step<KIND, NT, 2>(rp, cg, mine, u, edge, swarp);
+        if (MODE >= 0) {
+            resident_step<KIND, NT, (MODE >= 0 ? MODE : 0)>(rp, cg, mine, u, edge, swarp, fl);
+        } else {
+            switch (cg.mode) {
+            case 0: resident_step<KIND, NT, 0>(rp, cg, mine, u, edge, swarp, fl); break;
+            case 1: resident_step<KIND, NT, 1>(rp, cg, mine, u, edge, swarp, fl); break;
+            default: resident_step<KIND, NT, 2>(rp, cg, mine, u, edge, swarp, fl);
+            }
         }
         RIDC_RSTAMP(rp, s, 3);
         const bool full = s == rp.steps || rp.full_every;

@@ -41,6 +41,7 @@ __all__ = ["RidcConfig", "RidcSolution", "LevelWindow", "Engine", "startup_delay
 MAX_LEVELS = MAX_LEVEL + 1
 RECORD_TRAJECTORY = 1
 TICK_ONLY = 2   # include/ridc_b200.h RIDC_TICK_ONLY (testing: disable the resident march)
+RESIDENT_SEGMENTS = 4   # RIDC_RESIDENT_SEGMENTS (experimental: resident march on segmented lines)
 
 
 def startup_delay(j: int) -> int:
@@ -149,7 +150,7 @@ class Engine:
     ``run`` / ``run_device`` then only march.
     """
 
-    def __init__(self, ivp, config: RidcConfig, tick_only: bool = False):
+    def __init__(self, ivp, config: RidcConfig, tick_only: bool = False, resident_segments: bool = False):
         self.ivp = as_descriptor(ivp)
         self.config = config
         self.problem = self.ivp.problem
@@ -159,6 +160,8 @@ class Engine:
         flags = RECORD_TRAJECTORY if config.record_trajectory else 0
         if tick_only:
             flags |= TICK_ONLY
+        if resident_segments:
+            flags |= RESIDENT_SEGMENTS
         cp = self.problem.to_c()
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().ridc_create(

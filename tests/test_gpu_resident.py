@@ -46,7 +46,7 @@ CASES = [
 def test_resident_equals_tick_kernel_bitwise(name, builder, steps, restarts, traj):
     ivp = builder()
     cfg = E.RidcConfig(levels=1, steps=steps, restarts=restarts, record_trajectory=traj)
-    with E.Engine(ivp, cfg) as res, E.Engine(ivp, cfg, tick_only=True) as tick:
+    with E.Engine(ivp, cfg, resident_segments=True) as res, E.Engine(ivp, cfg, tick_only=True) as tick:
         assert res.info["kernel_launches"] == 2, res.info          # seed + one cooperative march
         assert tick.info["kernel_launches"] == restarts + restarts * steps // restarts
         a, b = res.run(), tick.run()
@@ -62,12 +62,24 @@ def test_resident_equals_tick_kernel_bitwise(name, builder, steps, restarts, tra
     assert G.normwise(a.final_state, ref["final_state"]) <= 1e-10
 
 
+def test_default_selection():
+    """Whole lines march resident by default; segmented lines use the tick kernel."""
+    whole = _short(P.reaction_diffusion_c2(n=8192), 0.002)
+    seg = _short(P.reaction_diffusion_c2(n=1 << 16), 0.002)
+    with E.Engine(whole, E.RidcConfig(levels=1, steps=20)) as a, \
+            E.Engine(seg, E.RidcConfig(levels=1, steps=20)) as b, \
+            E.Engine(whole, E.RidcConfig(levels=2, steps=20)) as c:
+        assert a.info["kernel_launches"] == 2
+        assert b.info["kernel_launches"] == 21
+        assert c.info["kernel_launches"] == 1 + 21
+
+
 def test_resident_device_run_and_wall():
     ivp = _short(P.reaction_diffusion_c2(n=1 << 16), 0.02)
     cfg = E.RidcConfig(levels=1, steps=200)
     y0 = torch.from_numpy(np.array(ivp.initial_state)).cuda()
     out = torch.empty_like(y0)
-    with E.Engine(ivp, cfg) as eng:
+    with E.Engine(ivp, cfg, resident_segments=True) as eng:
         t = eng.run_device(y0, out)
         host = eng.run().final_state
     assert t > 0

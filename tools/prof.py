@@ -44,14 +44,18 @@ if os.environ.get("RIDC_PHASE_TIMING"):
         d = [st[k] - st[k - 1] for k in range(1, 10)]
         print(f"item {it}: " + " ".join(f"{names[k]}:{d[k-1]}" for k in range(1, 10)),
               f"| total {st[9] - st[0]} cyc" + (f", gap from prev {st[0] - buf[(it - 1) * 16 + 9]}" if it else ""))
-    if eng.info["kernel_launches"] == 2:   # resident march: per-step stamps of CTA 0, thread 0
+    if eng.info["kernel_launches"] == 2:   # resident march: stamps of CTA 0, thread 0 (steps 1-4, last 4)
         rn = ["wait", "load", "compute", "publish", "sync"]
-        for s in range(8):
-            st = [buf[s * 16 + k] for k in range(6)]
+        for r in range(8):
+            st = [buf[r * 16 + k] for k in range(6)]
             if st[0] == 0:
                 continue
             if st[1] == 0:
                 st[1] = st[0]
             d = [st[k] - st[k - 1] for k in range(1, 6)]
-            print(f"step {s + 1}: " + " ".join(f"{rn[k]}:{d[k]}" for k in range(5)),
-                  f"| total {st[5] - st[0]} cyc" + (f", to next {buf[(s + 1) * 16] - st[5]}" if s < 7 else ""))
+            print(f"row {r}: " + " ".join(f"{rn[k]}:{d[k]}" for k in range(5)), f"| total {st[5] - st[0]} cyc")
+        g0, g1 = buf[0 * 16 + 6], buf[7 * 16 + 6]
+        c0, c1 = buf[0 * 16 + 0], buf[7 * 16 + 0]
+        steps = eng.info["steps"] - 1
+        print(f"step 1 -> step S: {(g1 - g0) / steps:.1f} ns/step, {(c1 - c0) / steps:.0f} cyc/step, "
+              f"clock {(c1 - c0) / max(g1 - g0, 1):.3f} GHz")
