@@ -259,7 +259,7 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         const char* st = stage + (size_t)s * L::STAGE;
         mbar_wait(&full[s], (uint32_t)((n / NSTAGE) & 1));
         if (a == 0) RIDC_STAMP(sv, item_no, 1);
-        const double ca = it.ca[a], cs = it.cs[a], cn = it.cn[a];
+        const NodeCoef nc = node_coef<KIND>(pb, it.ca[a], it.cs[a], it.cn[a]);
         if (mine) {
 #pragma unroll
             for (int i = 0; i < K / 2; ++i) {
@@ -269,9 +269,8 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
                     vn = lds128(swz(st + L::ROWB, tid, i));
                     vs = lds128(swz(st + 2 * L::ROWB, tid, i));
                 }
-                accumulate_point<KIND>(pb, ca, cs, cn, v.x, vn.x, vs.x, P[2 * i], WS[2 * i], WX[2 * i]);
-                accumulate_point<KIND>(pb, ca, cs, cn, v.y, vn.y, vs.y, P[2 * i + 1], WS[2 * i + 1],
-                                       WX[2 * i + 1]);
+                accumulate_point<KIND>(nc, v.x, vn.x, vs.x, P[2 * i], WS[2 * i], WX[2 * i]);
+                accumulate_point<KIND>(nc, v.y, vn.y, vs.y, P[2 * i + 1], WS[2 * i + 1], WX[2 * i + 1]);
             }
         }
         if (a + 1 < it.nnodes) {   // the last node's stage is released after the store (scratch)

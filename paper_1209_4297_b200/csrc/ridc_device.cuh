@@ -53,7 +53,6 @@ struct DevSolve {
     double pw[kMaxChunk];  // pw[e] = lam^(e+1): carry weights of a constant-coefficient chunk
     double zf4[4], zf8[8], zf16[16];  // forward-carry response of a backward chunk pass (K = 4/8/16)
     double mp8[10], mp16[10];         // M^(2^i), M = lam^K (repeated squaring of pw[K-1]), K = 8/16
-    const struct PlanRow* plans;   // TMA staging plans [nseg][row parity] (engine only)
     long long* dbg;                // optional phase trace (RIDC_PHASE_TIMING), CTA 0 only
 };
 
@@ -259,25 +258,64 @@ __device__ __forceinline__ Geo make_geo(const DevProblem& pb, const DevSolve& sv
     return g;
 }
 
-// Fold one node value into the pointwise accumulators (see item_body):
-//   P  += ca u + cn * (pointwise parts of f^N: reaction, y-stencil, y-advection)
-//   WS += cs u
-//   WX += cn u (x-advection) | cn u^2 (Burgers flux)
+// Per-node coefficients of the pointwise accumulation (uniform over an item).
+// A window node w with weights (ca, cs, cn) contributes
+//   ca w + cn (pointwise parts of f^N(w)) + cs f^S(w) + cn (x-parts of f^N(w)),
+// the pointwise part factored per kind so that it costs 1-3 FMAs per point:
+//   RD_1D   ca w + cn rho w(1-w)                    = (a + b w) w
+//   RD_2D   ... + cn dyy (wn - 2w + ws)             = (a + b w) w + c (wn + ws)
+//   AD_2D   ca w + cn (cy (ws - w) + dyy (wn - 2w + ws)) = a w + b ws + c wn
+//   AD_1D, Burgers: ca w (the x-advection / flux goes through WX)
+struct NodeCoef {
+    double a, b, c;   // pointwise factors (see above)
+    double cs, cn;    // weights of the x-stencil accumulators
+};
+
 template <int KIND>
-__device__ __forceinline__ void accumulate_point(const DevProblem& pb, double ca, double cs, double cn,
-                                                 double v, double vn, double vs, double& P,
+__device__ __forceinline__ NodeCoef node_coef(const DevProblem& pb, double ca, double cs, double cn)
+{
+    NodeCoef k;
+    k.cs = cs;
+    k.cn = cn;
+    k.b = 0.0;
+    k.c = 0.0;
+    if (KIND == RD_1D) {
+        k.a = fma(cn, pb.rho, ca);
+        k.b = -(cn * pb.rho);
+    } else if (KIND == RD_2D) {
+        k.a = fma(-2.0 * cn, pb.cdy, fma(cn, pb.rho, ca));
+        k.b = -(cn * pb.rho);
+        k.c = cn * pb.cdy;
+    } else if (KIND == ADV_DIFF_2D) {
+        k.a = fma(-2.0 * cn, pb.cdy, fma(-cn, pb.cay, ca));
+        k.b = cn * (pb.cay + pb.cdy);
+        k.c = cn * pb.cdy;
+    } else {
+        k.a = ca;
+    }
+    return k;
+}
+
+// Fold one node value into the pointwise accumulators (see NodeCoef):
+//   P += pointwise part, WS += cs w, WX += cn w (x-advection) | cn w^2 (Burgers).
+// Branch-free: zero coefficients cost an FMA, never a select (callers keep
+// vn / vs finite -- zero when the y-neighbours were not loaded).
+template <int KIND>
+__device__ __forceinline__ void accumulate_point(const NodeCoef& k, double v, double vn, double vs, double& P,
                                                  double& WS, double& WX)
 {
-    // branch-free: zero coefficients cost one FMA, never a select (callers keep
-    // vn / vs finite -- zero when the y-neighbours were not loaded)
-    double p = fma(ca, v, P);
-    if (KIND == RD_1D) p = fma(cn, pb.rho * v * (1.0 - v), p);
-    if (KIND == RD_2D) p = fma(cn, fma(pb.rho * v, 1.0 - v, pb.cdy * (vn - 2.0 * v + vs)), p);
-    if (KIND == ADV_DIFF_2D) p = fma(cn, fma(pb.cay, vs - v, pb.cdy * (vn - 2.0 * v + vs)), p);
-    P = p;
-    WS = fma(cs, v, WS);
-    if (KIND == BURGERS_1D) WX = fma(cn, v * v, WX);
-    else if (KIND == ADV_DIFF_1D || KIND == ADV_DIFF_2D) WX = fma(cn, v, WX);
+    if (KIND == RD_1D) {
+        P = fma(fma(k.b, v, k.a), v, P);
+    } else if (KIND == RD_2D) {
+        P = fma(k.c, vn + vs, fma(fma(k.b, v, k.a), v, P));
+    } else if (KIND == ADV_DIFF_2D) {
+        P = fma(k.c, vn, fma(k.b, vs, fma(k.a, v, P)));
+    } else {
+        P = fma(k.a, v, P);
+    }
+    WS = fma(k.cs, v, WS);
+    if (KIND == BURGERS_1D) WX = fma(k.cn, v * v, WX);
+    else if (KIND == ADV_DIFF_1D || KIND == ADV_DIFF_2D) WX = fma(k.cn, v, WX);
 }
 
 template <int KMAX>
@@ -694,11 +732,10 @@ __device__ __forceinline__ void item_body(const DevProblem& pb, const DevSolve& 
         }
     };
     auto accumulate = [&](int a, const double* u) {
-        const double ca = it.ca[a], cs = it.cs[a], cn = it.cn[a];
+        const NodeCoef nc = node_coef<KIND>(pb, it.ca[a], it.cs[a], it.cn[a]);
 #pragma unroll
         for (int k = 0; k < KMAX; ++k)
-            accumulate_point<KIND>(pb, ca, cs, cn, u[k], two_d ? un[k] : 0.0, two_d ? us[k] : 0.0,
-                                   P[k], WS[k], WX[k]);
+            accumulate_point<KIND>(nc, u[k], two_d ? un[k] : 0.0, two_d ? us[k] : 0.0, P[k], WS[k], WX[k]);
     };
     const int nn = it.nnodes;
     if (prefetch) {

@@ -117,8 +117,11 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
 
 // The production tick kernel: persistent CTAs of NT compute threads; thread
 // 0 doubles as the TMA producer (ridc_chunk.cuh).  Items of the tick are
-// dealt round-robin: item i -> level slot i % nact, tile i / nact.
-template <int KIND, int NT, int ROWS, int NSTAGE>
+// dealt round-robin: item i -> level slot i % nact, tile i / nact.  MODE is
+// the solve mode all segments share (0 truncated, 1 cyclic whole line, 2
+// Dirichlet whole line), or -1 to dispatch per segment -- one mode per
+// kernel keeps the hot loop small in the instruction cache.
+template <int KIND, int NT, int ROWS, int NSTAGE, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_tick_chunk(EngineParams ep, TickParams tp, int ipl, const __grid_constant__ TmapSet tm)
 {
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(NT, 1)
         const int slot = i % tp.nact, tile = i / tp.nact;
         const int row = tile / nseg, seg = tile - row * nseg;
         const ChunkGeo cg = ep.cgeo[seg];
-        switch (cg.mode) {
+        switch (MODE >= 0 ? MODE : cg.mode) {
         case 0:
             chunk_item<KIND, NT, ROWS, NSTAGE, 0>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
                                                   full, empty, n, refill, swarp, ep.err, ino, fl);
@@ -288,6 +291,7 @@ struct ChunkCfg {
     int id;
     int nt, rows, nstage;
     size_t smem;
+    int mode;   // common segment mode (k_tick_chunk MODE), -1 mixed
 };
 
 #define RIDC_CHUNK_CONFIGS(X) \
@@ -308,6 +312,7 @@ ChunkCfg chunk_cfg_of(int id)
     c.rows = ROWS;
     c.nstage = NSTAGE;
     c.smem = ChunkSmem<NT, ROWS, NSTAGE>::BYTES + 1024;   // + 1 KiB for the 1024-B alignment
+    c.mode = -1;
     return c;
 }
 
@@ -328,11 +333,11 @@ ChunkCfg pick_chunk(int kind, int points)
 
 int chunk_points_max(int kind) { return (kind == ADV_DIFF_2D || kind == RD_2D) ? 256 * 16 : 512 * 16; }
 
-template <int KIND, int NT, int ROWS, int NSTAGE>
+template <int KIND, int NT, int ROWS, int NSTAGE, int MODE>
 cudaError_t launch_chunk_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
                            const TickParams& tp, int ipl, const TmapSet& tm)
 {
-    auto kfn = k_tick_chunk<KIND, NT, ROWS, NSTAGE>;
+    auto kfn = k_tick_chunk<KIND, NT, ROWS, NSTAGE, MODE>;
     static bool attr[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -360,10 +365,16 @@ cudaError_t launch_chunk_k(const ChunkCfg& c, int grid, cudaStream_t st, const E
                            const TickParams& tp, int ipl, const TmapSet& tm)
 {
     constexpr bool two_d = KIND == ADV_DIFF_2D || KIND == RD_2D;
+    // periodic kinds: truncated segments (0) or cyclic whole lines (1); Burgers:
+    // Dirichlet whole lines (2) or Dirichlet ends + truncated middles (-1)
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr int MA = periodic ? 0 : 2, MB = periodic ? 1 : -1;
+    if (periodic && c.mode != MA && c.mode != MB) return cudaErrorInvalidValue;
 #define RIDC_CHUNK_CASE(ID, NT, ROWS, NSTAGE)                                                  \
     if (c.id == ID && two_d == (ROWS == 3)) {                                                  \
         if constexpr (two_d == (ROWS == 3))                                                    \
-            return launch_chunk_t<KIND, NT, ROWS, NSTAGE>(grid, c.smem, st, ep, tp, ipl, tm);  \
+            return c.mode == MA ? launch_chunk_t<KIND, NT, ROWS, NSTAGE, MA>(grid, c.smem, st, ep, tp, ipl, tm) \
+                                : launch_chunk_t<KIND, NT, ROWS, NSTAGE, MB>(grid, c.smem, st, ep, tp, ipl, tm); \
     }
     RIDC_CHUNK_CONFIGS(RIDC_CHUNK_CASE)
 #undef RIDC_CHUNK_CASE
@@ -709,6 +720,14 @@ int make_chunk_solve(const DevProblem& pb, double coeff, int nsm, SolveSetup& ss
         ss.cgeo.push_back(cg);
     }
     ss.ccfg = pick_chunk(pb.kind, 16 * maxng);
+    ss.ccfg.mode = ss.cgeo[0].mode;
+    for (const ChunkGeo& g : ss.cgeo)
+        if (g.mode != ss.ccfg.mode) ss.ccfg.mode = -1;
+    if (pb.periodic && ss.ccfg.mode < 0) {
+        ss.err = "internal: periodic line with mixed segment modes";
+        return RIDC_E_CONFIG;
+    }
+    if (!pb.periodic && ss.ccfg.mode != 2) ss.ccfg.mode = -1;
     if (maxng > ss.ccfg.nt) {
         ss.err = "internal: item larger than the chunk kernel";
         return RIDC_E_CONFIG;

@@ -102,8 +102,9 @@ __device__ __forceinline__ void resident_step(const ResidentParams& rp, const Ch
     }
     // the predictor's single node: ca = 1, cs = 0, cn = dt (build_item, level 0)
     if (mine) {
+        const NodeCoef nc = node_coef<KIND>(rp.pb, 1.0, 0.0, rp.dt);
 #pragma unroll
-        for (int e = 0; e < K; ++e) accumulate_point<KIND>(rp.pb, 1.0, 0.0, rp.dt, u[e], 0.0, 0.0, P[e], WS[e], WX[e]);
+        for (int e = 0; e < K; ++e) accumulate_point<KIND>(nc, u[e], 0.0, 0.0, P[e], WS[e], WX[e]);
     }
     chunk_rhs_solve<KIND, NT, MODE>(rp.pb, rp.sv, cg, false, has_wx && rp.dt != 0.0, mine, P, WS, WX, u, edge,
                                     swarp, 99, fl);
