@@ -330,6 +330,22 @@ def run_ours(args):
                     extra[f"order{p}_1gpu"] = {"value": n * nt * len(ts) / sum(ts),
                                                "ms_per_solve": sum(ts) / len(ts) * 1e3,
                                                "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps)}
+            # the paper's ARK comparators on the same grid and dt (steppers.integrate_ark)
+            from paper_1209_4297_b200.steppers import ArkEngine
+            from paper_1209_4297_b200.tableaus import imex3_tableau, imex4_tableau
+            ivp = sysm.ivp
+            for name, tab in (("imex3", imex3_tableau()), ("imex4", imex4_tableau())):
+                with ArkEngine(ivp, tab, ivp.t_start, ivp.t_end, nt) as ae:
+                    ae.run_device(y0, out)
+                    ts = []
+                    for _ in range(2):
+                        flush.zero_()
+                        torch.cuda.synchronize()
+                        ts.append(ae.run_device(y0, out))
+                    extra[f"{name}_1gpu"] = {"value": n * nt * len(ts) / sum(ts),
+                                             "ms_per_solve": sum(ts) / len(ts) * 1e3,
+                                             "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps),
+                                             "launches_per_solve": ae.info["kernel_launches"]}
         line["ridc_orders_1gpu"] = extra
         line["cpu_baseline"] = cpu_sample(sysm, order, nt, budget_s=args.cpu_budget)
     else:

@@ -193,6 +193,29 @@ int ridc_pipe_info(const ridc_pipe *p, ridc_info *info);
 int ridc_pipe_destroy(ridc_pipe *p);
 const char *ridc_pipe_last_error(const ridc_pipe *p);
 
+/* ---------------------------------------------------------------------------
+ * ARK (IMEX) comparators on the device: the coupled DIRK / explicit pair step
+ * of steppers.ark_step (steppers.py:122-142) marched by integrate_ark
+ * (steppers.py:145-155), stage sums as kernels.stage_accumulate
+ * (kernels.py:149-158).  Tableaus are s x s row-major (tableaus.py:82-127 for
+ * imex3 / imex4): a_implicit lower triangular, a_explicit strictly lower.
+ * Non-finite results raise RIDC_E_NONFINITE with the reference's message
+ * "ARK march produced non-finite entries at step k".
+ */
+typedef struct ridc_ark_ctx ridc_ark_ctx;
+
+int ridc_ark_create(const ridc_problem *problem, double t_start, double t_end,
+                    int64_t steps, int32_t stages, const double *a_implicit,
+                    const double *a_explicit, const double *b_implicit,
+                    const double *b_explicit, int32_t device, ridc_ark_ctx **out);
+int ridc_ark_run(ridc_ark_ctx *ctx, const double *y0_host, double *final_host,
+                 double *wall_seconds);
+int ridc_ark_run_device(ridc_ark_ctx *ctx, const double *y0_dev, double *final_dev,
+                        double *wall_seconds);
+int ridc_ark_info(const ridc_ark_ctx *ctx, int64_t *kernel_launches, int32_t *items_per_step);
+int ridc_ark_destroy(ridc_ark_ctx *ctx);
+const char *ridc_ark_last_error(const ridc_ark_ctx *ctx);
+
 #ifdef __cplusplus
 }
 #endif

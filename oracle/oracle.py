@@ -161,3 +161,35 @@ def run(pd, y0, levels, steps, restarts, dt, weights, workers=1, record_trajecto
                          max_steps, ctypes.byref(wall)))
     return {"final_state": final, "level_finals": lf, "trajectory": traj,
             "wall_seconds": wall.value}
+
+
+def ark(pd, a_implicit, a_explicit, b_implicit, b_explicit, y0, t0, t1, steps):
+    """integrate_ark / ark_step (steppers.py:122-155) with stage_accumulate's
+    summation order (kernels.py:149-158: out = y, then += dt*aI*ks + dt*aE*kn per
+    stage j); the shifted solves are orc_solve (Thomas / Sherman-Morrison) in
+    place of the dense QR.  Raises RuntimeError with the reference's message on
+    a non-finite step (steppers.py:153-154)."""
+    a_implicit, a_explicit = np.asarray(a_implicit), np.asarray(a_explicit)
+    b_implicit, b_explicit = np.asarray(b_implicit), np.asarray(b_explicit)
+    dt = (t1 - t0) / steps
+    s = b_implicit.shape[0]
+    y = np.array(y0, dtype=np.float64)
+    n = y.shape[0]
+    for k in range(steps):
+        ks = np.empty((s, n))
+        kn = np.empty((s, n))
+        for i in range(s):
+            rhs = y.copy()
+            for j in range(i):
+                rhs += (dt * a_implicit[i, j]) * ks[j] + (dt * a_explicit[i, j]) * kn[j]
+            aii = a_implicit[i, i]
+            ys = rhs if aii == 0.0 else solve(pd, aii * dt, rhs)
+            ks[i] = stiff(pd, ys)
+            kn[i] = nonstiff(pd, ys)
+        out = y.copy()
+        for j in range(s):
+            out += (dt * b_implicit[j]) * ks[j] + (dt * b_explicit[j]) * kn[j]
+        y = out
+        if not np.isfinite(y).all():
+            raise RuntimeError(f"ARK march produced non-finite entries at step {k + 1}")
+    return y

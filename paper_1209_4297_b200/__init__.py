@@ -16,5 +16,7 @@ from .engine import (Engine, LevelWindow, RidcConfig, RidcSolution, correct_step
                      predict_step, restart_partition, run_pipelined, run_serial,
                      startup_delay)
 from .studies import integrate_scheme, scheme_levels
+from .tableaus import ButcherPair, imex3_tableau, imex4_tableau
+from .steppers import ArkEngine, ark_step, fbe_step, integrate_ark
 
 __version__ = "0.1.0"

@@ -58,6 +58,13 @@ SIGNATURES = {
     "ridc_pipe_info": (ctypes.c_int, [_vp, _P(RidcInfo)]),
     "ridc_pipe_destroy": (ctypes.c_int, [_vp]),
     "ridc_pipe_last_error": (ctypes.c_char_p, [_vp]),
+    "ridc_ark_create": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp, _vp,
+                                       ctypes.c_int32, _P(_vp)]),
+    "ridc_ark_run": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
+    "ridc_ark_run_device": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
+    "ridc_ark_info": (ctypes.c_int, [_vp, _P(ctypes.c_int64), _P(ctypes.c_int32)]),
+    "ridc_ark_destroy": (ctypes.c_int, [_vp]),
+    "ridc_ark_last_error": (ctypes.c_char_p, [_vp]),
 }
 
 
@@ -88,4 +95,10 @@ def check(code: int, ctx=None) -> None:
 def check_pipe(code: int, pipe=None) -> None:
     if code:
         msg = lib().ridc_pipe_last_error(pipe)
+        raise_for_status(code, msg.decode() if msg else "")
+
+
+def check_ark(code: int, ark=None) -> None:
+    if code:
+        msg = lib().ridc_ark_last_error(ark)
         raise_for_status(code, msg.decode() if msg else "")

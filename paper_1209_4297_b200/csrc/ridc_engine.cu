@@ -66,6 +66,8 @@ struct TickParams {
     int nact;
     int level[kMaxLevels];
     long long target[kMaxLevels];
+    DevSolve sv;             // factors of this launch's shifted solve (RIDC: ep.sv; ARK: per stage)
+    const StepItem* pre;     // precomputed item descriptors (ARK stages), or null: build_item
 };
 
 __device__ __forceinline__ long long slot_index(const EngineParams& ep, int lev, long long s, long long off = -1)
@@ -134,11 +136,20 @@ __global__ void __launch_bounds__(NT, 1)
     __shared__ StepItem items[kMaxLevels];   // one descriptor per active level (shared by all its tiles)
     __shared__ Aff swarp[2 * (NT / 32) + 1];
     const int total = tp.nact * ipl;
-    const int nseg = ep.sv.nseg, ny = ep.pb.ny;
+    const DevSolve& sv = tp.sv;
+    const int nseg = sv.nseg, ny = ep.pb.ny;
     // programmatic dependent launch: let the next tick's grid get scheduled now;
     // its CTAs run this prologue as SMs free up and wait (below) before reading
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (threadIdx.x < tp.nact) build_item(ep, tp.level[threadIdx.x], tp.target[threadIdx.x], items[threadIdx.x]);
+    static_assert(sizeof(StepItem) % 8 == 0, "StepItem is copied as 8-byte words");
+    if (tp.pre) {   // precomputed descriptors (ARK stages); the step number comes per launch
+        for (int k = threadIdx.x; k < tp.nact * (int)(sizeof(StepItem) / 8); k += blockDim.x)
+            reinterpret_cast<long long*>(items)[k] = reinterpret_cast<const long long*>(tp.pre)[k];
+        __syncthreads();
+        if (threadIdx.x < tp.nact) items[threadIdx.x].target = tp.target[threadIdx.x];
+    } else if (threadIdx.x < tp.nact) {
+        build_item(ep, tp.level[threadIdx.x], tp.target[threadIdx.x], items[threadIdx.x]);
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
             mbar_init(&full[i], 1);
@@ -174,22 +185,22 @@ __global__ void __launch_bounds__(NT, 1)
     };
     long long n = 0;
     int ino = 0;
-    const FastLane fl = fast_lane<kChunk>(ep.sv);
+    const FastLane fl = fast_lane<kChunk>(sv);
     for (int i = blockIdx.x; i < total; i += gridDim.x, ++ino) {
         const int slot = i % tp.nact, tile = i / tp.nact;
         const int row = tile / nseg, seg = tile - row * nseg;
         const ChunkGeo cg = ep.cgeo[seg];
         switch (MODE >= 0 ? MODE : cg.mode) {
         case 0:
-            chunk_item<KIND, NT, ROWS, NSTAGE, 0>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+            chunk_item<KIND, NT, ROWS, NSTAGE, 0>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
                                                   full, empty, n, refill, swarp, ep.err, ino, fl);
             break;
         case 1:
-            chunk_item<KIND, NT, ROWS, NSTAGE, 1>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+            chunk_item<KIND, NT, ROWS, NSTAGE, 1>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
                                                   full, empty, n, refill, swarp, ep.err, ino, fl);
             break;
         default:
-            chunk_item<KIND, NT, ROWS, NSTAGE, 2>(ep.pb, ep.sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+            chunk_item<KIND, NT, ROWS, NSTAGE, 2>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
                                                   full, empty, n, refill, swarp, ep.err, ino, fl);
         }
         csync<NT>();   // edge / scan scratch reuse by the next item
@@ -886,6 +897,7 @@ int capture_graph(ridc_ctx* c)
         for (long long k = 1; k <= c->ticks && le == cudaSuccess; ++k) {
             TickParams tp;
             memset(&tp, 0, sizeof tp);
+            tp.sv = ep.sv;
             for (int j = 0; j < L; ++j) {
                 const long long t = k - delay(j);
                 if (t >= 1 && t <= c->per) {
@@ -1518,6 +1530,7 @@ int pipe_enqueue(ridc_pipe* p, int interval, long long* launches)
         }
         TickParams tp;
         memset(&tp, 0, sizeof tp);
+        tp.sv = ep.sv;
         tp.nact = 1;
         tp.level[0] = j;
         tp.target[0] = t;
@@ -1843,5 +1856,348 @@ const char* ridc_pipe_last_error(const ridc_pipe* p)
     if (p && !p->err.empty()) return p->err.c_str();
     return g_last_error.c_str();
 }
+
+}  // extern "C"
+
+// ================================================================ ARK (IMEX) steps
+//
+// The paper's comparators (steppers.ark_step / integrate_ark, steppers.py:122-155;
+// tableaus.py imex3/imex4) on the same device machinery as the RIDC levels.
+// Stage i's right-hand side  y_n + dt sum_{j<i} (aI_ij f^S(Y_j) + aE_ij f^N(Y_j))
+// (kernels.stage_accumulate, kernels.py:149-158) is exactly a window item:
+// node Y_j with weights (ca, cs, cn) = (j == 0 ? 1 : 0, dt aI_ij, dt aE_ij),
+// f^S / f^N recomputed from the stored stage states by the stencils; the
+// stage solve (I - aI_ii dt L_S) uses that stage's own factors (identity
+// factors lam = 0, g = 1 when aI_ii = 0 and for the final combination).
+// One tiling serves every stage: it is built for the largest shift, whose
+// truncation halo bounds all the others.  One tick-kernel launch per stage,
+// the whole march captured in one CUDA graph.
+
+namespace {
+
+struct ArkSolve {
+    DevSolve sv;
+    double* d_tab = nullptr;
+};
+
+}  // namespace
+
+struct ridc_ark_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevProblem pb;
+    SolveSetup ss;             // tiling + layout (largest shift)
+    int nsm = 148;
+    int stages = 0;
+    long long steps = 0;
+    double dt = 0;
+    long long V = 0, Vs = 0, cap = 0;
+    double* d_ring = nullptr;  // slots: y (2, alternating by step parity), stage states Y_i at 2 + i
+    ChunkGeo* d_cgeo = nullptr;
+    StepItem* d_items = nullptr;   // [parity][item]
+    int nitems = 0;
+    std::vector<ArkSolve> solves;  // per item
+    double* d_y0 = nullptr;
+    unsigned long long* d_err = nullptr;
+    EngineParams ep;
+    TmapSet tm;
+    cudaGraphExec_t gexec = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    long long launches = 0;
+    std::string err;
+};
+
+namespace {
+
+int ark_fail(ridc_ark_ctx* a, int code, const std::string& m) { return fail(a ? &a->err : nullptr, code, m); }
+
+// Identity "solve": lam = 0, g = 1 makes both recurrences and every carry exact copies.
+DevSolve identity_solve(const DevSolve& tiling)
+{
+    DevSolve sv;
+    memset(&sv, 0, sizeof sv);
+    sv.lam = 0.0;
+    sv.g = 1.0;
+    sv.halo = tiling.halo;
+    sv.tile = tiling.tile;
+    sv.nseg = tiling.nseg;
+    return sv;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, int64_t steps, int32_t stages,
+                    const double* a_implicit, const double* a_explicit, const double* b_implicit,
+                    const double* b_explicit, int32_t device, ridc_ark_ctx** out)
+{
+    if (!out) return fail(nullptr, RIDC_E_CONFIG, "out is NULL");
+    *out = nullptr;
+    int rc = validate_problem(problem);
+    if (rc) return rc;
+    if (steps < 1) return fail(nullptr, RIDC_E_CONFIG, "steps must be positive");
+    if (!(t_start < t_end)) return fail(nullptr, RIDC_E_CONFIG, "need t_start < t_end");
+    if (stages < 1 || stages + 1 > kMaxNodes)
+        return fail(nullptr, RIDC_E_CONFIG, "ARK stage count out of range");
+    if (!a_implicit || !a_explicit || !b_implicit || !b_explicit)
+        return fail(nullptr, RIDC_E_CONFIG, "NULL tableau");
+    const int s = stages;
+    for (int i = 0; i < s; ++i)
+        for (int j = 0; j < s; ++j) {
+            if (j > i && a_implicit[i * s + j] != 0.0)
+                return fail(nullptr, RIDC_E_CONFIG, "a_implicit must be lower triangular");
+            if (j >= i && a_explicit[i * s + j] != 0.0)
+                return fail(nullptr, RIDC_E_CONFIG, "a_explicit must be strictly lower triangular");
+        }
+    ridc_ark_ctx* a = new ridc_ark_ctx();
+    auto bail = [&](int code) {
+        std::string m = a->err.empty() ? g_last_error : a->err;
+        ridc_ark_destroy(a);
+        g_last_error = m;
+        return code;
+    };
+#define ARK_TRY(expr)                                                                        \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            a->err = std::string(#expr " failed: ") + cudaGetErrorString(_e);               \
+            return bail(RIDC_E_CUDA);                                                        \
+        }                                                                                    \
+    } while (0)
+    a->device = device;
+    a->pb = make_problem(problem);
+    a->stages = s;
+    a->steps = steps;
+    a->dt = (t_end - t_start) / (double)steps;   // integrate_ark: uniform dt
+    a->V = (long long)problem->nx * problem->ny;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        a->err = "cudaSetDevice failed";
+        return bail(RIDC_E_CUDA);
+    }
+    if (cudaDeviceGetAttribute(&a->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) a->nsm = 148;
+    double amax = 0.0;
+    for (int i = 0; i < s; ++i) amax = std::max(amax, a_implicit[i * s + i]);
+    if ((rc = make_chunk_solve(a->pb, amax * a->dt, a->nsm, a->ss)) != RIDC_OK) {
+        a->err = a->ss.err;
+        return bail(rc);
+    }
+    a->Vs = (long long)a->pb.ny * a->ss.lay.P;
+    a->cap = 2 + s;
+    ARK_TRY(cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking));
+    ARK_TRY(cudaEventCreate(&a->ev0));
+    ARK_TRY(cudaEventCreate(&a->ev1));
+    ARK_TRY(cudaMalloc(&a->d_ring, (size_t)a->cap * a->Vs * sizeof(double)));
+    ARK_TRY(cudaMemset(a->d_ring, 0, (size_t)a->cap * a->Vs * sizeof(double)));   // Dirichlet ghosts stay 0
+    ARK_TRY(cudaMalloc(&a->d_cgeo, a->ss.cgeo.size() * sizeof(ChunkGeo)));
+    ARK_TRY(cudaMemcpy(a->d_cgeo, a->ss.cgeo.data(), a->ss.cgeo.size() * sizeof(ChunkGeo), cudaMemcpyHostToDevice));
+    ARK_TRY(cudaMalloc(&a->d_y0, (size_t)a->V * sizeof(double)));
+    ARK_TRY(cudaMalloc(&a->d_err, sizeof(unsigned long long)));
+    memset(&a->tm, 0, sizeof a->tm);
+    if ((rc = make_ring_map(&a->tm.map[0], a->d_ring, a->Vs, a->cap, a->ss.ccfg.nt, &a->err)) != RIDC_OK)
+        return bail(rc);
+    EngineParams& ep = a->ep;
+    memset(&ep, 0, sizeof ep);
+    ep.pb = a->pb;
+    ep.sv = a->ss.sv;
+    ep.V = a->V;
+    ep.Vs = a->Vs;
+    ep.dt = a->dt;
+    ep.levels = 1;
+    ep.ring[0] = a->d_ring;
+    ep.cap[0] = a->cap;
+    ep.err = a->d_err;
+    ep.lay = a->ss.lay;
+    ep.cgeo = a->d_cgeo;
+
+    // ---- the items of one step: stages with a nonzero diagonal or i > 0, then the final
+    // combination.  Y_0 aliases y_n when aI_00 = 0 (both paper tableaus).
+    const bool y0_alias = a_implicit[0] == 0.0;
+    auto slot_of_stage = [&](int j, int parity) -> long long { return (j == 0 && y0_alias) ? parity : 2 + j; };
+    std::vector<int> item_stage;   // stage index, s = final
+    for (int i = (y0_alias ? 1 : 0); i < s; ++i) item_stage.push_back(i);
+    item_stage.push_back(s);
+    a->nitems = (int)item_stage.size();
+    std::vector<StepItem> items(2 * a->nitems);
+    for (int parity = 0; parity < 2; ++parity)
+        for (int k = 0; k < a->nitems; ++k) {
+            const int i = item_stage[k];
+            const bool fin = i == s;
+            StepItem& it = items[parity * a->nitems + k];
+            memset(&it, 0, sizeof it);
+            it.level = fin ? 0 : 1;   // non-finite word: the final store of a step reports first
+            it.target = 0;            // the step number arrives per launch (TickParams.target)
+            int nn = 0;
+            auto add = [&](long long slot, double ca, double cs, double cn) {
+                it.vec[nn] = a->d_ring + slot * a->Vs;
+                it.vlev[nn] = 0;
+                it.vslot[nn] = slot;
+                it.ca[nn] = ca;
+                it.cs[nn] = cs;
+                it.cn[nn] = cn;
+                ++nn;
+            };
+            // y_n itself (ca = 1), merged with Y_0's stencil weights when Y_0 aliases it
+            const double* rs = fin ? b_implicit : a_implicit + i * s;
+            const double* rn = fin ? b_explicit : a_explicit + i * s;
+            const int upto = fin ? s : i;
+            if (y0_alias) add(parity, 1.0, upto > 0 ? a->dt * rs[0] : 0.0, upto > 0 ? a->dt * rn[0] : 0.0);
+            else add(parity, 1.0, 0.0, 0.0);
+            for (int j = y0_alias ? 1 : 0; j < upto; ++j)
+                if (rs[j] != 0.0 || rn[j] != 0.0) add(slot_of_stage(j, parity), 0.0, a->dt * rs[j], a->dt * rn[j]);
+            it.nnodes = nn;
+            const long long oslot = fin ? 1 - parity : slot_of_stage(i, parity);
+            it.out = a->d_ring + oslot * a->Vs;
+            it.out2 = nullptr;
+        }
+    // ---- per-item solves
+    a->solves.resize(a->nitems);
+    for (int k = 0; k < a->nitems; ++k) {
+        const int i = item_stage[k];
+        const double aii = i < s ? a_implicit[i * s + i] : 0.0;
+        ArkSolve& as = a->solves[k];
+        if (aii == 0.0) {
+            as.sv = identity_solve(a->ss.sv);
+            continue;
+        }
+        SolveSetup st;
+        make_factors(a->pb, aii * a->dt, st);
+        as.sv = st.sv;
+        as.sv.halo = a->ss.sv.halo;
+        as.sv.tile = a->ss.sv.tile;
+        as.sv.nseg = a->ss.sv.nseg;
+        if (!st.tab.empty()) {
+            ARK_TRY(cudaMalloc(&as.d_tab, st.tab.size() * sizeof(double)));
+            ARK_TRY(cudaMemcpy(as.d_tab, st.tab.data(), st.tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+            as.sv.tab_m = as.d_tab;
+            as.sv.tab_g = as.d_tab + as.sv.ntab;
+        }
+    }
+    ARK_TRY(cudaMalloc(&a->d_items, items.size() * sizeof(StepItem)));
+    ARK_TRY(cudaMemcpy(a->d_items, items.data(), items.size() * sizeof(StepItem), cudaMemcpyHostToDevice));
+
+    // ---- capture: seed y_0 into slot 0, then per step one launch per item
+    const int tiles = a->pb.ny * a->ss.sv.nseg;
+    cudaGraph_t graph = nullptr;
+    ARK_TRY(cudaStreamBeginCapture(a->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t le = cudaSuccess;
+    const int sb = (int)std::min<long long>((a->Vs + 255) / 256, 148 * 8);
+    k_seed_chunk<<<sb, 256, 0, a->stream>>>(a->d_y0, ep, -1);
+    le = cudaGetLastError();
+    long long launches = 1;
+    for (long long n = 0; n < steps && le == cudaSuccess; ++n) {
+        const int parity = (int)(n & 1);
+        for (int k = 0; k < a->nitems && le == cudaSuccess; ++k) {
+            TickParams tp;
+            memset(&tp, 0, sizeof tp);
+            tp.nact = 1;
+            tp.sv = a->solves[k].sv;
+            tp.pre = a->d_items + parity * a->nitems + k;
+            tp.target[0] = n + 1;
+            le = launch_chunk(a->pb.kind, a->ss.ccfg, std::min(a->nsm, tiles), a->stream, ep, tp, tiles, a->tm);
+            ++launches;
+        }
+    }
+    cudaError_t ce = cudaStreamEndCapture(a->stream, &graph);
+    if (le != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        a->err = std::string("ARK launch during capture: ") + cudaGetErrorString(le);
+        return bail(RIDC_E_CUDA);
+    }
+    ARK_TRY(ce);
+    cudaError_t ie = cudaGraphInstantiate(&a->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    ARK_TRY(ie);
+    a->launches = launches;
+#undef ARK_TRY
+    *out = a;
+    return RIDC_OK;
+}
+
+static int ark_march(ridc_ark_ctx* a, double* wall_seconds)
+{
+    CUDA_TRY(&a->err, cudaMemsetAsync(a->d_err, 0xff, sizeof(unsigned long long), a->stream));
+    CUDA_TRY(&a->err, cudaEventRecord(a->ev0, a->stream));
+    CUDA_TRY(&a->err, cudaGraphLaunch(a->gexec, a->stream));
+    CUDA_TRY(&a->err, cudaEventRecord(a->ev1, a->stream));
+    CUDA_TRY(&a->err, cudaEventSynchronize(a->ev1));
+    if (wall_seconds) {
+        float ms = 0.f;
+        CUDA_TRY(&a->err, cudaEventElapsedTime(&ms, a->ev0, a->ev1));
+        *wall_seconds = ms * 1e-3;
+    }
+    unsigned long long w = 0;
+    CUDA_TRY(&a->err, cudaMemcpy(&w, a->d_err, sizeof w, cudaMemcpyDeviceToHost));
+    if (w != ULLONG_MAX) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "ARK march produced non-finite entries at step %lld", (long long)(w >> 8));
+        return ark_fail(a, RIDC_E_NONFINITE, buf);   // steppers.py:153-154
+    }
+    return RIDC_OK;
+}
+
+static const double* ark_final(const ridc_ark_ctx* a) { return a->d_ring + (a->steps & 1) * a->Vs; }
+
+int ridc_ark_run(ridc_ark_ctx* a, const double* y0_host, double* final_host, double* wall_seconds)
+{
+    if (!a || !y0_host || !final_host) return ark_fail(a, RIDC_E_CONFIG, "NULL argument");
+    CUDA_TRY(&a->err, cudaSetDevice(a->device));
+    CUDA_TRY(&a->err, cudaMemcpyAsync(a->d_y0, y0_host, (size_t)a->V * sizeof(double), cudaMemcpyHostToDevice,
+                                      a->stream));
+    int rc = ark_march(a, wall_seconds);
+    if (rc) return rc;
+    const ChunkLayout& L = a->ss.lay;
+    CUDA_TRY(&a->err, cudaMemcpy2DAsync(final_host, (size_t)a->pb.nx * sizeof(double), ark_final(a) + L.GW,
+                                        (size_t)L.P * sizeof(double), (size_t)a->pb.nx * sizeof(double),
+                                        (size_t)a->pb.ny, cudaMemcpyDeviceToHost, a->stream));
+    CUDA_TRY(&a->err, cudaStreamSynchronize(a->stream));
+    return RIDC_OK;
+}
+
+int ridc_ark_run_device(ridc_ark_ctx* a, const double* y0_dev, double* final_dev, double* wall_seconds)
+{
+    if (!a || !y0_dev || !final_dev) return ark_fail(a, RIDC_E_CONFIG, "NULL argument");
+    CUDA_TRY(&a->err, cudaSetDevice(a->device));
+    CUDA_TRY(&a->err, cudaMemcpyAsync(a->d_y0, y0_dev, (size_t)a->V * sizeof(double), cudaMemcpyDeviceToDevice,
+                                      a->stream));
+    int rc = ark_march(a, wall_seconds);
+    if (rc) return rc;
+    const ChunkLayout& L = a->ss.lay;
+    CUDA_TRY(&a->err, cudaMemcpy2DAsync(final_dev, (size_t)a->pb.nx * sizeof(double), ark_final(a) + L.GW,
+                                        (size_t)L.P * sizeof(double), (size_t)a->pb.nx * sizeof(double),
+                                        (size_t)a->pb.ny, cudaMemcpyDeviceToDevice, a->stream));
+    CUDA_TRY(&a->err, cudaStreamSynchronize(a->stream));
+    return RIDC_OK;
+}
+
+int ridc_ark_info(const ridc_ark_ctx* a, int64_t* kernel_launches, int32_t* items_per_step)
+{
+    if (!a) return fail(nullptr, RIDC_E_CONFIG, "NULL argument");
+    if (kernel_launches) *kernel_launches = a->launches;
+    if (items_per_step) *items_per_step = a->nitems;
+    return RIDC_OK;
+}
+
+int ridc_ark_destroy(ridc_ark_ctx* a)
+{
+    if (!a) return RIDC_OK;
+    cudaSetDevice(a->device);
+    if (a->stream) cudaStreamSynchronize(a->stream);
+    if (a->gexec) cudaGraphExecDestroy(a->gexec);
+    for (ArkSolve& s : a->solves)
+        if (s.d_tab) cudaFree(s.d_tab);
+    if (a->d_ring) cudaFree(a->d_ring);
+    if (a->d_cgeo) cudaFree(a->d_cgeo);
+    if (a->d_items) cudaFree(a->d_items);
+    if (a->d_y0) cudaFree(a->d_y0);
+    if (a->d_err) cudaFree(a->d_err);
+    if (a->ev0) cudaEventDestroy(a->ev0);
+    if (a->ev1) cudaEventDestroy(a->ev1);
+    if (a->stream) cudaStreamDestroy(a->stream);
+    delete a;
+    return RIDC_OK;
+}
+
+const char* ridc_ark_last_error(const ridc_ark_ctx* a) { return a ? a->err.c_str() : g_last_error.c_str(); }
 
 }  // extern "C"

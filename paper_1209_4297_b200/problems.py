@@ -468,3 +468,24 @@ def exact_advection_diffusion(spec: AdvectionDiffusionSpec, t: float) -> np.ndar
     th = 2.0 * np.pi * spec.dx
     lam = (spec.c / spec.dx) * (np.exp(1j * th) - 1.0) + (2.0 * spec.d / spec.dx ** 2) * (math.cos(th) - 1.0)
     return 2.0 + np.imag(np.exp(lam * t) * np.exp(2j * np.pi * x))
+
+
+def reference_solution(problem, t_end: float, refinement: int, base_steps: int, solver=None) -> np.ndarray:
+    """Error baseline (problems.py:171-185): the same semi-discrete system marched
+    with the fourth-order ARK pair at ``refinement`` x the finest study step count,
+    on the device (steppers.integrate_ark)."""
+    from .steppers import integrate_ark
+    from .tableaus import imex4_tableau
+    if refinement < 8:
+        raise ConfigError(f"refinement must be >= 8, got {refinement}")
+    if base_steps < 1:
+        raise ConfigError("base_steps must be positive")
+    ivp = as_descriptor(problem)
+    return integrate_ark(ivp, imex4_tableau(), ivp.t_start, np.array(ivp.initial_state), t_end,
+                         refinement * base_steps)
+
+
+def error_norms(u: np.ndarray, ref: np.ndarray, dx: float) -> tuple:
+    """(max norm, dx-weighted discrete 2-norm) of u - ref (problems.py:188-193)."""
+    diff = np.asarray(u) - np.asarray(ref)
+    return float(np.abs(diff).max()), float(np.sqrt(dx * np.dot(diff, diff)))

@@ -28,3 +28,8 @@ def descriptor(d):
 def normwise(a, ref):
     """max|a - ref| / max|ref| (SURVEY.md §8c parity metric)."""
     return float(np.abs(np.asarray(a) - np.asarray(ref)).max() / np.abs(ref).max())
+
+
+def ark_cases():
+    cases, arrays = load()
+    return [c for c in cases if c["name"].startswith("ark/")], arrays

@@ -169,6 +169,37 @@ def main():
         add_run("rd2d_32x32_p3", rd2.problem, rd2.ivp.initial_state,
                 ref_ivp(rd2.problem, rd2.ivp.initial_state, 0.1), 0.1, 3, 30)
 
+        # --- ARK comparators (steppers.integrate_ark with the imex3 / imex4 pairs) --
+        from ridc import tableaus as RT
+
+        def add_ark(name, pd, ivp, y0, t_end, scheme, steps):
+            tab = RT.imex3_tableau() if scheme == "imex3" else RT.imex4_tableau()
+            solver = RS.ImplicitSolver()
+            final = RS.integrate_ark(ivp, tab, 0.0, np.array(y0), t_end, steps, solver)
+            arrays[f"ark/{name}/y0"] = np.asarray(y0)
+            arrays[f"ark/{name}/final"] = final
+            cases.append({"name": f"ark/{name}", "problem": desc_dict(pd), "t_end": t_end,
+                          "scheme": scheme, "steps": steps})
+            print(f"ark/{name}: |final|={np.abs(final).max():.6g}")
+
+        for scheme in ("imex3", "imex4"):
+            sysr = RP.build_advection_diffusion(RP.AdvectionDiffusionSpec(dx=1 / 128, t_end=0.5))
+            ours = P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 128, t_end=0.5))
+            add_ark(f"ad_n128_{scheme}", ours.problem, sysr.ivp, sysr.ivp.initial_state, 0.5, scheme, 40)
+            sysb = RP.build_burgers(RP.BurgersSpec(dx=1 / 256, t_end=0.5))
+            oursb = P.build_burgers(P.BurgersSpec(dx=1 / 256, t_end=0.5))
+            add_ark(f"bu_n255_{scheme}", oursb.problem, sysb.ivp, sysb.ivp.initial_state, 0.5, scheme, 500)
+        sysr = RP.build_advection_diffusion(RP.AdvectionDiffusionSpec(dx=1 / 1024, t_end=4.0))
+        ours = P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 1024, t_end=4.0))
+        add_ark("ad_c1_imex4", ours.problem, sysr.ivp, sysr.ivp.initial_state, 4.0, "imex4", 200)
+        rda = P.build_reaction_diffusion(P.ReactionDiffusionSpec(d=2e-2, n=512, t_end=0.4))
+        add_ark("rd_n512_stiff_imex3", rda.problem, ref_ivp(rda.problem, rda.ivp.initial_state, 0.4),
+                rda.ivp.initial_state, 0.4, "imex3", 40)
+        ad2a = P.build_advection_diffusion_2d(P.AdvectionDiffusion2DSpec(nx=32, ny=24, t_end=0.05,
+                                                                          dxx=2e-2, dyy=1e-3))
+        add_ark("ad2d_32x24_imex4", ad2a.problem, ref_ivp(ad2a.problem, ad2a.ivp.initial_state, 0.05),
+                ad2a.ivp.initial_state, 0.05, "imex4", 40)
+
         # --- single-step KATs ---------------------------------------------------
         solver = RS.ImplicitSolver()
         sc = RI.scalar_ivp(0.0, 1.0, 1.0, stiff_coeff=-1.0)

@@ -1,0 +1,80 @@
+"""Device ARK comparators (ridc_ark_*) vs the reference's integrate_ark
+golden vectors and the oracle; convergence orders 3 and 4 against the exact
+semi-discrete adv-diff solution (the paper's Fig. 4b / 6b comparators)."""
+
+import numpy as np
+import pytest
+
+import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle import oracle as O  # noqa: E402
+from paper_1209_4297_b200 import problems as P, steppers as S, studies  # noqa: E402
+from paper_1209_4297_b200.errors import NonFiniteStateError  # noqa: E402
+from paper_1209_4297_b200.tableaus import imex3_tableau, imex4_tableau  # noqa: E402
+
+ARK, ARR = G.ark_cases()
+
+
+def _tab(scheme):
+    return imex3_tableau() if scheme == "imex3" else imex4_tableau()
+
+
+@pytest.mark.parametrize("case", ARK, ids=[c["name"] for c in ARK])
+def test_device_ark_matches_reference_golden(case):
+    pd = G.descriptor(case["problem"])
+    y0 = ARR[case["name"] + "/y0"]
+    ivp = P.StructuredIVP(pd, 0.0, case["t_end"], y0)
+    tab = _tab(case["scheme"])
+    y = S.integrate_ark(ivp, tab, 0.0, y0, case["t_end"], case["steps"])
+    assert G.normwise(y, ARR[case["name"] + "/final"]) <= 1e-10
+    ref = O.ark(pd, tab.a_implicit, tab.a_explicit, tab.b_implicit, tab.b_explicit, y0, 0.0,
+                case["t_end"], case["steps"])
+    assert G.normwise(y, ref) <= 1e-10
+
+
+def test_segmented_long_line_against_oracle():
+    """C2-shaped grid (2^16 points, truncated-halo segments), imex4."""
+    s = P.reaction_diffusion_c2(n=1 << 16)
+    ivp = P.StructuredIVP(s.problem, 0.0, 0.002, s.ivp.initial_state)
+    tab = imex4_tableau()
+    with S.ArkEngine(ivp, tab, 0.0, 0.002, 20) as eng:
+        y, wall = eng.run(ivp.initial_state)
+        inf = eng.info
+    assert inf["items_per_step"] == tab.stages and inf["kernel_launches"] == 1 + 20 * tab.stages
+    ref = O.ark(s.problem, tab.a_implicit, tab.a_explicit, tab.b_implicit, tab.b_explicit,
+                ivp.initial_state, 0.0, 0.002, 20)
+    assert G.normwise(y, ref) <= 1e-10 and wall > 0
+
+
+@pytest.mark.parametrize("scheme,order", [("imex3", 3), ("imex4", 4)])
+def test_ark_order(scheme, order):
+    spec = P.AdvectionDiffusionSpec(dx=1 / 200, t_end=4.0)
+    s = P.build_advection_diffusion(spec)
+    exact = P.exact_advection_diffusion(spec, 4.0)
+    errs = [np.abs(studies.integrate_scheme(s, scheme, n)[0] - exact).max() for n in (50, 100, 200)]
+    slope = np.log(errs[-2] / errs[-1]) / np.log(2.0)
+    assert slope >= order - 0.3, (errs, slope)
+
+
+def test_ark_step_and_reference_solution():
+    s = P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 64, t_end=1.0))
+    tab = imex3_tableau()
+    y1 = S.ark_step(s, tab, 0.0, s.ivp.initial_state, 0.01)
+    ref = O.ark(s.problem, tab.a_implicit, tab.a_explicit, tab.b_implicit, tab.b_explicit,
+                s.ivp.initial_state, 0.0, 0.01, 1)
+    assert G.normwise(y1, ref) <= 1e-12
+    r = P.reference_solution(s, 1.0, 8, 10)
+    assert np.isfinite(r).all() and r.shape == s.ivp.initial_state.shape
+
+
+def test_ark_nonfinite_message():
+    s = P.build_burgers(P.BurgersSpec(dx=1 / 256, t_end=0.5))
+    with pytest.raises(NonFiniteStateError) as ei:
+        S.integrate_ark(s, imex3_tableau(), 0.0, s.ivp.initial_state, 0.5, 20)
+    assert str(ei.value).startswith("ARK march produced non-finite entries at step ")
