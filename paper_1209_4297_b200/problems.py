@@ -484,8 +484,3 @@ def reference_solution(problem, t_end: float, refinement: int, base_steps: int, 
     return integrate_ark(ivp, imex4_tableau(), ivp.t_start, np.array(ivp.initial_state), t_end,
                          refinement * base_steps)
 
-
-def error_norms(u: np.ndarray, ref: np.ndarray, dx: float) -> tuple:
-    """(max norm, dx-weighted discrete 2-norm) of u - ref (problems.py:188-193)."""
-    diff = np.asarray(u) - np.asarray(ref)
-    return float(np.abs(diff).max()), float(np.sqrt(dx * np.dot(diff, diff)))
