@@ -315,7 +315,7 @@ struct ChunkCfg {
     X(6, 256, 3, 2)
 
 template <int NT, int ROWS, int NSTAGE>
-ChunkCfg chunk_cfg_of(int id)
+ChunkCfg chunk_cfg_make(int id)
 {
     ChunkCfg c;
     c.id = id;
@@ -327,22 +327,42 @@ ChunkCfg chunk_cfg_of(int id)
     return c;
 }
 
+// the configuration with this id, as listed in RIDC_CHUNK_CONFIGS
+ChunkCfg chunk_cfg_of_id(int id)
+{
+#define RIDC_CFG_OF(ID, NT, ROWS, NSTAGE) \
+    if (id == ID) return chunk_cfg_make<NT, ROWS, NSTAGE>(ID);
+    RIDC_CHUNK_CONFIGS(RIDC_CFG_OF)
+#undef RIDC_CFG_OF
+    return chunk_cfg_make<512, 1, 3>(3);
+}
+
 // smallest config whose NT*16 points cover `points` (the item's staged range)
 ChunkCfg pick_chunk(int kind, int points)
 {
     const bool two_d = kind == ADV_DIFF_2D || kind == RD_2D;
     if (two_d) {
-        if (points <= 64 * 16) return chunk_cfg_of<64, 3, 3>(4);
-        if (points <= 128 * 16) return chunk_cfg_of<128, 3, 3>(5);
-        return chunk_cfg_of<256, 3, 2>(6);
+        if (points <= 64 * 16) return chunk_cfg_of_id(4);
+        if (points <= 128 * 16) return chunk_cfg_of_id(5);
+        return chunk_cfg_of_id(6);
     }
-    if (points <= 64 * 16) return chunk_cfg_of<64, 1, 4>(0);
-    if (points <= 128 * 16) return chunk_cfg_of<128, 1, 4>(1);
-    if (points <= 256 * 16) return chunk_cfg_of<256, 1, 4>(2);
-    return chunk_cfg_of<512, 1, 3>(3);
+    if (points <= 64 * 16) return chunk_cfg_of_id(0);
+    if (points <= 128 * 16) return chunk_cfg_of_id(1);
+    if (points <= 256 * 16) return chunk_cfg_of_id(2);
+    return chunk_cfg_of_id(3);
 }
 
-int chunk_points_max(int kind) { return (kind == ADV_DIFF_2D || kind == RD_2D) ? 256 * 16 : 512 * 16; }
+int chunk_points_max(int kind)
+{
+    if (kind == ADV_DIFF_2D || kind == RD_2D) return 256 * 16;
+    return 512 * 16;
+}
+
+// CTAs of the tick kernel per SM.  One: 4096-point items at two CTAs per SM
+// (256 threads, 3 stages) measured 1.7-2x slower than 8192-point items at one
+// (C5 sweep, N = 2^20..2^24): twice the halo overhead, and the static item
+// table keeps two CTAs from fitting the shared memory anyway.
+int chunk_ctas_per_sm(const ChunkCfg&) { return 1; }
 
 template <int KIND, int NT, int ROWS, int NSTAGE, int MODE>
 cudaError_t launch_chunk_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
@@ -907,7 +927,8 @@ int capture_graph(ridc_ctx* c)
                 }
             }
             if (tp.nact == 0) continue;
-            le = launch_chunk(c->pb.kind, c->ss.ccfg, std::min(c->nsm, tp.nact * items), c->stream, ep, tp,
+            le = launch_chunk(c->pb.kind, c->ss.ccfg, std::min(c->nsm * chunk_ctas_per_sm(c->ss.ccfg), tp.nact * items),
+                              c->stream, ep, tp,
                               items, c->tm);
             ++launches;
         }
@@ -1534,7 +1555,8 @@ int pipe_enqueue(ridc_pipe* p, int interval, long long* launches)
         tp.nact = 1;
         tp.level[0] = j;
         tp.target[0] = t;
-        cudaError_t le = launch_chunk(p->pb.kind, p->ss.ccfg, std::min(p->nsm, items), p->stream, ep, tp, items,
+        cudaError_t le = launch_chunk(p->pb.kind, p->ss.ccfg, std::min(p->nsm * chunk_ctas_per_sm(p->ss.ccfg), items),
+                                      p->stream, ep, tp, items,
                                       p->tm);
         if (le != cudaSuccess) return pipe_fail(p, RIDC_E_CUDA, std::string("tick launch: ") + cudaGetErrorString(le));
         ++n;
@@ -2094,7 +2116,8 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
             tp.sv = a->solves[k].sv;
             tp.pre = a->d_items + parity * a->nitems + k;
             tp.target[0] = n + 1;
-            le = launch_chunk(a->pb.kind, a->ss.ccfg, std::min(a->nsm, tiles), a->stream, ep, tp, tiles, a->tm);
+            le = launch_chunk(a->pb.kind, a->ss.ccfg, std::min(a->nsm * chunk_ctas_per_sm(a->ss.ccfg), tiles), a->stream,
+                              ep, tp, tiles, a->tm);
             ++launches;
         }
     }
