@@ -307,8 +307,13 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         const size_t rofs = (size_t)row * lay.P + lay.GW;   // data column 0 of my row
         double* o1 = it.out + rofs;
         double* o2 = it.out2 ? it.out2 + rofs : nullptr;
+        const bool mirror = o2 != nullptr;                  // item-uniform
         const int lo = cg.c0, hi = cg.c0 + cg.tlen;
         const int nx = pb.nx, GW = lay.GW;
+        // groups wholly inside the tile: [glo, ghi) relative to g0 (item-uniform)
+        const int glo = (lo - cg.g0 * K + K - 1) / K, ghi = (hi - cg.g0 * K) / K;
+        // only items touching a line end write periodic ghost copies
+        const bool ghosts = periodic && (lo < GW || hi > nx - GW);
 #pragma unroll
         for (int k = 0; k < K / 2; ++k) {
             const int q = tid + k * NT;           // 16-byte piece: group q/8, pair q%8
@@ -316,22 +321,22 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
             if (g < cg.ng) {
                 const double2 v = lds128(swz(sbufc, g, i));
                 const int c = (cg.g0 + g) * K + 2 * i;   // data column of v.x
-                if (c >= lo && c + 2 <= hi) {
+                if ((unsigned)(g - glo) < (unsigned)(ghi - glo)) {
                     chk = fma(v.x, 0.0, fma(v.y, 0.0, chk));
                     *reinterpret_cast<double2*>(o1 + c) = v;
-                    if (o2) *reinterpret_cast<double2*>(o2 + c) = v;
+                    if (mirror) *reinterpret_cast<double2*>(o2 + c) = v;
                 } else {
-                    if (c >= lo && c < hi) { chk = fma(v.x, 0.0, chk); o1[c] = v.x; if (o2) o2[c] = v.x; }
-                    if (c + 1 >= lo && c + 1 < hi) { chk = fma(v.y, 0.0, chk); o1[c + 1] = v.y; if (o2) o2[c + 1] = v.y; }
+                    if (c >= lo && c < hi) { chk = fma(v.x, 0.0, chk); o1[c] = v.x; if (mirror) o2[c] = v.x; }
+                    if (c + 1 >= lo && c + 1 < hi) { chk = fma(v.y, 0.0, chk); o1[c + 1] = v.y; if (mirror) o2[c + 1] = v.y; }
                 }
-                if (periodic && (c < GW || c + 2 > nx - GW)) {
+                if (ghosts && (c < GW || c + 2 > nx - GW)) {
                     const double vv2[2] = {v.x, v.y};
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int cc = c + h;
                         if (cc >= lo && cc < hi) {
-                            if (cc < GW) { o1[cc + nx] = vv2[h]; if (o2) o2[cc + nx] = vv2[h]; }
-                            if (cc >= nx - GW) { o1[cc - nx] = vv2[h]; if (o2) o2[cc - nx] = vv2[h]; }
+                            if (cc < GW) { o1[cc + nx] = vv2[h]; if (mirror) o2[cc + nx] = vv2[h]; }
+                            if (cc >= nx - GW) { o1[cc - nx] = vv2[h]; if (mirror) o2[cc - nx] = vv2[h]; }
                         }
                     }
                 }
