@@ -42,6 +42,10 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// phase-trace buffer (RIDC_PHASE_TIMING): 8 rows x 16 stamps of CTA 0, then per
+// CTA (entry, wait-done, exit) globaltimer of tick target 100
+constexpr int kDbgWords = 128 + 4 * 1024;
+
 struct EngineParams {
     DevProblem pb;
     DevSolve sv;
@@ -117,9 +121,21 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
     it.out2 = ep.mirror ? ep.mirror + ((ep.mirror_off + t) % ep.mirror_cap) * ep.Vs : nullptr;
 }
 
+// Item i of a tick -> (level slot, tile): tile = i % tiles, slot = (i / tiles
+// + tile) % nact.  A bijection (each tile meets every slot once), and a CTA
+// taking items b, b + grid, ... gets a mix of levels: with the plain
+// slot = i % nact a CTA would run the same level for every one of its items
+// whenever the grid is a multiple of nact, and the top level's CTAs ((j+2)
+// nodes per item) would set the tick time.
+__device__ __forceinline__ void item_of(int i, int tiles, int nact, int& slot, int& tile)
+{
+    tile = i % tiles;
+    slot = (i / tiles + tile) % nact;
+}
+
 // The production tick kernel: persistent CTAs of NT compute threads; thread
 // 0 doubles as the TMA producer (ridc_chunk.cuh).  Items of the tick are
-// dealt round-robin: item i -> level slot i % nact, tile i / nact.  MODE is
+// dealt round-robin over the CTAs (item_of).  MODE is
 // the solve mode all segments share (0 truncated, 1 cyclic whole line, 2
 // Dirichlet whole line), or -1 to dispatch per segment -- one mode per
 // kernel keeps the hot loop small in the instruction cache.
@@ -137,6 +153,18 @@ __global__ void __launch_bounds__(NT, 1)
     __shared__ Aff swarp[2 * (NT / 32) + 1];
     const int total = tp.nact * ipl;
     const DevSolve& sv = tp.sv;
+    // phase trace (RIDC_PHASE_TIMING): CTA 0 / thread 0 globaltimer at entry, after the
+    // grid dependency wait and at exit, row = target & 7 of the first active level
+    long long* tdbg = (sv.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? sv.dbg + (tp.target[0] & 7) * 16 : nullptr;
+    auto gtime = [] {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        return (long long)g;
+    };
+    if (tdbg) tdbg[10] = gtime();
+    long long* cdbg = (sv.dbg && threadIdx.x == 0 && tp.target[0] == 100 && blockIdx.x < 1024)
+                          ? sv.dbg + 128 + 4 * blockIdx.x : nullptr;
+    if (cdbg) cdbg[0] = gtime();
     const int nseg = sv.nseg, ny = ep.pb.ny;
     // programmatic dependent launch: let the next tick's grid get scheduled now;
     // its CTAs run this prologue as SMs free up and wait (below) before reading
@@ -161,7 +189,8 @@ __global__ void __launch_bounds__(NT, 1)
     // producer cursor (thread 0): next (item, node) to load and its load number
     LoadCursor pc{(int)blockIdx.x, 0, 0};
     auto issue_next = [&](int s) {
-        const int slot = pc.i % tp.nact, tile = pc.i / tp.nact;
+        int slot, tile;
+        item_of(pc.i, ipl, tp.nact, slot, tile);
         const int row = tile / nseg, seg = tile - row * nseg;
         const StepItem& it = items[slot];
         issue_chunk_node<NT, ROWS, NSTAGE>(tm, it.vlev[pc.a], it.vslot[pc.a], row, ny, ep.lay.gpr,
@@ -175,6 +204,8 @@ __global__ void __launch_bounds__(NT, 1)
     // everyone else reads / writes only after that load's barrier
     if (threadIdx.x == 0) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (tdbg) tdbg[11] = gtime();
+        if (cdbg) cdbg[1] = gtime();
         for (int k = 0; k < NSTAGE && pc.i < total; ++k) issue_next(k);
     }
     // after load n was released from stage s: wait for every warp, then load n + NSTAGE into s
@@ -187,7 +218,8 @@ __global__ void __launch_bounds__(NT, 1)
     int ino = 0;
     const FastLane fl = fast_lane<kChunk>(sv);
     for (int i = blockIdx.x; i < total; i += gridDim.x, ++ino) {
-        const int slot = i % tp.nact, tile = i / tp.nact;
+        int slot, tile;
+        item_of(i, ipl, tp.nact, slot, tile);
         const int row = tile / nseg, seg = tile - row * nseg;
         const ChunkGeo cg = ep.cgeo[seg];
         switch (MODE >= 0 ? MODE : cg.mode) {
@@ -205,6 +237,8 @@ __global__ void __launch_bounds__(NT, 1)
         }
         csync<NT>();   // edge / scan scratch reuse by the next item
     }
+    if (tdbg) tdbg[12] = gtime();
+    if (cdbg) cdbg[2] = gtime();
 }
 
 // state (plain [ny][nx]) -> slot 0 of every level ring, padded layout with ghosts
@@ -1141,8 +1175,8 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     CTX_TRY(cudaMemcpy(c->d_cgeo, c->ss.cgeo.data(), c->ss.cgeo.size() * sizeof(ChunkGeo),
                        cudaMemcpyHostToDevice));
     if (getenv("RIDC_PHASE_TIMING") && atoi(getenv("RIDC_PHASE_TIMING")) > 0) {
-        CTX_TRY(cudaMalloc(&c->d_dbg, 128 * sizeof(long long)));
-        CTX_TRY(cudaMemset(c->d_dbg, 0, 128 * sizeof(long long)));
+        CTX_TRY(cudaMalloc(&c->d_dbg, kDbgWords * sizeof(long long)));
+        CTX_TRY(cudaMemset(c->d_dbg, 0, kDbgWords * sizeof(long long)));
         c->ss.sv.dbg = c->d_dbg;
     }
     memset(&c->tm, 0, sizeof c->tm);
@@ -1389,7 +1423,7 @@ int ridc_debug_phase_trace(const ridc_ctx* c, long long* out, int n)
 {
     if (!c || !out || n < 128) return fail(nullptr, RIDC_E_CONFIG, "need a 128-entry buffer");
     if (!c->d_dbg) return fail(nullptr, RIDC_E_CONFIG, "create with RIDC_PHASE_TIMING=1");
-    CUDA_TRY(nullptr, cudaMemcpy(out, c->d_dbg, 128 * sizeof(long long), cudaMemcpyDeviceToHost));
+    CUDA_TRY(nullptr, cudaMemcpy(out, c->d_dbg, std::min(n, kDbgWords) * sizeof(long long), cudaMemcpyDeviceToHost));
     return RIDC_OK;
 }
 

@@ -34,8 +34,8 @@ print(f"{cfg['workload']} p={a.order} nt={nt}: {t*1e3:.3f} ms/solve, {t/ (nt + a
 if os.environ.get("RIDC_PHASE_TIMING"):
     import ctypes
     from paper_1209_4297_b200 import _lib
-    buf = (ctypes.c_longlong * 128)()
-    _lib.check(_lib.lib().ridc_debug_phase_trace(eng._h, buf, 128))
+    buf = (ctypes.c_longlong * (128 + 4096))()
+    _lib.check(_lib.lib().ridc_debug_phase_trace(eng._h, buf, 128 + 4096))
     names = ["start", "node0", "accum", "stencil", "fwd", "scan1", "carry+bwd", "scan2", "store0", "end"]
     for it in range(8):
         st = [buf[it * 16 + k] for k in range(10)]
@@ -44,6 +44,22 @@ if os.environ.get("RIDC_PHASE_TIMING"):
         d = [st[k] - st[k - 1] for k in range(1, 10)]
         print(f"item {it}: " + " ".join(f"{names[k]}:{d[k-1]}" for k in range(1, 10)),
               f"| total {st[9] - st[0]} cyc" + (f", gap from prev {st[0] - buf[(it - 1) * 16 + 9]}" if it else ""))
+    if eng.info["kernel_launches"] > 2:   # tick kernel: per-tick globaltimer (ns) of CTA 0
+        rows = sorted((buf[r * 16 + 10], buf[r * 16 + 11], buf[r * 16 + 12]) for r in range(8) if buf[r * 16 + 10])
+        for i, (a, b, c) in enumerate(rows):
+            gap = f", gap from prev exit {a - rows[i - 1][2]} ns" if i else ""
+            print(f"tick: entry->wait-done {b - a} ns, wait-done->exit {c - b} ns{gap}")
+        ctas = [(buf[128 + 4 * b], buf[128 + 4 * b + 1], buf[128 + 4 * b + 2]) for b in range(1024)
+                if buf[128 + 4 * b]]
+        if ctas:
+            t0 = min(c[0] for c in ctas)
+            ent = sorted(c[0] - t0 for c in ctas)
+            wd = sorted(c[1] - t0 for c in ctas)
+            ex = sorted(c[2] - t0 for c in ctas)
+            work = sorted(c[2] - c[1] for c in ctas)
+            print(f"tick 100, {len(ctas)} CTAs (ns from first entry): entry {ent[0]}..{ent[-1]}, "
+                  f"wait-done {wd[0]}..{wd[-1]}, exit {ex[0]}..{ex[-1]}, "
+                  f"work min/med/max {work[0]}/{work[len(work) // 2]}/{work[-1]}")
     if eng.info["kernel_launches"] == 2:   # resident march: stamps of CTA 0, thread 0 (steps 1-4, last 4)
         rn = ["wait", "load", "compute", "publish", "sync"]
         for r in range(8):
