@@ -1000,7 +1000,7 @@ int march(ridc_ctx* c, double* wall_seconds)
     CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
     if (c->resident) {
         const int nseg = c->ss.sv.nseg;
-        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, (nseg + 1) * sizeof(unsigned), c->stream));
+        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, (32 * nseg + 1) * sizeof(unsigned), c->stream));
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
         EngineParams ep = interval_params(c, 0);
         const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
@@ -1021,7 +1021,7 @@ int march(ridc_ctx* c, double* wall_seconds)
     }
     if (c->resident) {
         unsigned ab = 0;
-        CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_flags + c->ss.sv.nseg, sizeof ab, cudaMemcpyDeviceToHost));
+        CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_flags + 32 * c->ss.sv.nseg, sizeof ab, cudaMemcpyDeviceToHost));
         if (ab) return fail(&c->err, RIDC_E_PROTOCOL, "resident march: a neighbour segment wait timed out");
     }
     return check_err_word(c);
@@ -1063,7 +1063,7 @@ int setup_resident(ridc_ctx* c)
         cudaGetLastError();
         return RIDC_OK;
     }
-    CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, (nseg + 1) * sizeof(unsigned)));
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, (32 * nseg + 1) * sizeof(unsigned)));
     rp.pb = c->pb;
     rp.sv = ss.sv;
     rp.lay = ss.lay;
@@ -1077,7 +1077,7 @@ int setup_resident(ridc_ctx* c)
     rp.edge_w = W;
     rp.full_every = (c->flags & RIDC_RECORD_TRAJECTORY) ? 1 : 0;
     rp.flags = c->d_flags;
-    rp.abort = c->d_flags + nseg;
+    rp.abort = c->d_flags + 32 * nseg;
     rp.err = c->d_err;
     rp.spin_limit = 4000000000LL;   // ~2 s at 1.9 GHz per neighbour wait
     rp.dbg = c->d_dbg;

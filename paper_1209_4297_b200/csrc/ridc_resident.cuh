@@ -40,7 +40,7 @@ struct ResidentParams {
     long long per;           // steps per restart interval (error-step numbering)
     int edge_w;              // columns within edge_w of a tile end are published every step
     int full_every;          // 1: publish whole tiles every step (trajectory recording)
-    unsigned* flags;         // per segment: last published step (zeroed before the launch)
+    unsigned* flags;         // [segment][warp]: last published step (zeroed before the launch)
     unsigned long long* err; // earliest non-finite (step, level), atomicMin
     unsigned* abort;         // watchdog: set when a neighbour wait times out
     long long spin_limit;    // watchdog budget per wait (clock64 cycles)
@@ -74,6 +74,8 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v)
 {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+
+__device__ __forceinline__ int floor_div_dev(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 // 16 consecutive doubles from L2 (bypassing L1: other SMs wrote them)
 __device__ __forceinline__ void load_chunk_cg(const double* src, double (&u)[kChunk])
@@ -125,8 +127,35 @@ __device__ __forceinline__ bool chunk_finite(const double (&u)[kChunk])
     return c == c;
 }
 
+// Owner (segment, warp) of data column c (periodic: wrapped) in the tiling:
+// the warp whose thread holds c inside its segment's tile.  Groups are
+// 16-column aligned globally, so a thread's 16 columns have at most two owners
+// (two only across a periodic wrap with nx % 16 != 0).
+__device__ __forceinline__ int owner_flag(const ResidentParams& rp, int c)
+{
+    const int nx = rp.pb.nx, nseg = rp.sv.nseg, T = rp.sv.tile;
+    if (c < 0) c += nx;
+    else if (c >= nx) c -= nx;
+    int sg = min(c / T, nseg - 1);
+    while (sg > 0 && c < rp.cgeo[sg].c0) --sg;
+    while (sg + 1 < nseg && c >= rp.cgeo[sg].c0 + rp.cgeo[sg].tlen) ++sg;
+    const int t = floor_div_dev(c, kChunk) - rp.cgeo[sg].g0;
+    return sg * 32 + (t >> 5);
+}
+
 // MODE: the solve mode every segment shares (0 truncated, 1 cyclic whole
 // line, 2 Dirichlet ends), or -1 to dispatch per segment.
+//
+// Neighbour protocol (segmented lines): there is no per-step CTA barrier.
+// A warp holding tile columns a neighbour's halo reads (the "edge" warps)
+// stores them to ring slot s % cap after step s, then lane 0 release-stores
+// flag[segment][warp] = s.  A halo thread acquire-polls the one or two flags
+// owning its 16 columns before reloading them for step s+1.  Interior warps
+// never wait: they accumulate and run their local recurrences until the
+// block scan's barrier.  Ring slots are race-free because any step-s flag of
+// a neighbour implies that neighbour already consumed (through its block
+// scans) the step s-1 columns it read from us, and we only overwrite that
+// slot after seeing such a flag for step s.
 template <int KIND, int NT, int MODE>
 __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__ ResidentParams rp)
 {
@@ -135,25 +164,31 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
     constexpr bool periodic = KIND != BURGERS_1D;
     __shared__ double edge[4 * NT];
     __shared__ Aff swarp[2 * (NT / 32) + 1];
-    __shared__ int s_stop;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int seg = blockIdx.x, nseg = rp.sv.nseg;
     const ChunkGeo cg = rp.cgeo[seg];
     const bool mine = tid < cg.ng;
     const int col0 = (cg.g0 + tid) * K;   // data column of my first point
     const int lo = cg.c0, hi = cg.c0 + cg.tlen;
     const int nx = rp.pb.nx, GW = rp.lay.GW, W = rp.edge_w;
-    // halo chunk: (partly) outside my tile -- reloaded every step from the
-    // neighbour on that side (W < tile length: a halo reaches one neighbour)
+    // halo chunk: (partly) outside my tile -- reloaded every step from its owners
     const bool halo = mine && nseg > 1 && (col0 < lo || col0 + K > hi);
-    const int nb = !halo ? -1
-                         : (col0 < lo ? (seg > 0 ? seg - 1 : (periodic ? nseg - 1 : -1))
-                                      : (seg + 1 < nseg ? seg + 1 : (periodic ? 0 : -1)));
-    // interior chunk: all 16 columns in my tile and >= W from both ends (no
-    // neighbour reads them, no periodic ghost copies: W >= GW)
-    const bool interior = mine && col0 - lo >= W && hi - (col0 + K) >= W;
-    if (tid == 0) s_stop = 0;
-    __syncthreads();
+    int wf0 = -1, wf1 = -1;   // flags to acquire before the reload
+    if (halo) {
+        for (int e = 0; e < K; ++e) {
+            const int c = col0 + e;
+            if (c >= lo && c < hi) continue;                      // my own column
+            if (!periodic && (c < 0 || c >= nx)) continue;        // Dirichlet ghost (zero)
+            const int f = owner_flag(rp, c);
+            if (wf0 < 0) wf0 = f;
+            else if (f != wf0) wf1 = f;
+        }
+    }
+    // edge chunk: tile columns a neighbour's halo (or a periodic ghost) reads
+    const bool pub = mine && nseg > 1 && col0 + K > lo && col0 < hi && (col0 - lo < W || hi - (col0 + K) < W);
+    const bool pub_warp = __any_sync(0xffffffffu, pub);
+    const bool inside = mine && col0 >= lo && col0 + K <= hi;
+    unsigned* my_flag = rp.flags + seg * 32 + (tid >> 5);
 
     double u[K];
 #pragma unroll
@@ -161,6 +196,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
     if (mine) load_chunk_cg(rp.ring + GW + col0, u);   // slot 0: the seeded initial state
     long long cur = 0;                                  // ring slot of step s-1
     const FastLane fl = fast_lane<K>(rp.sv);
+    bool dead = false;                                  // watchdog fired: stop waiting, drain
 
     for (long long s = 1; s <= rp.steps; ++s) {
         const double* prev = rp.ring + cur * rp.Vs + GW;
@@ -168,19 +204,24 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
         double* out = rp.ring + cur * rp.Vs + GW;
         RIDC_RSTAMP(rp, s, 0);
         if (s > 1 && halo) {
-            // acquire the neighbour's step s-1 publication, then reload my chunk
-            if (nb >= 0) {
-                const unsigned want = (unsigned)(s - 1);
-                const long long t0 = clock64();
-                while (ld_acquire_u32(rp.flags + nb) < want)
+            const unsigned want = (unsigned)(s - 1);
+            const long long t0 = clock64();
+            for (int k = 0; k < 2; ++k) {
+                const int f = k == 0 ? wf0 : wf1;
+                if (f < 0) continue;
+                while (!dead && ld_acquire_u32(rp.flags + f) < want)
                     if (clock64() - t0 > rp.spin_limit || *(volatile unsigned*)rp.abort) {
                         atomicExch(rp.abort, 1u);
-                        s_stop = 1;
-                        break;
+                        dead = true;
                     }
             }
             RIDC_RSTAMP(rp, s, 1);
             load_chunk_cg(prev + col0, u);
+            if (!periodic) {   // Dirichlet ghosts beyond the line stay zero
+#pragma unroll
+                for (int e = 0; e < K; ++e)
+                    if (col0 + e < 0 || col0 + e >= nx) u[e] = 0.0;
+            }
         }
         RIDC_RSTAMP(rp, s, 2);
         if (MODE >= 0) {
@@ -195,22 +236,35 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
         RIDC_RSTAMP(rp, s, 3);
         const bool full = s == rp.steps || rp.full_every;
         bool bad = false;
-        if (interior) {
+        if (inside && !pub) {
             bad = !chunk_finite(u);
             if (full) {
 #pragma unroll
                 for (int e = 0; e < K; e += 2)
                     *reinterpret_cast<double2*>(out + col0 + e) = make_double2(u[e], u[e + 1]);
             }
+        } else if (inside) {
+            bad = !chunk_finite(u);
+#pragma unroll
+            for (int e = 0; e < K; e += 2)
+                *reinterpret_cast<double2*>(out + col0 + e) = make_double2(u[e], u[e + 1]);
+            if (periodic && (col0 < GW || col0 + K > nx - GW)) {
+#pragma unroll
+                for (int e = 0; e < K; ++e) {
+                    const int c = col0 + e;
+                    if (c < GW) out[c + nx] = u[e];
+                    if (c >= nx - GW) out[c - nx] = u[e];
+                }
+            }
         } else if (mine) {
-            // tile-edge chunk: per-column ownership, publication and periodic ghosts
+            // chunk straddling a tile end (or wholly in the halo)
             double chk = 0.0;
 #pragma unroll
             for (int e = 0; e < K; ++e) {
                 const int c = col0 + e;
                 if (c >= lo && c < hi) {
                     chk = fma(u[e], 0.0, chk);
-                    if (full || c - lo < W || hi - 1 - c < W) out[c] = u[e];
+                    if (pub || full) out[c] = u[e];
                     if (periodic && c < GW) out[c + nx] = u[e];
                     if (periodic && c >= nx - GW) out[c - nx] = u[e];
                 }
@@ -218,11 +272,13 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
             bad = chk != chk;
         }
         if (bad) atomicMin(rp.err, err_code((s - 1) % rp.per + 1, 0));
+        if (pub_warp) {
+            // the warp's stores, then one release of its step flag
+            __syncwarp();
+            if (lane == 0) st_release_u32(my_flag, (unsigned)s);
+        }
         RIDC_RSTAMP(rp, s, 4);
-        __syncthreads();   // publication complete (and shared scratch free for the next step)
         RIDC_RSTAMP(rp, s, 5);
-        if (s_stop) return;
-        if (nseg > 1 && tid == 0) st_release_u32(rp.flags + seg, (unsigned)s);
     }
 }
 

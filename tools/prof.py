@@ -16,6 +16,7 @@ ap.add_argument("--order", type=int, default=1)
 ap.add_argument("--nt", type=int, default=200)
 ap.add_argument("--points", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--resident", action="store_true", help="resident march on segmented lines (levels == 1)")
 a = ap.parse_args()
 sysm, nt, cfg = bench.workload(a.workload, a.points or None, None)
 full_nt = nt
@@ -25,7 +26,7 @@ from paper_1209_4297_b200 import problems as P  # noqa: E402
 ivp = sysm.ivp
 sysm = P.StructuredIVP(ivp.problem, ivp.t_start, ivp.t_start + (ivp.t_end - ivp.t_start) * nt / full_nt,
                        ivp.initial_state)
-eng = E.Engine(sysm, E.RidcConfig(levels=a.order, steps=nt))
+eng = E.Engine(sysm, E.RidcConfig(levels=a.order, steps=nt), resident_segments=a.resident)
 y0 = torch.from_numpy(np.array(sysm.initial_state)).cuda()
 out = torch.empty_like(y0)
 for _ in range(a.reps):

@@ -20,7 +20,7 @@ y0 = torch.from_numpy(np.array(sysm.initial_state)).cuda()
 out = torch.empty_like(y0)
 for rep in range(3):
     for tick in (False, True):
-        with E.Engine(sysm, E.RidcConfig(levels=1, steps=nt), tick_only=tick) as eng:
+        with E.Engine(sysm, E.RidcConfig(levels=1, steps=nt), tick_only=tick, resident_segments=not tick) as eng:
             eng.run_device(y0, out)
             ts = [eng.run_device(y0, out) for _ in range(3)]
         print(f"{wl} n={sysm.problem.dimension} {'tick' if tick else 'resident'}: {min(ts) / nt * 1e6:.2f} us/step (min of 3)", flush=True)
