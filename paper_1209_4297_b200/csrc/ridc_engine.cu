@@ -835,7 +835,9 @@ struct ridc_ctx {
     // resident single-level march (ridc_resident.cuh)
     bool resident = false;
     int res_mode = -1;             // common segment mode of the resident kernel (-1: mixed)
-    unsigned* d_flags = nullptr;   // per segment published step, then the abort word
+    unsigned* d_flags = nullptr;   // the watchdog abort word
+    uint4* d_mail = nullptr;       // tagged mailbox lines (2 parities x Vs)
+    unsigned tag_next = 1;         // next run's epoch
     ResidentParams rp;
     std::string err;
 };
@@ -1000,7 +1002,14 @@ int march(ridc_ctx* c, double* wall_seconds)
     CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
     if (c->resident) {
         const int nseg = c->ss.sv.nseg;
-        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, (32 * nseg + 1) * sizeof(unsigned), c->stream));
+        // each run tags its mailbox lines with a fresh epoch (no per-run clearing)
+        if ((unsigned long long)c->tag_next + c->steps + 2 >= 0xffffffffull) {
+            CUDA_TRY(&c->err, cudaMemsetAsync(c->d_mail, 0, 2 * (size_t)c->Vs * sizeof(uint4), c->stream));
+            c->tag_next = 1;
+        }
+        c->rp.tag0 = c->tag_next;
+        c->tag_next += (unsigned)c->steps + 1;
+        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, sizeof(unsigned), c->stream));
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
         EngineParams ep = interval_params(c, 0);
         const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
@@ -1021,7 +1030,7 @@ int march(ridc_ctx* c, double* wall_seconds)
     }
     if (c->resident) {
         unsigned ab = 0;
-        CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_flags + 32 * c->ss.sv.nseg, sizeof ab, cudaMemcpyDeviceToHost));
+        CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_flags, sizeof ab, cudaMemcpyDeviceToHost));
         if (ab) return fail(&c->err, RIDC_E_PROTOCOL, "resident march: a neighbour segment wait timed out");
     }
     return check_err_word(c);
@@ -1063,7 +1072,11 @@ int setup_resident(ridc_ctx* c)
         cudaGetLastError();
         return RIDC_OK;
     }
-    CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, (32 * nseg + 1) * sizeof(unsigned)));
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, sizeof(unsigned)));
+    if (nseg > 1) {
+        CUDA_TRY(&c->err, cudaMalloc(&c->d_mail, 2 * (size_t)c->Vs * sizeof(uint4)));
+        CUDA_TRY(&c->err, cudaMemset(c->d_mail, 0, 2 * (size_t)c->Vs * sizeof(uint4)));
+    }
     rp.pb = c->pb;
     rp.sv = ss.sv;
     rp.lay = ss.lay;
@@ -1076,8 +1089,8 @@ int setup_resident(ridc_ctx* c)
     rp.per = c->per;
     rp.edge_w = W;
     rp.full_every = (c->flags & RIDC_RECORD_TRAJECTORY) ? 1 : 0;
-    rp.flags = c->d_flags;
-    rp.abort = c->d_flags + 32 * nseg;
+    rp.mail = c->d_mail;
+    rp.abort = c->d_flags;
     rp.err = c->d_err;
     rp.spin_limit = 4000000000LL;   // ~2 s at 1.9 GHz per neighbour wait
     rp.dbg = c->d_dbg;
@@ -1290,6 +1303,7 @@ int ridc_destroy(ridc_ctx* c)
     if (c->d_y0) cudaFree(c->d_y0);
     if (c->d_err) cudaFree(c->d_err);
     if (c->d_flags) cudaFree(c->d_flags);
+    if (c->d_mail) cudaFree(c->d_mail);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);

@@ -40,7 +40,8 @@ struct ResidentParams {
     long long per;           // steps per restart interval (error-step numbering)
     int edge_w;              // columns within edge_w of a tile end are published every step
     int full_every;          // 1: publish whole tiles every step (trajectory recording)
-    unsigned* flags;         // [segment][warp]: last published step (zeroed before the launch)
+    uint4* mail;             // mailbox: 2 parities x Vs tagged lines (padded column index)
+    unsigned tag0;           // run epoch: step s is tagged tag0 + s
     unsigned long long* err; // earliest non-finite (step, level), atomicMin
     unsigned* abort;         // watchdog: set when a neighbour wait times out
     long long spin_limit;    // watchdog budget per wait (clock64 cycles)
@@ -73,6 +74,33 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p)
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v)
 {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Low-latency mailbox line (the LL format of NCCL's low-latency protocol): one
+// value per 16-byte line {lo32, tag, hi32, tag}, written by one vector store,
+// so a reader that sees both tags equal to the step it wants has the value --
+// no separate flag, no writer-side fence.
+__device__ __forceinline__ void st_line(uint4* p, double v, unsigned tag)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)b), "r"(tag),
+                 "r"((unsigned)(b >> 32)), "r"(tag)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_line(const uint4* p)
+{
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ double line_value(uint4 v)
+{
+    return __longlong_as_double((long long)(((unsigned long long)v.z << 32) | v.x));
 }
 
 __device__ __forceinline__ int floor_div_dev(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
@@ -127,35 +155,20 @@ __device__ __forceinline__ bool chunk_finite(const double (&u)[kChunk])
     return c == c;
 }
 
-// Owner (segment, warp) of data column c (periodic: wrapped) in the tiling:
-// the warp whose thread holds c inside its segment's tile.  Groups are
-// 16-column aligned globally, so a thread's 16 columns have at most two owners
-// (two only across a periodic wrap with nx % 16 != 0).
-__device__ __forceinline__ int owner_flag(const ResidentParams& rp, int c)
-{
-    const int nx = rp.pb.nx, nseg = rp.sv.nseg, T = rp.sv.tile;
-    if (c < 0) c += nx;
-    else if (c >= nx) c -= nx;
-    int sg = min(c / T, nseg - 1);
-    while (sg > 0 && c < rp.cgeo[sg].c0) --sg;
-    while (sg + 1 < nseg && c >= rp.cgeo[sg].c0 + rp.cgeo[sg].tlen) ++sg;
-    const int t = floor_div_dev(c, kChunk) - rp.cgeo[sg].g0;
-    return sg * 32 + (t >> 5);
-}
-
 // MODE: the solve mode every segment shares (0 truncated, 1 cyclic whole
 // line, 2 Dirichlet ends), or -1 to dispatch per segment.
 //
-// Neighbour protocol (segmented lines): there is no per-step CTA barrier.
-// A warp holding tile columns a neighbour's halo reads (the "edge" warps)
-// stores them to ring slot s % cap after step s, then lane 0 release-stores
-// flag[segment][warp] = s.  A halo thread acquire-polls the one or two flags
-// owning its 16 columns before reloading them for step s+1.  Interior warps
-// never wait: they accumulate and run their local recurrences until the
-// block scan's barrier.  Ring slots are race-free because any step-s flag of
-// a neighbour implies that neighbour already consumed (through its block
-// scans) the step s-1 columns it read from us, and we only overwrite that
-// slot after seeing such a flag for step s.
+// Neighbour protocol (segmented lines): no per-step CTA barrier, no fences.
+// Threads holding tile columns a neighbour's halo reads (edge chunks, and
+// their periodic ghost copies) write each new value as a tagged mailbox line
+// of parity s & 1 right after step s.  A halo thread polls the last line of
+// its chunk until the tag reads tag0 + s, then reads all 16 lines and re-polls
+// any whose tags are not yet current (one line in flight while waiting keeps
+// the polling traffic off the L2).  Interior warps never wait: they
+// accumulate and run their local recurrences until the block scan's barrier.
+// Parity buffers are race-free: a segment overwrites its step-s lines at step
+// s+2 only after reading the neighbour's step s+1 lines, which the neighbour
+// wrote after consuming (through its block scans) the step-s lines.
 template <int KIND, int NT, int MODE>
 __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__ ResidentParams rp)
 {
@@ -164,63 +177,60 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
     constexpr bool periodic = KIND != BURGERS_1D;
     __shared__ double edge[4 * NT];
     __shared__ Aff swarp[2 * (NT / 32) + 1];
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const int seg = blockIdx.x, nseg = rp.sv.nseg;
     const ChunkGeo cg = rp.cgeo[seg];
     const bool mine = tid < cg.ng;
     const int col0 = (cg.g0 + tid) * K;   // data column of my first point
     const int lo = cg.c0, hi = cg.c0 + cg.tlen;
     const int nx = rp.pb.nx, GW = rp.lay.GW, W = rp.edge_w;
-    // halo chunk: (partly) outside my tile -- reloaded every step from its owners
+    // halo chunk: (partly) outside my tile -- pulled every step from the mailbox
     const bool halo = mine && nseg > 1 && (col0 < lo || col0 + K > hi);
-    int wf0 = -1, wf1 = -1;   // flags to acquire before the reload
-    if (halo) {
-        for (int e = 0; e < K; ++e) {
-            const int c = col0 + e;
-            if (c >= lo && c < hi) continue;                      // my own column
-            if (!periodic && (c < 0 || c >= nx)) continue;        // Dirichlet ghost (zero)
-            const int f = owner_flag(rp, c);
-            if (wf0 < 0) wf0 = f;
-            else if (f != wf0) wf1 = f;
-        }
-    }
     // edge chunk: tile columns a neighbour's halo (or a periodic ghost) reads
     const bool pub = mine && nseg > 1 && col0 + K > lo && col0 < hi && (col0 - lo < W || hi - (col0 + K) < W);
-    const bool pub_warp = __any_sync(0xffffffffu, pub);
     const bool inside = mine && col0 >= lo && col0 + K <= hi;
-    unsigned* my_flag = rp.flags + seg * 32 + (tid >> 5);
+    // the chunk line polled first: my last column outside the tile (Dirichlet
+    // ghosts beyond the line are zero and never pushed)
+    int probe = -1;
+    if (halo)
+        for (int e = 0; e < K; ++e) {
+            const int c = col0 + e;
+            if ((c < lo || c >= hi) && (periodic || (c >= 0 && c < nx))) probe = e;
+        }
 
     double u[K];
 #pragma unroll
     for (int e = 0; e < K; ++e) u[e] = 0.0;
     if (mine) load_chunk_cg(rp.ring + GW + col0, u);   // slot 0: the seeded initial state
-    long long cur = 0;                                  // ring slot of step s-1
     const FastLane fl = fast_lane<K>(rp.sv);
     bool dead = false;                                  // watchdog fired: stop waiting, drain
 
     for (long long s = 1; s <= rp.steps; ++s) {
-        const double* prev = rp.ring + cur * rp.Vs + GW;
-        cur = cur + 1 == rp.cap ? 0 : cur + 1;
-        double* out = rp.ring + cur * rp.Vs + GW;
         RIDC_RSTAMP(rp, s, 0);
         if (s > 1 && halo) {
-            const unsigned want = (unsigned)(s - 1);
+            const unsigned want = rp.tag0 + (unsigned)(s - 1);
+            const uint4* box = rp.mail + (size_t)((s - 1) & 1) * rp.Vs + GW + col0;
             const long long t0 = clock64();
-            for (int k = 0; k < 2; ++k) {
-                const int f = k == 0 ? wf0 : wf1;
-                if (f < 0) continue;
-                while (!dead && ld_acquire_u32(rp.flags + f) < want)
-                    if (clock64() - t0 > rp.spin_limit || *(volatile unsigned*)rp.abort) {
-                        atomicExch(rp.abort, 1u);
-                        dead = true;
-                    }
+            auto timed_out = [&] {
+                if (!dead && (clock64() - t0 > rp.spin_limit || *(volatile unsigned*)rp.abort)) {
+                    atomicExch(rp.abort, 1u);
+                    dead = true;
+                }
+                return dead;
+            };
+            if (probe >= 0) {
+                uint4 pv = ld_line(box + probe);
+                while ((pv.y != want || pv.w != want) && !timed_out()) pv = ld_line(box + probe);
             }
-            RIDC_RSTAMP(rp, s, 1);
-            load_chunk_cg(prev + col0, u);
-            if (!periodic) {   // Dirichlet ghosts beyond the line stay zero
+            uint4 v[K];
 #pragma unroll
-                for (int e = 0; e < K; ++e)
-                    if (col0 + e < 0 || col0 + e >= nx) u[e] = 0.0;
+            for (int e = 0; e < K; ++e) v[e] = ld_line(box + e);
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+                const int c = col0 + e;
+                if (!periodic && (c < 0 || c >= nx)) { u[e] = 0.0; continue; }   // Dirichlet ghost
+                while ((v[e].y != want || v[e].w != want) && !timed_out()) v[e] = ld_line(box + e);
+                u[e] = line_value(v[e]);
             }
         }
         RIDC_RSTAMP(rp, s, 2);
@@ -234,49 +244,44 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
             }
         }
         RIDC_RSTAMP(rp, s, 3);
+        // push the edge columns of step s (and their periodic ghost copies)
+        if (pub) {
+            const unsigned tag = rp.tag0 + (unsigned)s;
+            uint4* box = rp.mail + (size_t)(s & 1) * rp.Vs + GW;
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+                const int c = col0 + e;
+                if (c >= lo && c < hi) {
+                    st_line(box + c, u[e], tag);
+                    if (periodic && c < GW) st_line(box + c + nx, u[e], tag);
+                    if (periodic && c >= nx - GW) st_line(box + c - nx, u[e], tag);
+                }
+            }
+        }
+        // finite check over my tile columns; the whole tile to the ring at the end
         const bool full = s == rp.steps || rp.full_every;
+        double* out = full ? rp.ring + (s % rp.cap) * rp.Vs + GW : nullptr;   // trajectory: cap = steps + 1
         bool bad = false;
-        if (inside && !pub) {
+        if (inside) {
             bad = !chunk_finite(u);
             if (full) {
 #pragma unroll
                 for (int e = 0; e < K; e += 2)
                     *reinterpret_cast<double2*>(out + col0 + e) = make_double2(u[e], u[e + 1]);
             }
-        } else if (inside) {
-            bad = !chunk_finite(u);
-#pragma unroll
-            for (int e = 0; e < K; e += 2)
-                *reinterpret_cast<double2*>(out + col0 + e) = make_double2(u[e], u[e + 1]);
-            if (periodic && (col0 < GW || col0 + K > nx - GW)) {
-#pragma unroll
-                for (int e = 0; e < K; ++e) {
-                    const int c = col0 + e;
-                    if (c < GW) out[c + nx] = u[e];
-                    if (c >= nx - GW) out[c - nx] = u[e];
-                }
-            }
         } else if (mine) {
-            // chunk straddling a tile end (or wholly in the halo)
             double chk = 0.0;
 #pragma unroll
             for (int e = 0; e < K; ++e) {
                 const int c = col0 + e;
                 if (c >= lo && c < hi) {
                     chk = fma(u[e], 0.0, chk);
-                    if (pub || full) out[c] = u[e];
-                    if (periodic && c < GW) out[c + nx] = u[e];
-                    if (periodic && c >= nx - GW) out[c - nx] = u[e];
+                    if (full) out[c] = u[e];
                 }
             }
             bad = chk != chk;
         }
         if (bad) atomicMin(rp.err, err_code((s - 1) % rp.per + 1, 0));
-        if (pub_warp) {
-            // the warp's stores, then one release of its step flag
-            __syncwarp();
-            if (lane == 0) st_release_u32(my_flag, (unsigned)s);
-        }
         RIDC_RSTAMP(rp, s, 4);
         RIDC_RSTAMP(rp, s, 5);
     }
