@@ -70,9 +70,8 @@ typedef struct ridc_ctx ridc_ctx;
 #define RIDC_RECORD_TRAJECTORY 1u  /* RidcConfig.record_trajectory */
 #define RIDC_TICK_ONLY 2u          /* never use the resident single-level march (testing:
                                       it must agree bitwise with the tick kernel) */
-#define RIDC_RESIDENT_SEGMENTS 4u  /* also use it for multi-segment lines (experimental: on
-                                      B200 its per-step inter-CTA flag latency makes it no
-                                      faster than the tick kernel there) */
+#define RIDC_RESIDENT_SEGMENTS 4u  /* accepted for compatibility: segmented lines march
+                                      resident by default */
 
 /* Engine geometry / accounting, for reports and tests. */
 typedef struct ridc_info {
