@@ -26,7 +26,7 @@
 
 namespace ridc {
 
-constexpr int kChunk = 16;   // points per thread (one 128-byte group)
+constexpr int kChunk = 16;   // points per 128-byte group (and per thread in the 1-D configs)
 
 // Per-segment item geometry (host table).
 struct ChunkGeo {
@@ -42,11 +42,14 @@ struct TmapSet {
     CUtensorMap map[kMaxLevels];   // one per level ring: {16, groups/slot, slots}
 };
 
-// Layout of the staged rows of one node in a stage.
-template <int NT, int ROWS, int NSTAGE>
+// Layout of the staged rows of one node in a stage.  NT threads of KC points
+// each cover NG = NT*KC/16 groups (KC = 16: one group per thread; KC = 8: two
+// threads per group, for 16-warp CTAs on 4096-point lines).
+template <int NT, int ROWS, int NSTAGE, int KC = kChunk>
 struct ChunkSmem {
-    static constexpr int BR = NT < 256 ? NT : 256;              // groups per box
-    static constexpr int ROWB = NT * 128;                        // bytes per staged row
+    static constexpr int NG = NT * KC / kChunk;                  // groups per item
+    static constexpr int BR = NG < 256 ? NG : 256;              // groups per box
+    static constexpr int ROWB = NG * 128;                        // bytes per staged row
     static constexpr int STAGE = ROWS * ROWB;                    // bytes per stage
     static constexpr size_t OFF_EDGE = (size_t)NSTAGE * STAGE;   // 4*NT doubles: chunk edges
     static constexpr size_t OFF_BAR = OFF_EDGE + 4 * NT * sizeof(double);
@@ -83,12 +86,12 @@ __device__ __forceinline__ const char* swz(const char* rowbase, int g, int i)
 
 // Issue the tensor copies of node a of an item: ROWS rows (2-D: r, r-1, r+1)
 // x ceil(ng / BR) boxes of BR groups.
-template <int NT, int ROWS, int NSTAGE>
+template <int NT, int ROWS, int NSTAGE, int KC>
 __device__ __forceinline__ void issue_chunk_node(const TmapSet& tm, int lev, long long slot, int row,
                                                  int ny, int gpr, int gdata, const ChunkGeo& cg,
                                                  char* st, uint64_t* full)
 {
-    using L = ChunkSmem<NT, ROWS, NSTAGE>;
+    using L = ChunkSmem<NT, ROWS, NSTAGE, KC>;
     const int nbox = (cg.ng + L::BR - 1) / L::BR;
     mbar_arrive_expect_tx(full, (uint32_t)(ROWS * nbox * L::BR * 128));
     const int rr[3] = {row, row == 0 ? ny - 1 : row - 1, row == ny - 1 ? 0 : row + 1};
@@ -107,20 +110,18 @@ namespace ridc {
 // pointwise accumulators of thread t's chunk; rhs receives the new state.
 // Shared by the tick kernel (TMA-staged nodes) and the resident FEBE kernel
 // (register-held state), so both produce bitwise the same states.
-template <int KIND, int NT, int MODE>
+template <int KIND, int NT, int MODE, int K = kChunk>
 __device__ __forceinline__ void chunk_rhs_solve(const DevProblem& pb, const DevSolve& sv, const ChunkGeo& cg,
                                                 bool need_ws, bool need_wx, bool mine,
-                                                const double (&P)[kChunk], const double (&WS)[kChunk],
-                                                const double (&WX)[kChunk], double (&rhs)[kChunk],
+                                                const double (&P)[K], const double (&WS)[K],
+                                                const double (&WX)[K], double (&rhs)[K],
                                                 double* edge, Aff* swarp, int item_no, FastLane fl)
 {
-    constexpr int K = kChunk;
     constexpr bool periodic = KIND != BURGERS_1D;
     constexpr bool has_wx = KIND == ADV_DIFF_1D || KIND == BURGERS_1D || KIND == ADV_DIFF_2D;
     const int tid = threadIdx.x;
     // ---- phase 2: x-stencils; the neighbour chunks' edge values via shared memory
-    const int gbase = cg.g0 + tid;                  // my group (data-relative)
-    const int col0 = gbase * K;                     // data column of my first point
+    const int col0 = cg.g0 * kChunk + tid * K;      // data column of my first point
     int nlast = K - 1;                              // my last valid point (whole lines: partial chunk)
     if (MODE == 1 || MODE == 2) nlast = min(K, cg.s_end - tid * K) - 1;
     need_wx = need_wx && has_wx;
@@ -135,7 +136,9 @@ __device__ __forceinline__ void chunk_rhs_solve(const DevProblem& pb, const DevS
         edge[2 * NT + tid] = WX[0];
         edge[3 * NT + tid] = lastwx;
         csync<NT>();
-        const int nthr = cg.ng;
+        // threads holding data: whole staged groups (truncated segments), or the
+        // line's positions (whole lines may end inside a group)
+        const int nthr = MODE == 0 ? cg.ng * (kChunk / K) : (cg.s_end + K - 1) / K;
         const bool first = tid == 0, last = tid == nthr - 1;
         if (!first) { wsl = edge[NT + tid - 1]; wxl = edge[3 * NT + tid - 1]; }
         else if (MODE == 1) { wsl = edge[NT + nthr - 1]; wxl = edge[3 * NT + nthr - 1]; }   // cyclic
@@ -234,19 +237,22 @@ struct ChunkLayout {
 
 // One chunk-layout item.  MODE: 0 truncated (fast_solve), 1 cyclic whole
 // line, 2 exact Dirichlet start/end with coefficient tables.
-template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, class Refill>
+template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, int KC, class Refill>
 __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve& sv, const ChunkLayout& lay,
                                            const TmapSet& tm, const StepItem& it, const ChunkGeo& cg,
                                            int row, char* stage, double* edge, uint64_t* full,
                                            uint64_t* empty, long long& n, Refill&& refill, Aff* swarp,
                                            unsigned long long* err, int item_no, FastLane fl)
 {
-    using L = ChunkSmem<NT, ROWS, NSTAGE>;
-    constexpr int K = kChunk;
+    using L = ChunkSmem<NT, ROWS, NSTAGE, KC>;
+    constexpr int K = KC;                     // points per thread
+    constexpr int HP = kChunk / KC;           // threads per group
     constexpr bool periodic = KIND != BURGERS_1D;
     constexpr bool two_d = ROWS == 3;
     const int tid = threadIdx.x, lane = tid & 31;
-    const bool mine = tid < cg.ng;            // owns a staged group
+    const int gq = tid / HP;                  // my group
+    const int ip0 = (tid % HP) * (K / 2);     // my first element pair within it
+    const bool mine = gq < cg.ng;             // owns (part of) a staged group
 
     double P[K], WS[K], WX[K];
 #pragma unroll
@@ -263,11 +269,11 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         if (mine) {
 #pragma unroll
             for (int i = 0; i < K / 2; ++i) {
-                const double2 v = lds128(swz(st, tid, i));
+                const double2 v = lds128(swz(st, gq, ip0 + i));
                 double2 vn = make_double2(0.0, 0.0), vs = make_double2(0.0, 0.0);
                 if (two_d) {
-                    vn = lds128(swz(st + L::ROWB, tid, i));
-                    vs = lds128(swz(st + 2 * L::ROWB, tid, i));
+                    vn = lds128(swz(st + L::ROWB, gq, ip0 + i));
+                    vs = lds128(swz(st + 2 * L::ROWB, gq, ip0 + i));
                 }
                 accumulate_point<KIND>(nc, v.x, vn.x, vs.x, P[2 * i], WS[2 * i], WX[2 * i]);
                 accumulate_point<KIND>(nc, v.y, vn.y, vs.y, P[2 * i + 1], WS[2 * i + 1], WX[2 * i + 1]);
@@ -290,7 +296,8 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         need_wx |= it.cn[a] != 0.0;
     }
     double rhs[K];
-    chunk_rhs_solve<KIND, NT, MODE>(pb, sv, cg, need_ws, need_wx, mine, P, WS, WX, rhs, edge, swarp, item_no, fl);
+    chunk_rhs_solve<KIND, NT, MODE, K>(pb, sv, cg, need_ws, need_wx, mine, P, WS, WX, rhs, edge, swarp, item_no,
+                                       fl);
     RIDC_STAMP(sv, item_no, 8);
 
     // ---- phase 5: store.  Chunks go to shared memory swizzled (conflict-free),
@@ -298,7 +305,7 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
     // coalesced 512-byte warp stores (+ periodic ghosts, + the pipeline mirror).
     if (mine)
 #pragma unroll
-        for (int i = 0; i < K / 2; ++i) sts128(const_cast<char*>(swz(sbufc, tid, i)), rhs[2 * i], rhs[2 * i + 1]);
+        for (int i = 0; i < K / 2; ++i) sts128(const_cast<char*>(swz(sbufc, gq, ip0 + i)), rhs[2 * i], rhs[2 * i + 1]);
     // order these generic shared writes before the TMA that will refill this stage
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     csync<NT>();
@@ -311,7 +318,7 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         const int lo = cg.c0, hi = cg.c0 + cg.tlen;
         const int nx = pb.nx, GW = lay.GW;
         // groups wholly inside the tile: [glo, ghi) relative to g0 (item-uniform)
-        const int glo = (lo - cg.g0 * K + K - 1) / K, ghi = (hi - cg.g0 * K) / K;
+        const int glo = (lo - cg.g0 * kChunk + kChunk - 1) / kChunk, ghi = (hi - cg.g0 * kChunk) / kChunk;
         // only items touching a line end write periodic ghost copies
         const bool ghosts = periodic && (lo < GW || hi > nx - GW);
 #pragma unroll
@@ -320,7 +327,7 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
             const int g = q >> 3, i = q & 7;
             if (g < cg.ng) {
                 const double2 v = lds128(swz(sbufc, g, i));
-                const int c = (cg.g0 + g) * K + 2 * i;   // data column of v.x
+                const int c = (cg.g0 + g) * kChunk + 2 * i;   // data column of v.x
                 if ((unsigned)(g - glo) < (unsigned)(ghi - glo)) {
                     chk = fma(v.x, 0.0, fma(v.y, 0.0, chk));
                     *reinterpret_cast<double2*>(o1 + c) = v;

@@ -139,11 +139,11 @@ __device__ __forceinline__ void item_of(int i, int tiles, int nact, int& slot, i
 // the solve mode all segments share (0 truncated, 1 cyclic whole line, 2
 // Dirichlet whole line), or -1 to dispatch per segment -- one mode per
 // kernel keeps the hot loop small in the instruction cache.
-template <int KIND, int NT, int ROWS, int NSTAGE, int MODE>
+template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, int KC>
 __global__ void __launch_bounds__(NT, 1)
     k_tick_chunk(EngineParams ep, TickParams tp, int ipl, const __grid_constant__ TmapSet tm)
 {
-    using L = ChunkSmem<NT, ROWS, NSTAGE>;
+    using L = ChunkSmem<NT, ROWS, NSTAGE, KC>;
     extern __shared__ __align__(1024) char smraw[];
     char* stage = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     double* edge = reinterpret_cast<double*>(stage + L::OFF_EDGE);
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(NT, 1)
         item_of(pc.i, ipl, tp.nact, slot, tile);
         const int row = tile / nseg, seg = tile - row * nseg;
         const StepItem& it = items[slot];
-        issue_chunk_node<NT, ROWS, NSTAGE>(tm, it.vlev[pc.a], it.vslot[pc.a], row, ny, ep.lay.gpr,
+        issue_chunk_node<NT, ROWS, NSTAGE, KC>(tm, it.vlev[pc.a], it.vslot[pc.a], row, ny, ep.lay.gpr,
                                            ep.lay.gdata, ep.cgeo[seg], stage + (size_t)s * L::STAGE,
                                            &full[s]);
         if (++pc.a == it.nnodes) { pc.a = 0; pc.i += gridDim.x; }
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(NT, 1)
     };
     long long n = 0;
     int ino = 0;
-    const FastLane fl = fast_lane<kChunk>(sv);
+    const FastLane fl = fast_lane<KC>(sv);
     for (int i = blockIdx.x; i < total; i += gridDim.x, ++ino) {
         int slot, tile;
         item_of(i, ipl, tp.nact, slot, tile);
@@ -224,15 +224,15 @@ __global__ void __launch_bounds__(NT, 1)
         const ChunkGeo cg = ep.cgeo[seg];
         switch (MODE >= 0 ? MODE : cg.mode) {
         case 0:
-            chunk_item<KIND, NT, ROWS, NSTAGE, 0>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+            chunk_item<KIND, NT, ROWS, NSTAGE, 0, KC>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
                                                   full, empty, n, refill, swarp, ep.err, ino, fl);
             break;
         case 1:
-            chunk_item<KIND, NT, ROWS, NSTAGE, 1>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+            chunk_item<KIND, NT, ROWS, NSTAGE, 1, KC>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
                                                   full, empty, n, refill, swarp, ep.err, ino, fl);
             break;
         default:
-            chunk_item<KIND, NT, ROWS, NSTAGE, 2>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
+            chunk_item<KIND, NT, ROWS, NSTAGE, 2, KC>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
                                                   full, empty, n, refill, swarp, ep.err, ino, fl);
         }
         csync<NT>();   // edge / scan scratch reuse by the next item
@@ -335,20 +335,21 @@ cudaError_t launch_item_t(int items, size_t smem, cudaStream_t st, const DevProb
 struct ChunkCfg {
     int id;
     int nt, rows, nstage;
+    int kc;     // points per thread (16: one group per thread; 8: two threads per group)
     size_t smem;
     int mode;   // common segment mode (k_tick_chunk MODE), -1 mixed
 };
 
 #define RIDC_CHUNK_CONFIGS(X) \
-    X(0, 64, 1, 4)            \
-    X(1, 128, 1, 4)           \
-    X(2, 256, 1, 4)           \
-    X(3, 512, 1, 3)           \
-    X(4, 64, 3, 3)            \
-    X(5, 128, 3, 3)           \
-    X(6, 256, 3, 2)
+    X(0, 64, 1, 4, 16)        \
+    X(1, 128, 1, 4, 16)       \
+    X(2, 256, 1, 4, 16)       \
+    X(3, 512, 1, 3, 16)       \
+    X(4, 64, 3, 3, 16)        \
+    X(5, 128, 3, 3, 16)       \
+    X(6, 512, 3, 2, 8)
 
-template <int NT, int ROWS, int NSTAGE>
+template <int NT, int ROWS, int NSTAGE, int KC>
 ChunkCfg chunk_cfg_make(int id)
 {
     ChunkCfg c;
@@ -356,19 +357,23 @@ ChunkCfg chunk_cfg_make(int id)
     c.nt = NT;
     c.rows = ROWS;
     c.nstage = NSTAGE;
-    c.smem = ChunkSmem<NT, ROWS, NSTAGE>::BYTES + 1024;   // + 1 KiB for the 1024-B alignment
+    c.kc = KC;
+    c.smem = ChunkSmem<NT, ROWS, NSTAGE, KC>::BYTES + 1024;   // + 1 KiB for the 1024-B alignment
     c.mode = -1;
     return c;
 }
 
+// 128-byte groups (16 points) one item of this configuration stages per row
+int chunk_groups(const ChunkCfg& c) { return c.nt * c.kc / 16; }
+
 // the configuration with this id, as listed in RIDC_CHUNK_CONFIGS
 ChunkCfg chunk_cfg_of_id(int id)
 {
-#define RIDC_CFG_OF(ID, NT, ROWS, NSTAGE) \
-    if (id == ID) return chunk_cfg_make<NT, ROWS, NSTAGE>(ID);
+#define RIDC_CFG_OF(ID, NT, ROWS, NSTAGE, KC) \
+    if (id == ID) return chunk_cfg_make<NT, ROWS, NSTAGE, KC>(ID);
     RIDC_CHUNK_CONFIGS(RIDC_CFG_OF)
 #undef RIDC_CFG_OF
-    return chunk_cfg_make<512, 1, 3>(3);
+    return chunk_cfg_make<512, 1, 3, 16>(3);
 }
 
 // smallest config whose NT*16 points cover `points` (the item's staged range)
@@ -378,7 +383,7 @@ ChunkCfg pick_chunk(int kind, int points)
     if (two_d) {
         if (points <= 64 * 16) return chunk_cfg_of_id(4);
         if (points <= 128 * 16) return chunk_cfg_of_id(5);
-        return chunk_cfg_of_id(6);
+        return chunk_cfg_of_id(6);   // 512 threads x 8 points: 16 warps per 4096-point line
     }
     if (points <= 64 * 16) return chunk_cfg_of_id(0);
     if (points <= 128 * 16) return chunk_cfg_of_id(1);
@@ -398,11 +403,11 @@ int chunk_points_max(int kind)
 // table keeps two CTAs from fitting the shared memory anyway.
 int chunk_ctas_per_sm(const ChunkCfg&) { return 1; }
 
-template <int KIND, int NT, int ROWS, int NSTAGE, int MODE>
+template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, int KC>
 cudaError_t launch_chunk_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
                            const TickParams& tp, int ipl, const TmapSet& tm)
 {
-    auto kfn = k_tick_chunk<KIND, NT, ROWS, NSTAGE, MODE>;
+    auto kfn = k_tick_chunk<KIND, NT, ROWS, NSTAGE, MODE, KC>;
     static bool attr[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -435,11 +440,11 @@ cudaError_t launch_chunk_k(const ChunkCfg& c, int grid, cudaStream_t st, const E
     constexpr bool periodic = KIND != BURGERS_1D;
     constexpr int MA = periodic ? 0 : 2, MB = periodic ? 1 : -1;
     if (periodic && c.mode != MA && c.mode != MB) return cudaErrorInvalidValue;
-#define RIDC_CHUNK_CASE(ID, NT, ROWS, NSTAGE)                                                  \
+#define RIDC_CHUNK_CASE(ID, NT, ROWS, NSTAGE, KC)                                              \
     if (c.id == ID && two_d == (ROWS == 3)) {                                                  \
         if constexpr (two_d == (ROWS == 3))                                                    \
-            return c.mode == MA ? launch_chunk_t<KIND, NT, ROWS, NSTAGE, MA>(grid, c.smem, st, ep, tp, ipl, tm) \
-                                : launch_chunk_t<KIND, NT, ROWS, NSTAGE, MB>(grid, c.smem, st, ep, tp, ipl, tm); \
+            return c.mode == MA ? launch_chunk_t<KIND, NT, ROWS, NSTAGE, MA, KC>(grid, c.smem, st, ep, tp, ipl, tm) \
+                                : launch_chunk_t<KIND, NT, ROWS, NSTAGE, MB, KC>(grid, c.smem, st, ep, tp, ipl, tm); \
     }
     RIDC_CHUNK_CONFIGS(RIDC_CHUNK_CASE)
 #undef RIDC_CHUNK_CASE
@@ -793,7 +798,7 @@ int make_chunk_solve(const DevProblem& pb, double coeff, int nsm, SolveSetup& ss
         return RIDC_E_CONFIG;
     }
     if (!pb.periodic && ss.ccfg.mode != 2) ss.ccfg.mode = -1;
-    if (maxng > ss.ccfg.nt) {
+    if (maxng > chunk_groups(ss.ccfg)) {
         ss.err = "internal: item larger than the chunk kernel";
         return RIDC_E_CONFIG;
     }
@@ -878,11 +883,11 @@ PfnEncodeTiled encode_tiled()
 
 // A ring of `cap` slots as a 3-D tensor {16 doubles, Vs/16 groups, cap slots},
 // boxes of BR groups, 128-byte swizzle (ridc_chunk.cuh).
-int make_ring_map(CUtensorMap* map, double* base, long long Vs, long long cap, int nt, std::string* err)
+int make_ring_map(CUtensorMap* map, double* base, long long Vs, long long cap, int ng, std::string* err)
 {
     PfnEncodeTiled enc = encode_tiled();
     if (!enc) return fail(err, RIDC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const int BR = nt < 256 ? nt : 256;
+    const int BR = ng < 256 ? ng : 256;   // ChunkSmem::BR
     cuuint64_t dims[3] = {16, (cuuint64_t)(Vs / 16), (cuuint64_t)cap};
     cuuint64_t strides[2] = {128, (cuuint64_t)Vs * 8};
     cuuint32_t box[3] = {16, (cuuint32_t)BR, 1};
@@ -1213,7 +1218,7 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         // ny padded rows per slot; zeroed once: Dirichlet ghosts stay 0 forever
         CTX_TRY(cudaMalloc(&c->d_ring[j], (size_t)cap * c->Vs * sizeof(double)));
         CTX_TRY(cudaMemset(c->d_ring[j], 0, (size_t)cap * c->Vs * sizeof(double)));
-        if ((rc = make_ring_map(&c->tm.map[j], c->d_ring[j], c->Vs, cap, c->ss.ccfg.nt, &c->err)) != RIDC_OK)
+        if ((rc = make_ring_map(&c->tm.map[j], c->d_ring[j], c->Vs, cap, chunk_groups(c->ss.ccfg), &c->err)) != RIDC_OK)
             return bail(rc);
     }
     CTX_TRY(cudaMalloc(&c->d_y0, 2 * (size_t)c->V * sizeof(double)));
@@ -1726,10 +1731,10 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     P_TRY(cudaMemset(p->own_base, 0, (size_t)2 * p->Vs * sizeof(double)));
     p->own = p->own_base;
     memset(&p->tm, 0, sizeof p->tm);
-    if ((rc = make_ring_map(&p->tm.map[level], p->own, p->Vs, 2, p->ss.ccfg.nt, &p->err)) != RIDC_OK)
+    if ((rc = make_ring_map(&p->tm.map[level], p->own, p->Vs, 2, chunk_groups(p->ss.ccfg), &p->err)) != RIDC_OK)
         return bail(rc);
     if (level > 0 &&
-        (rc = make_ring_map(&p->tm.map[level - 1], p->inbox, p->Vs, p->inbox_cap, p->ss.ccfg.nt, &p->err)) != RIDC_OK)
+        (rc = make_ring_map(&p->tm.map[level - 1], p->inbox, p->Vs, p->inbox_cap, chunk_groups(p->ss.ccfg), &p->err)) != RIDC_OK)
         return bail(rc);
 #undef P_TRY
     *out = p;
@@ -2075,7 +2080,7 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
     ARK_TRY(cudaMalloc(&a->d_y0, (size_t)a->V * sizeof(double)));
     ARK_TRY(cudaMalloc(&a->d_err, sizeof(unsigned long long)));
     memset(&a->tm, 0, sizeof a->tm);
-    if ((rc = make_ring_map(&a->tm.map[0], a->d_ring, a->Vs, a->cap, a->ss.ccfg.nt, &a->err)) != RIDC_OK)
+    if ((rc = make_ring_map(&a->tm.map[0], a->d_ring, a->Vs, a->cap, chunk_groups(a->ss.ccfg), &a->err)) != RIDC_OK)
         return bail(rc);
     EngineParams& ep = a->ep;
     memset(&ep, 0, sizeof ep);
