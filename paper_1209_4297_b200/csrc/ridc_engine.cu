@@ -42,6 +42,9 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// top-ring slots while the trajectory is streamed to host memory
+constexpr long long kTrajDepth = 8;
+
 // phase-trace buffer (RIDC_PHASE_TIMING): 8 rows x 16 stamps of CTA 0, then per
 // CTA (entry, wait-done, exit) globaltimer of tick target 100
 constexpr int kDbgWords = 128 + 4 * 1024;
@@ -838,6 +841,13 @@ struct ridc_ctx {
     long long launches = 0;
     long long ring_vectors = 0;
     // resident single-level march (ridc_resident.cuh)
+    // trajectory streaming (§8f rank 3): the top ring keeps kTrajDepth slots and
+    // every step is drained to pinned host memory by a copy stream
+    bool traj_stream = false;
+    cudaStream_t cstream = nullptr;
+    double* h_traj = nullptr;      // pinned (steps+1) x V
+    cudaEvent_t ev_prod = nullptr;
+    std::vector<cudaEvent_t> ev_copy;
     bool resident = false;
     int res_mode = -1;             // common segment mode of the resident kernel (-1: mixed)
     unsigned* d_flags = nullptr;   // the watchdog abort word
@@ -935,6 +945,24 @@ int capture_graph(ridc_ctx* c)
     CUDA_TRY(&c->err, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     long long launches = 0;
     cudaError_t le = cudaSuccess;
+    // trajectory streaming: after the top level writes global step g into slot
+    // g % cap, the copy stream drains it to row g of the pinned host buffer;
+    // the tick that reuses the slot waits for that copy
+    const long long tcap = c->cap[L - 1];
+    auto drain = [&](long long g, const double* slot) {
+        if (!c->traj_stream || le != cudaSuccess) return;
+        const ChunkLayout& Ly = c->ss.lay;
+        if ((le = cudaEventRecord(c->ev_prod, c->stream)) != cudaSuccess) return;
+        if ((le = cudaStreamWaitEvent(c->cstream, c->ev_prod, 0)) != cudaSuccess) return;
+        le = cudaMemcpy2DAsync(c->h_traj + (size_t)g * c->V, (size_t)c->pb.nx * sizeof(double), slot + Ly.GW,
+                               (size_t)Ly.P * sizeof(double), (size_t)c->pb.nx * sizeof(double), (size_t)c->pb.ny,
+                               cudaMemcpyDeviceToHost, c->cstream);
+        if (le == cudaSuccess) le = cudaEventRecord(c->ev_copy[g % tcap], c->cstream);
+    };
+    auto slot_free = [&](long long g) {   // before the top level writes global step g
+        if (c->traj_stream && le == cudaSuccess && g >= tcap)
+            le = cudaStreamWaitEvent(c->stream, c->ev_copy[g % tcap], 0);
+    };
     for (int r = 0; r < c->restarts && le == cudaSuccess; ++r) {
         EngineParams ep = interval_params(c, r);
         if (r == 0) {
@@ -942,6 +970,7 @@ int capture_graph(ridc_ctx* c)
             k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
             le = cudaGetLastError();
             ++launches;
+            drain(0, ep.ring[L - 1] + (ep.off[L - 1] % tcap) * c->Vs);   // trajectory row 0: the initial state
         } else {
             // next interval's state0 = the top level's final: plain copy through d_y0
             EngineParams prev = interval_params(c, r - 1);
@@ -968,11 +997,22 @@ int capture_graph(ridc_ctx* c)
                 }
             }
             if (tp.nact == 0) continue;
+            const long long ttop = k - delay(L - 1);   // the top level's target this tick
+            const bool top_active = ttop >= 1 && ttop <= c->per;
+            if (top_active) slot_free((long long)r * c->per + ttop);
+            if (le != cudaSuccess) break;
             le = launch_chunk(c->pb.kind, c->ss.ccfg, std::min(c->nsm * chunk_ctas_per_sm(c->ss.ccfg), tp.nact * items),
                               c->stream, ep, tp,
                               items, c->tm);
             ++launches;
+            if (top_active)
+                drain((long long)r * c->per + ttop,
+                      ep.ring[L - 1] + ((ep.off[L - 1] + ttop) % tcap) * c->Vs);
         }
+    }
+    if (c->traj_stream && le == cudaSuccess) {   // rejoin the copy stream
+        if ((le = cudaEventRecord(c->ev_prod, c->cstream)) == cudaSuccess)
+            le = cudaStreamWaitEvent(c->stream, c->ev_prod, 0);
     }
     cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
     if (le != cudaSuccess) {
@@ -1059,7 +1099,9 @@ int setup_resident(ridc_ctx* c)
     const SolveSetup& ss = c->ss;
     const int nseg = ss.sv.nseg;
     const bool one_d = c->pb.kind == ADV_DIFF_1D || c->pb.kind == BURGERS_1D || c->pb.kind == RD_1D;
-    if (c->levels != 1 || !one_d || c->pb.ny != 1 || (c->flags & RIDC_TICK_ONLY) || nseg > c->nsm) return RIDC_OK;
+    if (c->levels != 1 || !one_d || c->pb.ny != 1 || (c->flags & RIDC_TICK_ONLY) || nseg > c->nsm ||
+        c->traj_stream)
+        return RIDC_OK;
     // whole lines: one CTA marches alone, 2x faster than a launch per step;
     // segmented lines: one co-resident CTA per segment exchanging truncation-halo
     // edges through tagged mailbox lines, ~1.3x faster than the tick kernel (C2)
@@ -1209,10 +1251,19 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         c->ss.sv.dbg = c->d_dbg;
     }
     memset(&c->tm, 0, sizeof c->tm);
+    if (flags & RIDC_RECORD_TRAJECTORY) {
+        // keep the whole trajectory on the device when it fits comfortably, else stream it
+        size_t freeb = 0, totalb = 0;
+        cudaMemGetInfo(&freeb, &totalb);
+        const double traj_bytes = (double)(steps + 1) * (double)c->Vs * sizeof(double);
+        const char* e = getenv("RIDC_TRAJ_STREAM");
+        c->traj_stream = e ? atoi(e) > 0 : traj_bytes > 0.5 * (double)freeb;
+    }
     for (int j = 0; j < levels; ++j) {
         const bool top = j == levels - 1;
         long long cap = top ? 2 : 2LL * j + 3;
-        if (top && (flags & RIDC_RECORD_TRAJECTORY)) cap = steps + 1;
+        if (top && (flags & RIDC_RECORD_TRAJECTORY)) cap = c->traj_stream ? std::min<long long>(kTrajDepth, steps + 1)
+                                                                           : steps + 1;
         c->cap[j] = cap;
         c->ring_vectors += cap;
         // ny padded rows per slot; zeroed once: Dirichlet ghosts stay 0 forever
@@ -1220,6 +1271,19 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         CTX_TRY(cudaMemset(c->d_ring[j], 0, (size_t)cap * c->Vs * sizeof(double)));
         if ((rc = make_ring_map(&c->tm.map[j], c->d_ring[j], c->Vs, cap, chunk_groups(c->ss.ccfg), &c->err)) != RIDC_OK)
             return bail(rc);
+    }
+    if (c->traj_stream) {
+        if (cudaHostAlloc(&c->h_traj, (size_t)(steps + 1) * c->V * sizeof(double), cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            c->h_traj = nullptr;
+            c->err = "trajectory needs " + std::to_string((double)(steps + 1) * c->V * 8 / 1e9) +
+                     " GB of pinned host memory; allocation failed";
+            return bail(RIDC_E_CONFIG);
+        }
+        CTX_TRY(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        CTX_TRY(cudaEventCreateWithFlags(&c->ev_prod, cudaEventDisableTiming));
+        c->ev_copy.assign((size_t)c->cap[levels - 1], nullptr);
+        for (auto& ev : c->ev_copy) CTX_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
     CTX_TRY(cudaMalloc(&c->d_y0, 2 * (size_t)c->V * sizeof(double)));
     CTX_TRY(cudaMalloc(&c->d_err, sizeof(unsigned long long)));
@@ -1266,10 +1330,12 @@ int ridc_run(ridc_ctx* c, const double* y0_host, double* final_host, double* lev
         for (int j = 0; j < c->levels; ++j)
             CUDA_TRY(&c->err, copy_out(c, level_finals_host + (size_t)j * c->V, final_slot(c, j),
                                        cudaMemcpyDeviceToHost));
-    if (traj_host)
+    if (traj_host && !c->traj_stream)
         CUDA_TRY(&c->err, copy_out(c, traj_host, c->d_ring[c->levels - 1], cudaMemcpyDeviceToHost,
                                    c->steps + 1));
     CUDA_TRY(&c->err, cudaStreamSynchronize(c->stream));
+    if (traj_host && c->traj_stream)   // drained during the march (the graph joins the copy stream)
+        memcpy(traj_host, c->h_traj, (size_t)(c->steps + 1) * c->V * sizeof(double));
     return RIDC_OK;
 }
 
@@ -1322,6 +1388,11 @@ int ridc_destroy(ridc_ctx* c)
     if (c->d_mail) cudaFree(c->d_mail);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->ev_prod) cudaEventDestroy(c->ev_prod);
+    for (cudaEvent_t ev : c->ev_copy)
+        if (ev) cudaEventDestroy(ev);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
+    if (c->h_traj) cudaFreeHost(c->h_traj);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return RIDC_OK;
