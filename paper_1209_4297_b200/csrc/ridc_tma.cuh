@@ -56,8 +56,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
         : "memory");
 }
 
-// As mbar_wait, but gives up when *abortp becomes non-zero (persistent kernel watchdog).
-
 // Thread 0's cursor over this CTA's global load sequence: items
 // i = blockIdx.x + m*gridDim.x, nodes 0..nnodes-1 each.  Load n lands in
 // stage n % NSTAGE.
