@@ -365,6 +365,7 @@ def run_ours(args):
             barrier()
             e0.record()
             y0.copy_(y0h, non_blocking=True)
+            torch.cuda.current_stream().synchronize()   # the pipeline runs on its own stream
             runner.run_device(y0, out)
             finh.copy_(out, non_blocking=True)
             e1.record()
