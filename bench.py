@@ -292,6 +292,8 @@ def run_ours(args):
                 "bytes_per_launch": bytes_launch, "launch_us": per_launch_s * 1e6}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            # level-steps/s = p N Nt / wall (work done by all levels)
+            "level_steps_per_s": order * n * nt * args.steps / t_max,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "gpu_launches": int(launches_per_step * args.steps)}
@@ -332,6 +334,7 @@ def run_ours(args):
                         torch.cuda.synchronize()
                         ts.append(e2.run_device(y0, out))
                     extra[f"order{p}_1gpu"] = {"value": n * nt * len(ts) / sum(ts),
+                                               "level_steps_per_s": p * n * nt * len(ts) / sum(ts),
                                                "ms_per_solve": sum(ts) / len(ts) * 1e3,
                                                "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps)}
             # the paper's ARK comparators on the same grid and dt (steppers.integrate_ark)
