@@ -143,7 +143,7 @@ __device__ __forceinline__ void item_of(int i, int tiles, int nact, int& slot, i
 // Dirichlet whole line), or -1 to dispatch per segment -- one mode per
 // kernel keeps the hot loop small in the instruction cache.
 template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, int KC>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, ROWS == 3 && NSTAGE == 1 ? 2 : 1)
     k_tick_chunk(EngineParams ep, TickParams tp, int ipl, const __grid_constant__ TmapSet tm)
 {
     using L = ChunkSmem<NT, ROWS, NSTAGE, KC>;
@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(NT, 1)
     double* edge = reinterpret_cast<double*>(stage + L::OFF_EDGE);
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + L::OFF_BAR);
     uint64_t* empty = full + NSTAGE;
-    __shared__ StepItem items[kMaxLevels];   // one descriptor per active level (shared by all its tiles)
+    // one descriptor per active level (shared by all its tiles), after the stages
+    StepItem* items = reinterpret_cast<StepItem*>(stage + L::BYTES);
     __shared__ Aff swarp[2 * (NT / 32) + 1];
     const int total = tp.nact * ipl;
     const DevSolve& sv = tp.sv;
@@ -350,7 +351,8 @@ struct ChunkCfg {
     X(3, 512, 1, 3, 16)       \
     X(4, 64, 3, 3, 16)        \
     X(5, 128, 3, 3, 16)       \
-    X(6, 512, 3, 2, 8)
+    X(6, 512, 3, 2, 8)        \
+    X(7, 256, 3, 1, 16)
 
 template <int NT, int ROWS, int NSTAGE, int KC>
 ChunkCfg chunk_cfg_make(int id)
@@ -379,6 +381,31 @@ ChunkCfg chunk_cfg_of_id(int id)
     return chunk_cfg_make<512, 1, 3, 16>(3);
 }
 
+// CTAs of the tick kernel per SM.  1-D: one (4096-point items at two CTAs per
+// SM measured 1.7-2x slower than 8192-point items at one: twice the halo
+// overhead).  2-D single-stage config: two when both fit the shared memory,
+// so one CTA's x-line solve overlaps the other's row loads.
+int chunk_ctas_per_sm(const ChunkCfg& c, int nact = kMaxLevels)
+{
+    if (c.rows == 3 && c.nstage == 1 && 2 * (c.smem + (size_t)nact * sizeof(StepItem) + 1024) <= 228 * 1024)
+        return 2;
+    return 1;
+}
+
+// 2-D lines of 4096: the single-stage 256 x 16 config (id 7, same 256 groups
+// per item as id 6, so the same tiling and tensor maps) when two CTAs of it
+// fit an SM with `max_nact` item descriptors: one CTA's x-line solve then
+// overlaps the other's row loads (C3 FEBE 150 -> 119 us/tick, C4 703 -> 446).
+// With many levels per tick the descriptors crowd it to one CTA per SM and
+// the double-buffered 512 x 8 config (id 6) is faster.
+void prefer_two_per_sm(ChunkCfg& c, int max_nact)
+{
+    if (c.id != 6) return;
+    ChunkCfg t = chunk_cfg_of_id(7);
+    t.mode = c.mode;
+    if (chunk_ctas_per_sm(t, max_nact) == 2) c = t;
+}
+
 // smallest config whose NT*16 points cover `points` (the item's staged range)
 ChunkCfg pick_chunk(int kind, int points)
 {
@@ -400,11 +427,6 @@ int chunk_points_max(int kind)
     return 512 * 16;
 }
 
-// CTAs of the tick kernel per SM.  One: 4096-point items at two CTAs per SM
-// (256 threads, 3 stages) measured 1.7-2x slower than 8192-point items at one
-// (C5 sweep, N = 2^20..2^24): twice the halo overhead, and the static item
-// table keeps two CTAs from fitting the shared memory anyway.
-int chunk_ctas_per_sm(const ChunkCfg&) { return 1; }
 
 template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, int KC>
 cudaError_t launch_chunk_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
@@ -416,14 +438,15 @@ cudaError_t launch_chunk_t(int grid, size_t smem, cudaStream_t st, const EngineP
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     if (!attr[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(smem + kMaxLevels * sizeof(StepItem)));
         if (e != cudaSuccess) return e;
         attr[dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = smem + (size_t)tp.nact * sizeof(StepItem);   // + the active levels' items
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1001,7 +1024,8 @@ int capture_graph(ridc_ctx* c)
             const bool top_active = ttop >= 1 && ttop <= c->per;
             if (top_active) slot_free((long long)r * c->per + ttop);
             if (le != cudaSuccess) break;
-            le = launch_chunk(c->pb.kind, c->ss.ccfg, std::min(c->nsm * chunk_ctas_per_sm(c->ss.ccfg), tp.nact * items),
+            le = launch_chunk(c->pb.kind, c->ss.ccfg,
+                              std::min(c->nsm * chunk_ctas_per_sm(c->ss.ccfg, tp.nact), tp.nact * items),
                               c->stream, ep, tp,
                               items, c->tm);
             ++launches;
@@ -1220,6 +1244,7 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
         c->err = c->ss.err;
         return bail(rc);
     }
+    prefer_two_per_sm(c->ss.ccfg, levels);
     c->Vs = (long long)c->pb.ny * c->ss.lay.P;
 #define CTX_TRY(expr)                                                                        \
     do {                                                                                     \
@@ -1690,7 +1715,7 @@ int pipe_enqueue(ridc_pipe* p, int interval, long long* launches)
         tp.nact = 1;
         tp.level[0] = j;
         tp.target[0] = t;
-        cudaError_t le = launch_chunk(p->pb.kind, p->ss.ccfg, std::min(p->nsm * chunk_ctas_per_sm(p->ss.ccfg), items),
+        cudaError_t le = launch_chunk(p->pb.kind, p->ss.ccfg, std::min(p->nsm * chunk_ctas_per_sm(p->ss.ccfg, 1), items),
                                       p->stream, ep, tp, items,
                                       p->tm);
         if (le != cudaSuccess) return pipe_fail(p, RIDC_E_CUDA, std::string("tick launch: ") + cudaGetErrorString(le));
@@ -1776,6 +1801,7 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
         p->err = p->ss.err;
         return bail(rc);
     }
+    prefer_two_per_sm(p->ss.ccfg, levels);   // the single-device engine's choice: bitwise the same states
     p->Vs = (long long)p->pb.ny * p->ss.lay.P;
     P_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     P_TRY(cudaEventCreate(&p->ev0));
@@ -2139,6 +2165,7 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
         a->err = a->ss.err;
         return bail(rc);
     }
+    prefer_two_per_sm(a->ss.ccfg, 1);
     a->Vs = (long long)a->pb.ny * a->ss.lay.P;
     a->cap = 2 + s;
     ARK_TRY(cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking));
@@ -2251,7 +2278,7 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
             tp.sv = a->solves[k].sv;
             tp.pre = a->d_items + parity * a->nitems + k;
             tp.target[0] = n + 1;
-            le = launch_chunk(a->pb.kind, a->ss.ccfg, std::min(a->nsm * chunk_ctas_per_sm(a->ss.ccfg), tiles), a->stream,
+            le = launch_chunk(a->pb.kind, a->ss.ccfg, std::min(a->nsm * chunk_ctas_per_sm(a->ss.ccfg, 1), tiles), a->stream,
                               ep, tp, tiles, a->tm);
             ++launches;
         }
