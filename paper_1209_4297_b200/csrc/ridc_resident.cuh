@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
     constexpr int K = kChunk;
     constexpr bool periodic = KIND != BURGERS_1D;
     __shared__ double edge[4 * NT];
+    __shared__ double xpush[4][32 * 17];   // per edge warp: transpose buffer of the coalesced push
+    __shared__ int s_pubw[NT / 32];
     __shared__ Aff swarp[2 * (NT / 32) + 1];
     const int tid = threadIdx.x;
     const int seg = blockIdx.x, nseg = rp.sv.nseg;
@@ -189,6 +191,18 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
     // edge chunk: tile columns a neighbour's halo (or a periodic ghost) reads
     const bool pub = mine && nseg > 1 && col0 + K > lo && col0 < hi && (col0 - lo < W || hi - (col0 + K) < W);
     const bool inside = mine && col0 >= lo && col0 + K <= hi;
+    // edge warps (holding pushed columns) get a transpose slot for coalesced pushes
+    const int lane = tid & 31, wid = tid >> 5;
+    const unsigned pub_mask = __ballot_sync(0xffffffffu, pub);
+    if (lane == 0) s_pubw[wid] = pub_mask != 0u;
+    __syncthreads();
+    int pslot = -1;
+    if (pub_mask) {
+        pslot = 0;
+        for (int w = 0; w < wid; ++w) pslot += s_pubw[w];
+        if (pslot >= 4) pslot = -1;   // more than four edge warps: scattered push for the rest
+    }
+    const int wcol0 = col0 - lane * K;   // first column of my warp's 32 chunks
     // the chunk line polled first: my last column outside the tile (Dirichlet
     // ghosts beyond the line are zero and never pushed)
     int probe = -1;
@@ -245,7 +259,28 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
         }
         RIDC_RSTAMP(rp, s, 3);
         // push the edge columns of step s (and their periodic ghost copies)
-        if (pub) {
+        if (pslot >= 0) {
+            // coalesced push: transpose through shared memory, then 32 consecutive lines per store
+            double* xb = xpush[pslot];
+            if (pub) {
+#pragma unroll
+                for (int e = 0; e < K; ++e) xb[lane * 17 + e] = u[e];
+            }
+            __syncwarp();
+            const unsigned tag = rp.tag0 + (unsigned)s;
+            uint4* box = rp.mail + (size_t)(s & 1) * rp.Vs + GW;
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                const int idx = i * 32 + lane, c = wcol0 + idx;
+                if (((pub_mask >> (idx >> 4)) & 1u) && c >= lo && c < hi) {
+                    const double val = xb[(idx >> 4) * 17 + (idx & 15)];
+                    st_line(box + c, val, tag);
+                    if (periodic && c < GW) st_line(box + c + nx, val, tag);
+                    if (periodic && c >= nx - GW) st_line(box + c - nx, val, tag);
+                }
+            }
+            __syncwarp();
+        } else if (pub) {
             const unsigned tag = rp.tag0 + (unsigned)s;
             uint4* box = rp.mail + (size_t)(s & 1) * rp.Vs + GW;
 #pragma unroll
