@@ -170,6 +170,56 @@ class SequentialPipeline:
             r.close()
 
 
+class ConcurrentPipeline:
+    """All levels' pipeline ranks in one process, each driven by its own host
+    thread on its own stream, with the DEFAULT (small) inbox rings: the
+    producers run ahead only as far as the consumers' release counters allow,
+    so the watermark / backpressure protocol is exercised exactly as across
+    GPUs (``devices`` may list one device per rank; one device for all is
+    allowed -- every wait is a stream-memory wait, no kernel ever spins on
+    another rank)."""
+
+    def __init__(self, ivp, config, devices=(0,)):
+        self.config = config
+        L = config.levels
+        devs = [devices[j % len(devices)] for j in range(L)]
+        self.ranks = [PipelineRank(ivp, config, j, L, devs[j]) for j in range(L)]
+        blobs = [r.blob for r in self.ranks]
+        for r in self.ranks:
+            r.connect(blobs)
+        self.ivp = self.ranks[0].ivp
+
+    def run(self, y0=None):
+        import threading
+        y0 = self.ivp.initial_state if y0 is None else y0
+        s0 = [D.to_device(y0, r.device) for r in self.ranks]
+        finals = [None] * len(self.ranks)
+        secs = [0.0] * len(self.ranks)
+        for interval in range(self.config.restarts):
+            errs = []
+
+            def work(j):
+                try:
+                    finals[j], t = self.ranks[j].run_interval(interval, s0[j])
+                    secs[j] += t
+                except Exception as exc:   # surfaced below
+                    errs.append(exc)
+            th = [threading.Thread(target=work, args=(j,)) for j in range(len(self.ranks))]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            if errs:
+                raise errs[0]
+            s0 = [finals[-1].to(f"cuda:{r.device}") for r in self.ranks]
+        self.device_seconds = max(secs)   # the slowest rank's device time (all intervals)
+        return D.to_host(finals[-1]), [D.to_host(f) for f in finals]
+
+    def close(self):
+        for r in self.ranks:
+            r.close()
+
+
 def run_pipelined_distributed(ivp, config, device: Optional[int] = None):
     """run_pipelined with one level per GPU; call on every rank (torchrun).
 

@@ -15,7 +15,7 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from paper_1209_4297_b200 import engine as E, problems as P  # noqa: E402
-from paper_1209_4297_b200.distributed import SequentialPipeline  # noqa: E402
+from paper_1209_4297_b200.distributed import ConcurrentPipeline, SequentialPipeline  # noqa: E402
 
 CASES = [
     ("ad-c1-p2", lambda: P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 1024, t_end=0.4)), 2, 100, 1),
@@ -33,6 +33,25 @@ def test_pipeline_equals_engine_bitwise(name, builder, levels, steps, restarts):
     ref = E.run_serial(s, cfg)
     pipe = SequentialPipeline(s, cfg)
     try:
+        final, level_finals = pipe.run()
+    finally:
+        pipe.close()
+    assert np.array_equal(final, ref.final_state)
+    for j in range(levels):
+        assert np.array_equal(level_finals[j], ref.level_finals[j])
+
+
+@pytest.mark.parametrize("name,builder,levels,steps,restarts", CASES, ids=[c[0] for c in CASES])
+def test_concurrent_pipeline_small_rings_bitwise(name, builder, levels, steps, restarts):
+    """All ranks at once, one host thread and stream each, default inbox rings
+    (2j+5 slots): the backpressure (release counters) and watermark waits are
+    live, as across GPUs; the result must still equal the engine bitwise."""
+    s = builder()
+    cfg = E.RidcConfig(levels=levels, steps=steps, restarts=restarts, watchdog_seconds=30.0)
+    ref = E.run_serial(s, cfg)
+    pipe = ConcurrentPipeline(s, cfg)
+    try:
+        assert all(r.info["ring_vectors"] < steps for r in pipe.ranks[1:])
         final, level_finals = pipe.run()
     finally:
         pipe.close()
