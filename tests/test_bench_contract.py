@@ -1,0 +1,40 @@
+"""bench.py's reference arm runs on the CPU (the oracle port) and prints one
+JSON line with the driver's contract keys; under torchrun the non-zero ranks
+exit without output (the bench contract)."""
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(args, env=None):
+    e = dict(os.environ)
+    e.update(env or {})
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=300, env=e, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    return r.stdout.strip()
+
+
+def test_reference_arm_contract():
+    out = _run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--sample-steps", "4"])
+    lines = [ln for ln in out.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e", "impl"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["config"]["workload"] == "c2-reaction-diffusion-1d" and d["config"]["points"] == 1 << 20
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["dtype"] == "f64" and d["vs_baseline"] is None
+
+
+def test_reference_arm_nonzero_rank_is_silent():
+    out = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0"],
+               env={"RANK": "1", "WORLD_SIZE": "2"})
+    assert out == ""
