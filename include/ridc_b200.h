@@ -215,6 +215,25 @@ int ridc_ark_info(const ridc_ark_ctx *ctx, int64_t *kernel_launches, int32_t *it
 int ridc_ark_destroy(ridc_ark_ctx *ctx);
 const char *ridc_ark_last_error(const ridc_ark_ctx *ctx);
 
+/* ---------------------------------------------------------------------------
+ * 2-D row shards under the levels: the grid's rows
+ * split into nshards contiguous shards, each running every level on its rows
+ * plus one ghost row per side, the boundary rows of every newly written slot
+ * exchanged after each tick.  This group runs all shards on one device in
+ * lockstep and reproduces ridc_run bitwise; 2-D kinds only.
+ */
+typedef struct ridc_shards ridc_shards;
+
+int ridc_shards_create(const ridc_problem *problem, double t_start, double t_end,
+                       int32_t levels, int64_t steps, int32_t restarts,
+                       const double *weights, int64_t nweights, int32_t nshards,
+                       int32_t device, ridc_shards **out);
+int ridc_shards_run(ridc_shards *g, const double *y0_host, double *final_host,
+                    double *wall_seconds);
+int ridc_shards_info(const ridc_shards *g, int64_t *kernel_launches);
+int ridc_shards_destroy(ridc_shards *g);
+const char *ridc_shards_last_error(const ridc_shards *g);
+
 #ifdef __cplusplus
 }
 #endif

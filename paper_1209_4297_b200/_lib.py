@@ -65,6 +65,12 @@ SIGNATURES = {
     "ridc_ark_info": (ctypes.c_int, [_vp, _P(ctypes.c_int64), _P(ctypes.c_int32)]),
     "ridc_ark_destroy": (ctypes.c_int, [_vp]),
     "ridc_ark_last_error": (ctypes.c_char_p, [_vp]),
+    "ridc_shards_create": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                                          _vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _P(_vp)]),
+    "ridc_shards_run": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
+    "ridc_shards_info": (ctypes.c_int, [_vp, _P(ctypes.c_int64)]),
+    "ridc_shards_destroy": (ctypes.c_int, [_vp]),
+    "ridc_shards_last_error": (ctypes.c_char_p, [_vp]),
 }
 
 
@@ -101,4 +107,10 @@ def check_pipe(code: int, pipe=None) -> None:
 def check_ark(code: int, ark=None) -> None:
     if code:
         msg = lib().ridc_ark_last_error(ark)
+        raise_for_status(code, msg.decode() if msg else "")
+
+
+def check_shards(code: int, g=None) -> None:
+    if code:
+        msg = lib().ridc_shards_last_error(g)
         raise_for_status(code, msg.decode() if msg else "")

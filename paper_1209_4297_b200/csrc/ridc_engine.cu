@@ -66,6 +66,7 @@ struct EngineParams {
     double* mirror;            // pipeline: consumer's inbox ring (peer memory), or null
     long long mirror_cap, mirror_off;
     ChunkLayout lay;           // padded row layout (ghost columns)
+    int row0;                  // first computed row (1 for a row shard with ghost rows 0 and ny-1)
     const ChunkGeo* cgeo;      // per-segment item geometry
 };
 
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(NT, ROWS == 3 && NSTAGE == 1 ? 2 : 1)
     auto issue_next = [&](int s) {
         int slot, tile;
         item_of(pc.i, ipl, tp.nact, slot, tile);
-        const int row = tile / nseg, seg = tile - row * nseg;
+        const int row = ep.row0 + tile / nseg, seg = tile - (tile / nseg) * nseg;
         const StepItem& it = items[slot];
         issue_chunk_node<NT, ROWS, NSTAGE, KC>(tm, it.vlev[pc.a], it.vslot[pc.a], row, ny, ep.lay.gpr,
                                            ep.lay.gdata, ep.cgeo[seg], stage + (size_t)s * L::STAGE,
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(NT, ROWS == 3 && NSTAGE == 1 ? 2 : 1)
     for (int i = blockIdx.x; i < total; i += gridDim.x, ++ino) {
         int slot, tile;
         item_of(i, ipl, tp.nact, slot, tile);
-        const int row = tile / nseg, seg = tile - row * nseg;
+        const int row = ep.row0 + tile / nseg, seg = tile - (tile / nseg) * nseg;
         const ChunkGeo cg = ep.cgeo[seg];
         switch (MODE >= 0 ? MODE : cg.mode) {
         case 0:
@@ -2384,5 +2385,252 @@ int ridc_ark_destroy(ridc_ark_ctx* a)
 }
 
 const char* ridc_ark_last_error(const ridc_ark_ctx* a) { return a ? a->err.c_str() : g_last_error.c_str(); }
+
+}  // extern "C"
+
+// ================================================================ 2-D row shards (§8f rank 4)
+//
+// The y-direction of the 2-D kinds is explicit (only the x-lines are solved
+// implicitly), so a 2-D state splits into row shards that need, per tick, only
+// each neighbour's boundary row of every slot just written: shard s owns rows
+// [r0, r0 + n) and keeps them as local rows 1..n of an (n + 2)-row layout
+// whose rows 0 and n + 1 are ghosts of the neighbours' rows (periodic in y).
+// Every level runs on every shard (the shards sit UNDER the levels), the
+// tiling in x is the unsharded one, and the y-neighbours carry the same
+// values, so a sharded run equals the unsharded engine bitwise.
+//
+// This group drives S shards on ONE device in lockstep (one graph: per tick
+// the S tick launches, then 2 S row copies per active level).  Across GPUs
+// the same per-tick boundary-row exchange becomes peer copies / NCCL
+// send-recv between neighbouring ranks; that transport is the next step.
+
+struct ridc_shards {
+    int device = 0;
+    int nshards = 0;
+    int levels = 0;
+    long long steps = 0, per = 0, ticks = 0;
+    int restarts = 0;
+    int nx = 0, ny = 0;
+    std::vector<ridc_ctx*> sh;
+    std::vector<int> r0, n;
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    long long launches = 0;
+    std::string err;
+};
+
+namespace {
+
+int shard_fail(ridc_shards* g, int code, const std::string& m) { return fail(g ? &g->err : nullptr, code, m); }
+
+// padded row `row` of ring j, slot index `slot` of shard context c
+double* shard_row(ridc_ctx* c, int j, long long slot, int row)
+{
+    return c->d_ring[j] + slot * c->Vs + (size_t)row * c->ss.lay.P;
+}
+
+int capture_shards(ridc_shards* g)
+{
+    const int S = g->nshards, L = g->levels;
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(&g->err, cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t le = cudaSuccess;
+    long long launches = 0;
+    const int sb_max = 148 * 8;
+    for (int r = 0; r < g->restarts && le == cudaSuccess; ++r) {
+        for (int s = 0; s < S && le == cudaSuccess; ++s) {
+            ridc_ctx* c = g->sh[s];
+            EngineParams ep = interval_params(c, r);
+            const int sb = (int)std::min<long long>((c->Vs + 255) / 256, sb_max);
+            if (r == 0) {
+                k_seed_chunk<<<sb, 256, 0, g->stream>>>(c->d_y0, ep, -1);
+            } else {
+                // the top level's final of the previous interval, ghosts included
+                // (refreshed by the last tick's exchange)
+                EngineParams prev = interval_params(c, r - 1);
+                const double* src = prev.ring[L - 1] + ((prev.off[L - 1] + c->per) % prev.cap[L - 1]) * c->Vs;
+                const ChunkLayout& Ly = c->ss.lay;
+                le = cudaMemcpy2DAsync(c->d_y0 + c->V, (size_t)c->pb.nx * sizeof(double), src + Ly.GW,
+                                       (size_t)Ly.P * sizeof(double), (size_t)c->pb.nx * sizeof(double),
+                                       (size_t)c->pb.ny, cudaMemcpyDeviceToDevice, g->stream);
+                if (le == cudaSuccess) k_seed_chunk<<<sb, 256, 0, g->stream>>>(c->d_y0 + c->V, ep, -1);
+            }
+            if (le == cudaSuccess) le = cudaGetLastError();
+            ++launches;
+        }
+        for (long long k = 1; k <= g->ticks && le == cudaSuccess; ++k) {
+            TickParams tp;
+            memset(&tp, 0, sizeof tp);
+            for (int j = 0; j < L; ++j) {
+                const long long t = k - delay(j);
+                if (t >= 1 && t <= g->per) {
+                    tp.level[tp.nact] = j;
+                    tp.target[tp.nact] = t;
+                    ++tp.nact;
+                }
+            }
+            if (tp.nact == 0) continue;
+            for (int s = 0; s < S && le == cudaSuccess; ++s) {
+                ridc_ctx* c = g->sh[s];
+                EngineParams ep = interval_params(c, r);
+                tp.sv = ep.sv;
+                const int items = g->n[s] * c->ss.sv.nseg;   // owned rows only
+                le = launch_chunk(c->pb.kind, c->ss.ccfg,
+                                  std::min(c->nsm * chunk_ctas_per_sm(c->ss.ccfg, tp.nact), tp.nact * items), g->stream,
+                                  ep, tp, items, c->tm);
+                ++launches;
+            }
+            // boundary rows of every slot written this tick -> the neighbours' ghost rows
+            for (int a = 0; a < tp.nact && le == cudaSuccess; ++a) {
+                const int j = tp.level[a];
+                for (int s = 0; s < S && le == cudaSuccess; ++s) {
+                    ridc_ctx* c = g->sh[s];
+                    ridc_ctx* up = g->sh[(s + S - 1) % S];
+                    ridc_ctx* dn = g->sh[(s + 1) % S];
+                    EngineParams ep = interval_params(c, r);
+                    const long long slot = (ep.off[j] + tp.target[a]) % ep.cap[j];
+                    const size_t rowb = (size_t)c->ss.lay.P * sizeof(double);
+                    le = cudaMemcpyAsync(shard_row(up, j, slot, g->n[(s + S - 1) % S] + 1), shard_row(c, j, slot, 1),
+                                         rowb, cudaMemcpyDeviceToDevice, g->stream);
+                    if (le == cudaSuccess)
+                        le = cudaMemcpyAsync(shard_row(dn, j, slot, 0), shard_row(c, j, slot, g->n[s]), rowb,
+                                             cudaMemcpyDeviceToDevice, g->stream);
+                }
+            }
+        }
+    }
+    cudaError_t ce = cudaStreamEndCapture(g->stream, &graph);
+    if (le != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        return shard_fail(g, RIDC_E_CUDA, std::string("shard capture: ") + cudaGetErrorString(le));
+    }
+    CUDA_TRY(&g->err, ce);
+    cudaError_t ie = cudaGraphInstantiate(&g->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    CUDA_TRY(&g->err, ie);
+    g->launches = launches;
+    return RIDC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ridc_shards_destroy(ridc_shards* g)
+{
+    if (!g) return RIDC_OK;
+    cudaSetDevice(g->device);
+    if (g->stream) cudaStreamSynchronize(g->stream);
+    if (g->gexec) cudaGraphExecDestroy(g->gexec);
+    for (ridc_ctx* c : g->sh) ridc_destroy(c);
+    if (g->ev0) cudaEventDestroy(g->ev0);
+    if (g->ev1) cudaEventDestroy(g->ev1);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+    return RIDC_OK;
+}
+
+int ridc_shards_create(const ridc_problem* problem, double t_start, double t_end, int32_t levels, int64_t steps,
+                       int32_t restarts, const double* weights, int64_t nweights, int32_t nshards, int32_t device,
+                       ridc_shards** out)
+{
+    if (!out) return fail(nullptr, RIDC_E_CONFIG, "out is NULL");
+    *out = nullptr;
+    int rc = validate_problem(problem);
+    if (rc) return rc;
+    if (problem->kind != RIDC_ADV_DIFF_2D && problem->kind != RIDC_REACTION_DIFFUSION_2D)
+        return fail(nullptr, RIDC_E_CONFIG, "row shards need a 2-D kind (explicit in y)");
+    if (nshards < 2 || nshards > problem->ny) return fail(nullptr, RIDC_E_CONFIG, "need 2 <= shards <= ny");
+    ridc_shards* g = new ridc_shards();
+    g->device = device;
+    g->nshards = nshards;
+    g->levels = levels;
+    g->steps = steps;
+    g->restarts = restarts;
+    g->nx = problem->nx;
+    g->ny = problem->ny;
+    for (int s = 0; s < nshards; ++s) {
+        const int a = (int)((long long)problem->ny * s / nshards), b = (int)((long long)problem->ny * (s + 1) / nshards);
+        g->r0.push_back(a);
+        g->n.push_back(b - a);
+        ridc_problem sub = *problem;
+        sub.ny = b - a + 2;   // owned rows + one ghost row on each side
+        ridc_ctx* c = nullptr;
+        rc = ridc_create(&sub, t_start, t_end, levels, steps, restarts, weights, nweights, device, RIDC_TICK_ONLY, &c);
+        if (rc) {
+            const std::string m = g_last_error;
+            ridc_shards_destroy(g);
+            g_last_error = m;
+            return rc;
+        }
+        c->ep.row0 = 1;   // compute rows 1..n; rows 0 and n+1 are the neighbours' ghosts
+        g->sh.push_back(c);
+    }
+    g->per = g->sh[0]->per;
+    g->ticks = g->sh[0]->ticks;
+    auto bail = [&](int code) {
+        const std::string m = g->err.empty() ? g_last_error : g->err;
+        ridc_shards_destroy(g);
+        g_last_error = m;
+        return code;
+    };
+    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) {
+        g->err = "stream / event creation failed";
+        return bail(RIDC_E_CUDA);
+    }
+    if ((rc = capture_shards(g)) != RIDC_OK) return bail(rc);
+    *out = g;
+    return RIDC_OK;
+}
+
+int ridc_shards_run(ridc_shards* g, const double* y0_host, double* final_host, double* wall_seconds)
+{
+    if (!g || !y0_host || !final_host) return shard_fail(g, RIDC_E_CONFIG, "NULL argument");
+    CUDA_TRY(&g->err, cudaSetDevice(g->device));
+    const size_t rowb = (size_t)g->nx * sizeof(double);
+    const int S = g->nshards;
+    // each shard's initial state: its rows plus the wrapped neighbour rows
+    for (int s = 0; s < S; ++s) {
+        ridc_ctx* c = g->sh[s];
+        for (int lr = 0; lr < g->n[s] + 2; ++lr) {
+            const int gr = (g->r0[s] - 1 + lr + g->ny) % g->ny;
+            CUDA_TRY(&g->err, cudaMemcpyAsync(c->d_y0 + (size_t)lr * g->nx, y0_host + (size_t)gr * g->nx, rowb,
+                                              cudaMemcpyHostToDevice, g->stream));
+        }
+        CUDA_TRY(&g->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), g->stream));
+    }
+    CUDA_TRY(&g->err, cudaEventRecord(g->ev0, g->stream));
+    CUDA_TRY(&g->err, cudaGraphLaunch(g->gexec, g->stream));
+    CUDA_TRY(&g->err, cudaEventRecord(g->ev1, g->stream));
+    CUDA_TRY(&g->err, cudaEventSynchronize(g->ev1));
+    if (wall_seconds) {
+        float ms = 0.f;
+        CUDA_TRY(&g->err, cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+        *wall_seconds = ms * 1e-3;
+    }
+    for (int s = 0; s < S; ++s) {
+        ridc_ctx* c = g->sh[s];
+        int rc = check_err_word(c);
+        if (rc) return shard_fail(g, rc, c->err);
+        const ChunkLayout& Ly = c->ss.lay;
+        const double* fin = final_slot(c, g->levels - 1) + (size_t)1 * Ly.P;   // owned rows 1..n
+        CUDA_TRY(&g->err, cudaMemcpy2DAsync(final_host + (size_t)g->r0[s] * g->nx, rowb, fin + Ly.GW,
+                                            (size_t)Ly.P * sizeof(double), rowb, (size_t)g->n[s],
+                                            cudaMemcpyDeviceToHost, g->stream));
+    }
+    CUDA_TRY(&g->err, cudaStreamSynchronize(g->stream));
+    return RIDC_OK;
+}
+
+int ridc_shards_info(const ridc_shards* g, int64_t* kernel_launches)
+{
+    if (!g) return fail(nullptr, RIDC_E_CONFIG, "NULL argument");
+    if (kernel_launches) *kernel_launches = g->launches;
+    return RIDC_OK;
+}
+
+const char* ridc_shards_last_error(const ridc_shards* g) { return g ? g->err.c_str() : g_last_error.c_str(); }
 
 }  // extern "C"

@@ -240,3 +240,50 @@ def run_pipelined_distributed(ivp, config, device: Optional[int] = None):
     sec = pr.run_device(y0, out)
     pr.close()
     return D.to_host(out), sec
+
+
+class RowShardGroup:
+    """2-D row shards under the levels on one device
+    (``ridc_shards_*``): every shard runs all levels on its rows plus one ghost
+    row per side, and the boundary rows of each newly written slot are
+    exchanged after every tick.  Equals the unsharded engine bitwise."""
+
+    def __init__(self, ivp, config, nshards: int, device: int = 0):
+        self.ivp = as_descriptor(ivp)
+        self.config = config
+        self.problem = self.ivp.problem
+        dt = (self.ivp.t_end - self.ivp.t_start) / config.steps
+        w = pack_weight_tables(config.levels, dt)
+        D.require_cuda(device)
+        cp = self.problem.to_c()
+        h = ctypes.c_void_p()
+        _lib.check_shards(_lib.lib().ridc_shards_create(
+            ctypes.byref(cp), float(self.ivp.t_start), float(self.ivp.t_end), config.levels, config.steps,
+            config.restarts, w.ctypes.data, w.shape[0], int(nshards), device, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def kernel_launches(self) -> int:
+        n = ctypes.c_int64(0)
+        _lib.check_shards(_lib.lib().ridc_shards_info(self._h, ctypes.byref(n)), self._h)
+        return n.value
+
+    def run(self, y0=None):
+        """-> (final_state, device seconds)."""
+        y0 = np.ascontiguousarray(self.ivp.initial_state if y0 is None else y0, dtype=np.float64)
+        out = np.empty_like(y0)
+        sec = ctypes.c_double(0.0)
+        _lib.check_shards(_lib.lib().ridc_shards_run(self._h, y0.ctypes.data, out.ctypes.data,
+                                                     ctypes.byref(sec)), self._h)
+        return out, sec.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().ridc_shards_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
