@@ -228,6 +228,18 @@ int ridc_shards_create(const ridc_problem *problem, double t_start, double t_end
                        int32_t levels, int64_t steps, int32_t restarts,
                        const double *weights, int64_t nweights, int32_t nshards,
                        int32_t device, ridc_shards **out);
+/* The same shards, one stream per shard on devices[s] (neighbours may share a
+ * device): per tick each shard waits until both neighbours copied their
+ * boundary rows of the previous tick into its ghost rows (device-side
+ * mailbox, cuStreamWaitValue64), runs its tick, copies its own boundary rows
+ * into the neighbours' ghost rows (peer copies across devices) and raises
+ * their mailboxes.  No host synchronisation per tick; a stalled neighbour
+ * becomes RIDC_E_PROTOCOL after watchdog_seconds. */
+int ridc_shards_create_multi(const ridc_problem *problem, double t_start, double t_end,
+                             int32_t levels, int64_t steps, int32_t restarts,
+                             const double *weights, int64_t nweights, int32_t nshards,
+                             const int32_t *devices, double watchdog_seconds,
+                             ridc_shards **out);
 int ridc_shards_run(ridc_shards *g, const double *y0_host, double *final_host,
                     double *wall_seconds);
 int ridc_shards_info(const ridc_shards *g, int64_t *kernel_launches);

@@ -67,6 +67,9 @@ SIGNATURES = {
     "ridc_ark_last_error": (ctypes.c_char_p, [_vp]),
     "ridc_shards_create": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
                                           _vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _P(_vp)]),
+    "ridc_shards_create_multi": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int32, ctypes.c_int64,
+                                                ctypes.c_int32, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _d,
+                                                _P(_vp)]),
     "ridc_shards_run": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
     "ridc_shards_info": (ctypes.c_int, [_vp, _P(ctypes.c_int64)]),
     "ridc_shards_destroy": (ctypes.c_int, [_vp]),

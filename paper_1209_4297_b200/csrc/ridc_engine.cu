@@ -2417,6 +2417,14 @@ struct ridc_shards {
     cudaGraphExec_t gexec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
+    // multi-stream mode (one stream per shard, possibly one device per shard):
+    // per shard a mailbox {got_up, got_dn} = last global tick whose boundary row
+    // the upper / lower neighbour has copied into this shard's ghost row
+    bool multi = false;
+    std::vector<unsigned long long*> mbox;
+    std::vector<cudaEvent_t> sev0, sev1;
+    double watchdog = 30.0;
+    long long epoch = 0;           // mailbox counters of run m start above epoch (no per-run reset)
     std::string err;
 };
 
@@ -2513,6 +2521,92 @@ int capture_shards(ridc_shards* g)
     return RIDC_OK;
 }
 
+// Multi-stream shard interval (one stream per shard; shards may sit on
+// different devices).  Per tick k (global tick G = interval * ticks + k):
+//   wait until both neighbours delivered tick G-1 into my ghost rows
+//   (cuStreamWaitValue64 on my mailbox), run the tick, copy my boundary rows
+//   of every slot just written into the neighbours' ghost rows (peer copies
+//   over NVLink across devices), then raise their mailboxes to G.
+// A neighbour delivers tick G only after finishing tick G, so when my copy
+// of tick G+1 lands in its ghost row of a slot, its last read of that slot's
+// old content (at tick G at the latest) is done: skew is at most one tick.
+int enqueue_shard(ridc_shards* g, int s, int interval)
+{
+    // (global tick numbers below are offset by the run epoch)
+    const DriverOps& ops = driver_ops();
+    if (!ops.wait || !ops.write) return shard_fail(g, RIDC_E_CUDA, "stream memory operations unavailable");
+    const int S = g->nshards, L = g->levels;
+    ridc_ctx* c = g->sh[s];
+    const int su = (s + S - 1) % S, sd = (s + 1) % S;
+    ridc_ctx* up = g->sh[su];
+    ridc_ctx* dn = g->sh[sd];
+    CUstream cs = reinterpret_cast<CUstream>(c->stream);
+    CUDA_TRY(&g->err, cudaSetDevice(c->device));
+    EngineParams ep = interval_params(c, interval);
+    const long long G0 = g->epoch + (long long)interval * g->ticks;
+    const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
+    auto wait_both = [&](long long G) -> int {
+        if (G <= 0) return RIDC_OK;
+        if (ops.wait(cs, (CUdeviceptr)(g->mbox[s] + 0), (cuuint64_t)G, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+            ops.wait(cs, (CUdeviceptr)(g->mbox[s] + 1), (cuuint64_t)G, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return shard_fail(g, RIDC_E_CUDA, "cuStreamWaitValue64 (shard mailbox) failed");
+        return RIDC_OK;
+    };
+    int rc;
+    if (interval == 0) {
+        k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
+    } else {
+        // the previous interval's top final with ghost rows the neighbours refreshed
+        if ((rc = wait_both(G0)) != RIDC_OK) return rc;   // the last tick of the previous interval
+        EngineParams prev = interval_params(c, interval - 1);
+        const double* src = prev.ring[L - 1] + ((prev.off[L - 1] + c->per) % prev.cap[L - 1]) * c->Vs;
+        const ChunkLayout& Ly = c->ss.lay;
+        CUDA_TRY(&g->err, cudaMemcpy2DAsync(c->d_y0 + c->V, (size_t)c->pb.nx * sizeof(double), src + Ly.GW,
+                                            (size_t)Ly.P * sizeof(double), (size_t)c->pb.nx * sizeof(double),
+                                            (size_t)c->pb.ny, cudaMemcpyDeviceToDevice, c->stream));
+        k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0 + c->V, ep, -1);
+    }
+    CUDA_TRY(&g->err, cudaGetLastError());
+    const size_t rowb = (size_t)c->ss.lay.P * sizeof(double);
+    for (long long k = 1; k <= g->ticks; ++k) {
+        TickParams tp;
+        memset(&tp, 0, sizeof tp);
+        tp.sv = ep.sv;
+        for (int j = 0; j < L; ++j) {
+            const long long t = k - delay(j);
+            if (t >= 1 && t <= g->per) {
+                tp.level[tp.nact] = j;
+                tp.target[tp.nact] = t;
+                ++tp.nact;
+            }
+        }
+        const long long G = G0 + k;
+        if ((k > 1 || interval > 0) && (rc = wait_both(G - 1)) != RIDC_OK) return rc;
+        if (tp.nact > 0) {
+            const int items = g->n[s] * c->ss.sv.nseg;
+            cudaError_t le = launch_chunk(c->pb.kind, c->ss.ccfg,
+                                          std::min(c->nsm * chunk_ctas_per_sm(c->ss.ccfg, tp.nact), tp.nact * items),
+                                          c->stream, ep, tp, items, c->tm);
+            if (le != cudaSuccess) return shard_fail(g, RIDC_E_CUDA, std::string("shard tick: ") + cudaGetErrorString(le));
+            for (int a = 0; a < tp.nact; ++a) {
+                const int j = tp.level[a];
+                const long long slot = (ep.off[j] + tp.target[a]) % ep.cap[j];
+                CUDA_TRY(&g->err, cudaMemcpyAsync(shard_row(up, j, slot, g->n[su] + 1), shard_row(c, j, slot, 1), rowb,
+                                                  cudaMemcpyDefault, c->stream));
+                CUDA_TRY(&g->err, cudaMemcpyAsync(shard_row(dn, j, slot, 0), shard_row(c, j, slot, g->n[s]), rowb,
+                                                  cudaMemcpyDefault, c->stream));
+            }
+        }
+        // my rows of tick G are in both neighbours' ghosts (the upper neighbour's
+        // lower ghost: its got_dn; the lower neighbour's upper ghost: its got_up)
+        if (ops.write(cs, (CUdeviceptr)(g->mbox[su] + 1), (cuuint64_t)G, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS ||
+            ops.write(cs, (CUdeviceptr)(g->mbox[sd] + 0), (cuuint64_t)G, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return shard_fail(g, RIDC_E_CUDA, "cuStreamWriteValue64 (shard mailbox) failed");
+        ++g->launches;
+    }
+    return RIDC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -2523,6 +2617,12 @@ int ridc_shards_destroy(ridc_shards* g)
     cudaSetDevice(g->device);
     if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->gexec) cudaGraphExecDestroy(g->gexec);
+    for (size_t s = 0; s < g->mbox.size(); ++s) {
+        if (s < g->sh.size() && g->sh[s]) cudaSetDevice(g->sh[s]->device);
+        if (g->mbox[s]) cudaFree(g->mbox[s]);
+        if (s < g->sev0.size() && g->sev0[s]) cudaEventDestroy(g->sev0[s]);
+        if (s < g->sev1.size() && g->sev1[s]) cudaEventDestroy(g->sev1[s]);
+    }
     for (ridc_ctx* c : g->sh) ridc_destroy(c);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
@@ -2585,9 +2685,67 @@ int ridc_shards_create(const ridc_problem* problem, double t_start, double t_end
     return RIDC_OK;
 }
 
+static int shards_run_multi(ridc_shards* g, const double* y0_host, double* final_host, double* wall_seconds)
+{
+    const size_t rowb = (size_t)g->nx * sizeof(double);
+    const int S = g->nshards;
+    for (int s = 0; s < S; ++s) {
+        ridc_ctx* c = g->sh[s];
+        CUDA_TRY(&g->err, cudaSetDevice(c->device));
+        for (int lr = 0; lr < g->n[s] + 2; ++lr) {
+            const int gr = (g->r0[s] - 1 + lr + g->ny) % g->ny;
+            CUDA_TRY(&g->err, cudaMemcpyAsync(c->d_y0 + (size_t)lr * g->nx, y0_host + (size_t)gr * g->nx, rowb,
+                                              cudaMemcpyHostToDevice, c->stream));
+        }
+        CUDA_TRY(&g->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+        CUDA_TRY(&g->err, cudaEventRecord(g->sev0[s], c->stream));
+    }
+    int rc;
+    for (int r = 0; r < g->restarts; ++r)
+        for (int s = 0; s < S; ++s)
+            if ((rc = enqueue_shard(g, s, r)) != RIDC_OK) return rc;
+    for (int s = 0; s < S; ++s) {
+        CUDA_TRY(&g->err, cudaSetDevice(g->sh[s]->device));
+        CUDA_TRY(&g->err, cudaEventRecord(g->sev1[s], g->sh[s]->stream));
+    }
+    // watchdog: a shard whose neighbour never delivers turns into PipelineProtocolError
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int s = 0; s < S; ++s) {
+        for (;;) {
+            cudaSetDevice(g->sh[s]->device);
+            cudaError_t q = cudaEventQuery(g->sev1[s]);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) return shard_fail(g, RIDC_E_CUDA, cudaGetErrorString(q));
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > g->watchdog)
+                return shard_fail(g, RIDC_E_PROTOCOL, "row shards made no progress within the watchdog");
+            std::this_thread::sleep_for(std::chrono::microseconds(200));
+        }
+    }
+    g->epoch += (long long)g->restarts * g->ticks + 1;
+    double wall = 0.0;
+    for (int s = 0; s < S; ++s) {
+        ridc_ctx* c = g->sh[s];
+        CUDA_TRY(&g->err, cudaSetDevice(c->device));
+        float ms = 0.f;
+        CUDA_TRY(&g->err, cudaEventElapsedTime(&ms, g->sev0[s], g->sev1[s]));
+        wall = std::max(wall, ms * 1e-3);
+        rc = check_err_word(c);
+        if (rc) return shard_fail(g, rc, c->err);
+        const ChunkLayout& Ly = c->ss.lay;
+        const double* fin = final_slot(c, g->levels - 1) + (size_t)1 * Ly.P;
+        CUDA_TRY(&g->err, cudaMemcpy2DAsync(final_host + (size_t)g->r0[s] * g->nx, rowb, fin + Ly.GW,
+                                            (size_t)Ly.P * sizeof(double), rowb, (size_t)g->n[s],
+                                            cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(&g->err, cudaStreamSynchronize(c->stream));
+    }
+    if (wall_seconds) *wall_seconds = wall;
+    return RIDC_OK;
+}
+
 int ridc_shards_run(ridc_shards* g, const double* y0_host, double* final_host, double* wall_seconds)
 {
     if (!g || !y0_host || !final_host) return shard_fail(g, RIDC_E_CONFIG, "NULL argument");
+    if (g->multi) return shards_run_multi(g, y0_host, final_host, wall_seconds);
     CUDA_TRY(&g->err, cudaSetDevice(g->device));
     const size_t rowb = (size_t)g->nx * sizeof(double);
     const int S = g->nshards;
@@ -2632,5 +2790,76 @@ int ridc_shards_info(const ridc_shards* g, int64_t* kernel_launches)
 }
 
 const char* ridc_shards_last_error(const ridc_shards* g) { return g ? g->err.c_str() : g_last_error.c_str(); }
+
+int ridc_shards_create_multi(const ridc_problem* problem, double t_start, double t_end, int32_t levels,
+                             int64_t steps, int32_t restarts, const double* weights, int64_t nweights,
+                             int32_t nshards, const int32_t* devices, double watchdog_seconds, ridc_shards** out)
+{
+    if (!out || !devices) return fail(nullptr, RIDC_E_CONFIG, "NULL argument");
+    *out = nullptr;
+    int rc = validate_problem(problem);
+    if (rc) return rc;
+    if (problem->kind != RIDC_ADV_DIFF_2D && problem->kind != RIDC_REACTION_DIFFUSION_2D)
+        return fail(nullptr, RIDC_E_CONFIG, "row shards need a 2-D kind (explicit in y)");
+    if (nshards < 2 || nshards > problem->ny) return fail(nullptr, RIDC_E_CONFIG, "need 2 <= shards <= ny");
+    if (!driver_ops().wait || !driver_ops().write)
+        return fail(nullptr, RIDC_E_CUDA, "stream memory operations unavailable");
+    ridc_shards* g = new ridc_shards();
+    g->multi = true;
+    g->device = devices[0];
+    g->nshards = nshards;
+    g->levels = levels;
+    g->steps = steps;
+    g->restarts = restarts;
+    g->nx = problem->nx;
+    g->ny = problem->ny;
+    g->watchdog = watchdog_seconds > 0 ? watchdog_seconds : 30.0;
+    auto bail = [&](int code) {
+        const std::string m = g->err.empty() ? g_last_error : g->err;
+        ridc_shards_destroy(g);
+        g_last_error = m;
+        return code;
+    };
+    for (int s = 0; s < nshards; ++s) {
+        const int a = (int)((long long)problem->ny * s / nshards), b = (int)((long long)problem->ny * (s + 1) / nshards);
+        g->r0.push_back(a);
+        g->n.push_back(b - a);
+        ridc_problem sub = *problem;
+        sub.ny = b - a + 2;
+        ridc_ctx* c = nullptr;
+        rc = ridc_create(&sub, t_start, t_end, levels, steps, restarts, weights, nweights, devices[s], RIDC_TICK_ONLY,
+                         &c);
+        if (rc) return bail(rc);
+        c->ep.row0 = 1;
+        g->sh.push_back(c);
+        unsigned long long* mb = nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (cudaSetDevice(devices[s]) != cudaSuccess || cudaMalloc(&mb, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(mb, 0, 2 * sizeof(unsigned long long)) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
+            cudaEventCreate(&e1) != cudaSuccess) {
+            g->err = "shard mailbox / event allocation failed";
+            return bail(RIDC_E_CUDA);
+        }
+        g->mbox.push_back(mb);
+        g->sev0.push_back(e0);
+        g->sev1.push_back(e1);
+    }
+    // peer access between neighbouring shards on different devices
+    for (int s = 0; s < nshards; ++s)
+        for (int nb : {(s + nshards - 1) % nshards, (s + 1) % nshards}) {
+            if (devices[s] == devices[nb]) continue;
+            cudaSetDevice(devices[s]);
+            cudaError_t e = cudaDeviceEnablePeerAccess(devices[nb], 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                g->err = std::string("peer access: ") + cudaGetErrorString(e);
+                return bail(RIDC_E_CUDA);
+            }
+            cudaGetLastError();
+        }
+    g->per = g->sh[0]->per;
+    g->ticks = g->sh[0]->ticks;
+    *out = g;
+    return RIDC_OK;
+}
 
 }  // extern "C"

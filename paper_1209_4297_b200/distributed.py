@@ -243,12 +243,15 @@ def run_pipelined_distributed(ivp, config, device: Optional[int] = None):
 
 
 class RowShardGroup:
-    """2-D row shards under the levels on one device
-    (``ridc_shards_*``): every shard runs all levels on its rows plus one ghost
-    row per side, and the boundary rows of each newly written slot are
-    exchanged after every tick.  Equals the unsharded engine bitwise."""
+    """2-D row shards under the levels (``ridc_shards_*``):
+    every shard runs all levels on its rows plus one ghost row per side, and
+    the boundary rows of each newly written slot are exchanged after every
+    tick.  ``devices=None``: all shards on ``device`` in lockstep (one graph);
+    ``devices=[d0, d1, ...]``: one stream per shard on its device with
+    device-side mailboxes and peer copies (devices may repeat).  Either way
+    the result equals the unsharded engine bitwise."""
 
-    def __init__(self, ivp, config, nshards: int, device: int = 0):
+    def __init__(self, ivp, config, nshards: int, device: int = 0, devices=None):
         self.ivp = as_descriptor(ivp)
         self.config = config
         self.problem = self.ivp.problem
@@ -257,9 +260,18 @@ class RowShardGroup:
         D.require_cuda(device)
         cp = self.problem.to_c()
         h = ctypes.c_void_p()
-        _lib.check_shards(_lib.lib().ridc_shards_create(
-            ctypes.byref(cp), float(self.ivp.t_start), float(self.ivp.t_end), config.levels, config.steps,
-            config.restarts, w.ctypes.data, w.shape[0], int(nshards), device, ctypes.byref(h)))
+        if devices is None:
+            _lib.check_shards(_lib.lib().ridc_shards_create(
+                ctypes.byref(cp), float(self.ivp.t_start), float(self.ivp.t_end), config.levels, config.steps,
+                config.restarts, w.ctypes.data, w.shape[0], int(nshards), device, ctypes.byref(h)))
+        else:
+            devs = (ctypes.c_int32 * int(nshards))(*[int(devices[s % len(devices)]) for s in range(int(nshards))])
+            for d in set(devs):
+                D.require_cuda(d)
+            _lib.check_shards(_lib.lib().ridc_shards_create_multi(
+                ctypes.byref(cp), float(self.ivp.t_start), float(self.ivp.t_end), config.levels, config.steps,
+                config.restarts, w.ctypes.data, w.shape[0], int(nshards), devs, float(config.watchdog_seconds),
+                ctypes.byref(h)))
         self._h = h
 
     @property

@@ -41,6 +41,20 @@ def test_row_shards_equal_engine_bitwise(name, builder, levels, steps, restarts,
     assert np.array_equal(final, ref.final_state)
 
 
+@pytest.mark.parametrize("name,builder,levels,steps,restarts,nshards", CASES, ids=[c[0] for c in CASES])
+def test_row_shards_multistream_equal_engine_bitwise(name, builder, levels, steps, restarts, nshards):
+    """One stream per shard (all on device 0 here): the device-side mailbox
+    protocol that runs across GPUs, with shards free to drift by a tick."""
+    s = builder()
+    cfg = E.RidcConfig(levels=levels, steps=steps, restarts=restarts, watchdog_seconds=30.0)
+    ref = E.run_serial(s, cfg)
+    with RowShardGroup(s, cfg, nshards, devices=[0]) as g:
+        a, _ = g.run()
+        b, sec = g.run()   # a second run: mailbox epochs, no reset
+    assert sec > 0
+    assert np.array_equal(a, ref.final_state) and np.array_equal(b, ref.final_state)
+
+
 def test_row_shards_reject_1d_and_too_many():
     s1 = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=1024, d=1e-3, t_end=0.01))
     with pytest.raises(ConfigError):
