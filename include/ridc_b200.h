@@ -17,6 +17,12 @@
  *                                     driven by states instead of f^S/f^N rows
  *   ridc_pipe_*              the one-level-per-GPU lagged pipeline
  *                                     (engine.py:349-459, LevelBuffer :284-331)
+ *   ridc_ark_*               replace  steppers.ark_step / integrate_ark
+ *                                     (steppers.py:122-155) with
+ *                                     kernels.stage_accumulate (kernels.py:149-158)
+ *                                     for the tableaus.py imex3 / imex4 pairs
+ *   ridc_shards_*            2-D row shards under the levels (no reference
+ *                                     analogue)
  *
  * Conventions.  All pointers are plain; no torch types.  "_host" buffers are
  * caller-owned host memory; "_dev" buffers are caller-owned device memory on
