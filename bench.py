@@ -234,8 +234,10 @@ def run_ours(args):
         launches_per_step = runner.kernel_launches
         tick_launches = runner.tick_launches
         # this rank's level-step bytes per point; the producer side also writes the
-        # consumer's inbox copy (8 B/pt over NVLink, counted on the consumer)
-        lev_bytes = bytes_per_point(rank) + (8 if rank < world - 1 else 0)
+        # consumer's inbox copy (8 B/pt over NVLink, counted on the consumer);
+        # per launch of the level-step kernel (resident: a whole interval)
+        resident = runner.resident
+        lev_bytes = (bytes_per_point(rank) + (8 if rank < world - 1 else 0)) * nt / max(tick_launches, 1)
     else:
         eng = E.Engine(sysm, E.RidcConfig(levels=order, steps=nt))
         y0 = torch.from_numpy(np.array(sysm.ivp.initial_state)).cuda()
@@ -286,7 +288,11 @@ def run_ours(args):
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": ("k_resident_febe (whole FEBE march in one launch: registers-resident chunks, "
+                "kernel": (("k_resident_levels (this rank's level: whole interval in one launch, "
+                            "registers-resident chunks, TMA-staged window of the producer level, "
+                            "per-segment publish/release flags, tile stores into the consumer's inbox over NVLink)")
+                           if world > 1 and resident else
+                           "k_resident_febe (whole FEBE march in one launch: registers-resident chunks, "
                            "stencil + factored tridiagonal solve per step, halo edges via tagged L2 mailbox)"
                            if resident else "k_tick_chunk (fused level-step: stencils + factored tridiagonal solve)"),
                 "bytes_per_launch": bytes_launch, "launch_us": per_launch_s * 1e6}

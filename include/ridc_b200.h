@@ -74,8 +74,9 @@ typedef struct ridc_ctx ridc_ctx;
 
 /* run flags */
 #define RIDC_RECORD_TRAJECTORY 1u  /* RidcConfig.record_trajectory */
-#define RIDC_TICK_ONLY 2u          /* never use the resident single-level march (testing:
-                                      it must agree bitwise with the tick kernel) */
+#define RIDC_TICK_ONLY 2u          /* never use the resident marches -- single-level FEBE or
+                                      the multi-level one (testing: they must agree bitwise
+                                      with the tick kernel) */
 #define RIDC_RESIDENT_SEGMENTS 4u  /* accepted for compatibility: segmented lines march
                                       resident by default */
 
@@ -195,6 +196,17 @@ int ridc_pipe_connect(ridc_pipe *p, const void *prev_blob, const void *next_blob
 int ridc_pipe_run_interval(ridc_pipe *p, int32_t interval, const double *state0_dev,
                            double *final_dev, double *wall_seconds);
 int ridc_pipe_info(const ridc_pipe *p, ridc_info *info);
+/* Resident level march (default where the line qualifies: 1-D, one
+ * co-resident CTA per segment): the rank's whole interval is ONE cooperative
+ * launch whose CTAs poll per-segment publish / release flags in peer memory
+ * (the LevelBuffer watermark / released protocol, engine.py:299-331) instead
+ * of per-step stream memory operations.  enable = 0 selects the per-step
+ * tick kernel + stream memops.  Call before ridc_pipe_export on EVERY rank
+ * (the mode travels in the blob; neighbours must agree).  Never run ranks
+ * of the resident mode concurrently on one device (their kernels wait on
+ * each other).  ridc_pipe_resident reports the mode in effect. */
+int ridc_pipe_set_resident(ridc_pipe *p, int32_t enable);
+int ridc_pipe_resident(const ridc_pipe *p);
 int ridc_pipe_destroy(ridc_pipe *p);
 const char *ridc_pipe_last_error(const ridc_pipe *p);
 

@@ -56,6 +56,8 @@ SIGNATURES = {
     "ridc_pipe_connect": (ctypes.c_int, [_vp, _vp, _vp]),
     "ridc_pipe_run_interval": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, _dp]),
     "ridc_pipe_info": (ctypes.c_int, [_vp, _P(RidcInfo)]),
+    "ridc_pipe_set_resident": (ctypes.c_int, [_vp, ctypes.c_int32]),
+    "ridc_pipe_resident": (ctypes.c_int, [_vp]),
     "ridc_pipe_destroy": (ctypes.c_int, [_vp]),
     "ridc_pipe_last_error": (ctypes.c_char_p, [_vp]),
     "ridc_ark_create": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp, _vp,

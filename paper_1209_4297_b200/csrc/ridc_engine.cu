@@ -35,6 +35,7 @@
 #include "ridc_tma.cuh"
 #include "ridc_chunk.cuh"
 #include "ridc_resident.cuh"
+#include "ridc_levels.cuh"
 
 using namespace ridc;
 
@@ -551,6 +552,74 @@ cudaError_t resident_dispatch(int kind, int nt, int mode, bool launch, int grid,
     }
 }
 
+// ---- resident level march (ridc_levels.cuh): every lane a group of nseg CTAs
+constexpr int kResStages = 2;
+
+template <int KIND, int NT, int MODE>
+cudaError_t levels_t(bool launch, int grid, cudaStream_t st, const LevelsParams& lp, const TmapSet& tm,
+                     int* per_sm)
+{
+    auto kfn = k_resident_levels<KIND, NT, MODE, kResStages>;
+    const size_t smem = ChunkSmem<NT, 1, kResStages, kChunk>::BYTES + 1024;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, NT, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // every level's segments co-resident (flag waits)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, lp, tm);
+}
+
+template <int KIND>
+cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const LevelsParams& lp,
+                     const TmapSet& tm, int* per_sm)
+{
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr int MA = periodic ? 0 : 2, MB = periodic ? 1 : -1;
+    if (mode != MA && mode != MB) {
+        if (periodic) return cudaErrorInvalidValue;
+        mode = MB;
+    }
+#define RIDC_LEV_NT(NT)                                                                          \
+    case NT:                                                                                     \
+        return mode == MA ? levels_t<KIND, NT, MA>(launch, grid, st, lp, tm, per_sm)             \
+                          : levels_t<KIND, NT, MB>(launch, grid, st, lp, tm, per_sm);
+    switch (nt) {
+        RIDC_LEV_NT(64)
+        RIDC_LEV_NT(128)
+        RIDC_LEV_NT(256)
+        RIDC_LEV_NT(512)
+    default: return cudaErrorInvalidValue;
+    }
+#undef RIDC_LEV_NT
+}
+
+// launch == false: occupancy query into *per_sm
+cudaError_t levels_dispatch(int kind, int nt, int mode, bool launch, int grid, cudaStream_t st,
+                            const LevelsParams& lp, const TmapSet& tm, int* per_sm)
+{
+    switch (kind) {
+    case ADV_DIFF_1D: return levels_k<ADV_DIFF_1D>(nt, mode, launch, grid, st, lp, tm, per_sm);
+    case BURGERS_1D: return levels_k<BURGERS_1D>(nt, mode, launch, grid, st, lp, tm, per_sm);
+    case RD_1D: return levels_k<RD_1D>(nt, mode, launch, grid, st, lp, tm, per_sm);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
 cudaError_t launch_item(int kind, const LaunchCfg& c, int items, cudaStream_t st,
                         const DevProblem& pb, const DevSolve& sv, const StepItem& it,
                         unsigned long long* err)
@@ -832,6 +901,60 @@ int make_chunk_solve(const DevProblem& pb, double coeff, int nsm, SolveSetup& ss
     return RIDC_OK;
 }
 
+// Resident level march geometry (ridc_levels.cuh): the producer segments
+// whose tiles (or periodic ghost copies) a consumer segment's staged columns
+// read, the converse, the edge width pushed through the halo mailbox and the
+// common segment mode.  false: the line does not qualify.
+struct ResGeo {
+    std::vector<int> deps, readers;   // [nseg][kResDeps], -1 padded
+    int edge_w = 0;
+    int mode = -1;
+};
+
+bool res_geometry(const DevProblem& pb, const SolveSetup& ss, ResGeo& g)
+{
+    const int nseg = ss.sv.nseg, nx = pb.nx;
+    if (!(pb.kind == ADV_DIFF_1D || pb.kind == BURGERS_1D || pb.kind == RD_1D) || pb.ny != 1) return false;
+    if (ss.ccfg.rows != 1 || ss.ccfg.kc != kChunk || (int)ss.cgeo.size() != nseg) return false;
+    int ext = 0;
+    for (const ChunkGeo& c : ss.cgeo) {
+        ext = std::max(ext, c.c0 - 16 * c.g0);
+        ext = std::max(ext, 16 * (c.g0 + c.ng) - (c.c0 + c.tlen));
+    }
+    const int W = std::max(ext, ss.lay.GW);
+    for (const ChunkGeo& c : ss.cgeo)
+        if (nseg > 1 && (ext >= c.tlen || W >= c.tlen)) return false;
+    std::vector<int> owner(nx, -1);
+    for (int s = 0; s < nseg; ++s)
+        for (int c = ss.cgeo[s].c0; c < ss.cgeo[s].c0 + ss.cgeo[s].tlen; ++c) owner[c] = s;
+    g.deps.assign((size_t)nseg * kResDeps, -1);
+    g.readers.assign((size_t)nseg * kResDeps, -1);
+    std::vector<int> nr(nseg, 0);
+    for (int k = 0; k < nseg; ++k) {
+        const ChunkGeo& c = ss.cgeo[k];
+        int nd = 0;
+        for (int x = 16 * c.g0; x < 16 * (c.g0 + c.ng); ++x) {
+            int col = x;
+            if (pb.periodic) col = ((x % nx) + nx) % nx;
+            else if (col < 0 || col >= nx) continue;
+            const int o = owner[col];
+            if (o < 0) return false;
+            bool seen = false;
+            for (int q = 0; q < nd; ++q) seen |= g.deps[k * kResDeps + q] == o;
+            if (seen) continue;
+            if (nd == kResDeps) return false;
+            g.deps[k * kResDeps + nd++] = o;
+            if (nr[o] == kResDeps) return false;
+            g.readers[o * kResDeps + nr[o]++] = k;
+        }
+    }
+    g.edge_w = W;
+    g.mode = ss.cgeo[0].mode;
+    for (const ChunkGeo& c : ss.cgeo)
+        if (c.mode != g.mode) g.mode = -1;
+    return true;
+}
+
 }  // namespace
 
 // ================================================================ context
@@ -878,6 +1001,19 @@ struct ridc_ctx {
     uint4* d_mail = nullptr;       // tagged mailbox lines (2 parities x Vs)
     unsigned tag_next = 1;         // next run's epoch
     ResidentParams rp;
+    // resident level march (ridc_levels.cuh): levels >= 2 on a 1-D line, one
+    // co-resident CTA group per level, device-side flags between the levels
+    bool reslev = false;
+    int reslev_mode = -1;
+    double* d_inbox[kMaxLevels] = {};   // level j's inbox: level j-1's states (j >= 1)
+    long long in_cap = 0;
+    unsigned long long* d_lflags = nullptr;   // pub [L][nseg], then rel [L][nseg]
+    uint4* d_lmail = nullptr;                 // L x 2 parities x Vs tagged lines
+    LevelLane* d_lanes = nullptr;
+    int* d_geo = nullptr;                     // deps [nseg][4], then readers [nseg][4]
+    TmapSet tm_in;
+    LevelsParams lp;
+    unsigned long long lepoch = 0;
     std::string err;
 };
 
@@ -948,6 +1084,7 @@ EngineParams interval_params(ridc_ctx* c, int interval)
 const double* final_slot(ridc_ctx* c, int level)
 {
     if (c->resident) return c->d_ring[0] + (c->steps % c->cap[0]) * c->Vs;   // one launch, global steps
+    if (c->reslev) return c->d_ring[level] + c->Vs;                              // slot 1: the final tile
     EngineParams ep = interval_params(c, c->restarts - 1);
     return ep.ring[level] + ((ep.off[level] + c->per) % ep.cap[level]) * c->Vs;
 }
@@ -1067,9 +1204,73 @@ int check_err_word(ridc_ctx* c)
     return RIDC_OK;
 }
 
+// One resident level-march launch per restart interval (ridc_levels.cuh):
+// seed every level's own slot 0 and inbox slot 0 with the interval's state0,
+// march, then the top level's final becomes the next state0.
+// false in *fell_back: the cooperative launch could not get the SMs.
+int march_reslev(ridc_ctx* c, bool* fell_back)
+{
+    *fell_back = false;
+    const int L = c->levels, nseg = c->ss.sv.nseg;
+    if ((unsigned long long)c->tag_next + (unsigned long long)c->restarts * (c->per + 1) + 2 >= 0xffffffffull) {
+        if (c->d_lmail)
+            CUDA_TRY(&c->err, cudaMemsetAsync(c->d_lmail, 0, (size_t)L * 2 * c->Vs * sizeof(uint4), c->stream));
+        c->tag_next = 1;
+    }
+    CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, sizeof(unsigned), c->stream));
+    const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
+    for (int r = 0; r < c->restarts; ++r) {
+        const double* src = c->d_y0;
+        if (r > 0) {
+            CUDA_TRY(&c->err, copy_out(c, c->d_y0 + c->V, final_slot(c, L - 1), cudaMemcpyDeviceToDevice));
+            src = c->d_y0 + c->V;
+        }
+        EngineParams sp;
+        memset(&sp, 0, sizeof sp);
+        sp.pb = c->pb;
+        sp.lay = c->ss.lay;
+        sp.levels = L;
+        for (int j = 0; j < L; ++j) {
+            sp.ring[j] = c->d_ring[j];
+            sp.cap[j] = c->cap[j];
+        }
+        k_seed_chunk<<<sb, 256, 0, c->stream>>>(src, sp, -1);
+        CUDA_TRY(&c->err, cudaGetLastError());
+        for (int j = 0; j < L; ++j) {
+            sp.ring[j] = c->d_inbox[j];
+            sp.cap[j] = c->in_cap;
+        }
+        k_seed_chunk<<<sb, 256, 0, c->stream>>>(src, sp, -1);
+        CUDA_TRY(&c->err, cudaGetLastError());
+        LevelsParams lp = c->lp;
+        lp.epoch = ++c->lepoch;
+        lp.tag0 = c->tag_next;
+        c->tag_next += (unsigned)c->per + 1;
+        const cudaError_t le = levels_dispatch(c->pb.kind, c->ss.ccfg.nt, c->reslev_mode, true, L * nseg,
+                                               c->stream, lp, c->tm_in, nullptr);
+        if (le == cudaErrorCooperativeLaunchTooLarge && r == 0) {
+            cudaGetLastError();
+            *fell_back = true;
+            return RIDC_OK;
+        }
+        CUDA_TRY(&c->err, le);
+    }
+    return RIDC_OK;
+}
+
 int march(ridc_ctx* c, double* wall_seconds)
 {
     CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+    if (c->reslev) {
+        CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
+        bool fb = false;
+        int rc = march_reslev(c, &fb);
+        if (rc) return rc;
+        if (fb) {   // the SMs are shared right now: the tick kernel's graph for good
+            c->reslev = false;
+            if ((rc = capture_graph(c)) != RIDC_OK) return rc;
+        }
+    }
     if (c->resident) {
         const int nseg = c->ss.sv.nseg;
         // each run tags its mailbox lines with a fresh epoch (no per-run clearing)
@@ -1098,7 +1299,7 @@ int march(ridc_ctx* c, double* wall_seconds)
             CUDA_TRY(&c->err, le);
         }
     }
-    if (!c->resident) {
+    if (!c->resident && !c->reslev) {
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
         CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
     }
@@ -1109,7 +1310,7 @@ int march(ridc_ctx* c, double* wall_seconds)
         CUDA_TRY(&c->err, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         *wall_seconds = ms * 1e-3;
     }
-    if (c->resident) {
+    if (c->resident || c->reslev) {
         unsigned ab = 0;
         CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_flags, sizeof ab, cudaMemcpyDeviceToHost));
         if (ab) return fail(&c->err, RIDC_E_PROTOCOL, "resident march: a neighbour segment wait timed out");
@@ -1179,6 +1380,98 @@ int setup_resident(ridc_ctx* c)
     rp.dbg = c->d_dbg;
     c->resident = true;
     c->launches = 2;
+    return RIDC_OK;
+}
+
+// Resident level march for levels >= 2 on a 1-D line: every level's segments
+// co-resident (L x nseg CTAs, one per SM), no trajectory recording.
+int setup_reslev(ridc_ctx* c)
+{
+    const int L = c->levels, nseg = c->ss.sv.nseg;
+    if (L < 2 || (c->flags & (RIDC_TICK_ONLY | RIDC_RECORD_TRAJECTORY)) || c->traj_stream) return RIDC_OK;
+    if (getenv("RIDC_NO_RESIDENT_LEVELS") && atoi(getenv("RIDC_NO_RESIDENT_LEVELS")) > 0) return RIDC_OK;
+    ResGeo g;
+    if (!res_geometry(c->pb, c->ss, g)) return RIDC_OK;
+    LevelsParams& lp = c->lp;
+    memset(&lp, 0, sizeof lp);
+    int per_sm = 0;
+    const cudaError_t oe = levels_dispatch(c->pb.kind, c->ss.ccfg.nt, g.mode, false, 0, c->stream, lp, c->tm,
+                                           &per_sm);
+    if (oe != cudaSuccess || per_sm * c->nsm < L * nseg) {
+        if (getenv("RIDC_DEBUG"))
+            fprintf(stderr, "ridc: resident level march unavailable (%s, %d blocks/SM x %d SMs < %d)\n",
+                    cudaGetErrorString(oe), per_sm, c->nsm, L * nseg);
+        cudaGetLastError();
+        return RIDC_OK;
+    }
+    c->reslev_mode = g.mode;
+    c->in_cap = 16;   // >= j + 2 for every level (deadlock-free), slack for the producers to run ahead
+    memset(&c->tm_in, 0, sizeof c->tm_in);
+    for (int j = 1; j < L; ++j) {
+        const size_t b = (size_t)c->in_cap * c->Vs * sizeof(double);
+        CUDA_TRY(&c->err, cudaMalloc(&c->d_inbox[j], b));
+        CUDA_TRY(&c->err, cudaMemset(c->d_inbox[j], 0, b));   // Dirichlet ghosts stay 0
+        c->ring_vectors += c->in_cap;
+        int rc = make_ring_map(&c->tm_in.map[j], c->d_inbox[j], c->Vs, c->in_cap, chunk_groups(c->ss.ccfg), &c->err);
+        if (rc) return rc;
+    }
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_lflags, (size_t)2 * L * nseg * sizeof(unsigned long long)));
+    CUDA_TRY(&c->err, cudaMemset(c->d_lflags, 0, (size_t)2 * L * nseg * sizeof(unsigned long long)));
+    if (nseg > 1) {
+        CUDA_TRY(&c->err, cudaMalloc(&c->d_lmail, (size_t)L * 2 * c->Vs * sizeof(uint4)));
+        CUDA_TRY(&c->err, cudaMemset(c->d_lmail, 0, (size_t)L * 2 * c->Vs * sizeof(uint4)));
+    }
+    if (!c->d_flags) CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, sizeof(unsigned)));
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_geo, 2 * g.deps.size() * sizeof(int)));
+    CUDA_TRY(&c->err, cudaMemcpy(c->d_geo, g.deps.data(), g.deps.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(&c->err, cudaMemcpy(c->d_geo + g.deps.size(), g.readers.data(), g.readers.size() * sizeof(int),
+                                 cudaMemcpyHostToDevice));
+    unsigned long long* pub = c->d_lflags;
+    unsigned long long* rel = c->d_lflags + (size_t)L * nseg;
+    std::vector<LevelLane> lanes(L);
+    for (int j = 0; j < L; ++j) {
+        LevelLane& ln = lanes[j];
+        memset(&ln, 0, sizeof ln);
+        ln.level = j;
+        ln.in_map = j;
+        ln.own0 = c->d_ring[j];
+        ln.fin = c->d_ring[j] + c->Vs;
+        ln.in_off = 0;
+        ln.in_cap = c->in_cap;
+        ln.in_pub = pub + (size_t)j * nseg;
+        ln.in_rel = rel + (size_t)j * nseg;
+        if (j < L - 1) {
+            ln.out = c->d_inbox[j + 1];
+            ln.out_off = 0;
+            ln.out_cap = c->in_cap;
+            ln.out_pub = pub + (size_t)(j + 1) * nseg;
+            ln.out_rel = rel + (size_t)(j + 1) * nseg;
+        }
+        ln.mail = c->d_lmail ? c->d_lmail + (size_t)j * 2 * c->Vs : nullptr;
+    }
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_lanes, L * sizeof(LevelLane)));
+    CUDA_TRY(&c->err, cudaMemcpy(c->d_lanes, lanes.data(), L * sizeof(LevelLane), cudaMemcpyHostToDevice));
+    lp.pb = c->pb;
+    lp.sv = c->ss.sv;
+    lp.lay = c->ss.lay;
+    lp.cgeo = c->d_cgeo;
+    lp.lanes = c->d_lanes;
+    lp.deps = c->d_geo;
+    lp.readers = c->d_geo + g.deps.size();
+    lp.weights = c->d_weights;
+    for (int j = 0; j < kMaxLevels; ++j) {
+        lp.steady_off[j] = c->steady_off[j];
+        lp.startup_off[j] = c->startup_off[j];
+    }
+    lp.dt = c->dt;
+    lp.per = c->per;
+    lp.Vs = c->Vs;
+    lp.edge_w = g.edge_w;
+    lp.err = c->d_err;
+    lp.abort = c->d_flags;
+    lp.spin_limit = 4000000000LL;   // ~2 s at 1.9 GHz per wait
+    c->reslev = true;
+    c->launches = 3LL * c->restarts;   // per interval: two seeds + one march
     return RIDC_OK;
 }
 
@@ -1334,7 +1627,8 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     ep.lay = c->ss.lay;
     ep.cgeo = c->d_cgeo;
     if ((rc = setup_resident(c)) != RIDC_OK) return bail(rc);
-    if (!c->resident && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
+    if (!c->resident && (rc = setup_reslev(c)) != RIDC_OK) return bail(rc);
+    if (!c->resident && !c->reslev && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
 #undef CTX_TRY
     *out = c;
     return RIDC_OK;
@@ -1412,6 +1706,12 @@ int ridc_destroy(ridc_ctx* c)
     if (c->d_err) cudaFree(c->d_err);
     if (c->d_flags) cudaFree(c->d_flags);
     if (c->d_mail) cudaFree(c->d_mail);
+    for (int j = 0; j < kMaxLevels; ++j)
+        if (c->d_inbox[j]) cudaFree(c->d_inbox[j]);
+    if (c->d_lflags) cudaFree(c->d_lflags);
+    if (c->d_lmail) cudaFree(c->d_lmail);
+    if (c->d_lanes) cudaFree(c->d_lanes);
+    if (c->d_geo) cudaFree(c->d_geo);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev_prod) cudaEventDestroy(c->ev_prod);
@@ -1589,7 +1889,9 @@ const DriverOps& driver_ops()
 }
 
 constexpr uint32_t kBlobMagic = 0x52494443u;   // "RIDC"
-constexpr size_t kFlagBytes = 256;             // wm (+0), rel (+8), then the inbox ring
+constexpr size_t kFlagBytes = 4096;            // wm (+0), rel (+8), pub[nseg] (+256), relv[nseg] (+2048), then the inbox ring
+constexpr size_t kPubOff = 256, kRelOff = 2048;
+constexpr int kPipeMaxSeg = (int)((kRelOff - kPubOff) / 8);
 
 struct PipeBlob {
     uint32_t magic;
@@ -1598,6 +1900,7 @@ struct PipeBlob {
     uint64_t direct;       // mailbox base (valid inside the exporting process)
     int64_t inbox_cap;
     int64_t vs;
+    int32_t resident;      // resident level march (device-side flags) vs stream memops
 };
 
 }  // namespace
@@ -1631,6 +1934,19 @@ struct ridc_pipe {
     std::vector<int> st, su;
     std::map<int, cudaGraphExec_t> graphs;
     long long launches = 0;
+    // resident level march (ridc_levels.cuh): one launch per interval, the
+    // watermark / release protocol as per-segment flags polled in the kernel
+    bool reslev_ok = false, reslev = false;
+    int reslev_mode = -1;
+    ResGeo rgeo;
+    int* d_geo = nullptr;
+    uint4* d_lmail = nullptr;
+    unsigned* d_abort = nullptr;
+    LevelLane* d_lanes = nullptr;   // one per interval (filled at connect)
+    unsigned long long* in_rel = nullptr;    // producer's relv (peer)
+    unsigned long long* out_pub = nullptr;   // consumer's pub (peer)
+    unsigned long long lepoch = 0;
+    unsigned tag_next = 1;
     std::string err;
 };
 
@@ -1834,6 +2150,32 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     if (level > 0 &&
         (rc = make_ring_map(&p->tm.map[level - 1], p->inbox, p->Vs, p->inbox_cap, chunk_groups(p->ss.ccfg), &p->err)) != RIDC_OK)
         return bail(rc);
+    // resident level march: 1-D lines whose segments fit one co-resident CTA each
+    if (levels >= 2 && p->ss.sv.nseg <= kPipeMaxSeg && res_geometry(p->pb, p->ss, p->rgeo) &&
+        !(getenv("RIDC_NO_RESIDENT_LEVELS") && atoi(getenv("RIDC_NO_RESIDENT_LEVELS")) > 0)) {
+        LevelsParams lp;
+        memset(&lp, 0, sizeof lp);
+        int per_sm = 0;
+        const cudaError_t oe = levels_dispatch(p->pb.kind, p->ss.ccfg.nt, p->rgeo.mode, false, 0, p->stream, lp,
+                                               p->tm, &per_sm);
+        if (oe == cudaSuccess && per_sm * p->nsm >= p->ss.sv.nseg) {
+            p->reslev_ok = p->reslev = true;
+            p->reslev_mode = p->rgeo.mode;
+            const int nseg = p->ss.sv.nseg;
+            const std::vector<int>& d = p->rgeo.deps;
+            P_TRY(cudaMalloc(&p->d_geo, 2 * d.size() * sizeof(int)));
+            P_TRY(cudaMemcpy(p->d_geo, d.data(), d.size() * sizeof(int), cudaMemcpyHostToDevice));
+            P_TRY(cudaMemcpy(p->d_geo + d.size(), p->rgeo.readers.data(), d.size() * sizeof(int),
+                             cudaMemcpyHostToDevice));
+            P_TRY(cudaMalloc(&p->d_abort, sizeof(unsigned)));
+            P_TRY(cudaMalloc(&p->d_lanes, (size_t)restarts * sizeof(LevelLane)));
+            if (nseg > 1) {
+                P_TRY(cudaMalloc(&p->d_lmail, 2 * (size_t)p->Vs * sizeof(uint4)));
+                P_TRY(cudaMemset(p->d_lmail, 0, 2 * (size_t)p->Vs * sizeof(uint4)));
+            }
+        }
+        cudaGetLastError();
+    }
 #undef P_TRY
     *out = p;
     return RIDC_OK;
@@ -1851,6 +2193,7 @@ int ridc_pipe_export(ridc_pipe* p, void* blob)
     b.direct = (uint64_t)(uintptr_t)p->mailbox;
     b.inbox_cap = p->inbox_cap;
     b.vs = p->Vs;
+    b.resident = p->reslev ? 1 : 0;
     PIPE_TRY(p, cudaSetDevice(p->device));
     PIPE_TRY(p, cudaIpcGetMemHandle(&b.handle, p->mailbox));
     memcpy(blob, &b, sizeof b);
@@ -1863,6 +2206,9 @@ static int open_blob(ridc_pipe* p, const void* blob, int want_level, char** base
     memcpy(&b, blob, sizeof b);
     if (b.magic != kBlobMagic || b.level != want_level || b.vs != p->Vs)
         return pipe_fail(p, RIDC_E_PROTOCOL, "pipeline handle from an incompatible rank");
+    if ((b.resident != 0) != p->reslev)
+        return pipe_fail(p, RIDC_E_CONFIG, "neighbour ranks disagree on the resident level march "
+                                           "(ridc_pipe_set_resident before ridc_pipe_export on every rank)");
     if (b.pid == (int32_t)getpid()) {
         *base = reinterpret_cast<char*>((uintptr_t)b.direct);
         if (b.device != p->device) {
@@ -1894,12 +2240,37 @@ int ridc_pipe_connect(ridc_pipe* p, const void* prev_blob, const void* next_blob
     if (prev_blob) {
         if ((rc = open_blob(p, prev_blob, j - 1, &base, 0, &cap)) != RIDC_OK) return rc;
         p->prev_rel = reinterpret_cast<unsigned long long*>(base + 8);
+        p->in_rel = reinterpret_cast<unsigned long long*>(base + kRelOff);
     }
     if (next_blob) {
         if ((rc = open_blob(p, next_blob, j + 1, &base, 1, &cap)) != RIDC_OK) return rc;
         p->next_wm = reinterpret_cast<unsigned long long*>(base);
         p->next_inbox = reinterpret_cast<double*>(base + kFlagBytes);
         p->next_cap = cap;
+        p->out_pub = reinterpret_cast<unsigned long long*>(base + kPubOff);
+    }
+    if (p->reslev) {   // one lane per interval: slots and offsets follow the global step numbers
+        std::vector<LevelLane> lanes(p->restarts);
+        for (int r = 0; r < p->restarts; ++r) {
+            const long long g0 = (long long)r * p->per;
+            LevelLane& ln = lanes[r];
+            memset(&ln, 0, sizeof ln);
+            ln.level = j;
+            ln.in_map = j > 0 ? j - 1 : 0;
+            ln.own0 = p->own + (g0 % 2) * p->Vs;
+            ln.fin = p->own + ((g0 + p->per) % 2) * p->Vs;
+            ln.in_off = g0;
+            ln.in_cap = p->inbox_cap;
+            ln.in_pub = reinterpret_cast<unsigned long long*>(p->mailbox + kPubOff);
+            ln.in_rel = p->in_rel;
+            ln.out = j < top ? p->next_inbox : nullptr;
+            ln.out_off = g0;
+            ln.out_cap = p->next_cap;
+            ln.out_pub = p->out_pub;
+            ln.out_rel = reinterpret_cast<unsigned long long*>(p->mailbox + kRelOff);
+            ln.mail = p->d_lmail;
+        }
+        PIPE_TRY(p, cudaMemcpy(p->d_lanes, lanes.data(), lanes.size() * sizeof(LevelLane), cudaMemcpyHostToDevice));
     }
     return RIDC_OK;
 }
@@ -1932,7 +2303,43 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
     // the interval's ops: captured into a graph on first use (memops included)
     auto it = p->graphs.find(interval);
     long long launches = 0;
-    if (it == p->graphs.end()) {
+    if (p->reslev) {
+        const int nseg = p->ss.sv.nseg;
+        if (p->tag_next + (unsigned long long)p->per + 2 >= 0xffffffffull) {
+            if (p->d_lmail) PIPE_TRY(p, cudaMemsetAsync(p->d_lmail, 0, 2 * (size_t)p->Vs * sizeof(uint4), p->stream));
+            p->tag_next = 1;
+        }
+        PIPE_TRY(p, cudaMemsetAsync(p->d_abort, 0, sizeof(unsigned), p->stream));
+        LevelsParams lp;
+        memset(&lp, 0, sizeof lp);
+        lp.pb = p->pb;
+        lp.sv = p->ss.sv;
+        lp.lay = p->ss.lay;
+        lp.cgeo = p->d_cgeo;
+        lp.lanes = p->d_lanes + interval;
+        lp.deps = p->d_geo;
+        lp.readers = p->d_geo + p->rgeo.deps.size();
+        lp.weights = p->d_weights;
+        for (int k = 0; k < kMaxLevels; ++k) {
+            lp.steady_off[k] = p->st[k];
+            lp.startup_off[k] = p->su[k];
+        }
+        lp.dt = p->dt;
+        lp.per = p->per;
+        lp.Vs = p->Vs;
+        lp.epoch = ++p->lepoch;   // every rank runs its intervals in the same order: epochs agree
+        lp.tag0 = p->tag_next;
+        p->tag_next += (unsigned)p->per + 1;
+        lp.edge_w = p->rgeo.edge_w;
+        lp.err = p->d_err;
+        lp.abort = p->d_abort;
+        lp.spin_limit = (long long)(p->watchdog * 2.0e9);
+        const cudaError_t le = levels_dispatch(p->pb.kind, p->ss.ccfg.nt, p->reslev_mode, true, nseg, p->stream,
+                                               lp, p->tm, nullptr);
+        if (le != cudaSuccess)
+            return pipe_fail(p, RIDC_E_CUDA, std::string("resident level march launch: ") + cudaGetErrorString(le));
+        launches = 1;
+    } else if (it == p->graphs.end()) {
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t exec = nullptr;
         bool captured = false;
@@ -1984,6 +2391,16 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
         PIPE_TRY(p, cudaEventElapsedTime(&ms, p->ev0, p->ev1));
         *wall_seconds = ms * 1e-3;
     }
+    if (p->reslev) {
+        unsigned ab = 0;
+        PIPE_TRY(p, cudaMemcpy(&ab, p->d_abort, sizeof ab, cudaMemcpyDeviceToHost));
+        if (ab) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "pipeline made no progress within %gs; waiting levels: %d@interval%d",
+                     p->watchdog, j, interval);
+            return pipe_fail(p, RIDC_E_PROTOCOL, buf);
+        }
+    }
     unsigned long long w = 0;
     PIPE_TRY(p, cudaMemcpy(&w, p->d_err, sizeof w, cudaMemcpyDeviceToHost));
     if (w != ULLONG_MAX) {
@@ -2003,7 +2420,7 @@ int ridc_pipe_info(const ridc_pipe* p, ridc_info* info)
     info->restarts = p->restarts;
     info->steps = p->steps;
     info->ticks_per_interval = p->per;
-    info->kernel_launches = p->per;
+    info->kernel_launches = p->reslev ? 1 : p->per;   /* per interval */
     info->tile = p->ss.sv.tile;
     info->halo = p->ss.sv.halo;
     info->items_per_level = p->pb.ny * p->ss.sv.nseg;
@@ -2028,12 +2445,25 @@ int ridc_pipe_destroy(ridc_pipe* p)
     if (p->d_tab) cudaFree(p->d_tab);
     if (p->d_cgeo) cudaFree(p->d_cgeo);
     if (p->d_err) cudaFree(p->d_err);
+    if (p->d_geo) cudaFree(p->d_geo);
+    if (p->d_lmail) cudaFree(p->d_lmail);
+    if (p->d_abort) cudaFree(p->d_abort);
+    if (p->d_lanes) cudaFree(p->d_lanes);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     if (p->stream) cudaStreamDestroy(p->stream);
     delete p;
     return RIDC_OK;
 }
+
+int ridc_pipe_set_resident(ridc_pipe* p, int32_t enable)
+{
+    if (!p) return pipe_fail(nullptr, RIDC_E_CONFIG, "NULL pipe");
+    p->reslev = enable && p->reslev_ok;
+    return RIDC_OK;
+}
+
+int ridc_pipe_resident(const ridc_pipe* p) { return p && p->reslev ? 1 : 0; }
 
 const char* ridc_pipe_last_error(const ridc_pipe* p)
 {

@@ -56,7 +56,8 @@ class PipelineRank:
     """
 
     def __init__(self, ivp, config, rank: int, world: int, device: int = 0,
-                 inbox_capacity: int = 0, exchange: Optional[Callable] = None):
+                 inbox_capacity: int = 0, exchange: Optional[Callable] = None,
+                 resident: bool = True):
         if config.levels != world:
             raise ConfigError(f"one level per GPU: levels ({config.levels}) must equal ranks ({world})")
         self.ivp = as_descriptor(ivp)
@@ -73,6 +74,10 @@ class PipelineRank:
             config.steps, config.restarts, self.weights.ctypes.data, self.weights.shape[0],
             rank, device, int(inbox_capacity), float(config.watchdog_seconds), ctypes.byref(h)))
         self._h = h
+        # resident level march (one launch per interval, in-kernel flag waits)
+        # where the line qualifies; every rank must choose the same (the blob
+        # carries it and connect checks it)
+        _lib.check_pipe(_lib.lib().ridc_pipe_set_resident(self._h, 1 if resident else 0), self._h)
         nb = _lib.lib().ridc_pipe_handle_bytes()
         blob = ctypes.create_string_buffer(nb)
         _lib.check_pipe(_lib.lib().ridc_pipe_export(self._h, blob), self._h)
@@ -93,12 +98,18 @@ class PipelineRank:
         return {f: getattr(inf, f) for f, _ in inf._fields_}
 
     @property
+    def resident(self) -> bool:
+        return bool(_lib.lib().ridc_pipe_resident(self._h))
+
+    @property
     def kernel_launches(self) -> int:
-        return self.config.steps      # one tick kernel per step of this level
+        # one resident launch per interval, or one tick kernel per step
+        return self.config.restarts if self.resident else self.config.steps
 
     @property
     def tick_launches(self) -> int:
-        return self.config.steps
+        """Launches of the level-step kernel per run (resident: one per interval)."""
+        return self.config.restarts if self.resident else self.config.steps
 
     def run_interval(self, r: int, state0_dev):
         out = D.torch().empty_like(state0_dev)
@@ -183,7 +194,9 @@ class ConcurrentPipeline:
         self.config = config
         L = config.levels
         devs = [devices[j % len(devices)] for j in range(L)]
-        self.ranks = [PipelineRank(ivp, config, j, L, devs[j]) for j in range(L)]
+        # stream-memop ranks: every wait is a stream wait, so ranks sharing one
+        # device cannot deadlock (resident ranks would spin on each other)
+        self.ranks = [PipelineRank(ivp, config, j, L, devs[j], resident=False) for j in range(L)]
         blobs = [r.blob for r in self.ranks]
         for r in self.ranks:
             r.connect(blobs)

@@ -223,8 +223,10 @@ def test_restart_trend():
 
 def test_engine_info_and_launch_count():
     s = P.reaction_diffusion_c2(n=1 << 16)
-    with E.Engine(s, E.RidcConfig(levels=4, steps=100)) as eng:
+    with E.Engine(s, E.RidcConfig(levels=4, steps=100), tick_only=True) as eng:
         inf = eng.info
         assert inf["ticks_per_interval"] == 100 + 6
-        assert inf["kernel_launches"] == 1 + 106
+        assert inf["kernel_launches"] == 1 + 106   # seed + one tick launch per tick
+    with E.Engine(s, E.RidcConfig(levels=4, steps=100, restarts=2)) as eng:
+        assert eng.info["kernel_launches"] == 3 * 2   # resident level march: 2 seeds + 1 launch per interval
         assert inf["halo"] > 0 and inf["items_per_level"] >= 8
