@@ -43,6 +43,13 @@ namespace {
 
 thread_local std::string g_last_error;
 
+int env_int(const char* name, int def)
+{
+    const char* e = getenv(name);
+    const int v = e ? atoi(e) : def;
+    return v > 0 ? v : def;
+}
+
 // top-ring slots while the trajectory is streamed to host memory
 constexpr long long kTrajDepth = 8;
 
@@ -555,12 +562,12 @@ cudaError_t resident_dispatch(int kind, int nt, int mode, bool launch, int grid,
 // ---- resident level march (ridc_levels.cuh): every lane a group of nseg CTAs
 constexpr int kResStages = 2;
 
-template <int KIND, int NT, int MODE>
+template <int KIND, int NT, int MODE, bool SYS>
 cudaError_t levels_t(bool launch, int grid, cudaStream_t st, const LevelsParams& lp, const TmapSet& tm,
                      int* per_sm)
 {
-    auto kfn = k_resident_levels<KIND, NT, MODE, kResStages>;
-    const size_t smem = ChunkSmem<NT, 1, kResStages, kChunk>::BYTES + 1024;
+    auto kfn = k_resident_levels<KIND, NT, MODE, kResStages, SYS>;
+    const size_t smem = LevSmem<NT, kResStages>::BYTES + 1024;
     static bool attr[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -584,7 +591,7 @@ cudaError_t levels_t(bool launch, int grid, cudaStream_t st, const LevelsParams&
     return cudaLaunchKernelEx(&cfg, kfn, lp, tm);
 }
 
-template <int KIND>
+template <int KIND, bool SYS>
 cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const LevelsParams& lp,
                      const TmapSet& tm, int* per_sm)
 {
@@ -596,8 +603,8 @@ cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, c
     }
 #define RIDC_LEV_NT(NT)                                                                          \
     case NT:                                                                                     \
-        return mode == MA ? levels_t<KIND, NT, MA>(launch, grid, st, lp, tm, per_sm)             \
-                          : levels_t<KIND, NT, MB>(launch, grid, st, lp, tm, per_sm);
+        return mode == MA ? levels_t<KIND, NT, MA, SYS>(launch, grid, st, lp, tm, per_sm)        \
+                          : levels_t<KIND, NT, MB, SYS>(launch, grid, st, lp, tm, per_sm);
     switch (nt) {
         RIDC_LEV_NT(64)
         RIDC_LEV_NT(128)
@@ -608,16 +615,22 @@ cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, c
 #undef RIDC_LEV_NT
 }
 
-// launch == false: occupancy query into *per_sm
+// launch == false: occupancy query into *per_sm.  sys: flags at system scope
+// (levels on different GPUs), else GPU scope (every level on this device).
 cudaError_t levels_dispatch(int kind, int nt, int mode, bool launch, int grid, cudaStream_t st,
-                            const LevelsParams& lp, const TmapSet& tm, int* per_sm)
+                            const LevelsParams& lp, const TmapSet& tm, int* per_sm, bool sys)
 {
+#define RIDC_LEV_KIND(K)                                                                   \
+    case K:                                                                                \
+        return sys ? levels_k<K, true>(nt, mode, launch, grid, st, lp, tm, per_sm)          \
+                   : levels_k<K, false>(nt, mode, launch, grid, st, lp, tm, per_sm);
     switch (kind) {
-    case ADV_DIFF_1D: return levels_k<ADV_DIFF_1D>(nt, mode, launch, grid, st, lp, tm, per_sm);
-    case BURGERS_1D: return levels_k<BURGERS_1D>(nt, mode, launch, grid, st, lp, tm, per_sm);
-    case RD_1D: return levels_k<RD_1D>(nt, mode, launch, grid, st, lp, tm, per_sm);
+        RIDC_LEV_KIND(ADV_DIFF_1D)
+        RIDC_LEV_KIND(BURGERS_1D)
+        RIDC_LEV_KIND(RD_1D)
     default: return cudaErrorInvalidValue;
     }
+#undef RIDC_LEV_KIND
 }
 
 cudaError_t launch_item(int kind, const LaunchCfg& c, int items, cudaStream_t st,
@@ -1247,7 +1260,7 @@ int march_reslev(ridc_ctx* c, bool* fell_back)
         lp.tag0 = c->tag_next;
         c->tag_next += (unsigned)c->per + 1;
         const cudaError_t le = levels_dispatch(c->pb.kind, c->ss.ccfg.nt, c->reslev_mode, true, L * nseg,
-                                               c->stream, lp, c->tm_in, nullptr);
+                                               c->stream, lp, c->tm_in, nullptr, false);
         if (le == cudaErrorCooperativeLaunchTooLarge && r == 0) {
             cudaGetLastError();
             *fell_back = true;
@@ -1396,7 +1409,7 @@ int setup_reslev(ridc_ctx* c)
     memset(&lp, 0, sizeof lp);
     int per_sm = 0;
     const cudaError_t oe = levels_dispatch(c->pb.kind, c->ss.ccfg.nt, g.mode, false, 0, c->stream, lp, c->tm,
-                                           &per_sm);
+                                           &per_sm, false);
     if (oe != cudaSuccess || per_sm * c->nsm < L * nseg) {
         if (getenv("RIDC_DEBUG"))
             fprintf(stderr, "ridc: resident level march unavailable (%s, %d blocks/SM x %d SMs < %d)\n",
@@ -1405,7 +1418,7 @@ int setup_reslev(ridc_ctx* c)
         return RIDC_OK;
     }
     c->reslev_mode = g.mode;
-    c->in_cap = 16;   // >= j + 2 for every level (deadlock-free), slack for the producers to run ahead
+    c->in_cap = 16;   // >= j + 3 for every level (window + deferred publication: deadlock-free), + slack
     memset(&c->tm_in, 0, sizeof c->tm_in);
     for (int j = 1; j < L; ++j) {
         const size_t b = (size_t)c->in_cap * c->Vs * sizeof(double);
@@ -1467,6 +1480,7 @@ int setup_reslev(ridc_ctx* c)
     lp.per = c->per;
     lp.Vs = c->Vs;
     lp.edge_w = g.edge_w;
+    lp.pub_every = env_int("RIDC_PUB_EVERY", 4);
     lp.err = c->d_err;
     lp.abort = c->d_flags;
     lp.spin_limit = 4000000000LL;   // ~2 s at 1.9 GHz per wait
@@ -2157,7 +2171,7 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
         memset(&lp, 0, sizeof lp);
         int per_sm = 0;
         const cudaError_t oe = levels_dispatch(p->pb.kind, p->ss.ccfg.nt, p->rgeo.mode, false, 0, p->stream, lp,
-                                               p->tm, &per_sm);
+                                               p->tm, &per_sm, true);
         if (oe == cudaSuccess && per_sm * p->nsm >= p->ss.sv.nseg) {
             p->reslev_ok = p->reslev = true;
             p->reslev_mode = p->rgeo.mode;
@@ -2331,11 +2345,13 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
         lp.tag0 = p->tag_next;
         p->tag_next += (unsigned)p->per + 1;
         lp.edge_w = p->rgeo.edge_w;
+        lp.pub_every = env_int("RIDC_PUB_EVERY", 4);
+        lp.diag = env_int("RIDC_LEV_DIAG", 0);
         lp.err = p->d_err;
         lp.abort = p->d_abort;
         lp.spin_limit = (long long)(p->watchdog * 2.0e9);
         const cudaError_t le = levels_dispatch(p->pb.kind, p->ss.ccfg.nt, p->reslev_mode, true, nseg, p->stream,
-                                               lp, p->tm, nullptr);
+                                               lp, p->tm, nullptr, true);
         if (le != cudaSuccess)
             return pipe_fail(p, RIDC_E_CUDA, std::string("resident level march launch: ") + cudaGetErrorString(le));
         launches = 1;

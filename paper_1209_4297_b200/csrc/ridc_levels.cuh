@@ -20,8 +20,9 @@
 //            -> release the producer's slots I no longer need (per segment)
 //            -> if not the top level: wait until the consumer released the
 //               slot I overwrite, store my tile (+ periodic ghosts) into the
-//               consumer's inbox with coalesced stores, publish my segment's
-//               flag (release at system scope).
+//               consumer's inbox with coalesced stores; its flag (release at
+//               system scope) is raised after the next step's solve, once
+//               the stores drained (the last step's at once).
 //
 // The lanes table says where each level's rings and flags live.  One launch
 // may hold every level of a line (one GPU: the CTA groups of all levels are
@@ -41,6 +42,18 @@
 namespace ridc {
 
 constexpr int kResDeps = 4;   // producer segments one consumer segment reads (and vice versa)
+
+// Dynamic shared memory of the level kernel: NSTAGE TMA stages of the window
+// nodes (the tick kernel's swizzled 1-row stage), the scratch holding my new
+// state for the coalesced stores, the stencil edges, the stage mbarriers.
+template <int NT, int NSTAGE>
+struct LevSmem {
+    static constexpr int STAGE = NT * 128;   // ChunkSmem<NT, 1, NSTAGE, 16>::STAGE
+    static constexpr size_t OFF_SCR = (size_t)NSTAGE * STAGE;
+    static constexpr size_t OFF_EDGE = OFF_SCR + STAGE;
+    static constexpr size_t OFF_BAR = OFF_EDGE + 4 * NT * sizeof(double);
+    static constexpr size_t BYTES = OFF_BAR + 2 * NSTAGE * sizeof(uint64_t);
+};
 
 struct LevelLane {
     int level;                     // j
@@ -71,6 +84,8 @@ struct LevelsParams {
     long long per;                 // steps of this interval
     long long Vs;
     unsigned long long epoch;      // flag value of step t: epoch << 32 | t
+    int pub_every;                 // publish the consumer's flag every this many steps (>= 1)
+    int diag;                      // diagnostics only (RIDC_LEV_DIAG): bit 0 skips the tile stores
     unsigned tag0;                 // mailbox tag of step t: tag0 + t
     int edge_w;                    // columns within edge_w of a tile end are pushed every step
     unsigned long long* err;
@@ -78,59 +93,90 @@ struct LevelsParams {
     long long spin_limit;
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p)
+// Flag accesses at system scope (SYS: the levels sit on different GPUs and
+// the flags / data cross NVLink) or GPU scope (every level on this device).
+template <bool SYS>
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p)
 {
     unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (SYS) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
-__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v)
+// Publication: every store of the CTA ordered before this thread (a CTA
+// barrier) becomes visible before the flag (release fence + relaxed store).
+template <bool SYS>
+__device__ __forceinline__ void publish_u64(unsigned long long* p, unsigned long long v)
 {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    if (SYS) asm volatile("fence.acq_rel.sys;\n\tst.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Spin (one thread) until flags[s] >= want for every listed segment.
-__device__ __forceinline__ bool wait_flags(const unsigned long long* flags, const int* segs,
-                                           unsigned long long want, const LevelsParams& rp, bool& dead)
+// Release counter: the window reads it covers are TMA loads whose data is
+// already in shared memory (their mbarriers completed), so no fence orders
+// them -- a relaxed store suffices.
+template <bool SYS>
+__device__ __forceinline__ void store_relaxed_u64(unsigned long long* p, unsigned long long v)
 {
+    if (SYS) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Spin (one thread) until flags[s] >= want for every listed segment.  `seen`
+// caches the smallest value observed at the last poll: a wait it already
+// covers costs nothing (the acquire that observed it ordered that data).
+template <bool SYS>
+__device__ __forceinline__ bool wait_flags(const unsigned long long* flags, const int* segs,
+                                           unsigned long long want, unsigned long long& seen,
+                                           const LevelsParams& rp, bool& dead)
+{
+    if (seen >= want) return true;
     const long long t0 = clock64();
+    unsigned long long lo = ~0ull;
     for (int k = 0; k < kResDeps; ++k) {
         const int s = segs[k];
         if (s < 0) break;
-        while (!dead && ld_acquire_sys_u64(flags + s) < want) {
+        unsigned long long v;
+        while (!dead && (v = ld_acquire_u64<SYS>(flags + s)) < want) {
             if (clock64() - t0 > rp.spin_limit || *(volatile unsigned*)rp.abort) {
                 atomicExch(rp.abort, 1u);
                 dead = true;
             }
         }
+        if (!dead) lo = v < lo ? v : lo;
     }
+    if (!dead) seen = lo;
     return !dead;
 }
 
-template <int KIND, int NT, int MODE, int NSTAGE>
+template <int KIND, int NT, int MODE, int NSTAGE, bool SYS>
 __global__ void __launch_bounds__(NT, 1)
     k_resident_levels(const __grid_constant__ LevelsParams rp, const __grid_constant__ TmapSet tm)
 {
     static_assert(KIND == ADV_DIFF_1D || KIND == BURGERS_1D || KIND == RD_1D, "1-D kinds only");
-    using L = ChunkSmem<NT, 1, NSTAGE, kChunk>;
+    using L = LevSmem<NT, NSTAGE>;
     constexpr int K = kChunk;
     constexpr bool periodic = KIND != BURGERS_1D;
     constexpr bool has_wx = KIND == ADV_DIFF_1D || KIND == BURGERS_1D;
     extern __shared__ __align__(1024) char smraw[];
     char* stage = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    char* scr = stage + L::OFF_SCR;   // my level's new state, swizzled like a stage
     double* edge = reinterpret_cast<double*>(stage + L::OFF_EDGE);
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + L::OFF_BAR);
     uint64_t* empty = full + NSTAGE;
-    __shared__ double xpush[4][32 * 17];
-    __shared__ int s_pubw[NT / 32];
     __shared__ Aff swarp[2 * (NT / 32) + 1];
     __shared__ int s_dead;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int nseg = rp.sv.nseg;
     const int seg = blockIdx.x % nseg;
-    const LevelLane& ln = rp.lanes[blockIdx.x / nseg];
+    // my lane's table in shared memory: read once, no per-step global reloads
+    // (stores to the rings could alias a global table) and no registers held
+    __shared__ LevelLane s_ln;
+    if (tid == 0) s_ln = rp.lanes[blockIdx.x / nseg];
+    __syncthreads();
+    const LevelLane& ln = s_ln;
     const int j = ln.level;
     double* const out = ln.out;
     const ChunkGeo cg = rp.cgeo[seg];
@@ -142,7 +188,6 @@ __global__ void __launch_bounds__(NT, 1)
     const bool pub = mine && nseg > 1 && col0 + K > lo && col0 < hi && (col0 - lo < W || hi - (col0 + K) < W);
     const bool inside = mine && col0 >= lo && col0 + K <= hi;
     const unsigned pub_mask = __ballot_sync(0xffffffffu, pub);
-    if (lane == 0) s_pubw[wid] = pub_mask != 0u;
     if (tid == 0) {
         s_dead = 0;
         for (int i = 0; i < NSTAGE; ++i) {
@@ -152,12 +197,6 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_fence_init();
     }
     __syncthreads();
-    int pslot = -1;
-    if (pub_mask) {
-        pslot = 0;
-        for (int w = 0; w < wid; ++w) pslot += s_pubw[w];
-        if (pslot >= 4) pslot = -1;
-    }
     const int wcol0 = col0 - lane * K;
     int probe = -1;
     if (halo)
@@ -176,6 +215,47 @@ __global__ void __launch_bounds__(NT, 1)
     bool dead = false;
     long long n = 0;   // TMA loads issued so far (load n lands in stage n % NSTAGE)
     const unsigned long long ep = rp.epoch << 32;
+    // thread 0's protocol state (shared memory: keeps it out of every thread's registers)
+    __shared__ unsigned long long seen_in, seen_rel;   // flag values already observed
+    __shared__ long long published;                    // last step whose flag is raised
+    if (tid == 0) { seen_in = 0; seen_rel = 0; published = 0; }
+
+    // Coalesced stores of step ts (in the scratch) into the consumer's inbox
+    // slot, + periodic ghost copies: issued at the start of the next step, so
+    // they drain while the halo threads wait and the solve runs
+    long long pend = 0;
+    auto store_tile = [&](long long ts) {
+        if (s_dead || (rp.diag & 1)) return;
+        double* o = out + ((ln.out_off + ts) % ln.out_cap) * rp.Vs + GW;
+        const int glo = (lo - cg.g0 * kChunk + kChunk - 1) / kChunk, ghi = (hi - cg.g0 * kChunk) / kChunk;
+        const bool ghosts = periodic && (lo < GW || hi > nx - GW);
+#pragma unroll
+        for (int k = 0; k < K / 2; ++k) {
+            const int q = tid + k * NT;
+            const int g = q >> 3, i = q & 7;
+            if (g < cg.ng) {
+                const double2 v = lds128(swz(scr, g, i));
+                const int c = (cg.g0 + g) * kChunk + 2 * i;
+                if ((unsigned)(g - glo) < (unsigned)(ghi - glo)) {
+                    *reinterpret_cast<double2*>(o + c) = v;
+                } else {
+                    if (c >= lo && c < hi) o[c] = v.x;
+                    if (c + 1 >= lo && c + 1 < hi) o[c + 1] = v.y;
+                }
+                if (ghosts && (c < GW || c + 2 > nx - GW)) {
+                    const double vv2[2] = {v.x, v.y};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int cc = c + h;
+                        if (cc >= lo && cc < hi) {
+                            if (cc < GW) o[cc + nx] = vv2[h];
+                            if (cc >= nx - GW) o[cc - nx] = vv2[h];
+                        }
+                    }
+                }
+            }
+        }
+    };
 
     for (long long t = 1; t <= rp.per; ++t) {
         // ---- window of level j-1 (build_item, ridc_engine.cu): steady t >= j
@@ -194,13 +274,14 @@ __global__ void __launch_bounds__(NT, 1)
                                                     stage + (size_t)s * L::STAGE, &full[s]);
         };
         if (j > 0 && tid == 0) {
-            if (wait_flags(ln.in_pub, deps, ep | (unsigned long long)(steady ? t : j), rp, dead)) {
+            if (wait_flags<SYS>(ln.in_pub, deps, ep | (unsigned long long)(steady ? t : j), seen_in, rp, dead)) {
                 // the producer's generic (peer) stores, acquired above, before the async-proxy reads
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 for (int a = 0; a < NSTAGE && a <= j; ++a) issue(a, n + a);
             }
             if (dead) s_dead = 1;
         }
+        if (pend) store_tile(pend);   // step t-1 to the consumer
         // ---- own-state halo chunks: the neighbours' step t-1 edges
         if (t > 1 && halo) {
             const unsigned want = rp.tag0 + (unsigned)(t - 1);
@@ -238,7 +319,6 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int e = 0; e < K; ++e) accumulate_point<KIND>(nc, u[e], 0.0, 0.0, P[e], WS[e], WX[e]);
         }
-        long long n_last = -1;
         if (j > 0) {
             __syncthreads();   // s_dead from thread 0's producer wait (CTA-uniform control flow)
             if (!s_dead) {
@@ -263,7 +343,6 @@ __global__ void __launch_bounds__(NT, 1)
                     if (lane == 0) mbar_arrive(&empty[s]);
                     if (tid == 0 && a + NSTAGE <= j) issue(a + NSTAGE, n + NSTAGE);
                 }
-                n_last = n - 1;
             }
         }
         need_wx = need_wx && has_wx;
@@ -283,13 +362,19 @@ __global__ void __launch_bounds__(NT, 1)
         }
 #pragma unroll
         for (int e = 0; e < K; ++e) u[e] = rhs[e];
-        // ---- my edge columns of step t for the neighbour segments' halos
-        if (pslot >= 0) {
-            double* xb = xpush[pslot];
-            if (pub) {
+        // deferred, batched publication: steps up to t-1 (their stores were
+        // ordered before the solve's block barriers), every pub_every steps --
+        // one release fence per batch instead of one per step
+        if (out && t > 1 && tid == 0 && !s_dead && (t - 1) % rp.pub_every == 0) {
+            publish_u64<SYS>(ln.out_pub + seg, ep | (unsigned long long)(t - 1));
+            published = t - 1;
+        }
+        // ---- step t into the scratch (swizzled groups), then my edge columns
+        // for the neighbour segments' halos straight from it (coalesced lines)
+        if (mine)
 #pragma unroll
-                for (int e = 0; e < K; ++e) xb[lane * 17 + e] = u[e];
-            }
+            for (int i = 0; i < K / 2; ++i) sts128(const_cast<char*>(swz(scr, tid, i)), u[2 * i], u[2 * i + 1]);
+        if (pub_mask) {
             __syncwarp();
             const unsigned tag = rp.tag0 + (unsigned)t;
             uint4* box = ln.mail + (size_t)(t & 1) * rp.Vs + GW;
@@ -297,78 +382,32 @@ __global__ void __launch_bounds__(NT, 1)
             for (int i = 0; i < K; ++i) {
                 const int idx = i * 32 + lane, c = wcol0 + idx;
                 if (((pub_mask >> (idx >> 4)) & 1u) && c >= lo && c < hi) {
-                    const double val = xb[(idx >> 4) * 17 + (idx & 15)];
+                    const int g = wid * 32 + (idx >> 4), e = idx & 15;
+                    const double val = *reinterpret_cast<const double*>(swz(scr, g, e >> 1) + 8 * (e & 1));
                     st_line(box + c, val, tag);
                     if (periodic && c < GW) st_line(box + c + nx, val, tag);
                     if (periodic && c >= nx - GW) st_line(box + c - nx, val, tag);
-                }
-            }
-            __syncwarp();
-        } else if (pub) {
-            const unsigned tag = rp.tag0 + (unsigned)t;
-            uint4* box = ln.mail + (size_t)(t & 1) * rp.Vs + GW;
-#pragma unroll
-            for (int e = 0; e < K; ++e) {
-                const int c = col0 + e;
-                if (c >= lo && c < hi) {
-                    st_line(box + c, u[e], tag);
-                    if (periodic && c < GW) st_line(box + c + nx, u[e], tag);
-                    if (periodic && c >= nx - GW) st_line(box + c - nx, u[e], tag);
                 }
             }
         }
         // every window read of this step is done (the scans' barriers): release
         // the producer's slots below my next window (LevelBuffer.release_through)
         if (j > 0 && tid == 0 && !dead)
-            st_release_sys_u64(ln.in_rel + seg, ep | (unsigned long long)(t + 1 - j > 0 ? t + 1 - j : 0));
-        // ---- publish step t to the consumer's inbox
+            store_relaxed_u64<SYS>(ln.in_rel + seg, ep | (unsigned long long)(t + 1 - j > 0 ? t + 1 - j : 0));
         if (out) {
-            const long long need = t - ln.out_cap + 1;   // my slot's previous step must be released
-            if (tid == 0 && need > 0 && !dead) {
-                if (!wait_flags(ln.out_rel, readers, ep | (unsigned long long)need, rp, dead)) s_dead = 1;
-            }
-            char* sb = stage + (size_t)(n_last >= 0 ? n_last % NSTAGE : 0) * L::STAGE;   // scratch
-            if (mine)
-#pragma unroll
-                for (int i = 0; i < K / 2; ++i) sts128(const_cast<char*>(swz(sb, tid, i)), u[2 * i], u[2 * i + 1]);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
-            if (!s_dead) {
-                double* o = out + ((ln.out_off + t) % ln.out_cap) * rp.Vs + GW;
-                const int glo = (lo - cg.g0 * kChunk + kChunk - 1) / kChunk, ghi = (hi - cg.g0 * kChunk) / kChunk;
-                const bool ghosts = periodic && (lo < GW || hi > nx - GW);
-#pragma unroll
-                for (int k = 0; k < K / 2; ++k) {
-                    const int q = tid + k * NT;
-                    const int g = q >> 3, i = q & 7;
-                    if (g < cg.ng) {
-                        const double2 v = lds128(swz(sb, g, i));
-                        const int c = (cg.g0 + g) * kChunk + 2 * i;
-                        if ((unsigned)(g - glo) < (unsigned)(ghi - glo)) {
-                            *reinterpret_cast<double2*>(o + c) = v;
-                        } else {
-                            if (c >= lo && c < hi) o[c] = v.x;
-                            if (c + 1 >= lo && c + 1 < hi) o[c + 1] = v.y;
-                        }
-                        if (ghosts && (c < GW || c + 2 > nx - GW)) {
-                            const double vv2[2] = {v.x, v.y};
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                const int cc = c + h;
-                                if (cc >= lo && cc < hi) {
-                                    if (cc < GW) o[cc + nx] = vv2[h];
-                                    if (cc >= nx - GW) o[cc - nx] = vv2[h];
-                                }
-                            }
-                        }
-                    }
+            // the consumer's slot of step t must be free before its stores (next step)
+            const long long need = t - ln.out_cap + 1;
+            if (tid == 0 && need > 0 && !dead && seen_rel < (ep | (unsigned long long)need)) {
+                // about to wait on the consumer: first publish what it may be waiting for
+                if (published < t - 1 && !s_dead) {
+                    publish_u64<SYS>(ln.out_pub + seg, ep | (unsigned long long)(t - 1));
+                    published = t - 1;
                 }
+                if (!wait_flags<SYS>(ln.out_rel, readers, ep | (unsigned long long)need, seen_rel, rp, dead))
+                    s_dead = 1;
             }
-            __syncthreads();   // every store issued (and the scratch read) before the flag
-            if (tid == 0 && !s_dead) {
-                __threadfence_system();
-                st_release_sys_u64(ln.out_pub + seg, ep | (unsigned long long)t);
-            }
+            __syncthreads();   // the whole scratch of step t, and the slot is free
+            pend = t;
         }
         // ---- finite check of my tile columns; the final tile at the end
         const bool last = t == rp.per;
@@ -395,6 +434,11 @@ __global__ void __launch_bounds__(NT, 1)
         if (bad) atomicMin(rp.err, err_code(t, j));
         // a timed-out wait (watchdog) leaves the remaining steps' waits
         // skipped: the CTA drains without blocking; the host reports it
+    }
+    if (out && pend) {   // the last step's tile, then its flag
+        store_tile(pend);
+        __syncthreads();
+        if (tid == 0 && !s_dead) publish_u64<SYS>(ln.out_pub + seg, ep | (unsigned long long)pend);
     }
 }
 
