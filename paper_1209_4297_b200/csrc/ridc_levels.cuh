@@ -257,6 +257,17 @@ __global__ void __launch_bounds__(NT, 1)
         }
     };
 
+    // thread 0: window node a of step tt (build_item's order) as TMA load m into stage m % NSTAGE
+    auto issue_node = [&](long long tt, int a, long long m) {
+        const int s = (int)(m % NSTAGE);
+        if (m >= NSTAGE) mbar_wait(&empty[s], (uint32_t)(((m - NSTAGE) / NSTAGE) & 1));
+        const long long ns = tt >= j ? tt - a : a;
+        const long long slot = (ln.in_off + ns) % ln.in_cap;
+        issue_chunk_node<NT, 1, NSTAGE, kChunk>(tm, ln.in_map, slot, 0, 1, rp.lay.gpr, rp.lay.gdata, cg,
+                                                stage + (size_t)s * L::STAGE, &full[s]);
+    };
+    unsigned pre_mask = 0;   // thread 0: first nodes of the next step already issued
+
     for (long long t = 1; t <= rp.per; ++t) {
         // ---- window of level j-1 (build_item, ridc_engine.cu): steady t >= j
         // nodes t, t-1, ..., t-j (i_new 0, i_old 1); startup nodes 0..j
@@ -265,20 +276,15 @@ __global__ void __launch_bounds__(NT, 1)
                           : steady ? rp.weights + rp.steady_off[j]
                                    : rp.weights + rp.startup_off[j] + (t - 1) * (j + 1);
         const int i_new = steady ? 0 : (int)t, i_old = steady ? 1 : (int)t - 1;
-        auto node_step = [&](int a) -> long long { return steady ? t - a : a; };
-        auto issue = [&](int a, long long m) {   // thread 0: window node a as load m
-            const int s = (int)(m % NSTAGE);
-            if (m >= NSTAGE) mbar_wait(&empty[s], (uint32_t)(((m - NSTAGE) / NSTAGE) & 1));
-            const long long slot = (ln.in_off + node_step(a)) % ln.in_cap;
-            issue_chunk_node<NT, 1, NSTAGE, kChunk>(tm, ln.in_map, slot, 0, 1, rp.lay.gpr, rp.lay.gdata, cg,
-                                                    stage + (size_t)s * L::STAGE, &full[s]);
-        };
         if (j > 0 && tid == 0) {
+            // the first NSTAGE nodes, unless prefetched during the previous step's solve
             if (wait_flags<SYS>(ln.in_pub, deps, ep | (unsigned long long)(steady ? t : j), seen_in, rp, dead)) {
                 // the producer's generic (peer) stores, acquired above, before the async-proxy reads
                 asm volatile("fence.proxy.async.global;" ::: "memory");
-                for (int a = 0; a < NSTAGE && a <= j; ++a) issue(a, n + a);
+                for (int a = 0; a < NSTAGE && a <= j; ++a)
+                    if (!(pre_mask & (1u << a))) issue_node(t, a, n + a);
             }
+            pre_mask = 0;
             if (dead) s_dead = 1;
         }
         if (pend) store_tile(pend);   // step t-1 to the consumer
@@ -341,7 +347,19 @@ __global__ void __launch_bounds__(NT, 1)
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
-                    if (tid == 0 && a + NSTAGE <= j) issue(a + NSTAGE, n + NSTAGE);
+                    if (tid == 0 && a + NSTAGE <= j) issue_node(t, a + NSTAGE, n + NSTAGE);
+                }
+                // prefetch: the next step's first nodes whose producer steps are
+                // already published stream in while this step solves
+                if (tid == 0 && t < rp.per && !dead) {
+                    const long long t1 = t + 1;
+                    for (int a = 0; a < NSTAGE && a <= j; ++a) {
+                        const long long ns = t1 >= j ? t1 - a : a;
+                        if (seen_in >= (ep | (unsigned long long)ns)) {   // acquired earlier: published
+                            issue_node(t1, a, n + a);
+                            pre_mask |= 1u << a;
+                        }
+                    }
                 }
             }
         }
