@@ -187,6 +187,38 @@ def run_reference(args):
     return 0
 
 
+def pipeline_ranks_alone(sysm, nt, febe_step_s, orders=(2, 4), nt_sample=200):
+    """The one-level-per-GPU pipeline's ranks, each timed ALONE on this GPU
+    (SequentialPipeline: ranks one after another, whole-run inboxes, inputs
+    already published; NVLink stores land in local HBM): per-step device time
+    of every rank = a lower bound of the p-GPU step on this workload (same dt,
+    nt_sample steps).  One GPU per box here, so N > 1 itself is not timed."""
+    from paper_1209_4297_b200 import distributed as PD
+    from paper_1209_4297_b200 import engine as E
+    from paper_1209_4297_b200 import problems as P
+    import torch
+    ivp = sysm.ivp
+    short = P.StructuredIVP(ivp.problem, ivp.t_start, ivp.t_start + (ivp.t_end - ivp.t_start) * nt_sample / nt,
+                            ivp.initial_state)
+    y0 = torch.from_numpy(np.array(ivp.initial_state)).cuda()
+    res = {"nt_sample": nt_sample, "febe_us_per_step": febe_step_s * 1e6}
+    for p in orders:
+        pipe = PD.SequentialPipeline(short, E.RidcConfig(levels=p, steps=nt_sample))
+        try:
+            best = [1e30] * p
+            for _ in range(3):
+                for j, rk in enumerate(pipe.ranks):
+                    _, sec = rk.run_interval(0, y0)
+                    best[j] = min(best[j], sec)
+            res[f"p{p}"] = {"resident": all(r.resident for r in pipe.ranks),
+                            "us_per_step": [b / nt_sample * 1e6 for b in best],
+                            "max_rank_vs_febe": max(best) / nt_sample / febe_step_s}
+        finally:
+            pipe.close()
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args):
     import torch
     from paper_1209_4297_b200 import engine as E
@@ -361,6 +393,8 @@ def run_ours(args):
                                              "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps),
                                              "launches_per_solve": ae.info["kernel_launches"]}
         line["ridc_orders_1gpu"] = extra
+        if not args.no_extra:
+            line["pipeline_ranks_alone"] = pipeline_ranks_alone(sysm, nt, t_max / args.steps / nt)
         line["cpu_baseline"] = cpu_sample(sysm, order, nt, budget_s=args.cpu_budget)
     else:
         # e2e at N GPUs: every rank copies y0 in from pinned host memory, the
