@@ -1,5 +1,6 @@
 """C5 grid-size sweep: 1-D reaction-diffusion, N = 2^16..2^26,
-orders 1/2/4 with all levels on one GPU.  The stiffness r = dt*d/dx^2 is held
+orders 1/2/4/8 with all levels on one GPU (resident marches where the
+line fits: FEBE up to ~2^20, all levels while levels x segments <= SMs).  The stiffness r = dt*d/dx^2 is held
 at the C2 value (~110) by scaling d with N; Nt is shortened with dt kept
 (so the solve geometry is the workload's).  Device time of whole solves
 (CUDA events inside ridc_run_device), L2 flushed between solves.
@@ -24,7 +25,7 @@ from paper_1209_4297_b200 import problems as P  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--exps", default="16,18,20,22,24,26")
-ap.add_argument("--orders", default="1,2,4")
+ap.add_argument("--orders", default="1,2,4,8")
 ap.add_argument("--nt", type=int, default=200)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--out", default="")
@@ -55,7 +56,11 @@ for ex in [int(x) for x in a.exps.split(",")]:
         bpp = sum(bench.bytes_per_point(j) for j in range(p))
         # steady ticks carry all p levels; fill ticks fewer: average bytes per tick
         gbs = bpp * n * a.nt / t / 1e9
-        row = {"points": n, "order": p, "nt": a.nt, "ms_per_solve": t * 1e3, "us_per_tick": tick_s * 1e6,
+        launches = info["kernel_launches"]
+        path = ("resident_febe" if p == 1 and launches == 2 else
+                "resident_levels" if p > 1 and launches == 3 else "tick_graph")
+        row = {"points": n, "order": p, "nt": a.nt, "path": path, "us_per_step": t / a.nt * 1e6,
+               "ms_per_solve": t * 1e3, "us_per_tick": tick_s * 1e6,
                "grid_pt_steps_per_s": n * a.nt / t, "alg_bytes_per_pt_tick": bpp,
                "achieved_gbs": gbs, "frac": gbs / peak, "items_per_level": info["items_per_level"],
                "r": info["r"]}
