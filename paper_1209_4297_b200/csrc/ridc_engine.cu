@@ -2346,7 +2346,6 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
         p->tag_next += (unsigned)p->per + 1;
         lp.edge_w = p->rgeo.edge_w;
         lp.pub_every = env_int("RIDC_PUB_EVERY", 4);
-        lp.diag = env_int("RIDC_LEV_DIAG", 0);
         lp.err = p->d_err;
         lp.abort = p->d_abort;
         lp.spin_limit = (long long)(p->watchdog * 2.0e9);

@@ -85,7 +85,6 @@ struct LevelsParams {
     long long Vs;
     unsigned long long epoch;      // flag value of step t: epoch << 32 | t
     int pub_every;                 // publish the consumer's flag every this many steps (>= 1)
-    int diag;                      // diagnostics only (RIDC_LEV_DIAG): bit 0 skips the tile stores
     unsigned tag0;                 // mailbox tag of step t: tag0 + t
     int edge_w;                    // columns within edge_w of a tile end are pushed every step
     unsigned long long* err;
@@ -225,7 +224,7 @@ __global__ void __launch_bounds__(NT, 1)
     // they drain while the halo threads wait and the solve runs
     long long pend = 0;
     auto store_tile = [&](long long ts) {
-        if (s_dead || (rp.diag & 1)) return;
+        if (s_dead) return;
         double* o = out + ((ln.out_off + ts) % ln.out_cap) * rp.Vs + GW;
         const int glo = (lo - cg.g0 * kChunk + kChunk - 1) / kChunk, ghi = (hi - cg.g0 * kChunk) / kChunk;
         const bool ghosts = periodic && (lo < GW || hi > nx - GW);

@@ -134,3 +134,27 @@ def test_pipeline_modes_must_agree():
     finally:
         a.close()
         b.close()
+
+
+def test_resident_rank_watchdog():
+    """A consumer rank whose producer never publishes: the in-kernel waits give
+    up after the watchdog and the rank raises PipelineProtocolError with the
+    reference's message shape (engine.py:432-439) -- no hang.  Nothing else
+    runs on the device, so no kernel waits on another kernel here."""
+    from paper_1209_4297_b200.distributed import PipelineRank
+    from paper_1209_4297_b200.errors import PipelineProtocolError
+    ivp = _c1(0.4)
+    cfg = E.RidcConfig(levels=2, steps=100, watchdog_seconds=0.5)
+    prod = PipelineRank(ivp, cfg, 0, 2, 0)
+    cons = PipelineRank(ivp, cfg, 1, 2, 0)
+    try:
+        assert cons.resident
+        prod.connect([prod.blob, cons.blob])
+        cons.connect([prod.blob, cons.blob])
+        y0 = torch.from_numpy(np.array(ivp.initial_state)).cuda()
+        with pytest.raises(PipelineProtocolError) as ei:
+            cons.run_interval(0, y0)          # level 1 alone: level 0 never runs
+        assert "made no progress" in str(ei.value)
+    finally:
+        prod.close()
+        cons.close()
