@@ -362,7 +362,7 @@ def run_ours(args):
         # extra orders with all levels on this GPU (configs[1]: "RIDC order 1-4 on 1 B200")
         extra = {}
         if not args.no_extra:
-            for p in (2, 4):
+            for p in (2, 3, 4):
                 if p == order:
                     continue
                 with E.Engine(sysm, E.RidcConfig(levels=p, steps=nt)) as e2:

@@ -1,4 +1,5 @@
-"""Per-rank device time of the one-level-per-GPU pipeline, measured on ONE GPU.
+"""Per-rank device time of the one-level-per-GPU pipeline, measured on ONE GPU
+(WORKLOAD=c2|c3|c4, ORDERS, NT).
 
 Every rank of ``SequentialPipeline`` runs alone (whole-run inbox rings, so its
 watermark waits are already satisfied and nothing waits on another rank): the
@@ -21,7 +22,7 @@ from paper_1209_4297_b200 import problems as P  # noqa: E402
 
 nt = int(os.environ.get("NT", "500"))
 orders = [int(x) for x in os.environ.get("ORDERS", "2,4").split(",")]
-sysm, full_nt, cfg = bench.workload("c2")
+sysm, full_nt, cfg = bench.workload(os.environ.get("WORKLOAD", "c2"))
 ivp = sysm.ivp
 sysm = P.StructuredIVP(ivp.problem, 0.0, ivp.t_end * nt / full_nt, ivp.initial_state)
 n = ivp.problem.dimension
@@ -43,7 +44,8 @@ for p in orders:
             _, sec = rk.run_interval(0, s0)
             best[j] = min(best[j], sec)
     for j in range(p):
-        row = {"what": f"pipe_rank_alone p={p} level={j}", "us_per_step": best[j] / nt * 1e6,
+        row = {"what": f"pipe_rank_alone p={p} level={j}", "workload": cfg["workload"],
+               "resident": pipe.ranks[j].resident, "us_per_step": best[j] / nt * 1e6,
                "ratio_vs_febe": best[j] / nt / febe}
         out.append(row)
         print(json.dumps(row), flush=True)
