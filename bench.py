@@ -279,8 +279,10 @@ def run_ours(args):
             return eng.run_device(y0, out)
         info = eng.info
         launches_per_step = info["kernel_launches"]
-        tick_launches = launches_per_step - 1   # the seed kernel aside
-        resident = launches_per_step == 2        # one resident march launch per solve
+        # resident FEBE: seed + one march; resident level march: 2 seeds + one
+        # march per interval; else the tick graph: seed + one launch per tick
+        resident = (order == 1 and launches_per_step == 2) or (order > 1 and launches_per_step == 3)
+        tick_launches = 1 if resident else launches_per_step - 1
         lev_bytes = sum(bytes_per_point(j) for j in range(order)) * nt / max(tick_launches, 1)
 
     for _ in range(max(args.warmup, 0)):
@@ -324,6 +326,9 @@ def run_ours(args):
                             "registers-resident chunks, TMA-staged window of the producer level, "
                             "per-segment publish/release flags, tile stores into the consumer's inbox over NVLink)")
                            if world > 1 and resident else
+                           "k_resident_levels (all levels on this GPU in one launch: a co-resident CTA group per "
+                           "level, registers-resident chunks, TMA-staged windows, per-segment flags)"
+                           if resident and order > 1 else
                            "k_resident_febe (whole FEBE march in one launch: registers-resident chunks, "
                            "stencil + factored tridiagonal solve per step, halo edges via tagged L2 mailbox)"
                            if resident else "k_tick_chunk (fused level-step: stencils + factored tridiagonal solve)"),
