@@ -1418,7 +1418,9 @@ int setup_reslev(ridc_ctx* c)
         return RIDC_OK;
     }
     c->reslev_mode = g.mode;
-    c->in_cap = 16;   // >= j + 3 for every level (window + deferred publication: deadlock-free), + slack
+    // >= j + 3 for every level (window + deferred publication: deadlock-free), + slack;
+    // RIDC_LEVEL_INBOX shrinks it (tests: backpressure on every step)
+    c->in_cap = std::max<long long>(env_int("RIDC_LEVEL_INBOX", 16), L + 2);
     memset(&c->tm_in, 0, sizeof c->tm_in);
     for (int j = 1; j < L; ++j) {
         const size_t b = (size_t)c->in_cap * c->Vs * sizeof(double);

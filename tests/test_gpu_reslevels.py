@@ -158,3 +158,22 @@ def test_resident_rank_watchdog():
     finally:
         prod.close()
         cons.close()
+
+
+@pytest.mark.parametrize("levels,pub_every", [(4, 4), (8, 1), (8, 7)])
+def test_resident_levels_tight_inboxes(monkeypatch, levels, pub_every):
+    """Inbox rings at the minimum (levels + 2 slots): producers block on their
+    consumers' release counters nearly every step, and must publish their
+    pending steps before blocking (batched publication would otherwise
+    deadlock).  Still bitwise the tick kernel."""
+    monkeypatch.setenv("RIDC_LEVEL_INBOX", "1")          # clamped up to levels + 2
+    monkeypatch.setenv("RIDC_PUB_EVERY", str(pub_every))
+    ivp = _short(P.reaction_diffusion_c2(n=1 << 15), 0.02)
+    cfg = E.RidcConfig(levels=levels, steps=200, restarts=2, watchdog_seconds=20.0)
+    with E.Engine(ivp, cfg) as res, E.Engine(ivp, cfg, tick_only=True) as tick:
+        assert res.info["kernel_launches"] == 3 * 2
+        assert res.info["ring_vectors"] < tick.info["ring_vectors"] + 16 * (levels - 1)
+        a, b = res.run(), tick.run()
+    assert np.array_equal(a.final_state, b.final_state)
+    for j in range(levels):
+        assert np.array_equal(a.level_finals[j], b.level_finals[j]), j
