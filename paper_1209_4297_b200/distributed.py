@@ -186,17 +186,20 @@ class ConcurrentPipeline:
     thread on its own stream, with the DEFAULT (small) inbox rings: the
     producers run ahead only as far as the consumers' release counters allow,
     so the watermark / backpressure protocol is exercised exactly as across
-    GPUs (``devices`` may list one device per rank; one device for all is
-    allowed -- every wait is a stream-memory wait, no kernel ever spins on
-    another rank)."""
+    GPUs.  ``devices`` may list one device per rank: the ranks then run the
+    resident level march (in-kernel flag waits across the GPUs).  Ranks that
+    share a device run the stream-memop path instead: every wait is a
+    stream-memory wait, no kernel ever spins on another rank."""
 
     def __init__(self, ivp, config, devices=(0,)):
         self.config = config
         L = config.levels
         devs = [devices[j % len(devices)] for j in range(L)]
-        # stream-memop ranks: every wait is a stream wait, so ranks sharing one
-        # device cannot deadlock (resident ranks would spin on each other)
-        self.ranks = [PipelineRank(ivp, config, j, L, devs[j], resident=False) for j in range(L)]
+        # ranks sharing a device use the stream-memop path: every wait is a
+        # stream wait, so they cannot deadlock (resident ranks would spin on
+        # each other); one rank per device runs the resident level march
+        resident = len(set(devs)) == L
+        self.ranks = [PipelineRank(ivp, config, j, L, devs[j], resident=resident) for j in range(L)]
         blobs = [r.blob for r in self.ranks]
         for r in self.ranks:
             r.connect(blobs)
