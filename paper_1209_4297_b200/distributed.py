@@ -103,8 +103,9 @@ class PipelineRank:
 
     @property
     def kernel_launches(self) -> int:
-        # one resident launch per interval, or one tick kernel per step
-        return self.config.restarts if self.resident else self.config.steps
+        """Our kernels per run: per interval the seed, then one resident march
+        launch or one tick kernel per step."""
+        return self.config.restarts + (self.config.restarts if self.resident else self.config.steps)
 
     @property
     def tick_launches(self) -> int:

@@ -109,7 +109,8 @@ def test_resident_pipeline_ranks_bitwise(name, builder, levels, steps, restarts)
     pipe = SequentialPipeline(ivp, cfg)
     try:
         assert all(r.resident for r in pipe.ranks)
-        assert all(r.kernel_launches == restarts for r in pipe.ranks)
+        assert all(r.kernel_launches == 2 * restarts for r in pipe.ranks)   # seed + march per interval
+        assert all(r.tick_launches == restarts for r in pipe.ranks)
         final, level_finals = pipe.run()
         final2, _ = pipe.run()
     finally:
