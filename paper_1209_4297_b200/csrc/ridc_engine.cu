@@ -562,11 +562,11 @@ cudaError_t resident_dispatch(int kind, int nt, int mode, bool launch, int grid,
 // ---- resident level march (ridc_levels.cuh): every lane a group of nseg CTAs
 constexpr int kResStages = 2;
 
-template <int KIND, int NT, int MODE, bool SYS>
+template <int KIND, int NT, int MODE, bool SYS, int MINB>
 cudaError_t levels_t(bool launch, int grid, cudaStream_t st, const LevelsParams& lp, const TmapSet& tm,
                      int* per_sm)
 {
-    auto kfn = k_resident_levels<KIND, NT, MODE, kResStages, SYS>;
+    auto kfn = k_resident_levels<KIND, NT, MODE, kResStages, SYS, MINB>;
     const size_t smem = LevSmem<NT, kResStages>::BYTES + 1024;
     static bool attr[64] = {};
     int dev = 0;
@@ -593,7 +593,7 @@ cudaError_t levels_t(bool launch, int grid, cudaStream_t st, const LevelsParams&
 
 template <int KIND, bool SYS>
 cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const LevelsParams& lp,
-                     const TmapSet& tm, int* per_sm)
+                     const TmapSet& tm, int* per_sm, bool dense)
 {
     constexpr bool periodic = KIND != BURGERS_1D;
     constexpr int MA = periodic ? 0 : 2, MB = periodic ? 1 : -1;
@@ -601,15 +601,16 @@ cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, c
         if (periodic) return cudaErrorInvalidValue;
         mode = MB;
     }
-#define RIDC_LEV_NT(NT)                                                                          \
-    case NT:                                                                                     \
-        return mode == MA ? levels_t<KIND, NT, MA, SYS>(launch, grid, st, lp, tm, per_sm)        \
-                          : levels_t<KIND, NT, MB, SYS>(launch, grid, st, lp, tm, per_sm);
+#define RIDC_LEV_NT(NT, MINB)                                                                    \
+        return mode == MA ? levels_t<KIND, NT, MA, SYS, MINB>(launch, grid, st, lp, tm, per_sm)  \
+                          : levels_t<KIND, NT, MB, SYS, MINB>(launch, grid, st, lp, tm, per_sm);
     switch (nt) {
-        RIDC_LEV_NT(64)
-        RIDC_LEV_NT(128)
-        RIDC_LEV_NT(256)
-        RIDC_LEV_NT(512)
+    case 64: RIDC_LEV_NT(64, 1)
+    case 128: RIDC_LEV_NT(128, 1)
+    case 256:
+        if (dense) { RIDC_LEV_NT(256, 2) }
+        RIDC_LEV_NT(256, 1)
+    case 512: RIDC_LEV_NT(512, 1)
     default: return cudaErrorInvalidValue;
     }
 #undef RIDC_LEV_NT
@@ -617,13 +618,14 @@ cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, c
 
 // launch == false: occupancy query into *per_sm.  sys: flags at system scope
 // (levels on different GPUs), else GPU scope (every level on this device).
+// dense: the two-CTAs-per-SM variant of the 4096-point items (single GPU only)
 cudaError_t levels_dispatch(int kind, int nt, int mode, bool launch, int grid, cudaStream_t st,
-                            const LevelsParams& lp, const TmapSet& tm, int* per_sm, bool sys)
+                            const LevelsParams& lp, const TmapSet& tm, int* per_sm, bool sys, bool dense = false)
 {
 #define RIDC_LEV_KIND(K)                                                                   \
     case K:                                                                                \
-        return sys ? levels_k<K, true>(nt, mode, launch, grid, st, lp, tm, per_sm)          \
-                   : levels_k<K, false>(nt, mode, launch, grid, st, lp, tm, per_sm);
+        return sys ? levels_k<K, true>(nt, mode, launch, grid, st, lp, tm, per_sm, false)   \
+                   : levels_k<K, false>(nt, mode, launch, grid, st, lp, tm, per_sm, dense);
     switch (kind) {
         RIDC_LEV_KIND(ADV_DIFF_1D)
         RIDC_LEV_KIND(BURGERS_1D)
@@ -1017,6 +1019,7 @@ struct ridc_ctx {
     // resident level march (ridc_levels.cuh): levels >= 2 on a 1-D line, one
     // co-resident CTA group per level, device-side flags between the levels
     bool reslev = false;
+    bool reslev_dense = false;   // two CTAs per SM (4096-point items)
     int reslev_mode = -1;
     double* d_inbox[kMaxLevels] = {};   // level j's inbox: level j-1's states (j >= 1)
     long long in_cap = 0;
@@ -1260,7 +1263,7 @@ int march_reslev(ridc_ctx* c, bool* fell_back)
         lp.tag0 = c->tag_next;
         c->tag_next += (unsigned)c->per + 1;
         const cudaError_t le = levels_dispatch(c->pb.kind, c->ss.ccfg.nt, c->reslev_mode, true, L * nseg,
-                                               c->stream, lp, c->tm_in, nullptr, false);
+                                               c->stream, lp, c->tm_in, nullptr, false, c->reslev_dense);
         if (le == cudaErrorCooperativeLaunchTooLarge && r == 0) {
             cudaGetLastError();
             *fell_back = true;
@@ -1408,8 +1411,14 @@ int setup_reslev(ridc_ctx* c)
     LevelsParams& lp = c->lp;
     memset(&lp, 0, sizeof lp);
     int per_sm = 0;
-    const cudaError_t oe = levels_dispatch(c->pb.kind, c->ss.ccfg.nt, g.mode, false, 0, c->stream, lp, c->tm,
-                                           &per_sm, false);
+    cudaError_t oe = levels_dispatch(c->pb.kind, c->ss.ccfg.nt, g.mode, false, 0, c->stream, lp, c->tm, &per_sm,
+                                     false, false);
+    c->reslev_dense = false;
+    if ((oe != cudaSuccess || per_sm * c->nsm < L * nseg) && c->ss.ccfg.nt == 256) {
+        cudaGetLastError();
+        oe = levels_dispatch(c->pb.kind, c->ss.ccfg.nt, g.mode, false, 0, c->stream, lp, c->tm, &per_sm, false, true);
+        c->reslev_dense = true;
+    }
     if (oe != cudaSuccess || per_sm * c->nsm < L * nseg) {
         if (getenv("RIDC_DEBUG"))
             fprintf(stderr, "ridc: resident level march unavailable (%s, %d blocks/SM x %d SMs < %d)\n",

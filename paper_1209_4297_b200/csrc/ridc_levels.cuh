@@ -149,8 +149,11 @@ __device__ __forceinline__ bool wait_flags(const unsigned long long* flags, cons
     return !dead;
 }
 
-template <int KIND, int NT, int MODE, int NSTAGE, bool SYS>
-__global__ void __launch_bounds__(NT, 1)
+// MINB = 2 (4096-point items, NT = 256): two CTAs per SM at the 128-register
+// cap, so twice the levels x segments fit the co-residency limit (2^16 points
+// at p = 8); chosen only when one CTA per SM does not fit (it spills)
+template <int KIND, int NT, int MODE, int NSTAGE, bool SYS, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB)
     k_resident_levels(const __grid_constant__ LevelsParams rp, const __grid_constant__ TmapSet tm)
 {
     static_assert(KIND == ADV_DIFF_1D || KIND == BURGERS_1D || KIND == RD_1D, "1-D kinds only");

@@ -24,6 +24,8 @@ cases = [
      (1, 2, 4, 8)),
     ("rd-2^16", short(P.reaction_diffusion_c2(n=1 << 16), 0.1), 1000, (2, 4, 8)),
     ("rd-2^17", short(P.reaction_diffusion_c2(n=1 << 17), 0.1), 1000, (2, 4)),
+    ("rd-2^16-r110", short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=1 << 16, d=1e-6 * 256.0)), 0.1),
+     1000, (2, 4, 8)),
 ]
 out = []
 for name, ivp, nt, orders in cases:
