@@ -66,6 +66,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// Bulk tensor store of a staged box (the TMA's 128-byte swizzle, as loaded)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
 __device__ __forceinline__ double2 lds128(const char* p)
 {
     double2 v;
@@ -307,9 +316,38 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
 #pragma unroll
         for (int i = 0; i < K / 2; ++i) sts128(const_cast<char*>(swz(sbufc, gq, ip0 + i)), rhs[2 * i], rhs[2 * i + 1]);
     // order these generic shared writes before the TMA that will refill this stage
+    // (and before the bulk tensor store below)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     csync<NT>();
-    {
+    // Whole lines of a multiple of 16 points (no mirror): the row leaves as bulk
+    // tensor stores of the swizzled scratch (one instruction per box, no per-thread
+    // store pass); periodic ghosts and the finite check come from registers.
+    const bool tma_out = (MODE == 1 || MODE == 2) && it.omap1 > 0 && it.out2 == nullptr && cg.g0 == 0 &&
+                         (pb.nx & 15) == 0 && cg.ng % L::BR == 0;
+    if (tma_out) {
+        if (tid == 0) {
+            for (int b = 0; b < cg.ng / L::BR; ++b)
+                tma_store_3d(&tm.map[it.omap1 - 1], sbufc + (size_t)b * L::BR * 128, 0,
+                             row * lay.gpr + lay.gdata + b * L::BR, (int)it.oslot);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        double chk = 0.0;
+        if (mine) {
+            const int c0 = gq * kChunk + ip0 * 2;   // data column of my first point
+            double* o1 = it.out + (size_t)row * lay.P + lay.GW;
+#pragma unroll
+            for (int e = 0; e < K; ++e) chk = fma(rhs[e], 0.0, chk);
+            if (periodic) {
+                if (c0 < lay.GW)
+#pragma unroll
+                    for (int e = 0; e < K; ++e) o1[c0 + e + pb.nx] = rhs[e];
+                if (c0 + K > pb.nx - lay.GW)
+#pragma unroll
+                    for (int e = 0; e < K; ++e) o1[c0 + e - pb.nx] = rhs[e];
+            }
+        }
+        if (chk != chk) atomicMin(err, err_code(it.target, it.level));
+    } else {
         double chk = 0.0;
         const size_t rofs = (size_t)row * lay.P + lay.GW;   // data column 0 of my row
         double* o1 = it.out + rofs;
@@ -351,10 +389,14 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
         }
         if (chk != chk) atomicMin(err, err_code(it.target, it.level));
     }
-    // release the last node's stage (used as scratch) to the producer
+    // release the last node's stage (used as scratch) to the producer, once the
+    // bulk store has read it
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s_last]);
-    if (tid == 0) refill(n_last, s_last);
+    if (tid == 0) {
+        if (tma_out) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        refill(n_last, s_last);
+    }
     RIDC_STAMP(sv, item_no, 9);
 }
 

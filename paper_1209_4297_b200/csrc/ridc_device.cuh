@@ -71,6 +71,9 @@ struct StepItem {
     double ca[kMaxNodes], cs[kMaxNodes], cn[kMaxNodes];
     double* out;
     double* out2;   // optional mirror (the consumer GPU's inbox slot, written over NVLink)
+    int omap1;      // tensor map of the output ring + 1 (0: no TMA store -- plain stores)
+    int opad;
+    long long oslot;   // slot of `out` in that ring
     int vlev[kMaxNodes];          // ring (level) of node a   (tensor-map staging)
     long long vslot[kMaxNodes];   // slot of node a in that ring
 };

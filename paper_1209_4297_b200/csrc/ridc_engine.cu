@@ -131,6 +131,10 @@ __device__ void build_item(const EngineParams& ep, int j, long long t, StepItem&
     it.nnodes = nn;
     it.out = ring_slot(ep, j, t, off);
     it.out2 = ep.mirror ? ep.mirror + ((ep.mirror_off + t) % ep.mirror_cap) * ep.Vs : nullptr;
+    // whole-line items store their row with one bulk tensor store (the level's ring map)
+    it.omap1 = ep.mirror ? 0 : j + 1;
+    it.opad = 0;
+    it.oslot = slot_index(ep, j, t, off);
 }
 
 // Item i of a tick -> (level slot, tile): tile = i % tiles, slot = (i / tiles
@@ -250,6 +254,8 @@ __global__ void __launch_bounds__(NT, ROWS == 3 && NSTAGE == 1 ? 2 : 1)
         }
         csync<NT>();   // edge / scan scratch reuse by the next item
     }
+    // the bulk tensor stores of the last items complete before the grid does
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (tdbg) tdbg[12] = gtime();
     if (cdbg) cdbg[2] = gtime();
 }
