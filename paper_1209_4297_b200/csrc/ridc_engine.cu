@@ -11,6 +11,12 @@
 // each: one cooperative launch marches every step with the state held in
 // registers (ridc_resident.cuh); only segment edges go through L2.
 //
+// Several levels on 1-D lines whose levels x segments fit the SMs: one
+// cooperative launch per restart interval, every level a CTA group, the
+// lagged pipeline between them driven by per-segment flags
+// (ridc_levels.cuh); the one-level-per-GPU pipeline ranks (ridc_pipe_*) run
+// the same kernel with one level each, flags and stores over NVLink.
+//
 // Level rings: level j < top keeps its last 2j+3 states in HBM (the greedy
 // schedule's live window for the reader j+1, which lags j+1 ticks); the top
 // level keeps 2 (or the whole trajectory when it is recorded).
