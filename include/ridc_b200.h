@@ -173,7 +173,7 @@ typedef struct ridc_pipe ridc_pipe;
 int64_t ridc_pipe_handle_bytes(void);
 
 /* Create the rank owning `level` (0..levels-1) on `device`.  inbox_capacity:
- * inbox ring slots (0: default 2*level+5; >= steps/restarts+1 makes every
+ * inbox ring slots (0: default 2*level+13; >= steps/restarts+1 makes every
  * rank runnable to completion without its consumer, e.g. ranks driven one
  * after another on one device).  watchdog_seconds bounds every wait
  * (PipelineProtocolError on expiry, engine.py:432-439). */

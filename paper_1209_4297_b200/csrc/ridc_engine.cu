@@ -2132,7 +2132,9 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     p->Vs = ((p->V + 1) & ~1LL) + 4;
     p->st = st;
     p->su = su;
-    p->inbox_cap = inbox_capacity > 0 ? inbox_capacity : 2LL * level + 5;
+    // default: the greedy schedule's window (2j+5) + 8 slots of run-ahead, so a
+    // producer rarely blocks on its consumer's release (or publishes early for it)
+    p->inbox_cap = inbox_capacity > 0 ? inbox_capacity : 2LL * level + 13;
     auto bail = [&](int code) {
         std::string m = p->err.empty() ? g_last_error : p->err;
         ridc_pipe_destroy(p);

@@ -192,7 +192,7 @@ class ConcurrentPipeline:
     share a device run the stream-memop path instead: every wait is a
     stream-memory wait, no kernel ever spins on another rank."""
 
-    def __init__(self, ivp, config, devices=(0,)):
+    def __init__(self, ivp, config, devices=(0,), inbox_capacity: int = 0):
         self.config = config
         L = config.levels
         devs = [devices[j % len(devices)] for j in range(L)]
@@ -200,7 +200,8 @@ class ConcurrentPipeline:
         # stream wait, so they cannot deadlock (resident ranks would spin on
         # each other); one rank per device runs the resident level march
         resident = len(set(devs)) == L
-        self.ranks = [PipelineRank(ivp, config, j, L, devs[j], resident=resident) for j in range(L)]
+        self.ranks = [PipelineRank(ivp, config, j, L, devs[j], inbox_capacity=inbox_capacity, resident=resident)
+                      for j in range(L)]
         blobs = [r.blob for r in self.ranks]
         for r in self.ranks:
             r.connect(blobs)

@@ -43,13 +43,14 @@ def test_pipeline_equals_engine_bitwise(name, builder, levels, steps, restarts):
 
 @pytest.mark.parametrize("name,builder,levels,steps,restarts", CASES, ids=[c[0] for c in CASES])
 def test_concurrent_pipeline_small_rings_bitwise(name, builder, levels, steps, restarts):
-    """All ranks at once, one host thread and stream each, default inbox rings
-    (2j+5 slots): the backpressure (release counters) and watermark waits are
-    live, as across GPUs; the result must still equal the engine bitwise."""
+    """All ranks at once, one host thread and stream each, small inbox rings
+    (2L+3 slots, the memop protocol's minimum for the top consumer): the
+    backpressure (release counters) and watermark waits are live, as across
+    GPUs; the result must still equal the engine bitwise."""
     s = builder()
     cfg = E.RidcConfig(levels=levels, steps=steps, restarts=restarts, watchdog_seconds=30.0)
     ref = E.run_serial(s, cfg)
-    pipe = ConcurrentPipeline(s, cfg)
+    pipe = ConcurrentPipeline(s, cfg, inbox_capacity=2 * levels + 3)
     try:
         assert all(r.info["ring_vectors"] < steps for r in pipe.ranks[1:])
         final, level_finals = pipe.run()

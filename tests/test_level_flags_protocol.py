@@ -116,7 +116,7 @@ def test_flag_protocol_minimum_rings(levels, pub_every):
 
 
 def test_flag_protocol_default_pipe_rings():
-    # the multi-GPU ranks' default inbox: 2j+5 slots (here the smallest, j = 1)
+    # the memop protocol's minimum inbox, 2j+5 slots (here j = 1; the ranks' default is 2j+13)
     run_model(4, per=60, cap=7, pub_every=4, seed=7)
 
 
