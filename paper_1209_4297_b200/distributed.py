@@ -114,6 +114,9 @@ class PipelineRank:
 
     def run_interval(self, r: int, state0_dev):
         out = D.torch().empty_like(state0_dev)
+        # the rank runs on its own stream: state0 (e.g. the NCCL re-seed
+        # broadcast of the previous interval) must be complete first
+        D.torch().cuda.current_stream(state0_dev.device).synchronize()
         sec = ctypes.c_double(0.0)
         _lib.check_pipe(_lib.lib().ridc_pipe_run_interval(
             self._h, r, state0_dev.data_ptr(), out.data_ptr(), ctypes.byref(sec)), self._h)
