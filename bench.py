@@ -350,7 +350,7 @@ def run_ours(args):
     # e2e: the host-buffer C-ABI call (H2D y0 + marching + D2H final)
     if world == 1:
         # pinned host buffers (the contract's "from pinned host memory")
-        y0p = torch.from_numpy(np.ascontiguousarray(sysm.ivp.initial_state)).pin_memory()
+        y0p = torch.from_numpy(np.array(sysm.ivp.initial_state, dtype=np.float64, order="C")).pin_memory()
         finp = torch.empty(n, dtype=torch.float64).pin_memory()
         y0h, fin = y0p.numpy(), finp.numpy()
         from paper_1209_4297_b200 import _lib
