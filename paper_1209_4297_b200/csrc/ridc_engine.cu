@@ -258,7 +258,11 @@ __global__ void __launch_bounds__(NT, ROWS == 3 && NSTAGE == 1 ? 2 : 1)
             chunk_item<KIND, NT, ROWS, NSTAGE, 2, KC>(ep.pb, sv, ep.lay, tm, items[slot], cg, row, stage, edge,
                                                   full, empty, n, refill, swarp, ep.err, ino, fl);
         }
-        csync<NT>();   // edge / scan scratch reuse by the next item
+        // 1-D: no barrier here; the next item writes `edge` / the scan scratch
+        // only after this item's store barrier, which follows its last reads of
+        // both. 2-D keeps it: without it the C3 x-line tick measured 115 -> 135 us
+        // (the warps drift apart and the two co-resident CTAs' loads collide).
+        if constexpr (ROWS == 3) csync<NT>();
     }
     // the bulk tensor stores of the last items complete before the grid does
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
