@@ -1,0 +1,189 @@
+// ridc_dispatch.cuh -- definitions of the per-kind launch entry points declared
+// in ridc_kernels.cuh (template instantiation happens in ridc_inst.cu only).
+#pragma once
+#include "ridc_kernels.cuh"
+
+namespace ridc {
+
+template <int KIND, int NT, int KMAX>
+cudaError_t launch_item_t(int items, size_t smem, cudaStream_t st, const DevProblem& pb,
+                          const DevSolve& sv, const StepItem& it, unsigned long long* err)
+{
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k_item<KIND, NT, KMAX>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    k_item<KIND, NT, KMAX><<<items, NT, smem, st>>>(pb, sv, it, err);
+    return cudaGetLastError();
+}
+
+#define RIDC_DISPATCH_CFG(FN, KIND, CFG, ...)                          \
+    ((CFG).id == 0 ? FN<KIND, 128, 8>(__VA_ARGS__)                     \
+     : (CFG).id == 1 ? FN<KIND, 256, 8>(__VA_ARGS__)                   \
+                     : FN<KIND, 512, 8>(__VA_ARGS__))
+
+template <int KIND>
+cudaError_t launch_item_k(const LaunchCfg& c, int items, cudaStream_t st, const DevProblem& pb,
+                          const DevSolve& sv, const StepItem& it, unsigned long long* err)
+{
+    return RIDC_DISPATCH_CFG(launch_item_t, KIND, c, items, c.smem, st, pb, sv, it, err);
+}
+
+template <int KIND, int NT, int ROWS, int NSTAGE, int MODE, int KC>
+cudaError_t launch_chunk_t(int grid, size_t smem, cudaStream_t st, const EngineParams& ep,
+                           const TickParams& tp, int ipl, const TmapSet& tm)
+{
+    auto kfn = k_tick_chunk<KIND, NT, ROWS, NSTAGE, MODE, KC>;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(smem + kMaxLevels * sizeof(StepItem)));
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem + (size_t)tp.nact * sizeof(StepItem);   // + the active levels' items
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, ep, tp, ipl, tm);
+}
+
+template <int KIND>
+cudaError_t launch_chunk_k(const ChunkCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
+                           const TickParams& tp, int ipl, const TmapSet& tm)
+{
+    constexpr bool two_d = KIND == ADV_DIFF_2D || KIND == RD_2D;
+    // periodic kinds: truncated segments (0) or cyclic whole lines (1); Burgers:
+    // Dirichlet whole lines (2) or Dirichlet ends + truncated middles (-1)
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr int MA = periodic ? 0 : 2, MB = periodic ? 1 : -1;
+    if (periodic && c.mode != MA && c.mode != MB) return cudaErrorInvalidValue;
+#define RIDC_CHUNK_CASE(ID, NT, ROWS, NSTAGE, KC)                                              \
+    if (c.id == ID && two_d == (ROWS == 3)) {                                                  \
+        if constexpr (two_d == (ROWS == 3))                                                    \
+            return c.mode == MA ? launch_chunk_t<KIND, NT, ROWS, NSTAGE, MA, KC>(grid, c.smem, st, ep, tp, ipl, tm) \
+                                : launch_chunk_t<KIND, NT, ROWS, NSTAGE, MB, KC>(grid, c.smem, st, ep, tp, ipl, tm); \
+    }
+    RIDC_CHUNK_CONFIGS(RIDC_CHUNK_CASE)
+#undef RIDC_CHUNK_CASE
+    return cudaErrorInvalidValue;
+}
+
+// ---- resident FEBE kernel (ridc_resident.cuh): same NT as the tick config
+// (the block scans' association, hence the rounding, depends on NT)
+template <int KIND, int NT, int MODE>
+cudaError_t resident_t(bool launch, int grid, cudaStream_t st, const ResidentParams& rp, int* per_sm)
+{
+    auto kfn = k_resident_febe<KIND, NT, MODE>;
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, NT, 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // all segments co-resident (neighbour waits)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, rp);
+}
+
+// mode: the common segment mode (0 truncated segments, 1 cyclic whole line,
+// 2 Dirichlet whole line) or -1 (mixed: Dirichlet ends + truncated middle)
+template <int KIND>
+cudaError_t resident_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const ResidentParams& rp,
+                       int* per_sm)
+{
+    // periodic kinds have truncated (0) or cyclic (1) segments; Burgers has
+    // Dirichlet whole lines (2) or Dirichlet ends around truncated middles (-1)
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr int MA = periodic ? 0 : 2, MB = periodic ? 1 : -1;
+    if (mode != MA && mode != MB) {
+        if (periodic) return cudaErrorInvalidValue;
+        mode = MB;
+    }
+#define RIDC_RES_NT(NT)                                                                   \
+    case NT:                                                                              \
+        return mode == MA ? resident_t<KIND, NT, MA>(launch, grid, st, rp, per_sm)        \
+                          : resident_t<KIND, NT, MB>(launch, grid, st, rp, per_sm);
+    switch (nt) {
+        RIDC_RES_NT(64)
+        RIDC_RES_NT(128)
+        RIDC_RES_NT(256)
+        RIDC_RES_NT(512)
+    default: return cudaErrorInvalidValue;
+    }
+#undef RIDC_RES_NT
+}
+
+template <int KIND, int NT, int MODE, bool SYS, int MINB>
+cudaError_t levels_t(bool launch, int grid, cudaStream_t st, const LevelsParams& lp, const TmapSet& tm,
+                     int* per_sm)
+{
+    auto kfn = k_resident_levels<KIND, NT, MODE, kResStages, SYS, MINB>;
+    const size_t smem = LevSmem<NT, kResStages>::BYTES + 1024;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, NT, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // every level's segments co-resident (flag waits)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, lp, tm);
+}
+
+template <int KIND, bool SYS>
+cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const LevelsParams& lp,
+                     const TmapSet& tm, int* per_sm, bool dense)
+{
+    constexpr bool periodic = KIND != BURGERS_1D;
+    constexpr int MA = periodic ? 0 : 2, MB = periodic ? 1 : -1;
+    if (mode != MA && mode != MB) {
+        if (periodic) return cudaErrorInvalidValue;
+        mode = MB;
+    }
+#define RIDC_LEV_NT(NT, MINB)                                                                    \
+        return mode == MA ? levels_t<KIND, NT, MA, SYS, MINB>(launch, grid, st, lp, tm, per_sm)  \
+                          : levels_t<KIND, NT, MB, SYS, MINB>(launch, grid, st, lp, tm, per_sm);
+    switch (nt) {
+    case 64: RIDC_LEV_NT(64, 1)
+    case 128: RIDC_LEV_NT(128, 1)
+    case 256:
+        if (dense) { RIDC_LEV_NT(256, 2) }
+        RIDC_LEV_NT(256, 1)
+    case 512: RIDC_LEV_NT(512, 1)
+    default: return cudaErrorInvalidValue;
+    }
+#undef RIDC_LEV_NT
+}
+
+}  // namespace ridc
