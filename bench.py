@@ -18,7 +18,14 @@ a bounded sample of the same workload.
 
 `--impl reference` times only that CPU port (the reference is Python+numba
 with dense O(N^2) solves and cannot run N = 2^20) and prints
-the same JSON line with "impl": "reference".
+the same JSON line with "impl": "reference" and the identical `config`.
+
+Under torchrun (N > 1) every rank owns one RIDC level (order = N) on its GPU
+(distributed.PipelineRank).  When fewer GPUs are visible than ranks (a
+one-GPU box), the ranks share the devices round-robin: the control plane
+runs over gloo, the ranks use the stream-memop pipeline (no in-kernel
+cross-rank waits) and the line says so ("ranks_share_devices": true) -- a
+functional run of the N > 1 path, not a scaling number.
 """
 
 import argparse
@@ -72,6 +79,24 @@ def workload(name, points=None, nt=None):
 def bytes_per_point(level):
     """Algorithmic HBM bytes per grid point of one level-step."""
     return 16 if level == 0 else 8 * (level + 3)
+
+
+def bench_config(cfg, order, world):
+    """The workload description both arms print (identical dicts)."""
+    c = dict(cfg)
+    c.update({"order": order, "levels_per_gpu": 1 if world > 1 else order,
+              "parallelism": f"levels-over-gpus{world}" if world > 1 else "1gpu",
+              "l2": "flushed between solves (512 MiB write); state stays resident within a solve"})
+    return c
+
+
+def host_cpus():
+    """Host cores the CPU legs could use (os.cpu_count, affinity mask)."""
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        aff = None
+    return {"host_cpu_count": os.cpu_count(), "affinity_cpus": aff}
 
 
 def hbm_peak():
@@ -143,10 +168,33 @@ def cpu_sample(sysm, levels, nt, budget_s=12.0):
     per_step = r["wall_seconds"] / probe
     steps = int(min(max(probe, budget_s / max(per_step, 1e-9)), nt))
     r = O.run(ivp.problem, ivp.initial_state, levels, nt, 1, dt, w, workers=levels, max_steps=steps)
-    return {"value": n * steps / r["wall_seconds"], "unit": UNIT, "cores": levels,
-            "kind": "port", "wall_seconds": r["wall_seconds"],
-            "sample": f"{steps} of {nt} time steps, {n} points, order {levels}, "
-                      f"{levels} thread(s) (one per level, as the reference's workers)"}
+    out = {"value": n * steps / r["wall_seconds"], "unit": UNIT, "cores": levels,
+           "kind": "port", "wall_seconds": r["wall_seconds"],
+           "sample": f"{steps} of {nt} time steps, {n} points, order {levels}, "
+                     f"{levels} thread(s) (one per level, as the reference's workers)"}
+    out.update(host_cpus())
+    return out
+
+
+def cpu_sample_ark(sysm, tab, name, nt, budget_s=4.0):
+    """The oracle's integrate_ark (numpy, one thread) on a bounded number of steps."""
+    from oracle import oracle as O
+    ivp = sysm.ivp
+    dt = (ivp.t_end - ivp.t_start) / nt
+    n = ivp.dimension
+    args = (np.asarray(tab.a_implicit), np.asarray(tab.a_explicit), np.asarray(tab.b_implicit),
+            np.asarray(tab.b_explicit))
+    t0 = time.perf_counter()
+    O.ark(ivp.problem, *args, ivp.initial_state, 0.0, dt, 1)
+    per = time.perf_counter() - t0
+    steps = int(min(max(1, budget_s / max(per, 1e-9)), nt))
+    t0 = time.perf_counter()
+    O.ark(ivp.problem, *args, ivp.initial_state, 0.0, dt * steps, steps)
+    wall = time.perf_counter() - t0
+    out = {"value": n * steps / wall, "unit": UNIT, "cores": 1, "kind": "port", "wall_seconds": wall,
+           "sample": f"{steps} of {nt} {name} steps, {n} points, 1 thread (numpy)"}
+    out.update(host_cpus())
+    return out
 
 
 def run_reference(args):
@@ -171,14 +219,17 @@ def run_reference(args):
         r = O.run(ivp.problem, ivp.initial_state, order, nt, 1, dt, w, workers=order, max_steps=sample)
         total += r["wall_seconds"]
     value = n * sample * args.steps / total
-    cfg.update({"order": order, "levels_per_gpu": order, "parallelism": "cpu-threads"})
+    cfg = bench_config(cfg, order, world)
+    cpu = {"value": value, "unit": UNIT, "cores": order, "kind": "port",
+           "sample": f"{sample} of {nt} time steps per bench step, {n} points, "
+                     f"{order} thread(s) (one per level)"}
+    cpu.update(host_cpus())
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": order, "kind": "port",
-                         "sample": f"{sample} of {nt} time steps per bench step, {n} points"},
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "CPU oracle port of the reference path (reference itself is dense O(N^2), "
                 "infeasible at this N)",
@@ -219,6 +270,42 @@ def pipeline_ranks_alone(sysm, nt, febe_step_s, orders=(2, 4), nt_sample=200):
     return res
 
 
+def _timed_solves(run_device, flush, reps):
+    import torch
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ts.append(run_device())
+    return ts
+
+
+def workload_line(name, order, flush, reps=2, nt=None):
+    """One extra 1-GPU workload (C3 / C4 shapes): device time of whole solves,
+    the dominant kernel's roofline (tick kernel, bytes per tick / tick time)."""
+    import torch
+    from paper_1209_4297_b200 import engine as E
+    sysm, nt, cfg = workload(name, None, nt)
+    n = sysm.ivp.dimension
+    y0 = torch.from_numpy(np.array(sysm.ivp.initial_state)).cuda()
+    out = torch.empty_like(y0)
+    with E.Engine(sysm, E.RidcConfig(levels=order, steps=nt)) as eng:
+        eng.run_device(y0, out)
+        ts = _timed_solves(lambda: eng.run_device(y0, out), flush, reps)
+        info = eng.info
+    t = sum(ts) / len(ts)
+    ticks = nt + order * (order - 1) // 2
+    bytes_tick = sum(bytes_per_point(j) for j in range(order)) * n   # steady tick, all levels active
+    peak, _ = hbm_peak()
+    achieved = bytes_tick * nt / ticks / (t / ticks) / 1e9 if ticks else 0.0
+    del y0, out
+    torch.cuda.empty_cache()
+    return {"workload": cfg["workload"], "points": n, "nt": nt, "order": order, "path": info["path_name"],
+            "value": n * nt / t, "unit": UNIT, "ms_per_solve": t * 1e3, "us_per_tick": t / ticks * 1e6,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "bytes_per_tick": bytes_tick}}
+
+
 def run_ours(args):
     import torch
     from paper_1209_4297_b200 import engine as E
@@ -229,11 +316,24 @@ def run_ours(args):
     local = _env_int("LOCAL_RANK", 0)
     if world != args.gpus:
         args.gpus = world if world > 1 else args.gpus
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    shared = world > 1 and ndev < world   # one-GPU box: ranks share the devices round-robin
+    dev = local % max(ndev, 1)
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")   # NCCL refuses two ranks on one device
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+
+    def reduce_max(x):
+        if dist is None:
+            return x
+        tt = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else "cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
 
     sysm, nt, cfg = workload(args.workload, args.points, args.nt)
     n = sysm.ivp.dimension
@@ -245,7 +345,6 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
-    resident = False
     if world > 1:
         # one level per GPU (levels = ranks): the NVLink point-to-point pipeline
         from paper_1209_4297_b200 import distributed as PD
@@ -256,19 +355,25 @@ def run_ours(args):
             out = [None] * world
             dist.all_gather_object(out, blob)
             return out
-        runner = PD.PipelineRank(sysm, E.RidcConfig(levels=order, steps=nt), rank, world, local,
-                                 exchange=exchange)
+
+        def gloo_bcast(x, is_top):   # re-seed broadcast over the gloo control plane
+            h = x.detach().cpu().clone()
+            dist.broadcast(h, src=world - 1)
+            return h.to(x.device)
+        runner = PD.PipelineRank(sysm, E.RidcConfig(levels=order, steps=nt), rank, world, dev,
+                                 exchange=exchange, resident=not shared)
         y0 = torch.from_numpy(np.array(sysm.ivp.initial_state)).cuda()
         out = torch.empty_like(y0)
+        bcast = gloo_bcast if shared else None
 
         def solve_device():
-            return runner.run_device(y0, out)
+            return runner.run_device(y0, out, broadcast=bcast)
         launches_per_step = runner.kernel_launches
         tick_launches = runner.tick_launches
         # this rank's level-step bytes per point; the producer side also writes the
         # consumer's inbox copy (8 B/pt over NVLink, counted on the consumer);
         # per launch of the level-step kernel (resident: a whole interval)
-        resident = runner.resident
+        path = runner.info["path"]
         lev_bytes = (bytes_per_point(rank) + (8 if rank < world - 1 else 0)) * nt / max(tick_launches, 1)
     else:
         eng = E.Engine(sysm, E.RidcConfig(levels=order, steps=nt))
@@ -277,19 +382,13 @@ def run_ours(args):
 
         def solve_device():
             return eng.run_device(y0, out)
-        info = eng.info
-        launches_per_step = info["kernel_launches"]
-        # resident FEBE: seed + one march; resident level march: 2 seeds + one
-        # march per interval; else the tick graph: seed + one launch per tick
-        resident = (order == 1 and launches_per_step == 2) or (order > 1 and launches_per_step == 3)
-        tick_launches = 1 if resident else launches_per_step - 1
-        lev_bytes = sum(bytes_per_point(j) for j in range(order)) * nt / max(tick_launches, 1)
+        launches_per_step = eng.info["kernel_launches"]
 
     for _ in range(max(args.warmup, 0)):
         solve_device()
     barrier()
     times = []
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     with clocks:
         barrier()
         for _ in range(args.steps):
@@ -298,41 +397,55 @@ def run_ours(args):
             times.append(solve_device())
         barrier()
     t_local = float(sum(times))
-    t_max = t_local
-    if dist is not None:
-        tt = torch.tensor([t_local], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = reduce_max(t_local)
     value = n * nt * args.steps / t_max
     ms_per_step = t_max / args.steps * 1e3
 
-    # roofline of the dominant kernel (the fused tick kernel): algorithmic bytes per
-    # launch / average launch duration over the timed region (events on its stream)
+    if world == 1:
+        # the path actually taken, read back from the engine after the timed runs
+        info = eng.info
+        path = info["path"]
+        launches_per_step = info["kernel_launches"]
+        # resident FEBE: seed + one march; resident level march: 2 seeds + one march
+        # per interval; else the tick graph: seed + one launch per tick
+        tick_launches = 1 if path != 0 else launches_per_step - 1
+        lev_bytes = sum(bytes_per_point(j) for j in range(order)) * nt / max(tick_launches, 1)
+    from paper_1209_4297_b200._lib import PATH_NAMES
+    path_name = PATH_NAMES.get(path, "?")
+
+    # roofline of the dominant kernel: algorithmic bytes per launch / average
+    # launch duration over the timed region (CUDA events on the library's stream)
     peak, peak_kind = hbm_peak()
     per_launch_s = t_local / (args.steps * max(tick_launches, 1))
     bytes_launch = lev_bytes * n
     achieved = bytes_launch / per_launch_s / 1e9
-    traffic = None
+    traffic, traffic_note = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(f"{cfg['workload']}/p{order}" + ("/resident" if resident else ""))
+                ent = json.load(f).get(f"{cfg['workload']}/p{order}/{path_name}")
+            if isinstance(ent, dict) and ent.get("nt") == nt:
+                traffic, traffic_note = ent["bytes_per_launch"], ent.get("source")
         except Exception:
             traffic = None
+    kernels = {
+        "resident_febe": "k_resident_febe (whole FEBE march in one launch: registers-resident chunks, "
+                         "stencil + factored tridiagonal solve per step, halo edges via tagged L2 mailbox)",
+        "resident_levels": ("k_resident_levels (this rank's level: whole interval in one launch, TMA-staged "
+                            "window, per-segment publish/release flags, tile stores into the consumer's inbox "
+                            "over NVLink)") if world > 1 else
+                           ("k_resident_levels (all levels on this GPU in one launch: a co-resident CTA group "
+                            "per level, registers-resident chunks, TMA-staged windows, per-segment flags)"),
+        "tick": "k_tick_chunk (fused level-step: stencils + factored tridiagonal solve)",
+    }
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": (("k_resident_levels (this rank's level: whole interval in one launch, "
-                            "registers-resident chunks, TMA-staged window of the producer level, "
-                            "per-segment publish/release flags, tile stores into the consumer's inbox over NVLink)")
-                           if world > 1 and resident else
-                           "k_resident_levels (all levels on this GPU in one launch: a co-resident CTA group per "
-                           "level, registers-resident chunks, TMA-staged windows, per-segment flags)"
-                           if resident and order > 1 else
-                           "k_resident_febe (whole FEBE march in one launch: registers-resident chunks, "
-                           "stencil + factored tridiagonal solve per step, halo edges via tagged L2 mailbox)"
-                           if resident else "k_tick_chunk (fused level-step: stencils + factored tridiagonal solve)"),
-                "bytes_per_launch": bytes_launch, "launch_us": per_launch_s * 1e6}
+                "kernel": kernels.get(path_name, path_name), "path": path_name,
+                "bytes_per_launch": bytes_launch, "launch_us": per_launch_s * 1e6,
+                "steps_per_launch": nt // max(tick_launches, 1) if path_name != "tick" else 1}
+    if traffic_note:
+        roofline["traffic_source"] = traffic_note
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             # level-steps/s = p N Nt / wall (work done by all levels)
@@ -340,10 +453,12 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "gpu_launches": int(launches_per_step * args.steps)}
-    cfg.update({"order": order, "levels_per_gpu": 1 if world > 1 else order,
-                "parallelism": f"levels-over-gpus{world}" if world > 1 else "1gpu",
-                "l2": "flushed between solves (512 MiB write); state stays resident within a solve"})
-    line["config"] = cfg
+    line["config"] = bench_config(cfg, order, world)
+    line["path"] = path_name
+    if shared:
+        line["ranks_share_devices"] = True
+        line["note"] = (f"{world} ranks on {ndev} visible GPU(s): stream-memop pipeline ranks time-sliced on "
+                        "shared devices -- a functional run of the N>1 path, not a scaling measurement")
     line["roofline"] = roofline
     line["clocks"] = clocks.summary()
 
@@ -364,7 +479,9 @@ def run_ours(args):
             walls.append(time.perf_counter() - t0)
         line["e2e"] = {"value": n * nt * len(walls) / sum(walls), "unit": UNIT,
                        "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n}
-        # extra orders with all levels on this GPU (configs[1]: "RIDC order 1-4 on 1 B200")
+        line["cpu_baseline"] = cpu_sample(sysm, order, nt, budget_s=args.cpu_budget)
+        # extra orders with all levels on this GPU (configs[1]: "RIDC order 1-4 on 1 B200"),
+        # each beside the CPU oracle with one thread per level (the reference's workers)
         extra = {}
         if not args.no_extra:
             for p in (2, 3, 4):
@@ -372,15 +489,13 @@ def run_ours(args):
                     continue
                 with E.Engine(sysm, E.RidcConfig(levels=p, steps=nt)) as e2:
                     e2.run_device(y0, out)
-                    ts = []
-                    for _ in range(2):
-                        flush.zero_()
-                        torch.cuda.synchronize()
-                        ts.append(e2.run_device(y0, out))
+                    ts = _timed_solves(lambda: e2.run_device(y0, out), flush, 2)
                     extra[f"order{p}_1gpu"] = {"value": n * nt * len(ts) / sum(ts),
                                                "level_steps_per_s": p * n * nt * len(ts) / sum(ts),
                                                "ms_per_solve": sum(ts) / len(ts) * 1e3,
-                                               "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps)}
+                                               "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps),
+                                               "path": e2.info["path_name"],
+                                               "cpu_baseline": cpu_sample(sysm, p, nt, budget_s=args.cpu_budget / 3)}
             # the paper's ARK comparators on the same grid and dt (steppers.integrate_ark)
             from paper_1209_4297_b200.steppers import ArkEngine
             from paper_1209_4297_b200.tableaus import imex3_tableau, imex4_tableau
@@ -388,19 +503,21 @@ def run_ours(args):
             for name, tab in (("imex3", imex3_tableau()), ("imex4", imex4_tableau())):
                 with ArkEngine(ivp, tab, ivp.t_start, ivp.t_end, nt) as ae:
                     ae.run_device(y0, out)
-                    ts = []
-                    for _ in range(2):
-                        flush.zero_()
-                        torch.cuda.synchronize()
-                        ts.append(ae.run_device(y0, out))
+                    ts = _timed_solves(lambda: ae.run_device(y0, out), flush, 2)
                     extra[f"{name}_1gpu"] = {"value": n * nt * len(ts) / sum(ts),
                                              "ms_per_solve": sum(ts) / len(ts) * 1e3,
                                              "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps),
-                                             "launches_per_solve": ae.info["kernel_launches"]}
+                                             "launches_per_solve": ae.info["kernel_launches"],
+                                             "cpu_baseline": cpu_sample_ark(sysm, tab, name, nt)}
         line["ridc_orders_1gpu"] = extra
         if not args.no_extra:
             line["pipeline_ranks_alone"] = pipeline_ranks_alone(sysm, nt, t_max / args.steps / nt)
-        line["cpu_baseline"] = cpu_sample(sysm, order, nt, budget_s=args.cpu_budget)
+            eng.close()
+            del y0, out
+            torch.cuda.empty_cache()
+            # the paper headline's shape (configs[2], C3: 2-D adv-diff 4096^2): FEBE on
+            # one GPU is the denominator of "RIDC-4 on 4 GPUs <= 1.1x FEBE on 1 GPU"
+            line["c3_1gpu"] = {f"order{p}": workload_line("c3", p, flush) for p in (1, 4)}
     else:
         # e2e at N GPUs: every rank copies y0 in from pinned host memory, the
         # pipeline marches, every rank reads the solution back; wall time of the
@@ -415,15 +532,15 @@ def run_ours(args):
             e0.record()
             y0.copy_(y0h, non_blocking=True)
             torch.cuda.current_stream().synchronize()   # the pipeline runs on its own stream
-            runner.run_device(y0, out)
+            runner.run_device(y0, out, broadcast=bcast)
             finh.copy_(out, non_blocking=True)
             e1.record()
             torch.cuda.synchronize()
             walls.append(e0.elapsed_time(e1) * 1e-3)
-        tw = torch.tensor([sum(walls)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-        line["e2e"] = {"value": n * nt * len(walls) / float(tw.item()), "unit": UNIT,
+        tw = reduce_max(sum(walls))
+        line["e2e"] = {"value": n * nt * len(walls) / tw, "unit": UNIT,
                        "h2d_bytes_per_step": 8 * n * world, "d2h_bytes_per_step": 8 * n * world}
+        runner.close()
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:

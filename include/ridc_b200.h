@@ -94,7 +94,15 @@ typedef struct ridc_info {
     int64_t ring_vectors;         /* device vectors held by all level rings */
     double lambda;                /* decay factor of the shifted operator's factors */
     double r;                     /* stiffness dt*d_x/h_x^2 */
+    int32_t path;                 /* marching path in effect (after the last run):
+                                     RIDC_PATH_TICK / _RESIDENT_FEBE / _RESIDENT_LEVELS */
+    int32_t fell_back;            /* 1: a resident march could not get its co-resident
+                                     SMs at run time and the tick graph replaced it */
 } ridc_info;
+
+#define RIDC_PATH_TICK 0             /* one fused tick kernel per pipeline tick (CUDA graph) */
+#define RIDC_PATH_RESIDENT_FEBE 1    /* one cooperative launch marches every FEBE step */
+#define RIDC_PATH_RESIDENT_LEVELS 2  /* one cooperative launch per interval, all levels */
 
 /*
  * Create a run context (RidcConfig validation engine.py:71-87, _prepare
@@ -121,6 +129,10 @@ int ridc_run_device(ridc_ctx *ctx, const double *y0_dev, double *final_dev,
                     double *wall_seconds);
 
 int ridc_info_get(const ridc_ctx *ctx, ridc_info *info);
+/* Watchdog of the resident marches' in-kernel neighbour waits
+ * (RidcConfig.watchdog_seconds, engine.py:432-439): a wait exceeding it
+ * aborts the march with RIDC_E_PROTOCOL.  Default 30 s. */
+int ridc_set_watchdog(ridc_ctx *ctx, double seconds);
 int ridc_destroy(ridc_ctx *ctx);
 const char *ridc_last_error(const ridc_ctx *ctx);   /* ctx may be NULL: thread's last error */
 
@@ -173,10 +185,14 @@ typedef struct ridc_pipe ridc_pipe;
 int64_t ridc_pipe_handle_bytes(void);
 
 /* Create the rank owning `level` (0..levels-1) on `device`.  inbox_capacity:
- * inbox ring slots (0: default 2*level+13; >= steps/restarts+1 makes every
- * rank runnable to completion without its consumer, e.g. ranks driven one
- * after another on one device).  watchdog_seconds bounds every wait
- * (PipelineProtocolError on expiry, engine.py:432-439). */
+ * inbox ring slots (0: default 2*level+13; at least level+3 -- the window of
+ * level+1 steps plus the deferred publication of the resident march -- else
+ * RIDC_E_CONFIG; >= steps/restarts+1 makes every rank runnable to completion
+ * without its consumer, e.g. ranks driven one after another on one device).
+ * watchdog_seconds bounds every wait (PipelineProtocolError on expiry,
+ * engine.py:432-439).  Watermark waits on a producer on ANOTHER device use
+ * CU_STREAM_WAIT_VALUE_FLUSH where the device supports flushing remote
+ * writes, else an in-kernel acquire poll at system scope. */
 int ridc_pipe_create(const ridc_problem *problem, double t_start, double t_end,
                      int32_t levels, int64_t steps, int32_t restarts,
                      const double *weights, int64_t nweights, int32_t level,

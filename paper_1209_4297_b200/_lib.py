@@ -25,7 +25,12 @@ class RidcInfo(ctypes.Structure):
         ("tile", ctypes.c_int32), ("halo", ctypes.c_int32), ("items_per_level", ctypes.c_int32),
         ("threads", ctypes.c_int32), ("ring_vectors", ctypes.c_int64),
         ("lam", ctypes.c_double), ("r", ctypes.c_double),
+        ("path", ctypes.c_int32), ("fell_back", ctypes.c_int32),
     ]
+
+
+PATH_TICK, PATH_RESIDENT_FEBE, PATH_RESIDENT_LEVELS = 0, 1, 2
+PATH_NAMES = {PATH_TICK: "tick", PATH_RESIDENT_FEBE: "resident_febe", PATH_RESIDENT_LEVELS: "resident_levels"}
 
 
 # name -> (restype, argtypes); every symbol include/ridc_b200.h declares
@@ -39,6 +44,7 @@ SIGNATURES = {
     "ridc_run": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _dp]),
     "ridc_run_device": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
     "ridc_info_get": (ctypes.c_int, [_vp, _P(RidcInfo)]),
+    "ridc_set_watchdog": (ctypes.c_int, [_vp, _d]),
     "ridc_destroy": (ctypes.c_int, [_vp]),
     "ridc_last_error": (ctypes.c_char_p, [_vp]),
     "ridc_op_apply": (ctypes.c_int, [_P(CProblem), ctypes.c_int32, _vp, _vp, ctypes.c_int32]),

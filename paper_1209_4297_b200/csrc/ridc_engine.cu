@@ -76,6 +76,30 @@ __global__ void k_seed_chunk(const double* __restrict__ src, EngineParams ep, lo
     }
 }
 
+// Wait on the device until *flag >= want: the consumer side of a watermark
+// written by a producer on ANOTHER device where the stream wait cannot flush
+// remote writes (CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES = 0).  The
+// system-scope acquire orders the producer's earlier peer stores (made
+// visible by the fence before its stream write of the watermark) before
+// every later kernel of this stream.  A wait beyond spin_limit cycles sets
+// *abort and returns (the host reports PipelineProtocolError).
+__global__ void k_wait_flag(const unsigned long long* flag, unsigned long long want, unsigned* abort,
+                            long long spin_limit)
+{
+    if (threadIdx.x != 0) return;
+    const long long t0 = clock64();
+    unsigned long long v;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+        if (v >= want) return;
+        if (clock64() - t0 > spin_limit || *(volatile unsigned*)abort) {
+            atomicExch(abort, 1u);
+            return;
+        }
+        __nanosleep(200);
+    }
+}
+
 template <int KIND>
 __global__ void k_apply(DevProblem pb, int op, const double* __restrict__ in, double* __restrict__ out)
 {
@@ -531,6 +555,8 @@ struct ridc_ctx {
     TmapSet tm_in;
     LevelsParams lp;
     unsigned long long lepoch = 0;
+    bool fell_back = false;        // a resident march was replaced by the tick graph at run time
+    double watchdog = 30.0;        // seconds per in-kernel neighbour wait (ridc_set_watchdog)
     std::string err;
 };
 
@@ -785,6 +811,7 @@ int march(ridc_ctx* c, double* wall_seconds)
         if (rc) return rc;
         if (fb) {   // the SMs are shared right now: the tick kernel's graph for good
             c->reslev = false;
+            c->fell_back = true;
             if ((rc = capture_graph(c)) != RIDC_OK) return rc;
         }
     }
@@ -810,6 +837,7 @@ int march(ridc_ctx* c, double* wall_seconds)
             // the tick kernel's graph, which needs no co-residency
             cudaGetLastError();
             c->resident = false;
+            c->fell_back = true;
             int rc = capture_graph(c);
             if (rc) return rc;
         } else {
@@ -893,7 +921,7 @@ int setup_resident(ridc_ctx* c)
     rp.mail = c->d_mail;
     rp.abort = c->d_flags;
     rp.err = c->d_err;
-    rp.spin_limit = 4000000000LL;   // ~2 s at 1.9 GHz per neighbour wait
+    rp.spin_limit = (long long)(c->watchdog * 2.0e9);   // clock64 cycles (~2 GHz) per neighbour wait
     rp.dbg = c->d_dbg;
     c->resident = true;
     c->launches = 2;
@@ -995,7 +1023,7 @@ int setup_reslev(ridc_ctx* c)
     lp.pub_every = env_int("RIDC_PUB_EVERY", 4);
     lp.err = c->d_err;
     lp.abort = c->d_flags;
-    lp.spin_limit = 4000000000LL;   // ~2 s at 1.9 GHz per wait
+    lp.spin_limit = (long long)(c->watchdog * 2.0e9);   // clock64 cycles (~2 GHz) per wait
     c->reslev = true;
     c->launches = 3LL * c->restarts;   // per interval: two seeds + one march
     return RIDC_OK;
@@ -1213,6 +1241,17 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->ring_vectors = c->ring_vectors;
     info->lambda = c->ss.sv.lam;
     info->r = c->ss.r;
+    info->path = c->resident ? RIDC_PATH_RESIDENT_FEBE : (c->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK);
+    info->fell_back = c->fell_back ? 1 : 0;
+    return RIDC_OK;
+}
+
+int ridc_set_watchdog(ridc_ctx* c, double seconds)
+{
+    if (!c || !(seconds > 0.0)) return fail(c ? &c->err : nullptr, RIDC_E_CONFIG, "watchdog must be positive");
+    c->watchdog = seconds;
+    c->rp.spin_limit = (long long)(seconds * 2.0e9);
+    c->lp.spin_limit = (long long)(seconds * 2.0e9);
     return RIDC_OK;
 }
 
@@ -1414,6 +1453,35 @@ const DriverOps& driver_ops()
     return ops;
 }
 
+// Wait until *flag >= want on stream st.  remote: the value (and the data it
+// publishes) is written from another device; the stream wait then needs
+// CU_STREAM_WAIT_VALUE_FLUSH so that later work sees the producer's earlier
+// remote writes -- or, where the device cannot flush remote writes, an
+// in-kernel system-scope acquire poll (k_wait_flag).
+cudaError_t wait_value(cudaStream_t st, const unsigned long long* flag, unsigned long long want, bool remote,
+                       bool can_flush, unsigned* abort, long long spin_limit)
+{
+    const DriverOps& ops = driver_ops();
+    if (remote && !can_flush) {
+        k_wait_flag<<<1, 32, 0, st>>>(flag, want, abort, spin_limit);
+        return cudaGetLastError();
+    }
+    const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (remote ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
+    return ops.wait(reinterpret_cast<CUstream>(st), (CUdeviceptr)flag, (cuuint64_t)want, flags) == CUDA_SUCCESS
+               ? cudaSuccess
+               : cudaErrorUnknown;
+}
+
+bool device_can_flush_remote(int device)
+{
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, device) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return v != 0;
+}
+
 constexpr uint32_t kBlobMagic = 0x52494443u;   // "RIDC"
 constexpr size_t kFlagBytes = 4096;            // wm (+0), rel (+8), pub[nseg] (+256), relv[nseg] (+2048), then the inbox ring
 constexpr size_t kPubOff = 256, kRelOff = 2048;
@@ -1473,6 +1541,8 @@ struct ridc_pipe {
     unsigned long long* out_pub = nullptr;   // consumer's pub (peer)
     unsigned long long lepoch = 0;
     unsigned tag_next = 1;
+    bool prev_remote = false;   // the producer (level - 1) sits on another device
+    bool can_flush = false;     // this device can flush remote writes after a stream wait
     std::string err;
 };
 
@@ -1543,8 +1613,9 @@ int pipe_enqueue(ridc_pipe* p, int interval, long long* launches)
     for (long long t = 1; t <= p->per; ++t) {
         if (j > 0) {
             const long long need = g0 + (t < j ? j : t);
-            if (ops.wait(cs, (CUdeviceptr)p->wm, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-                return pipe_fail(p, RIDC_E_CUDA, "cuStreamWaitValue64 (watermark) failed");
+            if (wait_value(p->stream, p->wm, (unsigned long long)need, p->prev_remote, p->can_flush, p->d_abort,
+                           (long long)(p->watchdog * 2.0e9)) != cudaSuccess)
+                return pipe_fail(p, RIDC_E_CUDA, "watermark wait failed");
         }
         if (j < top) {
             const long long need_rel = g0 + t - p->next_cap + 1;
@@ -1598,6 +1669,13 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     const long long per = steps / restarts;
     if (per < delay(levels) + 1) return pipe_fail(nullptr, RIDC_E_CONFIG, "restart interval shorter than the pipeline fill");
     if (!(t_start < t_end)) return pipe_fail(nullptr, RIDC_E_CONFIG, "need t_start < t_end");
+    if (level > 0 && inbox_capacity > 0 && inbox_capacity < level + 3) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "inbox_capacity %d too small for level %d: its window needs %d slots and "
+                                  "the deferred publication 2 more (>= %d)", inbox_capacity, level, level + 1,
+                 level + 3);
+        return pipe_fail(nullptr, RIDC_E_CONFIG, buf);
+    }
     const DriverOps& ops = driver_ops();
     if (!ops.wait || !ops.write) return pipe_fail(nullptr, RIDC_E_CUDA, "driver stream memory operations unavailable");
     std::vector<int> st, su;
@@ -1662,6 +1740,9 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     P_TRY(cudaMalloc(&p->d_cgeo, p->ss.cgeo.size() * sizeof(ChunkGeo)));
     P_TRY(cudaMemcpy(p->d_cgeo, p->ss.cgeo.data(), p->ss.cgeo.size() * sizeof(ChunkGeo), cudaMemcpyHostToDevice));
     P_TRY(cudaMalloc(&p->d_err, sizeof(unsigned long long)));
+    P_TRY(cudaMalloc(&p->d_abort, sizeof(unsigned)));
+    P_TRY(cudaMemset(p->d_abort, 0, sizeof(unsigned)));
+    p->can_flush = device_can_flush_remote(device);
     // mailbox: flags, then the inbox ring (cap slots of ny padded rows); zeroed: Dirichlet ghosts
     const size_t ring_bytes = (size_t)p->inbox_cap * p->Vs * sizeof(double);
     P_TRY(cudaMalloc(&p->mailbox, kFlagBytes + ring_bytes));
@@ -1695,7 +1776,6 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
             P_TRY(cudaMemcpy(p->d_geo, d.data(), d.size() * sizeof(int), cudaMemcpyHostToDevice));
             P_TRY(cudaMemcpy(p->d_geo + d.size(), p->rgeo.readers.data(), d.size() * sizeof(int),
                              cudaMemcpyHostToDevice));
-            P_TRY(cudaMalloc(&p->d_abort, sizeof(unsigned)));
             P_TRY(cudaMalloc(&p->d_lanes, (size_t)restarts * sizeof(LevelLane)));
             if (nseg > 1) {
                 P_TRY(cudaMalloc(&p->d_lmail, 2 * (size_t)p->Vs * sizeof(uint4)));
@@ -1728,7 +1808,8 @@ int ridc_pipe_export(ridc_pipe* p, void* blob)
     return RIDC_OK;
 }
 
-static int open_blob(ridc_pipe* p, const void* blob, int want_level, char** base, int slot, long long* cap)
+static int open_blob(ridc_pipe* p, const void* blob, int want_level, char** base, int slot, long long* cap,
+                     int* device)
 {
     PipeBlob b;
     memcpy(&b, blob, sizeof b);
@@ -1752,6 +1833,7 @@ static int open_blob(ridc_pipe* p, const void* blob, int want_level, char** base
         *base = reinterpret_cast<char*>(ptr);
     }
     *cap = b.inbox_cap;
+    *device = b.device;
     return RIDC_OK;
 }
 
@@ -1766,12 +1848,15 @@ int ridc_pipe_connect(ridc_pipe* p, const void* prev_blob, const void* next_blob
     long long cap = 0;
     char* base = nullptr;
     if (prev_blob) {
-        if ((rc = open_blob(p, prev_blob, j - 1, &base, 0, &cap)) != RIDC_OK) return rc;
+        int pdev = p->device;
+        if ((rc = open_blob(p, prev_blob, j - 1, &base, 0, &cap, &pdev)) != RIDC_OK) return rc;
+        p->prev_remote = pdev != p->device;
         p->prev_rel = reinterpret_cast<unsigned long long*>(base + 8);
         p->in_rel = reinterpret_cast<unsigned long long*>(base + kRelOff);
     }
     if (next_blob) {
-        if ((rc = open_blob(p, next_blob, j + 1, &base, 1, &cap)) != RIDC_OK) return rc;
+        int ndev = p->device;
+        if ((rc = open_blob(p, next_blob, j + 1, &base, 1, &cap, &ndev)) != RIDC_OK) return rc;
         p->next_wm = reinterpret_cast<unsigned long long*>(base);
         p->next_inbox = reinterpret_cast<double*>(base + kFlagBytes);
         p->next_cap = cap;
@@ -1827,6 +1912,7 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
         PIPE_TRY(p, cudaGetLastError());
     }
     PIPE_TRY(p, cudaMemsetAsync(p->d_err, 0xff, sizeof(unsigned long long), p->stream));
+    PIPE_TRY(p, cudaMemsetAsync(p->d_abort, 0, sizeof(unsigned), p->stream));
     PIPE_TRY(p, cudaEventRecord(p->ev0, p->stream));
     // the interval's ops: captured into a graph on first use (memops included)
     auto it = p->graphs.find(interval);
@@ -1837,7 +1923,6 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
             if (p->d_lmail) PIPE_TRY(p, cudaMemsetAsync(p->d_lmail, 0, 2 * (size_t)p->Vs * sizeof(uint4), p->stream));
             p->tag_next = 1;
         }
-        PIPE_TRY(p, cudaMemsetAsync(p->d_abort, 0, sizeof(unsigned), p->stream));
         LevelsParams lp;
         memset(&lp, 0, sizeof lp);
         lp.pb = p->pb;
@@ -1920,7 +2005,7 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
         PIPE_TRY(p, cudaEventElapsedTime(&ms, p->ev0, p->ev1));
         *wall_seconds = ms * 1e-3;
     }
-    if (p->reslev) {
+    {   // in-kernel waits (resident march, or k_wait_flag on a remote producer) that timed out
         unsigned ab = 0;
         PIPE_TRY(p, cudaMemcpy(&ab, p->d_abort, sizeof ab, cudaMemcpyDeviceToHost));
         if (ab) {
@@ -1957,6 +2042,7 @@ int ridc_pipe_info(const ridc_pipe* p, ridc_info* info)
     info->ring_vectors = 2 + (p->level > 0 ? p->inbox_cap : 0);
     info->lambda = p->ss.sv.lam;
     info->r = p->ss.r;
+    info->path = p->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK;
     return RIDC_OK;
 }
 
@@ -2504,11 +2590,18 @@ int enqueue_shard(ridc_shards* g, int s, int interval)
     EngineParams ep = interval_params(c, interval);
     const long long G0 = g->epoch + (long long)interval * g->ticks;
     const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
+    // got_up is written by the upper neighbour's stream, got_dn by the lower's
+    // (after their peer copies): remote writers need a flushing wait
+    const bool can_flush = device_can_flush_remote(c->device);
+    unsigned* abort = reinterpret_cast<unsigned*>(g->mbox[s] + 2);
+    const long long spin = (long long)(g->watchdog * 2.0e9);
     auto wait_both = [&](long long G) -> int {
         if (G <= 0) return RIDC_OK;
-        if (ops.wait(cs, (CUdeviceptr)(g->mbox[s] + 0), (cuuint64_t)G, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
-            ops.wait(cs, (CUdeviceptr)(g->mbox[s] + 1), (cuuint64_t)G, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-            return shard_fail(g, RIDC_E_CUDA, "cuStreamWaitValue64 (shard mailbox) failed");
+        if (wait_value(c->stream, g->mbox[s] + 0, (unsigned long long)G, up->device != c->device, can_flush, abort,
+                       spin) != cudaSuccess ||
+            wait_value(c->stream, g->mbox[s] + 1, (unsigned long long)G, dn->device != c->device, can_flush, abort,
+                       spin) != cudaSuccess)
+            return shard_fail(g, RIDC_E_CUDA, "shard mailbox wait failed");
         return RIDC_OK;
     };
     int rc;
@@ -2657,6 +2750,7 @@ static int shards_run_multi(ridc_shards* g, const double* y0_host, double* final
                                               cudaMemcpyHostToDevice, c->stream));
         }
         CUDA_TRY(&g->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+        CUDA_TRY(&g->err, cudaMemsetAsync(g->mbox[s] + 2, 0, sizeof(unsigned long long), c->stream));
         CUDA_TRY(&g->err, cudaEventRecord(g->sev0[s], c->stream));
     }
     int rc;
@@ -2681,6 +2775,12 @@ static int shards_run_multi(ridc_shards* g, const double* y0_host, double* final
         }
     }
     g->epoch += (long long)g->restarts * g->ticks + 1;
+    for (int s = 0; s < S; ++s) {   // an in-kernel mailbox wait that timed out
+        unsigned ab = 0;
+        CUDA_TRY(&g->err, cudaSetDevice(g->sh[s]->device));
+        CUDA_TRY(&g->err, cudaMemcpy(&ab, g->mbox[s] + 2, sizeof ab, cudaMemcpyDeviceToHost));
+        if (ab) return shard_fail(g, RIDC_E_PROTOCOL, "row shards made no progress within the watchdog");
+    }
     double wall = 0.0;
     for (int s = 0; s < S; ++s) {
         ridc_ctx* c = g->sh[s];
@@ -2793,8 +2893,9 @@ int ridc_shards_create_multi(const ridc_problem* problem, double t_start, double
         g->sh.push_back(c);
         unsigned long long* mb = nullptr;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (cudaSetDevice(devices[s]) != cudaSuccess || cudaMalloc(&mb, 2 * sizeof(unsigned long long)) != cudaSuccess ||
-            cudaMemset(mb, 0, 2 * sizeof(unsigned long long)) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
+        // {got_up, got_dn, abort word of the in-kernel waits, pad}
+        if (cudaSetDevice(devices[s]) != cudaSuccess || cudaMalloc(&mb, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(mb, 0, 4 * sizeof(unsigned long long)) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
             cudaEventCreate(&e1) != cudaSuccess) {
             g->err = "shard mailbox / event allocation failed";
             return bail(RIDC_E_CUDA);

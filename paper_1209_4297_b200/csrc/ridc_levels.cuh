@@ -260,7 +260,9 @@ __global__ void __launch_bounds__(NT, MINB)
     };
 
     // thread 0: window node a of step tt (build_item's order) as TMA load m into stage m % NSTAGE
+    long long issued = 0;   // thread 0: loads issued so far (load numbers < issued)
     auto issue_node = [&](long long tt, int a, long long m) {
+        if (m + 1 > issued) issued = m + 1;
         const int s = (int)(m % NSTAGE);
         if (m >= NSTAGE) mbar_wait(&empty[s], (uint32_t)(((m - NSTAGE) / NSTAGE) & 1));
         const long long ns = tt >= j ? tt - a : a;
@@ -460,6 +462,10 @@ __global__ void __launch_bounds__(NT, MINB)
         __syncthreads();
         if (tid == 0 && !s_dead) publish_u64<SYS>(ln.out_pub + seg, ep | (unsigned long long)pend);
     }
+    // a watchdog exit can leave prefetched window loads in flight: the CTA must
+    // not retire while the TMA still writes its shared memory
+    if (tid == 0)
+        for (long long m = n; m < issued; ++m) mbar_wait(&full[m % NSTAGE], (uint32_t)((m / NSTAGE) & 1));
 }
 
 }  // namespace ridc

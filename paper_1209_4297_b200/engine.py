@@ -30,13 +30,13 @@ from typing import Optional
 import numpy as np
 
 from . import _lib, device as D, ops
-from .errors import ConfigError, PipelineProtocolError
+from .errors import ConfigError, DimensionMismatch, PipelineProtocolError
 from .problems import StructuredIVP, as_descriptor
 from .quadrature import MAX_LEVEL, pack_weight_tables
 
 __all__ = ["RidcConfig", "RidcSolution", "LevelWindow", "Engine", "startup_delay",
            "restart_partition", "predict_step", "correct_step", "run_serial", "run_pipelined",
-           "schedule", "MAX_LEVELS"]
+           "pipeline_devices", "schedule", "MAX_LEVELS"]
 
 MAX_LEVELS = MAX_LEVEL + 1
 RECORD_TRAJECTORY = 1
@@ -169,12 +169,15 @@ class Engine:
             config.steps, config.restarts, self.weights.ctypes.data, self.weights.shape[0],
             config.device, flags, ctypes.byref(h)))
         self._h = h
+        _lib.check(_lib.lib().ridc_set_watchdog(self._h, float(config.watchdog_seconds)), self._h)
 
     @property
     def info(self) -> dict:
         inf = _lib.RidcInfo()
         _lib.check(_lib.lib().ridc_info_get(self._h, ctypes.byref(inf)), self._h)
-        return {f: getattr(inf, f) for f, _ in inf._fields_}
+        d = {f: getattr(inf, f) for f, _ in inf._fields_}
+        d["path_name"] = _lib.PATH_NAMES.get(d["path"], "?")
+        return d
 
     def run(self, y0=None) -> RidcSolution:
         """One full run from host memory (H2D, marching, D2H)."""
@@ -194,7 +197,22 @@ class Engine:
                             trace=_trace(self.config) if self.config.trace else None)
 
     def run_device(self, y0_dev, out_dev) -> float:
-        """March from a device-resident state into a device buffer; returns device seconds."""
+        """March from a device-resident state into a device buffer; returns device seconds.
+
+        Both tensors must be float64, contiguous, of the problem's dimension and
+        on the engine's device (the C-ABI takes no lengths).  The library runs on
+        its own stream, so the caller's current stream is synchronised first
+        (y0 may still be in production there)."""
+        t = D.torch()
+        n = self.problem.dimension
+        for name, x in (("y0", y0_dev), ("out", out_dev)):
+            if not isinstance(x, t.Tensor) or x.dtype != t.float64 or not x.is_cuda:
+                raise TypeError(f"{name} must be a float64 CUDA tensor")
+            if x.device.index != self.config.device:
+                raise ValueError(f"{name} is on cuda:{x.device.index}, the engine on cuda:{self.config.device}")
+            if x.numel() != n or not x.is_contiguous():
+                raise DimensionMismatch(f"{name} has length {x.numel()}, expected {n} (contiguous)")
+        t.cuda.current_stream(y0_dev.device).synchronize()
         wall = ctypes.c_double(0.0)
         _lib.check(_lib.lib().ridc_run_device(self._h, y0_dev.data_ptr(), out_dev.data_ptr(),
                                               ctypes.byref(wall)), self._h)
@@ -224,8 +242,38 @@ def run_serial(ivp, config: RidcConfig, solver=None) -> RidcSolution:
         return eng.run()
 
 
+def pipeline_devices(config: RidcConfig):
+    """GPUs the concurrent executor spreads the levels over: ``workers`` is the
+    GPU count, capped by the visible devices; level j runs on
+    GPU (device + j % g).  A single entry means one device."""
+    t = D.torch()
+    visible = t.cuda.device_count() if t.cuda.is_available() else 0
+    g = max(1, min(config.workers, visible - config.device))
+    return [config.device + (j % g) for j in range(config.levels)] if g > 1 else [config.device]
+
+
 def run_pipelined(ivp, config: RidcConfig, solver=None) -> RidcSolution:
-    """Concurrent executor semantics (engine.py:497-522); bitwise equal to run_serial."""
+    """Concurrent executor semantics (engine.py:497-522); bitwise equal to run_serial.
+
+    The reference's worker threads own levels round-robin (engine.py:447-456);
+    here ``workers`` > 1 with that many GPUs visible places level j on GPU
+    j % workers (distributed.ConcurrentPipeline: one host thread and stream
+    per level, device-side flags, peer stores over NVLink; with one level per
+    GPU each rank is one resident launch).  With one visible GPU, or when a
+    trajectory is recorded, every level marches on ``config.device``.  Either
+    way the states are bitwise those of run_serial (the tiling depends only on
+    the problem and dt)."""
+    devs = pipeline_devices(config)
+    if len(set(devs)) > 1 and not config.record_trajectory:
+        from .distributed import ConcurrentPipeline
+        pipe = ConcurrentPipeline(ivp, config, devices=devs)
+        try:
+            final, finals = pipe.run()
+            wall = pipe.device_seconds
+        finally:
+            pipe.close()
+        return RidcSolution(final_state=final, level_finals=finals, wall_seconds=wall,
+                            trace=_trace(config) if config.trace else None)
     with Engine(ivp, config) as eng:
         return eng.run()
 
@@ -236,24 +284,42 @@ def run_pipelined(ivp, config: RidcConfig, solver=None) -> RidcSolution:
 class LevelWindow:
     """Previous-level data at the stencil nodes, in weight order (engine.py:200-210).
 
-    Device-path form: ``states`` holds eta^{[j-1]} at the nodes (f^S and f^N
-    are recomputed on the device).  The reference form with ``fs``/``fn``
-    rows is accepted by :func:`correct_step` too.
+    The reference's constructor ``LevelWindow(fs, fn, new_index, old_index)``
+    (f^S / f^N rows of the previous level) works unchanged.  The device-path
+    form :meth:`from_states` carries eta^{[j-1]} at the nodes instead; f^S and
+    f^N are then recomputed from the states by the device stencils.
     """
 
-    states: np.ndarray
+    fs: Optional[np.ndarray]
+    fn: Optional[np.ndarray]
     new_index: int
     old_index: int
+    states: Optional[np.ndarray] = None
+
+    @classmethod
+    def from_states(cls, states, new_index: int, old_index: int) -> "LevelWindow":
+        return cls(None, None, new_index, old_index, states)
 
 
 def _resolve(ivp):
     return as_descriptor(ivp)
 
 
+def _step_device(x) -> int:
+    """The device a single step runs on: the input tensor's, else the current one."""
+    t = D.torch()
+    if isinstance(x, t.Tensor) and x.is_cuda:
+        return x.device.index
+    D.require_cuda()
+    return t.cuda.current_device()
+
+
 def predict_step(ivp, t_n: float, eta_n, dt: float, solver=None):
     """One predictor step -> (eta_new, f_stiff, f_nonstiff) at the new node (engine.py:193-197)."""
     pd = _resolve(ivp).problem
-    dev = 0
+    if dt <= 0:
+        raise ValueError(f"dt must be positive, got {dt}")
+    dev = _step_device(eta_n)
     eta_new = ops.level_step(pd, dt, eta_n, dev=dev)
     return eta_new, ops.stiff_value(pd, eta_new, dev), ops.nonstiff_value(pd, eta_new, dev)
 
@@ -264,22 +330,25 @@ def correct_step(level: int, ivp, t_n: float, eta_n, prev_level_window, weights,
     if level < 1:
         raise ValueError("correct_step needs level >= 1")
     pd = _resolve(ivp).problem
+    if dt <= 0:
+        raise ValueError(f"dt must be positive, got {dt}")
     w = np.asarray(getattr(weights, "weights", weights), dtype=np.float64)
     win = prev_level_window
     i_new, i_old = win.new_index, win.old_index
     k = w.shape[0]
     if not (0 <= i_new < k and 0 <= i_old < k):
         raise PipelineProtocolError("window indices out of range")
-    if hasattr(win, "states"):
+    dev = _step_device(eta_n)
+    if getattr(win, "states", None) is not None:
         states = np.asarray(win.states)
         if states.shape[0] != k:
             raise PipelineProtocolError(f"window holds {states.shape[0]} nodes, weights need {k}")
         cs = [w[a] - (dt if a == i_new else 0.0) for a in range(k)]
         cn = [w[a] - (dt if a == i_old else 0.0) for a in range(k)]
-        eta_new = ops.level_step(pd, dt, eta_n, list(states), cs, cn)
+        eta_new = ops.level_step(pd, dt, eta_n, list(states), cs, cn, dev=dev)
     else:
         fs, fn = np.asarray(win.fs), np.asarray(win.fn)
         if fs.shape[0] != k or fn.shape[0] != k:
             raise PipelineProtocolError(f"window holds {fs.shape[0]} nodes, weights need {k}")
-        eta_new = ops.level_step_rows(pd, dt, eta_n, fs, fn, w, i_new, i_old)
-    return eta_new, ops.stiff_value(pd, eta_new), ops.nonstiff_value(pd, eta_new)
+        eta_new = ops.level_step_rows(pd, dt, eta_n, fs, fn, w, i_new, i_old, dev=dev)
+    return eta_new, ops.stiff_value(pd, eta_new, dev), ops.nonstiff_value(pd, eta_new, dev)

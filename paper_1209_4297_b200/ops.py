@@ -14,18 +14,40 @@ import ctypes
 import numpy as np
 
 from . import _lib, device as D
+from .errors import DimensionMismatch
 from .problems import ProblemDescriptor
 
 OP_STIFF, OP_NONSTIFF = 0, 1
 
 
-def _dev(x, dev):
+def _check_len(n, *xs):
+    """Every input holds n points (before any device transfer)."""
+    for x in xs:
+        size = x.numel() if hasattr(x, "numel") else np.asarray(x).size
+        if size != n:
+            raise DimensionMismatch(f"state has length {size}, expected {n}")
+
+
+def _dev(x, dev, n):
+    """x as a contiguous float64 vector of n points on CUDA device `dev`.
+
+    The C-ABI takes no lengths (it writes nx*ny doubles), so the dimension is
+    checked here, as the reference's steppers._check_step_args does
+    (steppers.py:107-111): an undersized buffer raises DimensionMismatch
+    instead of becoming an out-of-bounds device write."""
     t = D.torch()
     if isinstance(x, t.Tensor):
         if x.dtype != t.float64 or not x.is_cuda:
             raise TypeError("device inputs must be float64 CUDA tensors")
-        return x.contiguous()
-    return D.to_device(x, dev)
+        if x.device.index != dev:
+            raise ValueError(f"tensor on cuda:{x.device.index}, the operation runs on cuda:{dev}")
+        if x.numel() != n:
+            raise DimensionMismatch(f"state has length {x.numel()}, expected {n}")
+        return x.contiguous().view(-1)
+    a = np.asarray(x)
+    if a.size != n:
+        raise DimensionMismatch(f"state has length {a.size}, expected {n}")
+    return D.to_device(a.reshape(-1), dev)
 
 
 def _out(x, like_tensor):
@@ -34,7 +56,7 @@ def _out(x, like_tensor):
 
 
 def _apply(pd: ProblemDescriptor, op: int, y, dev: int = 0):
-    yd = _dev(y, dev)
+    yd = _dev(y, dev, pd.dimension)
     out = D.torch().empty_like(yd)
     cp = pd.to_c()
     _lib.check(_lib.lib().ridc_op_apply(ctypes.byref(cp), op, yd.data_ptr(), out.data_ptr(), dev))
@@ -51,7 +73,7 @@ def nonstiff_value(pd: ProblemDescriptor, y, dev: int = 0):
 
 def solve_shifted(pd: ProblemDescriptor, coeff: float, rhs, dev: int = 0):
     """x with (I - coeff * L_S) x = rhs."""
-    rd = _dev(rhs, dev)
+    rd = _dev(rhs, dev, pd.dimension)
     x = D.torch().empty_like(rd)
     cp = pd.to_c()
     _lib.check(_lib.lib().ridc_op_solve(ctypes.byref(cp), float(coeff), rd.data_ptr(),
@@ -62,8 +84,9 @@ def solve_shifted(pd: ProblemDescriptor, coeff: float, rhs, dev: int = 0):
 def level_step(pd: ProblemDescriptor, dt: float, eta, window=(), cs=(), cn=(), dev: int = 0):
     """Fused level step: rhs = eta + dt f^N(eta) + sum_k cs_k f^S(w_k) + cn_k f^N(w_k);
     returns (I - dt L_S)^{-1} rhs."""
-    ed = _dev(eta, dev)
-    wins = [_dev(w, dev) for w in window]
+    _check_len(pd.dimension, eta, *window)
+    ed = _dev(eta, dev, pd.dimension)
+    wins = [_dev(w, dev, pd.dimension) for w in window]
     k = len(wins)
     out = D.torch().empty_like(ed)
     ptrs = (ctypes.c_void_p * max(k, 1))(*[w.data_ptr() for w in wins])
@@ -81,9 +104,13 @@ def level_step_rows(pd: ProblemDescriptor, dt: float, eta, fs_rows, fn_rows, w, 
                     dev: int = 0):
     """Reference-form corrector (LevelWindow with f^S/f^N rows, engine.py:177-187):
     rhs = eta + dt f^N(eta) - dt fs[i_new] - dt fn[i_old] + sum_a w_a (fs_a + fn_a)."""
-    ed = _dev(eta, dev)
+    _check_len(pd.dimension, eta)
     k = len(w)
-    rows = [_dev(r, dev) for r in list(fs_rows) + list(fn_rows)]
+    if len(fs_rows) != k or len(fn_rows) != k:
+        raise DimensionMismatch(f"window holds {len(fs_rows)}/{len(fn_rows)} rows, weights need {k}")
+    _check_len(pd.dimension, *fs_rows, *fn_rows)
+    ed = _dev(eta, dev, pd.dimension)
+    rows = [_dev(r, dev, pd.dimension) for r in list(fs_rows) + list(fn_rows)]
     ca = [w[a] - (dt if a == i_new else 0.0) for a in range(k)] + \
          [w[a] - (dt if a == i_old else 0.0) for a in range(k)]
     out = D.torch().empty_like(ed)

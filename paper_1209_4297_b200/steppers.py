@@ -110,7 +110,9 @@ def ark_step(ivp, tab: ButcherPair, t_n: float, y_n, dt: float, solver=None) -> 
     """One coupled DIRK/explicit step (steppers.py:122-142)."""
     y_n = np.asarray(y_n, dtype=np.float64)
     _check_step_args(as_descriptor(ivp).problem.dimension, y_n, dt)
-    with ArkEngine(ivp, tab, t_n, t_n + dt, 1) as eng:
+    # the problems are autonomous: march (0, dt) so the step uses the caller's dt
+    # bit for bit ((t_n + dt) - t_n can differ from dt in the last bits)
+    with ArkEngine(ivp, tab, 0.0, dt, 1) as eng:
         final, _ = eng.run(y_n)
     return final
 

@@ -9,9 +9,15 @@ HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def load():
-    with open(os.path.join(HERE, "cases.json")) as f:
-        cases = json.load(f)
-    arrays = dict(np.load(os.path.join(HERE, "golden.npz")))
+    """Both golden sets: golden.npz (make_golden.py) and golden_paper.npz
+    (make_golden.py --paper: the paper's run and C1 at T = 40)."""
+    cases, arrays = [], {}
+    for cj, npz in (("cases.json", "golden.npz"), ("cases_paper.json", "golden_paper.npz")):
+        if not os.path.exists(os.path.join(HERE, cj)):
+            continue
+        with open(os.path.join(HERE, cj)) as f:
+            cases += json.load(f)
+        arrays.update(dict(np.load(os.path.join(HERE, npz))))
     return cases, arrays
 
 

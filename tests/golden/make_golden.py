@@ -2,7 +2,8 @@
 
 Run in the build container (the only place /root/reference exists):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py           # golden.npz + cases.json
+    python tests/golden/make_golden.py --paper   # golden_paper.npz + cases_paper.json
 
 It imports the reference package read-only (PYTHONPATH=/root/reference/pkg/src),
 runs ``ridc.engine.run_serial`` / ``run_pipelined`` and single steps under
@@ -236,5 +237,41 @@ def main():
     print("wrote", len(arrays), "arrays")
 
 
+def paper_runs():
+    """The paper's own run (adv-diff c=0.1, d=1e-3,
+    dx=1e-3, T=40, 4000 steps, RIDC4 with 1 and 10 restarts) and C1 at the
+    paper horizon (dx=1/1024, T=40, 1000 steps: r ~ 42), through the
+    reference's own run_serial.  Written to golden_paper.npz / cases_paper.json
+    (kept apart from golden.npz so that re-running one set leaves the other
+    untouched)."""
+    arrays = {}
+    cases = []
+    with threadpool_limits(1):
+        for (name, dx, t_end, levels, steps, restarts) in [
+            ("paper_p4_r1", 1e-3, 40.0, 4, 4000, 1),
+            ("paper_p4_r10", 1e-3, 40.0, 4, 4000, 10),
+            ("ad_c1_T40_p1", 1 / 1024, 40.0, 1, 1000, 1),
+            ("ad_c1_T40_p4", 1 / 1024, 40.0, 4, 1000, 1),
+        ]:
+            spec = RP.AdvectionDiffusionSpec(dx=dx, t_end=t_end)
+            sysr = RP.build_advection_diffusion(spec)
+            ours = P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=dx, t_end=t_end))
+            sol = R.run_serial(sysr.ivp, R.RidcConfig(levels=levels, steps=steps, restarts=restarts))
+            arrays[f"{name}/y0"] = np.asarray(sysr.ivp.initial_state)
+            arrays[f"{name}/final"] = sol.final_state
+            arrays[f"{name}/level_finals"] = np.array(sol.level_finals)
+            cases.append({"name": name, "problem": desc_dict(ours.problem), "t_end": t_end, "levels": levels,
+                          "steps": steps, "restarts": restarts, "trajectory": False, "workers": 1,
+                          "ref_wall_seconds": sol.wall_seconds})
+            print(f"{name}: wall {sol.wall_seconds:.2f}s  |final|={np.abs(sol.final_state).max():.6g}", flush=True)
+    np.savez_compressed(os.path.join(HERE, "golden_paper.npz"), **arrays)
+    with open(os.path.join(HERE, "cases_paper.json"), "w") as f:
+        json.dump(cases, f, indent=1)
+    print("wrote", len(arrays), "arrays")
+
+
 if __name__ == "__main__":
-    main()
+    if "--paper" in sys.argv:
+        paper_runs()
+    else:
+        main()

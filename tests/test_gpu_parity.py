@@ -132,15 +132,12 @@ def test_predict_correct_kats(golden):
     assert np.abs(fs1 - arr["kat/predict/fs"]).max() <= 1e-9 * np.abs(arr["kat/predict/fs"]).max()
     assert np.abs(fn1 - arr["kat/predict/fn"]).max() <= 1e-9 * np.abs(arr["kat/predict/fn"]).max()
     w = steady_weights(2, dt)
-    win = E.LevelWindow(arr["kat/correct/window_states"], 0, 1)
+    win = E.LevelWindow.from_states(arr["kat/correct/window_states"], 0, 1)
     ec, _, _ = E.correct_step(2, sysm, 0.0, eta, win, w, dt)
     assert G.normwise(ec, arr["kat/correct/eta_new"]) <= 1e-13
-
-    class RefWindow:  # the reference's LevelWindow(fs, fn, new_index, old_index)
-        fs, fn = arr["kat/correct/fs_win"], arr["kat/correct/fn_win"]
-        new_index, old_index = 0, 1
-
-    ec2, _, _ = E.correct_step(2, sysm, 0.0, eta, RefWindow, w, dt)
+    # the reference's own constructor: LevelWindow(fs, fn, new_index, old_index)
+    ref_win = E.LevelWindow(arr["kat/correct/fs_win"], arr["kat/correct/fn_win"], 0, 1)
+    ec2, _, _ = E.correct_step(2, sysm, 0.0, eta, ref_win, w, dt)
     assert G.normwise(ec2, arr["kat/correct/eta_new"]) <= 1e-13
 
 
@@ -230,3 +227,17 @@ def test_engine_info_and_launch_count():
     with E.Engine(s, E.RidcConfig(levels=4, steps=100, restarts=2)) as eng:
         assert eng.info["kernel_launches"] == 3 * 2   # resident level march: 2 seeds + 1 launch per interval
         assert inf["halo"] > 0 and inf["items_per_level"] >= 8
+
+
+def test_burgers_layer_propagates_right():
+    """SPEC acceptance 10 (PAPER Fig. 5): at eps = 1e-3, desk scale, the steepest
+    descent of u sits strictly further right at t = 1 than at t = 0.2."""
+    s = P.burgers_desk()
+    steps = 1000
+    sol = E.run_serial(s, E.RidcConfig(levels=4, steps=steps, record_trajectory=True))
+    dx = s.problem.h_x
+    def front(u):
+        return int(np.argmin(np.diff(u))) * dx
+    x02 = front(sol.trajectory[steps // 5])
+    x1 = front(sol.trajectory[steps])
+    assert x1 > x02, (x02, x1)

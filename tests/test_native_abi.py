@@ -34,7 +34,7 @@ def test_struct_layout_matches_header():
     from paper_1209_4297_b200.problems import CProblem
     assert ctypes.sizeof(CProblem) == 4 * 4 + 7 * 8
     from paper_1209_4297_b200._lib import RidcInfo
-    assert ctypes.sizeof(RidcInfo) == 4 + 4 + 8 + 8 + 8 + 4 * 4 + 8 + 8 + 8
+    assert ctypes.sizeof(RidcInfo) == 4 + 4 + 8 + 8 + 8 + 4 * 4 + 8 + 8 + 8 + 4 + 4   # ..., path, fell_back
 
 
 def test_create_rejects_bad_config_without_gpu():
