@@ -56,10 +56,11 @@ def _env_int(name, default):
 def workload(name, points=None, nt=None):
     from paper_1209_4297_b200 import problems as P
     if name == "c2":
+        # dt = 1e-4 (r ~ 110 at 2^20 points) whatever Nt: --nt shortens the horizon
         n = points or (1 << 20)
-        sysm = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n))
-        return sysm, nt or 10000, {"workload": "c2-reaction-diffusion-1d", "points": n,
-                                    "nt": nt or 10000, "t_end": 1.0}
+        nt = nt or 10000
+        sysm = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, t_end=1e-4 * nt))
+        return sysm, nt, {"workload": "c2-reaction-diffusion-1d", "points": n, "nt": nt, "t_end": 1e-4 * nt}
     if name == "c1":
         sysm = P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 1024, t_end=4.0))
         return sysm, nt or 1000, {"workload": "c1-adv-diff-1d", "points": 1024, "nt": nt or 1000}
@@ -408,7 +409,7 @@ def run_ours(args):
         launches_per_step = info["kernel_launches"]
         # resident FEBE: seed + one march; resident level march: 2 seeds + one march
         # per interval; else the tick graph: seed + one launch per tick
-        tick_launches = 1 if path != 0 else launches_per_step - 1
+        tick_launches = 1 if path != 0 else launches_per_step - 1   # resident paths: one march launch
         lev_bytes = sum(bytes_per_point(j) for j in range(order)) * nt / max(tick_launches, 1)
     from paper_1209_4297_b200._lib import PATH_NAMES
     path_name = PATH_NAMES.get(path, "?")
@@ -437,6 +438,8 @@ def run_ours(args):
                             "over NVLink)") if world > 1 else
                            ("k_resident_levels (all levels on this GPU in one launch: a co-resident CTA group "
                             "per level, registers-resident chunks, TMA-staged windows, per-segment flags)"),
+        "carry_febe": "k_febe_carry (whole FEBE march in one launch: one tile per SM in registers, rhs + "
+                      "factored tridiagonal solve per step, tiles coupled by two tagged carries per step through L2)",
         "tick": "k_tick_chunk (fused level-step: stencils + factored tridiagonal solve)",
     }
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

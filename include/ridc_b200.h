@@ -95,7 +95,8 @@ typedef struct ridc_info {
     double lambda;                /* decay factor of the shifted operator's factors */
     double r;                     /* stiffness dt*d_x/h_x^2 */
     int32_t path;                 /* marching path in effect (after the last run):
-                                     RIDC_PATH_TICK / _RESIDENT_FEBE / _RESIDENT_LEVELS */
+                                     RIDC_PATH_TICK / _RESIDENT_FEBE / _RESIDENT_LEVELS /
+                                     _CARRY_FEBE */
     int32_t fell_back;            /* 1: a resident march could not get its co-resident
                                      SMs at run time and the tick graph replaced it */
 } ridc_info;
@@ -103,6 +104,8 @@ typedef struct ridc_info {
 #define RIDC_PATH_TICK 0             /* one fused tick kernel per pipeline tick (CUDA graph) */
 #define RIDC_PATH_RESIDENT_FEBE 1    /* one cooperative launch marches every FEBE step */
 #define RIDC_PATH_RESIDENT_LEVELS 2  /* one cooperative launch per interval, all levels */
+#define RIDC_PATH_CARRY_FEBE 3       /* one cooperative launch marches every FEBE step, tiles
+                                        exchange two carries per step (periodic RD lines) */
 
 /*
  * Create a run context (RidcConfig validation engine.py:71-87, _prepare

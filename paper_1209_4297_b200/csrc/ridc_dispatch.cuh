@@ -186,4 +186,23 @@ cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, c
 #undef RIDC_LEV_NT
 }
 
+// ---- carry-exchange FEBE march (ridc_febe_carry.cuh): nt threads (multiple of 32)
+template <int KIND>
+cudaError_t febe_carry_k(bool launch, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm)
+{
+    auto kfn = k_febe_carry<KIND>;
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, nt, 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // all tiles co-resident (neighbour carry waits)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, cp);
+}
+
 }  // namespace ridc

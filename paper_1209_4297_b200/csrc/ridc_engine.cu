@@ -555,6 +555,11 @@ struct ridc_ctx {
     TmapSet tm_in;
     LevelsParams lp;
     unsigned long long lepoch = 0;
+    // carry-exchange FEBE march (ridc_febe_carry.cuh): periodic RD lines, one tile per SM
+    bool carry = false;
+    int carry_nt = 0;
+    CarryParams cparams;
+    uint4* d_cmail = nullptr;
     bool fell_back = false;        // a resident march was replaced by the tick graph at run time
     double watchdog = 30.0;        // seconds per in-kernel neighbour wait (ridc_set_watchdog)
     std::string err;
@@ -822,7 +827,12 @@ int march(ridc_ctx* c, double* wall_seconds)
             CUDA_TRY(&c->err, cudaMemsetAsync(c->d_mail, 0, 2 * (size_t)c->Vs * sizeof(uint4), c->stream));
             c->tag_next = 1;
         }
+        if (c->carry && (unsigned long long)c->tag_next + c->steps + 2 >= 0xffffffffull) {
+            CUDA_TRY(&c->err, cudaMemsetAsync(c->d_cmail, 0, (size_t)4 * c->cparams.nseg * sizeof(uint4), c->stream));
+            c->tag_next = 1;
+        }
         c->rp.tag0 = c->tag_next;
+        c->cparams.tag0 = c->tag_next;
         c->tag_next += (unsigned)c->steps + 1;
         CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, sizeof(unsigned), c->stream));
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
@@ -830,13 +840,16 @@ int march(ridc_ctx* c, double* wall_seconds)
         const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
         k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
         CUDA_TRY(&c->err, cudaGetLastError());
-        const cudaError_t le = resident_dispatch(c->pb.kind, c->ss.ccfg.nt, c->res_mode, true, nseg, c->stream,
-                                                 c->rp, nullptr);
+        const cudaError_t le =
+            c->carry ? febe_carry_k<RD_1D>(true, c->cparams.nseg, c->carry_nt, c->stream, c->cparams, nullptr)
+                     : resident_dispatch(c->pb.kind, c->ss.ccfg.nt, c->res_mode, true, nseg, c->stream, c->rp,
+                                         nullptr);
         if (le == cudaErrorCooperativeLaunchTooLarge) {
             // the SMs are shared with other work right now: fall back (for good) to
             // the tick kernel's graph, which needs no co-residency
             cudaGetLastError();
             c->resident = false;
+            c->carry = false;
             c->fell_back = true;
             int rc = capture_graph(c);
             if (rc) return rc;
@@ -863,6 +876,77 @@ int march(ridc_ctx* c, double* wall_seconds)
     return check_err_word(c);
 }
 
+// Carry-exchange FEBE march (ridc_febe_carry.cuh): RIDC order 1 on a periodic
+// reaction-diffusion line of a multiple of 16 points, one tile per SM (<= 8192
+// points, >= 2 carry reaches + a warp).  *ok = false: the line does not qualify.
+int setup_carry(ridc_ctx* c, bool* ok)
+{
+    *ok = false;
+    const DevProblem& pb = c->pb;
+    if (pb.kind != RD_1D || pb.ny != 1 || (pb.nx & 15) || c->levels != 1) return RIDC_OK;
+    if (getenv("RIDC_NO_CARRY") && atoi(getenv("RIDC_NO_CARRY")) > 0) return RIDC_OK;
+    const double lam = c->ss.sv.lam;
+    const int hc = halo_of(lam);
+    const int nx = pb.nx;
+    int per_sm = 0;
+    CarryParams cp;
+    memset(&cp, 0, sizeof cp);
+    cudaError_t oe = febe_carry_k<RD_1D>(false, 0, kCarryMaxNT, c->stream, cp, &per_sm);
+    if (oe != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        return RIDC_OK;
+    }
+    // as many tiles as SMs (each tile a multiple of 16 points), fewer if a tile
+    // would be shorter than two carry reaches + one warp of chunks
+    int nseg = 0, T = 0;
+    for (int n = c->nsm; n >= 2; --n) {
+        const int t = 16 * ((nx + 16 * n - 1) / (16 * n));
+        const int ns = (nx + t - 1) / t;
+        const int tlast = nx - (ns - 1) * t;
+        if (t > 16 * kCarryMaxNT) break;                     // longer tiles than a CTA holds
+        if (ns >= 2 && t >= 2 * hc + 512 && tlast >= 2 * hc + 512) { nseg = ns; T = t; break; }
+    }
+    if (nseg < 2) return RIDC_OK;
+    const int nch = T / 16;
+    const int nt = 32 * ((nch + 31) / 32);
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_cmail, (size_t)2 * 2 * nseg * sizeof(uint4)));
+    CUDA_TRY(&c->err, cudaMemset(c->d_cmail, 0, (size_t)2 * 2 * nseg * sizeof(uint4)));
+    if (!c->d_flags) CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, sizeof(unsigned)));
+    cp.pb = pb;
+    cp.lam = lam;
+    const double g = c->ss.sv.g, dt = c->dt;
+    cp.aa = g * (1.0 + dt * pb.rho);   // g (u + dt rho u (1 - u)) = (aa + bb u) u
+    cp.bb = -(g * dt * pb.rho);
+    cp.inv1ml2 = 1.0 / (1.0 - lam * lam);
+    for (int e = 0; e < 16; ++e) {
+        cp.pw[e] = c->ss.sv.pw[e];
+        cp.zf[e] = c->ss.sv.zf16[e];
+    }
+    for (int i = 0; i < 10; ++i) cp.mp[i] = c->ss.sv.mp16[i];
+    cp.ring = c->d_ring[0];
+    cp.cap = c->cap[0];
+    cp.Vs = c->Vs;
+    cp.GW = c->ss.lay.GW;
+    cp.T = T;
+    cp.nx = nx;
+    cp.nseg = nseg;
+    cp.hc = hc;
+    cp.mail = c->d_cmail;
+    cp.steps = c->steps;
+    cp.per = c->per;
+    cp.full_every = (c->flags & RIDC_RECORD_TRAJECTORY) ? 1 : 0;
+    cp.err = c->d_err;
+    cp.abort = c->d_flags;
+    cp.spin_limit = (long long)(c->watchdog * 2.0e9);
+    c->cparams = cp;
+    c->carry = true;
+    c->carry_nt = nt;
+    c->resident = true;   // the resident FEBE path (final state in ring slot steps % cap)
+    c->launches = 2;
+    *ok = true;
+    return RIDC_OK;
+}
+
 // Resident single-level march: RIDC order 1 on a 1-D line whose segments fit
 // one co-resident CTA each, and whose halos reach only the adjacent segments.
 int setup_resident(ridc_ctx* c)
@@ -870,9 +954,14 @@ int setup_resident(ridc_ctx* c)
     const SolveSetup& ss = c->ss;
     const int nseg = ss.sv.nseg;
     const bool one_d = c->pb.kind == ADV_DIFF_1D || c->pb.kind == BURGERS_1D || c->pb.kind == RD_1D;
-    if (c->levels != 1 || !one_d || c->pb.ny != 1 || (c->flags & RIDC_TICK_ONLY) || nseg > c->nsm ||
-        c->traj_stream)
+    if (c->levels != 1 || !one_d || c->pb.ny != 1 || (c->flags & RIDC_TICK_ONLY) || c->traj_stream)
         return RIDC_OK;
+    if (nseg > 1) {   // segmented periodic RD: the carry-exchange march when the line qualifies
+        bool ok = false;
+        int rc = setup_carry(c, &ok);
+        if (rc || ok) return rc;
+    }
+    if (nseg > c->nsm) return RIDC_OK;
     // whole lines: one CTA marches alone, 2x faster than a launch per step;
     // segmented lines: one co-resident CTA per segment exchanging truncation-halo
     // edges through tagged mailbox lines, ~1.3x faster than the tick kernel (C2)
@@ -923,6 +1012,7 @@ int setup_resident(ridc_ctx* c)
     rp.err = c->d_err;
     rp.spin_limit = (long long)(c->watchdog * 2.0e9);   // clock64 cycles (~2 GHz) per neighbour wait
     rp.dbg = c->d_dbg;
+    rp.exp = getenv("RIDC_RES_EXP") ? atoi(getenv("RIDC_RES_EXP")) : 0;   // diagnostics only
     c->resident = true;
     c->launches = 2;
     return RIDC_OK;
@@ -1234,14 +1324,16 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->steps = c->steps;
     info->ticks_per_interval = c->ticks;
     info->kernel_launches = c->launches;
-    info->tile = c->ss.sv.tile;
-    info->halo = c->ss.sv.halo;
-    info->items_per_level = c->pb.ny * c->ss.sv.nseg;
-    info->threads = c->ss.ccfg.nt;
+    info->tile = c->carry ? c->cparams.T : c->ss.sv.tile;
+    info->halo = c->carry ? 0 : c->ss.sv.halo;   // the carry march exchanges carries, not halos
+    info->items_per_level = c->carry ? c->cparams.nseg : c->pb.ny * c->ss.sv.nseg;
+    info->threads = c->carry ? c->carry_nt : c->ss.ccfg.nt;
     info->ring_vectors = c->ring_vectors;
     info->lambda = c->ss.sv.lam;
     info->r = c->ss.r;
-    info->path = c->resident ? RIDC_PATH_RESIDENT_FEBE : (c->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK);
+    info->path = c->carry ? RIDC_PATH_CARRY_FEBE
+                          : c->resident ? RIDC_PATH_RESIDENT_FEBE
+                                        : (c->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK);
     info->fell_back = c->fell_back ? 1 : 0;
     return RIDC_OK;
 }
@@ -1252,6 +1344,7 @@ int ridc_set_watchdog(ridc_ctx* c, double seconds)
     c->watchdog = seconds;
     c->rp.spin_limit = (long long)(seconds * 2.0e9);
     c->lp.spin_limit = (long long)(seconds * 2.0e9);
+    c->cparams.spin_limit = (long long)(seconds * 2.0e9);
     return RIDC_OK;
 }
 
@@ -1271,6 +1364,7 @@ int ridc_destroy(ridc_ctx* c)
     if (c->d_err) cudaFree(c->d_err);
     if (c->d_flags) cudaFree(c->d_flags);
     if (c->d_mail) cudaFree(c->d_mail);
+    if (c->d_cmail) cudaFree(c->d_cmail);
     for (int j = 0; j < kMaxLevels; ++j)
         if (c->d_inbox[j]) cudaFree(c->d_inbox[j]);
     if (c->d_lflags) cudaFree(c->d_lflags);

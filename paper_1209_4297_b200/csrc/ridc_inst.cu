@@ -2,7 +2,7 @@
 // problem kind and ONE kernel family, selected at compile time:
 //   RIDC_INST_KIND  1..5 (ridc::Kind)
 //   RIDC_INST_PART  0: tick kernel + single-op item kernel
-//                   1: resident FEBE march (1-D kinds)
+//                   1: resident FEBE march (1-D kinds; + the carry-exchange march, RD)
 //                   2: resident level march, GPU-scope flags (1-D kinds)
 //                   3: resident level march, system-scope flags (1-D kinds)
 // __graft_entry__.build() compiles this file once per (kind, part) in
@@ -25,6 +25,9 @@ template cudaError_t launch_item_k<RIDC_INST_KIND>(const LaunchCfg&, int, cudaSt
                                                    const DevSolve&, const StepItem&, unsigned long long*);
 #elif RIDC_INST_PART == 1
 template cudaError_t resident_k<RIDC_INST_KIND>(int, int, bool, int, cudaStream_t, const ResidentParams&, int*);
+#if RIDC_INST_KIND == 3
+template cudaError_t febe_carry_k<RIDC_INST_KIND>(bool, int, int, cudaStream_t, const CarryParams&, int*);
+#endif
 #elif RIDC_INST_PART == 2
 template cudaError_t levels_k<RIDC_INST_KIND, false>(int, int, bool, int, cudaStream_t, const LevelsParams&,
                                                      const TmapSet&, int*, bool);

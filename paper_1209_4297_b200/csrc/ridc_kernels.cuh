@@ -12,6 +12,7 @@
 #include "ridc_chunk.cuh"
 #include "ridc_resident.cuh"
 #include "ridc_levels.cuh"
+#include "ridc_febe_carry.cuh"
 
 namespace ridc {
 
@@ -361,6 +362,8 @@ cudaError_t launch_item_k(const LaunchCfg& c, int items, cudaStream_t st, const 
 template <int KIND>
 cudaError_t resident_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const ResidentParams& rp,
                        int* per_sm);
+template <int KIND>
+cudaError_t febe_carry_k(bool launch, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm);
 template <int KIND, bool SYS>
 cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const LevelsParams& lp,
                      const TmapSet& tm, int* per_sm, bool dense);

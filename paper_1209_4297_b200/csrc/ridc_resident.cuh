@@ -46,6 +46,8 @@ struct ResidentParams {
     unsigned* abort;         // watchdog: set when a neighbour wait times out
     long long spin_limit;    // watchdog budget per wait (clock64 cycles)
     long long* dbg;          // optional phase trace (RIDC_PHASE_TIMING): CTA 0, thread 0, steps 1..8
+    int exp;                 // diagnostics only (RIDC_RES_EXP, wrong results): 1 skip the halo waits,
+                             // 2 skip the edge pushes -- isolates the exchange cost from the compute
 };
 
 // slots: steps 1..4 -> rows 0..3, steps S-3..S -> rows 4..7; col 6: globaltimer (ns) at row start
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
 
     for (long long s = 1; s <= rp.steps; ++s) {
         RIDC_RSTAMP(rp, s, 0);
-        if (s > 1 && halo) {
+        if (s > 1 && halo && !(rp.exp & 1)) {
             const unsigned want = rp.tag0 + (unsigned)(s - 1);
             const uint4* box = rp.mail + (size_t)((s - 1) & 1) * rp.Vs + GW + col0;
             const long long t0 = clock64();
@@ -259,7 +261,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_febe(const __grid_constant__
         }
         RIDC_RSTAMP(rp, s, 3);
         // push the edge columns of step s (and their periodic ghost copies)
-        if (pslot >= 0) {
+        if (rp.exp & 2) {
+        } else if (pslot >= 0) {
             // coalesced push: transpose through shared memory, then 32 consecutive lines per store
             double* xb = xpush[pslot];
             if (pub) {
