@@ -205,4 +205,84 @@ cudaError_t febe_carry_k(bool launch, int grid, int nt, cudaStream_t st, const C
     return cudaLaunchKernelEx(&cfg, kfn, cp);
 }
 
+// ---- streaming FEBE sweep (ridc_sweep.cuh): one persistent CTA per SM, PDL
+// between consecutive steps
+template <int KIND, int NT>
+cudaError_t sweep_t(int grid, cudaStream_t st, const SweepParams& sp, const TmapSet& tm, long long off,
+                    long long target)
+{
+    auto kfn = k_sweep_febe<KIND, NT>;
+    const size_t smem = sweep_smem<NT>() + ((sp.exp & 2) ? 100 * 1024 : 0);
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = (sp.exp & 1) ? 0 : 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, sp, tm, off, target);
+}
+
+// ---- 2-D streaming FEBE sweep (ridc_sweep2d.cuh): nx = 16 NT, 512 / NT CTAs per SM
+template <int KIND, int NT>
+cudaError_t sweep2d_t(int grid, cudaStream_t st, const Sweep2DParams& sp, const TmapSet& tm, long long off,
+                      long long target)
+{
+    auto kfn = k_sweep2d_febe<KIND, NT>;
+    const size_t smem = sweep2d_smem<NT>();
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, sp, tm, off, target);
+}
+
+template <int KIND>
+cudaError_t sweep2d_k(int nt, int grid, cudaStream_t st, const Sweep2DParams& sp, const TmapSet& tm, long long off,
+                      long long target)
+{
+    switch (nt) {
+    case 128: return sweep2d_t<KIND, 128>(grid, st, sp, tm, off, target);
+    case 256: return sweep2d_t<KIND, 256>(grid, st, sp, tm, off, target);
+    case 512: return sweep2d_t<KIND, 512>(grid, st, sp, tm, off, target);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// nt = 512 (one CTA per SM) or 256 (two CTAs per SM); grid = CTAs
+template <int KIND>
+cudaError_t sweep_k(int nt, int grid, cudaStream_t st, const SweepParams& sp, const TmapSet& tm, long long off,
+                    long long target)
+{
+    return nt == 256 ? sweep_t<KIND, 256>(grid, st, sp, tm, off, target)
+                     : sweep_t<KIND, 512>(grid, st, sp, tm, off, target);
+}
+
 }  // namespace ridc

@@ -560,6 +560,15 @@ struct ridc_ctx {
     int carry_nt = 0;
     CarryParams cparams;
     uint4* d_cmail = nullptr;
+    // streaming FEBE sweep (ridc_sweep.cuh): long periodic RD lines, one launch per step
+    bool sweep = false;
+    int sweep_nt = 256;
+    SweepParams sparams;
+    TmapSet tm_sweep;
+    // 2-D streaming FEBE sweep (ridc_sweep2d.cuh): every row read once per step
+    bool sweep2d = false;
+    int sweep2d_nt = 256;
+    Sweep2DParams s2params;
     bool fell_back = false;        // a resident march was replaced by the tick graph at run time
     double watchdog = 30.0;        // seconds per in-kernel neighbour wait (ridc_set_watchdog)
     std::string err;
@@ -710,10 +719,19 @@ int capture_graph(ridc_ctx* c)
             const bool top_active = ttop >= 1 && ttop <= c->per;
             if (top_active) slot_free((long long)r * c->per + ttop);
             if (le != cudaSuccess) break;
-            le = launch_chunk(c->pb.kind, c->ss.ccfg,
-                              std::min(c->nsm * chunk_ctas_per_sm(c->ss.ccfg, tp.nact), tp.nact * items),
-                              c->stream, ep, tp,
-                              items, c->tm);
+            if (c->sweep2d)   // 2-D FEBE: every CTA sweeps its row block, each row read once
+                le = c->pb.kind == ADV_DIFF_2D
+                         ? sweep2d_k<ADV_DIFF_2D>(c->sweep2d_nt, c->nsm * (512 / c->sweep2d_nt), c->stream,
+                                                  c->s2params, c->tm_sweep, ep.off[0], tp.target[0])
+                         : sweep2d_k<RD_2D>(c->sweep2d_nt, c->nsm * (512 / c->sweep2d_nt), c->stream, c->s2params,
+                                            c->tm_sweep, ep.off[0], tp.target[0]);
+            else if (c->sweep)   // FEBE on a long periodic line: every SM sweeps its range
+                le = sweep_k<RD_1D>(c->sweep_nt, c->nsm * (512 / c->sweep_nt), c->stream, c->sparams, c->tm_sweep,
+                                    ep.off[0], tp.target[0]);
+            else
+                le = launch_chunk(c->pb.kind, c->ss.ccfg,
+                                  std::min(c->nsm * chunk_ctas_per_sm(c->ss.ccfg, tp.nact), tp.nact * items),
+                                  c->stream, ep, tp, items, c->tm);
             ++launches;
             if (top_active)
                 drain((long long)r * c->per + ttop,
@@ -944,6 +962,109 @@ int setup_carry(ridc_ctx* c, bool* ok)
     c->resident = true;   // the resident FEBE path (final state in ring slot steps % cap)
     c->launches = 2;
     *ok = true;
+    return RIDC_OK;
+}
+
+// Streaming FEBE sweep (ridc_sweep.cuh): RIDC order 1 on a periodic
+// reaction-diffusion line too long to stay resident, a multiple of 16 points,
+// at least 1024 points per SM, carry reach <= 512.  Runs inside the captured
+// graph (one launch per step) in place of the tick kernel.
+int setup_sweep(ridc_ctx* c)
+{
+    const DevProblem& pb = c->pb;
+    if (c->resident || c->levels != 1 || pb.kind != RD_1D || pb.ny != 1 || (pb.nx & 15) ||
+        (c->flags & RIDC_TICK_ONLY) || c->ss.sv.nseg < 2)
+        return RIDC_OK;
+    if (getenv("RIDC_NO_SWEEP") && atoi(getenv("RIDC_NO_SWEEP")) > 0) return RIDC_OK;
+    const double lam = c->ss.sv.lam;
+    const int hc = halo_of(lam);
+    c->sweep_nt = env_int("RIDC_SWEEP_NT", 512) == 256 ? 256 : 512;
+    if (hc > 512 || pb.nx < 1024 * c->nsm * (512 / c->sweep_nt)) return RIDC_OK;
+    SweepParams& sp = c->sparams;
+    memset(&sp, 0, sizeof sp);
+    sp.pb = pb;
+    sp.lam = lam;
+    const double g = c->ss.sv.g, dt = c->dt;
+    sp.aa = g * (1.0 + dt * pb.rho);   // g (u + dt rho u (1 - u)) = (aa + bb u) u
+    sp.bb = -(g * dt * pb.rho);
+    for (int e = 0; e < 16; ++e) {
+        sp.pw[e] = c->ss.sv.pw[e];
+        sp.zf[e] = c->ss.sv.zf16[e];
+    }
+    for (int i = 0; i < 10; ++i) sp.mp[i] = c->ss.sv.mp16[i];
+    sp.ring = c->d_ring[0];
+    sp.cap = c->cap[0];
+    sp.Vs = c->Vs;
+    sp.GW = c->ss.lay.GW;
+    sp.gpr = c->ss.lay.gpr;
+    sp.gdata = c->ss.lay.gdata;
+    sp.nx = pb.nx;
+    sp.hc = hc;
+    sp.per = c->per;
+    sp.err = c->d_err;
+    sp.exp = getenv("RIDC_SWEEP_EXP") ? atoi(getenv("RIDC_SWEEP_EXP")) : 0;
+    memset(&c->tm_sweep, 0, sizeof c->tm_sweep);
+    int rc = make_ring_map(&c->tm_sweep.map[0], c->d_ring[0], c->Vs, c->cap[0], c->sweep_nt, &c->err);
+    if (rc) return rc;
+    c->sweep = true;
+    return RIDC_OK;
+}
+
+// 2-D streaming FEBE sweep (ridc_sweep2d.cuh): RIDC order 1 on the periodic
+// 2-D kinds with x-lines of 16 NT points (NT = 128 / 256 / 512: 2048 / 4096 /
+// 8192 columns) and at least two rows per CTA.
+int setup_sweep2d(ridc_ctx* c)
+{
+    const DevProblem& pb = c->pb;
+    if (c->levels != 1 || !(pb.kind == ADV_DIFF_2D || pb.kind == RD_2D) || (c->flags & RIDC_TICK_ONLY)) return RIDC_OK;
+    if (getenv("RIDC_NO_SWEEP") && atoi(getenv("RIDC_NO_SWEEP")) > 0) return RIDC_OK;
+    int nt = 0;
+    for (int t : {128, 256, 512})
+        if (pb.nx == 16 * t) nt = t;
+    if (!nt || pb.ny < 2 * c->nsm * (512 / nt)) return RIDC_OK;
+    // the tiling of the engine solves the same shifted operator: take its factors
+    SolveSetup fs;
+    make_factors(pb, c->dt, fs);
+    const double lam = fs.sv.lam, g = fs.sv.g, dt = c->dt;
+    Sweep2DParams& sp = c->s2params;
+    memset(&sp, 0, sizeof sp);
+    sp.pb = pb;
+    sp.lam = lam;
+    if (pb.kind == RD_2D) {   // (1 + dt rho - 2 dt cdy) w - dt rho w^2, neighbours dt cdy
+        sp.c0 = g * (1.0 + dt * pb.rho - 2.0 * dt * pb.cdy);
+        sp.c1 = -(g * dt * pb.rho);
+        sp.cs = g * dt * pb.cdy;
+        sp.cn = g * dt * pb.cdy;
+    } else {                  // upwind x / y advection + y-diffusion (eval_point, ridc_device.cuh)
+        sp.c0 = g * (1.0 - dt * pb.cax - dt * pb.cay - 2.0 * dt * pb.cdy);
+        sp.c1 = g * dt * pb.cax;
+        sp.cs = g * dt * (pb.cay + pb.cdy);
+        sp.cn = g * dt * pb.cdy;
+    }
+    double lS = 1.0;   // lam^nx
+    for (int i = 0; i < pb.nx; ++i) lS *= lam;
+    sp.cyc = 1.0 / (1.0 - lS);
+    for (int e = 0; e < 16; ++e) {
+        sp.pw[e] = fs.sv.pw[e];
+        sp.zf[e] = fs.sv.zf16[e];
+    }
+    for (int i = 0; i < 10; ++i) sp.mp[i] = fs.sv.mp16[i];
+    sp.ring = c->d_ring[0];
+    sp.cap = c->cap[0];
+    sp.Vs = c->Vs;
+    sp.P = c->ss.lay.P;
+    sp.GW = c->ss.lay.GW;
+    sp.gpr = c->ss.lay.gpr;
+    sp.gdata = c->ss.lay.gdata;
+    sp.nx = pb.nx;
+    sp.ny = pb.ny;
+    sp.per = c->per;
+    sp.err = c->d_err;
+    memset(&c->tm_sweep, 0, sizeof c->tm_sweep);
+    int rc = make_ring_map(&c->tm_sweep.map[0], c->d_ring[0], c->Vs, c->cap[0], nt, &c->err);
+    if (rc) return rc;
+    c->sweep2d_nt = nt;
+    c->sweep2d = true;
     return RIDC_OK;
 }
 
@@ -1272,6 +1393,8 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     ep.cgeo = c->d_cgeo;
     if ((rc = setup_resident(c)) != RIDC_OK) return bail(rc);
     if (!c->resident && (rc = setup_reslev(c)) != RIDC_OK) return bail(rc);
+    if ((rc = setup_sweep(c)) != RIDC_OK) return bail(rc);
+    if ((rc = setup_sweep2d(c)) != RIDC_OK) return bail(rc);
     if (!c->resident && !c->reslev && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
 #undef CTX_TRY
     *out = c;
@@ -1332,6 +1455,8 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->lambda = c->ss.sv.lam;
     info->r = c->ss.r;
     info->path = c->carry ? RIDC_PATH_CARRY_FEBE
+                 : (c->sweep && !c->resident) ? RIDC_PATH_SWEEP_FEBE
+                 : c->sweep2d ? RIDC_PATH_SWEEP2D_FEBE
                           : c->resident ? RIDC_PATH_RESIDENT_FEBE
                                         : (c->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK);
     info->fell_back = c->fell_back ? 1 : 0;

@@ -128,6 +128,16 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
             if ((31 - lane) & (1 << i)) mr *= cp.mp[i];
         }
     }
+    // lane-masked scan multipliers: a lane outside a shuffle step's reach gets 0,
+    // so every scan step is one unpredicated FMA (no selects)
+    double mf[5], mb[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        mf[i] = lane >= (1 << i) ? cp.mp[i] : 0.0;
+        mb[i] = lane + (1 << i) < 32 ? cp.mp[i] : 0.0;
+    }
+    double* const fin = cp.ring + cp.GW + c0 + i0;   // + slot * Vs
+    long long slot = 0;                              // ring slot of step s (s % cap, kept incrementally)
 
     double u[K];
     if (mine) {
@@ -153,19 +163,16 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
         // ---- forward carries (chunk multiplier M = lam^16, as fast_solve)
         double inc = bf;
 #pragma unroll
-        for (int i = 0; i < 5; ++i) {
-            const double t = __shfl_up_sync(FULL, inc, 1 << i);
-            if (lane >= (1 << i)) inc = fma(cp.mp[i], t, inc);
-        }
+        for (int i = 0; i < 5; ++i) inc = fma(mf[i], __shfl_up_sync(FULL, inc, 1 << i), inc);
         if (lane == 31) sx[warp] = inc;
         double ex = __shfl_up_sync(FULL, inc, 1);
         if (lane == 0) ex = 0.0;
         csync_n(NT);
         double wi = lane < NW ? sx[lane] : 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 4; ++i) {   // lanes < NW: warp totals (lanes >= NW carry zeros or ignored sums)
             const double t = __shfl_up_sync(FULL, wi, 1 << i);
-            if (lane >= (1 << i) && (1 << i) < NW) wi = fma(cp.mp[5 + i], t, wi);
+            if (lane >= (1 << i)) wi = fma(cp.mp[5 + i], t, wi);
         }
         double cw = __shfl_sync(FULL, wi, warp > 0 ? warp - 1 : 0);
         if (warp == 0) cw = 0.0;
@@ -181,10 +188,7 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
         }
         double rinc = mine ? fma(cf, cp.zf[0], x) : 0.0;
 #pragma unroll
-        for (int i = 0; i < 5; ++i) {
-            const double t = __shfl_down_sync(FULL, rinc, 1 << i);
-            if (lane + (1 << i) < 32) rinc = fma(cp.mp[i], t, rinc);
-        }
+        for (int i = 0; i < 5; ++i) rinc = fma(mb[i], __shfl_down_sync(FULL, rinc, 1 << i), rinc);
         if (lane == 0) sx[NW + warp] = rinc;
         double exr = __shfl_down_sync(FULL, rinc, 1);
         if (lane == 31) exr = 0.0;
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const double t = __shfl_up_sync(FULL, wr, 1 << i);
-            if (lane >= (1 << i) && (1 << i) < NW) wr = fma(cp.mp[5 + i], t, wr);
+            if (lane >= (1 << i)) wr = fma(cp.mp[5 + i], t, wr);
         }
         const int rl = NW - 1 - warp;
         double dw = __shfl_sync(FULL, wr, rl > 0 ? rl - 1 : 0);
@@ -230,12 +234,18 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
             for (int e = 0; e < K; ++e) u[e] = 0.0;
         } else {
             if (!chunk_finite(u)) atomicMin(cp.err, err_code((s - 1) % cp.per + 1, 0));
-            if (s == cp.steps || cp.full_every) {
-                double* out = cp.ring + (s % cp.cap) * cp.Vs + cp.GW + c0 + i0;
+            if (cp.full_every) {   // trajectory: every step to its slot (cap = steps + 1)
+                slot = slot + 1 == cp.cap ? 0 : slot + 1;
+                double* out = fin + slot * cp.Vs;
 #pragma unroll
                 for (int e = 0; e < K; e += 2) *reinterpret_cast<double2*>(out + e) = make_double2(u[e], u[e + 1]);
             }
         }
+    }
+    if (mine && !cp.full_every) {   // the final state to ring slot steps % cap
+        double* out = fin + (cp.steps % cp.cap) * cp.Vs;
+#pragma unroll
+        for (int e = 0; e < K; e += 2) *reinterpret_cast<double2*>(out + e) = make_double2(u[e], u[e + 1]);
     }
 }
 

@@ -19,6 +19,10 @@
 namespace ridc {
 
 #if RIDC_INST_PART == 0
+#if RIDC_INST_KIND >= 4
+template cudaError_t sweep2d_k<RIDC_INST_KIND>(int, int, cudaStream_t, const Sweep2DParams&, const TmapSet&,
+                                               long long, long long);
+#endif
 template cudaError_t launch_chunk_k<RIDC_INST_KIND>(const ChunkCfg&, int, cudaStream_t, const EngineParams&,
                                                     const TickParams&, int, const TmapSet&);
 template cudaError_t launch_item_k<RIDC_INST_KIND>(const LaunchCfg&, int, cudaStream_t, const DevProblem&,
@@ -27,6 +31,8 @@ template cudaError_t launch_item_k<RIDC_INST_KIND>(const LaunchCfg&, int, cudaSt
 template cudaError_t resident_k<RIDC_INST_KIND>(int, int, bool, int, cudaStream_t, const ResidentParams&, int*);
 #if RIDC_INST_KIND == 3
 template cudaError_t febe_carry_k<RIDC_INST_KIND>(bool, int, int, cudaStream_t, const CarryParams&, int*);
+template cudaError_t sweep_k<RIDC_INST_KIND>(int, int, cudaStream_t, const SweepParams&, const TmapSet&, long long,
+                                             long long);
 #endif
 #elif RIDC_INST_PART == 2
 template cudaError_t levels_k<RIDC_INST_KIND, false>(int, int, bool, int, cudaStream_t, const LevelsParams&,

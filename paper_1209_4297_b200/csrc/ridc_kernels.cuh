@@ -13,6 +13,8 @@
 #include "ridc_resident.cuh"
 #include "ridc_levels.cuh"
 #include "ridc_febe_carry.cuh"
+#include "ridc_sweep.cuh"
+#include "ridc_sweep2d.cuh"
 
 namespace ridc {
 
@@ -364,6 +366,12 @@ cudaError_t resident_k(int nt, int mode, bool launch, int grid, cudaStream_t st,
                        int* per_sm);
 template <int KIND>
 cudaError_t febe_carry_k(bool launch, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm);
+template <int KIND>
+cudaError_t sweep_k(int nt, int grid, cudaStream_t st, const SweepParams& sp, const TmapSet& tm, long long off,
+                    long long target);
+template <int KIND>
+cudaError_t sweep2d_k(int nt, int grid, cudaStream_t st, const Sweep2DParams& sp, const TmapSet& tm, long long off,
+                      long long target);
 template <int KIND, bool SYS>
 cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const LevelsParams& lp,
                      const TmapSet& tm, int* per_sm, bool dense);

@@ -38,9 +38,12 @@
 
 namespace ridc {
 
-constexpr int kSweepNT = 512;
 constexpr int kSweepStages = 3;
-constexpr int kSweepChunk = kSweepNT * 16;   // points per chunk
+constexpr int kSweepPend = 34;   // tail threads of a chunk: hc / 16 + 1 <= 33 (hc <= 512)
+// NT = 512: one CTA per SM, 8192-point chunks; NT = 256: two CTAs per SM,
+// 4096-point chunks (one CTA's dependent scan chain overlaps the other's)
+template <int NT>
+constexpr size_t sweep_smem() { return (size_t)kSweepStages * NT * 16 * sizeof(double) + 2 * kSweepStages * 8 + 1024; }
 
 struct SweepParams {
     DevProblem pb;
@@ -56,6 +59,7 @@ struct SweepParams {
     int hc;                    // carry reach (<= 512)
     long long per;             // error-step numbering
     unsigned long long* err;
+    int exp;                   // diagnostics (RIDC_SWEEP_EXP): 1 no PDL, 2 one CTA per SM, 4 late refill
 };
 
 __device__ __forceinline__ void stg256(double* p, double a, double b, double c, double d)
@@ -99,13 +103,13 @@ __device__ __forceinline__ void load16_wrap(const double* row, int c0, int nx, d
     }
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(kSweepNT, 1)
+template <int KIND, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
     k_sweep_febe(const __grid_constant__ SweepParams sp, const __grid_constant__ TmapSet tm, long long off,
                  long long target)
 {
     static_assert(KIND == RD_1D, "streaming FEBE sweep: periodic reaction-diffusion lines");
-    constexpr int NT = kSweepNT, K = 16, C = kSweepChunk, NW = NT / 32, NS = kSweepStages;
+    constexpr int K = 16, C = NT * K, NW = NT / 32, NS = kSweepStages;
     using L = ChunkSmem<NT, 1, NS, 16>;
     extern __shared__ __align__(1024) char smraw[];
     char* stage = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -113,6 +117,10 @@ __global__ void __launch_bounds__(kSweepNT, 1)
     uint64_t* empty = full + NS;
     __shared__ double sx[2 * NW];
     __shared__ double s_bc[2];   // broadcasts: [0] forward carry into the next chunk, [1] x at its first point
+    // tail threads park their chunk here one iteration (transposed: [e][slot], conflict-free)
+    __shared__ double s_pend[16 * kSweepPend];
+    // the 512 points after my range (the epilogue's truncated passes), prefetched by warp 0
+    __shared__ double s_next[512];
     const unsigned FULL = 0xffffffffu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -147,9 +155,10 @@ __global__ void __launch_bounds__(kSweepNT, 1)
     __syncthreads();
     auto issue = [&](int i) {   // thread 0: chunk i of my range into stage i % NS
         const int s = i % NS;
-        mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * L::BR * 128));
+        constexpr int NBOX = NT / L::BR;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(NBOX * L::BR * 128));
         const int g0 = sp.gdata + (R0 + i * Cr) / 16;
-        for (int b = 0; b < 2; ++b)
+        for (int b = 0; b < NBOX; ++b)
             tma_load_3d(stage + (size_t)s * L::STAGE + b * L::BR * 128, &tm.map[0], 0, g0 + b * L::BR, (int)src,
                         &full[s]);
     };
@@ -167,16 +176,30 @@ __global__ void __launch_bounds__(kSweepNT, 1)
         for (int e = 0; e < K; ++e) y = fma(lam, y, sweep_rhs(sp, u[e]));
         y = warp_fwd_incl(sp, y, lane);
         if (lane == 31) s_bc[0] = y;
+        // and the 512 points after my range, for the range-end pass
+        load16_wrap(usrc, R1 + 16 * lane, nx, u);
+#pragma unroll
+        for (int e = 0; e < K; ++e) s_next[16 * lane + e] = u[e];
     }
     __syncthreads();
     double cin = s_bc[0];   // forward carry into the current chunk (all threads)
 
     // tail threads (last hc points of a chunk) keep their chunk's block-local x one
     // iteration longer, until the next chunk's first x (the backward carry) is known
-    double pend[K];
-    int pend_col = -1;      // data column of pend[0], -1: nothing pending
-    double pend_m = 0.0;    // lam^(chunk end - my last point - 1) * lam = M^q (times pw[15-e])
     bool bad = false;
+    int pend_col = -1;      // data column of my parked chunk, -1: nothing pending
+    int pend_slot = 0;      // its s_pend slot
+    double pend_m = 0.0;    // M^q, q = chunks after mine in that chunk (times pw[15-e]: lam^(end - point))
+    auto pend_flush = [&](double d) {   // apply the backward carry d, check, store
+        const double dm = d * pend_m;
+        double w[K];
+#pragma unroll
+        for (int e = 0; e < K; ++e) w[e] = fma(dm, sp.pw[K - 1 - e], s_pend[e * kSweepPend + pend_slot]);
+        bad |= !chunk_finite(w);
+#pragma unroll
+        for (int e = 0; e < K; e += 4) stg256(udst + pend_col + e, w[e], w[e + 1], w[e + 2], w[e + 3]);
+        pend_col = -1;
+    };
 
     for (int i = 0; i < nch; ++i) {
         const int s = i % NS;
@@ -194,18 +217,21 @@ __global__ void __launch_bounds__(kSweepNT, 1)
             v[2 * q] = w.x;
             v[2 * q + 1] = w.y;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (tid == 0 && i + NS < nch) {
-            mbar_wait(&empty[s], (uint32_t)((i / NS) & 1));
-            issue(i + NS);
-        }
-        // ---- forward: rhs, local recurrence, block scan with the chunk's carry-in
+        // ---- forward: rhs, local recurrence (this consumes every loaded value:
+        // the stage is released only after the shared loads have returned --
+        // mbarrier.arrive does not wait for a warp's outstanding LDS), then
+        // the block scan with the chunk's carry-in
         double y = 0.0;
 #pragma unroll
         for (int e = 0; e < K; ++e) {
             y = fma(lam, y, sweep_rhs(sp, v[e]));
             v[e] = y;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (tid == 0 && i + NS < nch && !(sp.exp & 4)) {
+            mbar_wait(&empty[s], (uint32_t)((i / NS) & 1));
+            issue(i + NS);
         }
         const double bf = mine ? y : 0.0;
         double inc = warp_fwd_incl(sp, bf, lane);
@@ -213,6 +239,10 @@ __global__ void __launch_bounds__(kSweepNT, 1)
         double ex = __shfl_up_sync(FULL, inc, 1);
         if (lane == 0) ex = 0.0;
         __syncthreads();
+        if (tid == 0 && i + NS < nch && (sp.exp & 4)) {
+            mbar_wait(&empty[s], (uint32_t)((i / NS) & 1));
+            issue(i + NS);
+        }
         double wi = lane < NW ? sx[lane] : 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -258,24 +288,14 @@ __global__ void __launch_bounds__(kSweepNT, 1)
         if (tid == 0) s_bc[1] = v[0];
         __syncthreads();
         const double dprev = s_bc[1];
-        if (pend_col >= 0) {
-            const double dm = dprev * pend_m;
-#pragma unroll
-            for (int e = 0; e < K; ++e) pend[e] = fma(dm, sp.pw[K - 1 - e], pend[e]);
-            double chk = 0.0;
-#pragma unroll
-            for (int e = 0; e < K; ++e) chk = fma(pend[e], 0.0, chk);
-            bad |= chk != chk;
-#pragma unroll
-            for (int e = 0; e < K; e += 4) stg256(udst + pend_col + e, pend[e], pend[e + 1], pend[e + 2], pend[e + 3]);
-            pend_col = -1;
-        }
+        if (pend_col >= 0) pend_flush(dprev);
         // ---- store my points, or keep them pending when the next carry reaches them
         if (mine) {
             const int col = cbase + tid * K;
             if (K * (tid + 1) > len - sp.hc) {
+                pend_slot = tid - max(0, (len - sp.hc) / K);
 #pragma unroll
-                for (int e = 0; e < K; ++e) pend[e] = v[e];
+                for (int e = 0; e < K; ++e) s_pend[e * kSweepPend + pend_slot] = v[e];
                 pend_col = col;
                 pend_m = 1.0;   // M^(nthr - 1 - tid)
                 const int q = nthr - 1 - tid;
@@ -289,12 +309,14 @@ __global__ void __launch_bounds__(kSweepNT, 1)
             }
         }
     }
+    __syncthreads();   // every warp has read the last iteration's broadcasts before s_bc is reused
     // ---- range end: the backward carry at R1 (warp 0: the 512 points after it,
     // forward from this range's last y, then backward from zero), for the
     // pending tail of the last chunk
     if (warp == 0) {
         double u[K];
-        load16_wrap(usrc, R1 + 16 * lane, nx, u);
+#pragma unroll
+        for (int e = 0; e < K; ++e) u[e] = s_next[16 * lane + e];
         double y = 0.0;
 #pragma unroll
         for (int e = 0; e < K; ++e) {
@@ -316,14 +338,7 @@ __global__ void __launch_bounds__(kSweepNT, 1)
         if (lane == 0) s_bc[1] = xb;
     }
     __syncthreads();
-    if (pend_col >= 0) {
-        const double dm = s_bc[1] * pend_m;
-#pragma unroll
-        for (int e = 0; e < K; ++e) pend[e] = fma(dm, sp.pw[K - 1 - e], pend[e]);
-        bad |= !chunk_finite(pend);
-#pragma unroll
-        for (int e = 0; e < K; e += 4) stg256(udst + pend_col + e, pend[e], pend[e + 1], pend[e + 2], pend[e + 3]);
-    }
+    if (pend_col >= 0) pend_flush(s_bc[1]);
     if (bad) atomicMin(sp.err, err_code((target - 1) % sp.per + 1, 0));
 }
 

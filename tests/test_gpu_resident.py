@@ -101,3 +101,33 @@ def test_resident_device_run_and_wall():
         host = eng.run().final_state
     assert t > 0
     assert np.array_equal(out.cpu().numpy(), host)
+
+
+SWEEP_CASES = [
+    # (id, n, steps, restarts, trajectory): r ~ 110 as C2 (carry reach 438 < 512)
+    ("2^21", 1 << 21, 30, 1, False),
+    ("2^21-restarts-traj", 1 << 21, 24, 3, True),
+    ("uneven-ranges", (1 << 21) + 16 * 1235, 20, 1, False),
+    ("2^23", 1 << 23, 12, 1, False),
+]
+
+
+@pytest.mark.parametrize("name,n,steps,restarts,traj", SWEEP_CASES, ids=[c[0] for c in SWEEP_CASES])
+def test_sweep_febe_long_lines(name, n, steps, restarts, traj):
+    """Lines too long to stay resident: the streaming sweep (one launch per step,
+    every SM sweeps a contiguous range, csrc/ridc_sweep.cuh) against the tick
+    kernel (<= 1e-13: same solve, different association) and the oracle."""
+    ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
+                 1e-4 * steps)
+    cfg = E.RidcConfig(levels=1, steps=steps, restarts=restarts, record_trajectory=traj)
+    with E.Engine(ivp, cfg) as sw, E.Engine(ivp, cfg, tick_only=True) as tick:
+        assert sw.info["path_name"] == "sweep_febe", sw.info
+        a, b = sw.run(), tick.run()
+        a2 = sw.run()
+    assert np.array_equal(a.final_state, a2.final_state)
+    assert G.normwise(a.final_state, b.final_state) <= 1e-13
+    if traj:
+        assert G.normwise(a.trajectory, b.trajectory) <= 1e-13
+    dt = (ivp.t_end - ivp.t_start) / steps
+    ref = O.run(ivp.problem, ivp.initial_state, 1, steps, restarts, dt, pack_weight_tables(1, dt))
+    assert G.normwise(a.final_state, ref["final_state"]) <= 1e-10

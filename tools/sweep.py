@@ -56,9 +56,7 @@ for ex in [int(x) for x in a.exps.split(",")]:
         bpp = sum(bench.bytes_per_point(j) for j in range(p))
         # steady ticks carry all p levels; fill ticks fewer: average bytes per tick
         gbs = bpp * n * a.nt / t / 1e9
-        launches = info["kernel_launches"]
-        path = ("resident_febe" if p == 1 and launches == 2 else
-                "resident_levels" if p > 1 and launches == 3 else "tick_graph")
+        path = info["path_name"]   # read back from the engine after the runs
         row = {"points": n, "order": p, "nt": a.nt, "path": path, "us_per_step": t / a.nt * 1e6,
                "ms_per_solve": t * 1e3, "us_per_tick": tick_s * 1e6,
                "grid_pt_steps_per_s": n * a.nt / t, "alg_bytes_per_pt_tick": bpp,
