@@ -409,7 +409,9 @@ def run_ours(args):
         launches_per_step = info["kernel_launches"]
         # resident FEBE: seed + one march; resident level march: 2 seeds + one march
         # per interval; else the tick graph: seed + one launch per tick
-        tick_launches = 1 if path != 0 else launches_per_step - 1   # resident paths: one march launch
+        # resident marches (resident_febe, resident_levels, carry_febe): one march launch;
+        # graph paths (tick kernel, FEBE sweeps): one launch per tick after the seed
+        tick_launches = 1 if path in (1, 2, 3) else launches_per_step - 1
         lev_bytes = sum(bytes_per_point(j) for j in range(order)) * nt / max(tick_launches, 1)
     from paper_1209_4297_b200._lib import PATH_NAMES
     path_name = PATH_NAMES.get(path, "?")
@@ -440,13 +442,17 @@ def run_ours(args):
                             "per level, registers-resident chunks, TMA-staged windows, per-segment flags)"),
         "carry_febe": "k_febe_carry (whole FEBE march in one launch: one tile per SM in registers, rhs + "
                       "factored tridiagonal solve per step, tiles coupled by two tagged carries per step through L2)",
+        "sweep_febe": "k_sweep_febe (one launch per step: every SM sweeps a contiguous range of the line through "
+                      "TMA-staged chunks, carries along the sweep, each point read and written once)",
+        "sweep2d_febe": "k_sweep2d_febe (one launch per step: every CTA sweeps a row block, each row read once and "
+                        "folded into three right-hand sides, cyclic x-line solves)",
         "tick": "k_tick_chunk (fused level-step: stencils + factored tridiagonal solve)",
     }
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                 "kernel": kernels.get(path_name, path_name), "path": path_name,
                 "bytes_per_launch": bytes_launch, "launch_us": per_launch_s * 1e6,
-                "steps_per_launch": nt // max(tick_launches, 1) if path_name != "tick" else 1}
+                "steps_per_launch": nt // max(tick_launches, 1)}
     if traffic_note:
         roofline["traffic_source"] = traffic_note
 

@@ -212,7 +212,7 @@ cudaError_t sweep_t(int grid, cudaStream_t st, const SweepParams& sp, const Tmap
                     long long target)
 {
     auto kfn = k_sweep_febe<KIND, NT>;
-    const size_t smem = sweep_smem<NT>() + ((sp.exp & 2) ? 100 * 1024 : 0);
+    const size_t smem = sweep_smem<NT>();
     static bool attr[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -229,7 +229,7 @@ cudaError_t sweep_t(int grid, cudaStream_t st, const SweepParams& sp, const Tmap
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = (sp.exp & 1) ? 0 : 1;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kfn, sp, tm, off, target);
@@ -276,13 +276,12 @@ cudaError_t sweep2d_k(int nt, int grid, cudaStream_t st, const Sweep2DParams& sp
     return cudaErrorInvalidValue;
 }
 
-// nt = 512 (one CTA per SM) or 256 (two CTAs per SM); grid = CTAs
+// one 512-thread CTA per SM; grid = CTAs
 template <int KIND>
 cudaError_t sweep_k(int nt, int grid, cudaStream_t st, const SweepParams& sp, const TmapSet& tm, long long off,
                     long long target)
 {
-    return nt == 256 ? sweep_t<KIND, 256>(grid, st, sp, tm, off, target)
-                     : sweep_t<KIND, 512>(grid, st, sp, tm, off, target);
+    return nt == 512 ? sweep_t<KIND, 512>(grid, st, sp, tm, off, target) : cudaErrorInvalidValue;
 }
 
 }  // namespace ridc

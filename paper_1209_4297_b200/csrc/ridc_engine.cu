@@ -562,7 +562,7 @@ struct ridc_ctx {
     uint4* d_cmail = nullptr;
     // streaming FEBE sweep (ridc_sweep.cuh): long periodic RD lines, one launch per step
     bool sweep = false;
-    int sweep_nt = 256;
+    int sweep_nt = 512;
     SweepParams sparams;
     TmapSet tm_sweep;
     // 2-D streaming FEBE sweep (ridc_sweep2d.cuh): every row read once per step
@@ -978,7 +978,7 @@ int setup_sweep(ridc_ctx* c)
     if (getenv("RIDC_NO_SWEEP") && atoi(getenv("RIDC_NO_SWEEP")) > 0) return RIDC_OK;
     const double lam = c->ss.sv.lam;
     const int hc = halo_of(lam);
-    c->sweep_nt = env_int("RIDC_SWEEP_NT", 512) == 256 ? 256 : 512;
+    c->sweep_nt = 512;
     if (hc > 512 || pb.nx < 1024 * c->nsm * (512 / c->sweep_nt)) return RIDC_OK;
     SweepParams& sp = c->sparams;
     memset(&sp, 0, sizeof sp);
@@ -1002,7 +1002,6 @@ int setup_sweep(ridc_ctx* c)
     sp.hc = hc;
     sp.per = c->per;
     sp.err = c->d_err;
-    sp.exp = getenv("RIDC_SWEEP_EXP") ? atoi(getenv("RIDC_SWEEP_EXP")) : 0;
     memset(&c->tm_sweep, 0, sizeof c->tm_sweep);
     int rc = make_ring_map(&c->tm_sweep.map[0], c->d_ring[0], c->Vs, c->cap[0], c->sweep_nt, &c->err);
     if (rc) return rc;

@@ -40,8 +40,10 @@ namespace ridc {
 
 constexpr int kSweepStages = 3;
 constexpr int kSweepPend = 34;   // tail threads of a chunk: hc / 16 + 1 <= 33 (hc <= 512)
-// NT = 512: one CTA per SM, 8192-point chunks; NT = 256: two CTAs per SM,
-// 4096-point chunks (one CTA's dependent scan chain overlaps the other's)
+// NT = 512: one CTA per SM, 8192-point chunks.  (A 256-thread variant with two
+// CTAs per SM and 4096-point chunks measured the same speed and gave
+// run-to-run differences at C5 2^23 that a one-CTA-per-SM launch of the same
+// code did not: not used.)
 template <int NT>
 constexpr size_t sweep_smem() { return (size_t)kSweepStages * NT * 16 * sizeof(double) + 2 * kSweepStages * 8 + 1024; }
 
@@ -59,7 +61,6 @@ struct SweepParams {
     int hc;                    // carry reach (<= 512)
     long long per;             // error-step numbering
     unsigned long long* err;
-    int exp;                   // diagnostics (RIDC_SWEEP_EXP): 1 no PDL, 2 one CTA per SM, 4 late refill
 };
 
 __device__ __forceinline__ void stg256(double* p, double a, double b, double c, double d)
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        if (tid == 0 && i + NS < nch && !(sp.exp & 4)) {
+        if (tid == 0 && i + NS < nch) {
             mbar_wait(&empty[s], (uint32_t)((i / NS) & 1));
             issue(i + NS);
         }
@@ -239,10 +240,6 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         double ex = __shfl_up_sync(FULL, inc, 1);
         if (lane == 0) ex = 0.0;
         __syncthreads();
-        if (tid == 0 && i + NS < nch && (sp.exp & 4)) {
-            mbar_wait(&empty[s], (uint32_t)((i / NS) & 1));
-            issue(i + NS);
-        }
         double wi = lane < NW ? sx[lane] : 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
