@@ -276,6 +276,47 @@ cudaError_t sweep2d_k(int nt, int grid, cudaStream_t st, const Sweep2DParams& sp
     return cudaErrorInvalidValue;
 }
 
+// ---- 2-D level sweep (ridc_sweep2d_levels.cuh): one CTA of nx / 16 threads per SM
+template <int KIND, int NT>
+cudaError_t sweep2d_levels_t(int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+                             const SweepLevParams& sp, const TmapSet& tm)
+{
+    auto kfn = k_sweep2d_levels<KIND, NT>;
+    const size_t smem = SweepLevSmem<NT>::bytes(tp.nact);
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)SweepLevSmem<NT>::bytes(kMaxLevels));
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, ep, tp, sp, tm);
+}
+
+template <int KIND>
+cudaError_t sweep2d_levels_k(int nt, int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+                             const SweepLevParams& sp, const TmapSet& tm)
+{
+    switch (nt) {
+    case 256: return sweep2d_levels_t<KIND, 256>(grid, st, ep, tp, sp, tm);
+    case 512: return sweep2d_levels_t<KIND, 512>(grid, st, ep, tp, sp, tm);
+    }
+    return cudaErrorInvalidValue;
+}
+
 // one 512-thread CTA per SM; grid = CTAs
 template <int KIND>
 cudaError_t sweep_k(int nt, int grid, cudaStream_t st, const SweepParams& sp, const TmapSet& tm, long long off,

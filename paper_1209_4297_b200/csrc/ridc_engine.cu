@@ -569,6 +569,11 @@ struct ridc_ctx {
     bool sweep2d = false;
     int sweep2d_nt = 256;
     Sweep2DParams s2params;
+    // 2-D level sweep (ridc_sweep2d_levels.cuh): the ticks of levels >= 2 on 2-D grids
+    bool sweeplev = false;
+    int sweeplev_nt = 256;
+    SweepLevParams slparams;
+    TmapSet tm_lev;
     bool fell_back = false;        // a resident march was replaced by the tick graph at run time
     double watchdog = 30.0;        // seconds per in-kernel neighbour wait (ridc_set_watchdog)
     std::string err;
@@ -719,7 +724,12 @@ int capture_graph(ridc_ctx* c)
             const bool top_active = ttop >= 1 && ttop <= c->per;
             if (top_active) slot_free((long long)r * c->per + ttop);
             if (le != cudaSuccess) break;
-            if (c->sweep2d)   // 2-D FEBE: every CTA sweeps its row block, each row read once
+            if (c->sweeplev)   // 2-D levels: every CTA sweeps its row block for each active level
+                le = c->pb.kind == ADV_DIFF_2D
+                         ? sweep2d_levels_k<ADV_DIFF_2D>(c->sweeplev_nt, c->nsm, c->stream, ep, tp, c->slparams,
+                                                         c->tm_lev)
+                         : sweep2d_levels_k<RD_2D>(c->sweeplev_nt, c->nsm, c->stream, ep, tp, c->slparams, c->tm_lev);
+            else if (c->sweep2d)   // 2-D FEBE: every CTA sweeps its row block, each row read once
                 le = c->pb.kind == ADV_DIFF_2D
                          ? sweep2d_k<ADV_DIFF_2D>(c->sweep2d_nt, c->nsm * (512 / c->sweep2d_nt), c->stream,
                                                   c->s2params, c->tm_sweep, ep.off[0], tp.target[0])
@@ -1067,6 +1077,45 @@ int setup_sweep2d(ridc_ctx* c)
     return RIDC_OK;
 }
 
+// 2-D level sweep (ridc_sweep2d_levels.cuh): RIDC order >= 2 on the periodic
+// 2-D kinds with x-lines of 4096 or 8192 points and at least two rows per SM.
+int setup_sweep2d_levels(ridc_ctx* c)
+{
+    const DevProblem& pb = c->pb;
+    if (c->levels < 2 || !(pb.kind == ADV_DIFF_2D || pb.kind == RD_2D) || (c->flags & RIDC_TICK_ONLY)) return RIDC_OK;
+    if (getenv("RIDC_NO_SWEEP") && atoi(getenv("RIDC_NO_SWEEP")) > 0) return RIDC_OK;
+    const int nt = pb.nx == 4096 ? 256 : (pb.nx == 8192 ? 512 : 0);
+    if (!nt || pb.ny < 2 * c->nsm) return RIDC_OK;
+    SolveSetup fs;
+    make_factors(pb, c->dt, fs);
+    SweepLevParams& sp = c->slparams;
+    memset(&sp, 0, sizeof sp);
+    sp.lam = fs.sv.lam;
+    sp.g = fs.sv.g;
+    double lS = 1.0;   // lam^nx
+    for (int i = 0; i < pb.nx; ++i) lS *= sp.lam;
+    sp.cyc = 1.0 / (1.0 - lS);
+    for (int e = 0; e < 16; ++e) {
+        sp.pw[e] = fs.sv.pw[e];
+        sp.zf[e] = fs.sv.zf16[e];
+    }
+    for (int i = 0; i < 10; ++i) sp.mp[i] = fs.sv.mp16[i];
+    sp.P = c->ss.lay.P;
+    sp.GW = c->ss.lay.GW;
+    sp.gpr = c->ss.lay.gpr;
+    sp.gdata = c->ss.lay.gdata;
+    sp.nx = pb.nx;
+    sp.ny = pb.ny;
+    memset(&c->tm_lev, 0, sizeof c->tm_lev);
+    for (int j = 0; j < c->levels; ++j) {   // every level ring, boxes of 256 groups (4096 points)
+        int rc = make_ring_map(&c->tm_lev.map[j], c->d_ring[j], c->Vs, c->cap[j], 256, &c->err);
+        if (rc) return rc;
+    }
+    c->sweeplev_nt = nt;
+    c->sweeplev = true;
+    return RIDC_OK;
+}
+
 // Resident single-level march: RIDC order 1 on a 1-D line whose segments fit
 // one co-resident CTA each, and whose halos reach only the adjacent segments.
 int setup_resident(ridc_ctx* c)
@@ -1394,6 +1443,7 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     if (!c->resident && (rc = setup_reslev(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep2d(c)) != RIDC_OK) return bail(rc);
+    if ((rc = setup_sweep2d_levels(c)) != RIDC_OK) return bail(rc);
     if (!c->resident && !c->reslev && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
 #undef CTX_TRY
     *out = c;
@@ -1456,6 +1506,7 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->path = c->carry ? RIDC_PATH_CARRY_FEBE
                  : (c->sweep && !c->resident) ? RIDC_PATH_SWEEP_FEBE
                  : c->sweep2d ? RIDC_PATH_SWEEP2D_FEBE
+                 : c->sweeplev ? RIDC_PATH_SWEEP2D_LEVELS
                           : c->resident ? RIDC_PATH_RESIDENT_FEBE
                                         : (c->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK);
     info->fell_back = c->fell_back ? 1 : 0;

@@ -22,6 +22,8 @@ namespace ridc {
 #if RIDC_INST_KIND >= 4
 template cudaError_t sweep2d_k<RIDC_INST_KIND>(int, int, cudaStream_t, const Sweep2DParams&, const TmapSet&,
                                                long long, long long);
+template cudaError_t sweep2d_levels_k<RIDC_INST_KIND>(int, int, cudaStream_t, const EngineParams&,
+                                                      const TickParams&, const SweepLevParams&, const TmapSet&);
 #endif
 template cudaError_t launch_chunk_k<RIDC_INST_KIND>(const ChunkCfg&, int, cudaStream_t, const EngineParams&,
                                                     const TickParams&, int, const TmapSet&);

@@ -354,6 +354,12 @@ inline int chunk_points_max(int kind)
 // ---- resident level march (ridc_levels.cuh): every lane a group of nseg CTAs
 constexpr int kResStages = 2;
 
+}  // namespace ridc
+
+#include "ridc_sweep2d_levels.cuh"
+
+namespace ridc {
+
 // ---- launch entry points, one instantiation per problem kind (ridc_inst.cu)
 template <int KIND>
 cudaError_t launch_chunk_k(const ChunkCfg& c, int grid, cudaStream_t st, const EngineParams& ep,
@@ -372,6 +378,9 @@ cudaError_t sweep_k(int nt, int grid, cudaStream_t st, const SweepParams& sp, co
 template <int KIND>
 cudaError_t sweep2d_k(int nt, int grid, cudaStream_t st, const Sweep2DParams& sp, const TmapSet& tm, long long off,
                       long long target);
+template <int KIND>
+cudaError_t sweep2d_levels_k(int nt, int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+                             const SweepLevParams& sp, const TmapSet& tm);
 template <int KIND, bool SYS>
 cudaError_t levels_k(int nt, int mode, bool launch, int grid, cudaStream_t st, const LevelsParams& lp,
                      const TmapSet& tm, int* per_sm, bool dense);

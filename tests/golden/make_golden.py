@@ -252,6 +252,8 @@ def paper_runs():
             ("paper_p4_r10", 1e-3, 40.0, 4, 4000, 10),
             ("ad_c1_T40_p1", 1 / 1024, 40.0, 1, 1000, 1),
             ("ad_c1_T40_p4", 1 / 1024, 40.0, 4, 1000, 1),
+            # the engine's maximum order (12 levels, engine.py:47) on the C1 grid
+            ("ad_c1_p12", 1 / 1024, 0.4, 12, 200, 1),
         ]:
             spec = RP.AdvectionDiffusionSpec(dx=dx, t_end=t_end)
             sysr = RP.build_advection_diffusion(spec)

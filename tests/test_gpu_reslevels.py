@@ -69,9 +69,12 @@ def test_resident_levels_equal_tick_kernel_bitwise(name, builder, levels, steps,
     assert np.array_equal(a.final_state, a2.final_state)
     dt = (ivp.t_end - ivp.t_start) / steps
     ref = O.run(ivp.problem, ivp.initial_state, levels, steps, restarts, dt, pack_weight_tables(levels, dt))
-    # 12 levels amplify the rounding differences of the two solvers (Thomas on the
-    # CPU, factored recurrences here) to ~1e-10; the tick kernel is bitwise this
-    assert G.normwise(a.final_state, ref["final_state"]) <= (1e-10 if levels <= 8 else 1e-9)
+    # 12 levels amplify the rounding differences of any two solvers (the oracle's
+    # Thomas and the reference's dense QR already differ by 1.4e-10 there:
+    # _golden.tolerance); the tick kernel is bitwise this
+    err = G.normwise(a.final_state, ref["final_state"])
+    print(f"{name}: resident levels vs oracle {err:.3e}")
+    assert err <= G.tolerance(levels)
 
 
 def test_resident_levels_nonfinite_message():

@@ -67,3 +67,37 @@ def test_sweep2d_nonfinite_step():
         with pytest.raises(Exception) as ei:
             eng.run(y0)
     assert "non-finite entries at step 1" in str(ei.value)
+
+
+LEVEL_CASES = [
+    # (id, ivp builder, levels, steps, restarts, trajectory)
+    ("ad-4096x500-p2", lambda: _ad(4096, 500, 12), 2, 12, 1, False),
+    ("ad-4096x400-p4-r2", lambda: _ad(4096, 400, 24), 4, 24, 2, False),
+    ("rd-8192x320-p3", lambda: _rd(8192, 320, 10), 3, 10, 1, False),
+    ("rd-4096x300-p4-traj", lambda: _rd(4096, 300, 12), 4, 12, 1, True),
+]
+
+
+@pytest.mark.parametrize("name,builder,levels,steps,restarts,traj", LEVEL_CASES, ids=[c[0] for c in LEVEL_CASES])
+def test_sweep2d_levels_match_tick_and_oracle(name, builder, levels, steps, restarts, traj):
+    """RIDC orders >= 2 on 2-D grids: one row sweep per active level per tick
+    (csrc/ridc_sweep2d_levels.cuh), every level's final against the tick kernel
+    and the oracle."""
+    ivp = builder()
+    cfg = E.RidcConfig(levels=levels, steps=steps, restarts=restarts, record_trajectory=traj)
+    with E.Engine(ivp, cfg) as sw, E.Engine(ivp, cfg, tick_only=True) as tick:
+        assert sw.info["path_name"] == "sweep2d_levels", sw.info
+        a, b = sw.run(), tick.run()
+        a2 = sw.run()
+    assert np.array_equal(a.final_state, a2.final_state)
+    assert G.normwise(a.final_state, b.final_state) <= 1e-12
+    for j in range(levels):
+        assert G.normwise(a.level_finals[j], b.level_finals[j]) <= 1e-12, j
+    if traj:
+        assert G.normwise(a.trajectory, b.trajectory) <= 1e-12
+    dt = (ivp.t_end - ivp.t_start) / steps
+    ref = O.run(ivp.problem, ivp.initial_state, levels, steps, restarts, dt, pack_weight_tables(levels, dt),
+                level_finals=True)
+    assert G.normwise(a.final_state, ref["final_state"]) <= 1e-10
+    for j in range(levels):
+        assert G.normwise(a.level_finals[j], ref["level_finals"][j]) <= 1e-10, j

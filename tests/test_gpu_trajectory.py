@@ -43,8 +43,12 @@ def test_streamed_trajectory_equals_device_trajectory(levels, steps, restarts, n
     b, ib = _run(s, cfg, stream=True)
     assert ib["ring_vectors"] < ia["ring_vectors"]          # the top ring holds 8 slots, not steps + 1
     assert a.trajectory.shape == b.trajectory.shape == (steps + 1, n)
-    assert np.array_equal(a.trajectory, b.trajectory)
-    assert np.array_equal(a.final_state, b.final_state)
+    if ia["path_name"] == ib["path_name"]:
+        assert np.array_equal(a.trajectory, b.trajectory)
+        assert np.array_equal(a.final_state, b.final_state)
+    else:   # e.g. the carry-exchange march (device trajectory) vs the tick graph (streamed): same solve
+        assert G.normwise(a.trajectory, b.trajectory) <= 1e-13
+        assert G.normwise(a.final_state, b.final_state) <= 1e-13
     assert np.array_equal(b.trajectory[-1], b.final_state)
     assert np.array_equal(b.trajectory[0], s.ivp.initial_state)
 
