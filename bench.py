@@ -64,16 +64,17 @@ def workload(name, points=None, nt=None):
     if name == "c1":
         sysm = P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 1024, t_end=4.0))
         return sysm, nt or 1000, {"workload": "c1-adv-diff-1d", "points": 1024, "nt": nt or 1000}
+    # 2-D workloads: the configuration's dt (T / 1000) whatever Nt (explicit y-terms)
     if name == "c3":
         n = points or 4096
-        sysm = P.build_advection_diffusion_2d(P.AdvectionDiffusion2DSpec(nx=n, ny=n))
-        return sysm, nt or 1000, {"workload": "c3-adv-diff-2d", "points": n * n, "grid": [n, n],
-                                   "nt": nt or 1000}
+        nt = nt or 1000
+        sysm = P.build_advection_diffusion_2d(P.AdvectionDiffusion2DSpec(nx=n, ny=n, t_end=0.02 * nt / 1000))
+        return sysm, nt, {"workload": "c3-adv-diff-2d", "points": n * n, "grid": [n, n], "nt": nt}
     if name == "c4":
         n = points or 8192
-        sysm = P.build_reaction_diffusion_2d(P.ReactionDiffusion2DSpec(nx=n, ny=n))
-        return sysm, nt or 1000, {"workload": "c4-reaction-diffusion-2d", "points": n * n,
-                                   "grid": [n, n], "nt": nt or 1000}
+        nt = nt or 1000
+        sysm = P.build_reaction_diffusion_2d(P.ReactionDiffusion2DSpec(nx=n, ny=n, t_end=0.05 * nt / 1000))
+        return sysm, nt, {"workload": "c4-reaction-diffusion-2d", "points": n * n, "grid": [n, n], "nt": nt}
     raise SystemExit(f"unknown workload {name}")
 
 

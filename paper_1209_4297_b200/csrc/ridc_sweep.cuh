@@ -117,12 +117,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)NS * L::STAGE);
     uint64_t* empty = full + NS;
     __shared__ double sx[2 * NW];
-    // broadcasts: [0] forward carry into the next chunk, [1] x at a chunk's first point,
-    // [2] x just after my range (the range-end pass)
-    __shared__ double s_bc[3];
-    // tail threads park their chunk here until the next chunk's first x is known
-    // (two sets by chunk parity; transposed [e][slot]: conflict-free)
-    __shared__ double s_pend[2][16 * kSweepPend];
+    __shared__ double s_bc[2];   // broadcasts: [0] forward carry into the next chunk, [1] x at its first point
+    // tail threads park their chunk here one iteration (transposed: [e][slot], conflict-free)
+    __shared__ double s_pend[16 * kSweepPend];
     // the 512 points after my range (the epilogue's truncated passes), prefetched by warp 0
     __shared__ double s_next[512];
     const unsigned FULL = 0xffffffffu;
@@ -191,24 +188,18 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     // tail threads (last hc points of a chunk) keep their chunk's block-local x one
     // iteration longer, until the next chunk's first x (the backward carry) is known
     bool bad = false;
-    // per chunk parity: data column of my parked chunk (-1: none), its s_pend slot, and
-    // M^q (q = chunks after mine in that chunk; times pw[15-e]: lam^(end - point))
-    int pcol0 = -1, pcol1 = -1, pslot0 = 0, pslot1 = 0;
-    double pm0 = 0.0, pm1 = 0.0;
-    auto flush_set = [&](int& pcol, int pslot, double pm, const double* buf, double d) {
-        if (pcol < 0) return;
-        const double dm = d * pm;
+    int pend_col = -1;      // data column of my parked chunk, -1: nothing pending
+    int pend_slot = 0;      // its s_pend slot
+    double pend_m = 0.0;    // M^q, q = chunks after mine in that chunk (times pw[15-e]: lam^(end - point))
+    auto pend_flush = [&](double d) {   // apply the backward carry d, check, store
+        const double dm = d * pend_m;
         double w[K];
 #pragma unroll
-        for (int e = 0; e < K; ++e) w[e] = fma(dm, sp.pw[K - 1 - e], buf[e * kSweepPend + pslot]);
+        for (int e = 0; e < K; ++e) w[e] = fma(dm, sp.pw[K - 1 - e], s_pend[e * kSweepPend + pend_slot]);
         bad |= !chunk_finite(w);
 #pragma unroll
-        for (int e = 0; e < K; e += 4) stg256(udst + pcol + e, w[e], w[e + 1], w[e + 2], w[e + 3]);
-        pcol = -1;
-    };
-    auto pend_flush = [&](int par, double d) {   // apply the backward carry d, check, store
-        if (par) flush_set(pcol1, pslot1, pm1, s_pend[1], d);
-        else flush_set(pcol0, pslot0, pm0, s_pend[0], d);
+        for (int e = 0; e < K; e += 4) stg256(udst + pend_col + e, w[e], w[e + 1], w[e + 2], w[e + 3]);
+        pend_col = -1;
     };
 
     for (int i = 0; i < nch; ++i) {
@@ -249,8 +240,6 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         double ex = __shfl_up_sync(FULL, inc, 1);
         if (lane == 0) ex = 0.0;
         __syncthreads();
-        // chunk i-2's tail: its backward carry is chunk i-1's first x (thread 0, end of the last iteration)
-        if (i >= 2) pend_flush(i & 1, s_bc[1]);
         double wi = lane < NW ? sx[lane] : 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -292,24 +281,24 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         const double dc = fma(mr, dw, exr);
 #pragma unroll
         for (int e = 0; e < K; ++e) v[e] = fma(dc, sp.pw[K - 1 - e], fma(cf, sp.zf[e], v[e]));
-        // ---- my first x: the previous chunk's backward carry (read after the next barrier)
+        // ---- the previous chunk's tail: its backward carry is my first point's x
         if (tid == 0) s_bc[1] = v[0];
-        // ---- store my points, or park them when the next chunk's carry reaches them
+        __syncthreads();
+        const double dprev = s_bc[1];
+        if (pend_col >= 0) pend_flush(dprev);
+        // ---- store my points, or keep them pending when the next carry reaches them
         if (mine) {
             const int col = cbase + tid * K;
-            const int par = i & 1;
             if (K * (tid + 1) > len - sp.hc) {
-                const int slot = tid - max(0, (len - sp.hc) / K);
-                double* buf = s_pend[par];
+                pend_slot = tid - max(0, (len - sp.hc) / K);
 #pragma unroll
-                for (int e = 0; e < K; ++e) buf[e * kSweepPend + slot] = v[e];
-                double pm = 1.0;   // M^(nthr - 1 - tid)
+                for (int e = 0; e < K; ++e) s_pend[e * kSweepPend + pend_slot] = v[e];
+                pend_col = col;
+                pend_m = 1.0;   // M^(nthr - 1 - tid)
                 const int q = nthr - 1 - tid;
 #pragma unroll
                 for (int b = 0; b < 10; ++b)
-                    if (q & (1 << b)) pm *= sp.mp[b];
-                if (par) { pcol1 = col; pslot1 = slot; pm1 = pm; }
-                else { pcol0 = col; pslot0 = slot; pm0 = pm; }
+                    if (q & (1 << b)) pend_m *= sp.mp[b];
             } else {
                 bad |= !chunk_finite(v);
 #pragma unroll
@@ -317,9 +306,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
             }
         }
     }
-    __syncthreads();
-    // chunk nch-2's tail: the backward carry is the last chunk's first x
-    if (nch >= 2) pend_flush(nch & 1, s_bc[1]);
+    __syncthreads();   // every warp has read the last iteration's broadcasts before s_bc is reused
     // ---- range end: the backward carry at R1 (warp 0: the 512 points after it,
     // forward from this range's last y, then backward from zero), for the
     // pending tail of the last chunk
@@ -345,10 +332,10 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         }
         // x at my first point; the lanes above me contribute lam^(16 (l' - l)) ...
         double xb = warp_bwd_incl(sp, x, lane);   // lane 0: x at R1 (truncated at 512 points)
-        if (lane == 0) s_bc[2] = xb;
+        if (lane == 0) s_bc[1] = xb;
     }
     __syncthreads();
-    pend_flush((nch - 1) & 1, s_bc[2]);
+    if (pend_col >= 0) pend_flush(s_bc[1]);
     if (bad) atomicMin(sp.err, err_code((target - 1) % sp.per + 1, 0));
 }
 
