@@ -20,13 +20,17 @@
 // where hc is the truncation reach (lam^hc <= 2^-60, ridc_engine.cu halo_of)
 // and every dropped term is below lam^T ~ 1e-290 (tiles are >= 2 hc long).
 // c is the neighbour's LOCAL forward value (its own left carry contributes
-// lam^T), so each step needs exactly two messages per tile edge, both 16-byte
-// tagged lines in the LL format of the halo mailbox (ridc_resident.cuh):
+// lam^T), and d is the right neighbour's local first x plus the head
+// correction by MY OWN y_end -- which I can add myself.  So each step needs
+// two messages per tile edge that depend on nothing but the sender's own
+// step, both 16-byte tagged lines in the LL format of the halo mailbox
+// (ridc_resident.cuh):
 //   1. after the forward scan a tile publishes y_end (its last point's y);
-//   2. after its head correction it publishes x_begin (its first point's x).
+//   2. after the backward scan it publishes its first point's local x.
 // The head warp waits for the left neighbour's y_end, the tail warp for the
-// right neighbour's x_begin; every other warp runs straight into the next
-// step (their only coupling is the block scans' two barriers).
+// right neighbour's local x (one L2 round trip each, in parallel); every
+// other warp runs straight into the next step (their only coupling is the
+// block scans' two barriers).
 //
 // Against the truncated-halo march this computes 12% fewer points at C2, moves
 // 2 values per edge per step through L2 instead of ~440 tagged lines, and
@@ -96,6 +100,7 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
     static_assert(KIND == RD_1D, "carry-exchange FEBE: periodic reaction-diffusion lines");
     constexpr int K = 16;
     __shared__ double sx[2 * (kCarryMaxNT / 32)];
+    __shared__ double s_yend;   // y at my tile's last point (this step), for the tail warps
     const unsigned FULL = 0xffffffffu;
     const int NT = blockDim.x, NW = NT >> 5;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -178,7 +183,11 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
         if (warp == 0) cw = 0.0;
         const double cf = fma(ml, cw, ex);
         // 1. publish y at my tile's last point (the right neighbour's forward carry)
-        if (last && !dead) st_line(box + 2 * k, fma(cf, cp.pw[K - 1], bf), tag);
+        if (last) {
+            const double yend = fma(cf, cp.pw[K - 1], bf);
+            if (!dead) st_line(box + 2 * k, yend, tag);
+            s_yend = yend;   // read by the tail warps after the backward scan's barrier
+        }
         // ---- local backward recurrence (zero carry at the tile end)
         double x = 0.0;
 #pragma unroll
@@ -205,7 +214,10 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
         const double dc = fma(mr, dw, exr);
 #pragma unroll
         for (int e = 0; e < K; ++e) u[e] = fma(dc, cp.pw[K - 1 - e], fma(cf, cp.zf[e], u[e]));
-        // ---- head: the left neighbour's forward carry, then 2. publish x at my first point
+        // 2. publish my first point's LOCAL x (before my head correction): the left
+        // neighbour completes it with its own y_end, so neither carry waits on the other
+        if (tid == 0 && !dead) st_line(box + 2 * k + 1, u[0], tag);
+        // ---- head: the left neighbour's forward carry
         if (head_warp) {
             double c = 0.0;
             if (lane == 0) c = poll_line(box + 2 * kl, tag, cp, dead);
@@ -215,12 +227,16 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
 #pragma unroll
                 for (int e = 0; e < K; ++e) u[e] = fma(cm, cp.pw[e], u[e]);
             }
-            if (tid == 0 && !dead) st_line(box + 2 * k + 1, u[0], tag);
         }
-        // ---- tail: the right neighbour's backward carry
+        // ---- tail: the right neighbour's backward carry d = x at its first point =
+        // its local x there + its head correction by MY y_end (the very operations
+        // the neighbour applies to its own first point: bitwise the same d)
         if (tail_warp) {
             double d = 0.0;
-            if (lane == 0) d = poll_line(box + 2 * kr + 1, tag, cp, dead);
+            if (lane == 0) {
+                const double xl = poll_line(box + 2 * kr + 1, tag, cp, dead);
+                d = fma(s_yend * cp.inv1ml2, cp.pw[0], xl);
+            }
             d = __shfl_sync(FULL, d, 0);
             if (tail) {
                 const double dm = d * Mt;
