@@ -38,3 +38,15 @@ def test_reference_arm_nonzero_rank_is_silent():
     out = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0"],
                env={"RANK": "1", "WORLD_SIZE": "2"})
     assert out == ""
+
+
+def test_workloads_keep_the_configuration_dt():
+    """--nt shortens the horizon, never changes dt (explicit terms of the 2-D kinds)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for name, dt in (("c2", 1e-4), ("c3", 0.02 / 1000), ("c4", 0.05 / 1000)):
+        for nt in (None, 20):
+            sysm, n_t, cfg = bench.workload(name, 4096 if name != "c2" else None, nt)
+            ivp = sysm.ivp
+            assert abs((ivp.t_end - ivp.t_start) / n_t - dt) <= 1e-15, (name, nt)
+            assert cfg["nt"] == n_t
