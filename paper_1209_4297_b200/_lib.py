@@ -12,7 +12,10 @@ import threading
 from .errors import raise_for_status
 from .problems import CProblem
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libridc_b200.so")
+# RIDC_CHECKED=1 loads the checked build (RIDC_CHECK assertions compiled in,
+# __graft_entry__.build(checked=True)): diagnostics only, slower
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        "libridc_b200_checked.so" if os.environ.get("RIDC_CHECKED") == "1" else "libridc_b200.so")
 
 _lock = threading.Lock()
 _lib = None

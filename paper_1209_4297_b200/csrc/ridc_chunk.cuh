@@ -259,6 +259,8 @@ __device__ __forceinline__ void chunk_item(const DevProblem& pb, const DevSolve&
     constexpr bool periodic = KIND != BURGERS_1D;
     constexpr bool two_d = ROWS == 3;
     const int tid = threadIdx.x, lane = tid & 31;
+    RIDC_CHECK(row >= 0 && row < pb.ny && cg.c0 >= 0 && cg.c0 + cg.tlen <= pb.nx && cg.ng <= NT * KC / kChunk &&
+               it.nnodes >= 1 && it.nnodes <= kMaxNodes);
     const int gq = tid / HP;                  // my group
     const int ip0 = (tid % HP) * (K / 2);     // my first element pair within it
     const bool mine = gq < cg.ng;             // owns (part of) a staged group

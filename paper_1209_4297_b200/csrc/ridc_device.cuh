@@ -24,6 +24,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifdef RIDC_CHECKED
+#include <cstdio>
+#endif
 
 namespace ridc {
 
@@ -55,6 +58,23 @@ struct DevSolve {
     double mp8[10], mp16[10];         // M^(2^i), M = lam^K (repeated squaring of pw[K-1]), K = 8/16
     long long* dbg;                // optional phase trace (RIDC_PHASE_TIMING), CTA 0 only
 };
+
+// Checked build (RIDC_CHECKED: __graft_entry__.build(checked=True) ->
+// libridc_b200_checked.so): bounds and protocol assertions in the kernels, in
+// place of compute-sanitizer (closed on the GPU pool).  A failed check prints
+// the site and traps, which surfaces as a CUDA error on the host.
+#ifdef RIDC_CHECKED
+#define RIDC_CHECK(cond)                                                                     \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("RIDC_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,   \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                            \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define RIDC_CHECK(cond) do { } while (0)
+#endif
 
 // Phase trace: CTA 0, thread 0, first 8 items of a launch, 16 stamps each.
 #define RIDC_STAMP(sv, item_no, idx)                                                         \

@@ -115,7 +115,9 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
     const bool head_warp = warp * 32 * K < cp.hc;
     const bool tail_warp = (warp * 32 + 31) * K + K > Tk - cp.hc && warp * 32 < nch;
     const bool last = tid == nch - 1;           // owns the tile's last point: publishes y_end
+    RIDC_CHECK(nch <= (int)blockDim.x && Tk % K == 0 && Tk >= 2 * cp.hc && c0 + Tk <= cp.nx);
     const int kl = k == 0 ? nseg - 1 : k - 1, kr = k == nseg - 1 ? 0 : k + 1;
+    RIDC_CHECK(k < nseg && kl >= 0 && kl < nseg && kr >= 0 && kr < nseg);
     const double lam = cp.lam;
 
     // carry powers: M^t (head, with 1/(1 - lam^2)), M^(nch-1-t) (tail), M^lane, M^(31-lane)

@@ -49,6 +49,7 @@ struct TickParams {
 
 __device__ __forceinline__ long long slot_index(const EngineParams& ep, int lev, long long s, long long off = -1)
 {
+    RIDC_CHECK(lev >= 0 && lev < ep.levels && ep.cap[lev] > 0 && s >= 0);
     return ((off < 0 ? ep.off[lev] : off) + s) % ep.cap[lev];
 }
 

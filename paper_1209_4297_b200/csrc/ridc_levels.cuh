@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(NT, MINB)
     long long pend = 0;
     auto store_tile = [&](long long ts) {
         if (s_dead) return;
+        // LevelBuffer.publish's capacity rule (engine.py:305-318): the consumer released the slot
+        RIDC_CHECK(ts - ln.out_cap + 1 <= 0 || seen_rel >= (ep | (unsigned long long)(ts - ln.out_cap + 1)));
         double* o = out + ((ln.out_off + ts) % ln.out_cap) * rp.Vs + GW;
         const int glo = (lo - cg.g0 * kChunk + kChunk - 1) / kChunk, ghi = (hi - cg.g0 * kChunk) / kChunk;
         const bool ghosts = periodic && (lo < GW || hi > nx - GW);
@@ -267,6 +269,8 @@ __global__ void __launch_bounds__(NT, MINB)
         if (m >= NSTAGE) mbar_wait(&empty[s], (uint32_t)(((m - NSTAGE) / NSTAGE) & 1));
         const long long ns = tt >= j ? tt - a : a;
         const long long slot = (ln.in_off + ns) % ln.in_cap;
+        // the window reads only published producer steps (engine.py:363-371 _ready)
+        RIDC_CHECK(ns == 0 || seen_in >= (ep | (unsigned long long)ns));
         issue_chunk_node<NT, 1, NSTAGE, kChunk>(tm, ln.in_map, slot, 0, 1, rp.lay.gpr, rp.lay.gdata, cg,
                                                 stage + (size_t)s * L::STAGE, &full[s]);
     };

@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     // nch nearly equal chunks (multiples of 16 points): none shorter than the carry reach
     const int Cr = 16 * ((Lr + 16 * nch - 1) / (16 * nch));
     const long long src = (off + target - 1) % sp.cap, dst = (off + target) % sp.cap;
+    RIDC_CHECK(src != dst && Lr >= 1024 && Cr % 16 == 0 && Cr <= C && (nch - 1) * Cr < Lr && sp.hc <= 512);
     const double* usrc = sp.ring + src * sp.Vs + sp.GW;   // data column 0
     double* udst = sp.ring + dst * sp.Vs + sp.GW;
     const double lam = sp.lam;
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
             const int col = cbase + tid * K;
             if (K * (tid + 1) > len - sp.hc) {
                 pend_slot = tid - max(0, (len - sp.hc) / K);
+                RIDC_CHECK(pend_slot >= 0 && pend_slot < kSweepPend && col >= R0 && col + K <= R1);
 #pragma unroll
                 for (int e = 0; e < K; ++e) s_pend[e * kSweepPend + pend_slot] = v[e];
                 pend_col = col;

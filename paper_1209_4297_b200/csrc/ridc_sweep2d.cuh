@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     const int r0 = (int)((long long)cta * ny / G), r1 = (int)((long long)(cta + 1) * ny / G);
     const int nl = r1 - r0 + 2;                     // rows loaded: r0-1 .. r1
     const long long src = (off + target - 1) % sp.cap, dst = (off + target) % sp.cap;
+    RIDC_CHECK(src != dst && r1 > r0 && sp.nx == 16 * NT && (long long)sp.ny * sp.P <= sp.Vs);
     double* out0 = sp.ring + dst * sp.Vs + sp.GW + tid * K;   // + row * P
     const double lam = sp.lam;
 

@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(NT, 1)
         if (issued >= NS) mbar_wait(&empty[s], (uint32_t)(((issued - NS) / NS) & 1));
         int q = r0 - 1 + pc.k;
         q = q < 0 ? q + ny : (q >= ny ? q - ny : q);
+        RIDC_CHECK(q >= 0 && q < ny && it.vlev[pc.n] >= 0 && it.vlev[pc.n] < ep.levels &&
+                   it.vslot[pc.n] >= 0 && it.vslot[pc.n] < ep.cap[it.vlev[pc.n]]);
         mbar_arrive_expect_tx(&full[s], (uint32_t)(NBOX * BR * 128));
         for (int b = 0; b < NBOX; ++b)
             tma_load_3d(base + (size_t)s * S::ROWB + b * BR * 128, &tm.map[it.vlev[pc.n]], 0,
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(NT, 1)
     for (int a = 0; a < tp.nact; ++a) {
         const StepItem& it = items[a];
         const int nn = it.nnodes;
+        RIDC_CHECK(nn >= 1 && nn <= kMaxNodes && it.out == ep.ring[it.level] + it.oslot * ep.Vs);
         double* const out0 = it.out + sp.GW + tid * K;   // + row * P
         bool bad = false;
         // one grid row (k) of this level: every node's row folded into A, B and C

@@ -1,12 +1,14 @@
-"""Small marches of every kernel family, for compute-sanitizer (memcheck,
-synccheck, racecheck): the tick kernel (1-D segmented, whole-line, 2-D
-x-lines), the resident FEBE march (whole line and segmented, tagged mailbox),
-the resident level march (all levels on one GPU: per-segment flags, TMA
-window staging), the pipeline ranks (resident and stream-memop) and the ARK
-comparator.  Each case is checked against the CPU oracle so a sanitizer run
-also confirms the results.
+"""Small marches of every kernel family against the CPU oracle: the tick
+kernel (1-D segmented, whole-line, 2-D x-lines), the resident marches (FEBE:
+halo exchange and carry exchange; all levels), the streaming sweeps (1-D
+FEBE, 2-D FEBE, 2-D levels), the pipeline ranks and the ARK comparator.
+
+Run it under compute-sanitizer where that is available, or -- on the GPU pool,
+where compute-sanitizer is closed -- against the checked build, whose kernels
+assert their bounds and pipeline-protocol invariants (RIDC_CHECK, ridc_device.cuh):
 
     compute-sanitizer --tool memcheck python tools/sanitize.py [--cases a,b]
+    RIDC_CHECKED=1 python tools/sanitize.py      # __graft_entry__.build(checked=True) first
 """
 import argparse
 import os
@@ -39,7 +41,13 @@ def seg(n=1 << 15, steps=20):
 
 CASES = {
     "febe-whole": (lambda: c1(), 1, 10, {}),
-    "febe-seg": (lambda: seg(), 1, 20, {}),
+    "febe-carry": (lambda: seg(), 1, 20, {}),
+    "febe-halo-seg": (lambda: _short(P.build_burgers(P.BurgersSpec(dx=1 / (1 << 15))), 0.002), 1, 20, {}),
+    "febe-sweep": (lambda: seg(1 << 21, 10), 1, 10, {}),
+    "febe-sweep2d": (lambda: P.build_advection_diffusion_2d(P.AdvectionDiffusion2DSpec(
+        nx=4096, ny=600, t_end=0.02 * 6 / 1000)).ivp, 1, 6, {}),
+    "levels-sweep2d-p3": (lambda: P.build_reaction_diffusion_2d(P.ReactionDiffusion2DSpec(
+        nx=4096, ny=400, t_end=0.05 * 10 / 1000)).ivp, 3, 10, {}),
     "tick-seg-p3": (lambda: seg(), 3, 20, {"tick_only": True}),
     "levels-seg-p3": (lambda: seg(), 3, 20, {}),
     "levels-whole-p4": (lambda: c1(), 4, 20, {}),
@@ -103,7 +111,8 @@ def main():
         else:
             b, levels, steps, kw = CASES[name]
             check(name, b(), levels, steps, kw)
-    print("sanitize cases done")
+    from paper_1209_4297_b200 import _lib
+    print(f"sanitize cases done ({os.path.basename(_lib.LIB_PATH)})")
 
 
 if __name__ == "__main__":
