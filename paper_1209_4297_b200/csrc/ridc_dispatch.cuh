@@ -276,6 +276,35 @@ cudaError_t sweep2d_k(int nt, int grid, cudaStream_t st, const Sweep2DParams& sp
     return cudaErrorInvalidValue;
 }
 
+// ---- 1-D level sweep (ridc_sweep_levels.cuh): one 512-thread CTA per SM
+template <int KIND>
+cudaError_t sweep_levels_k(int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+                           const SweepParams& sp, const TmapSet& tm)
+{
+    auto kfn = k_sweep_levels<KIND>;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sweep_levels_smem(kMaxLevels));
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = sweep_levels_smem(tp.nact);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, ep, tp, sp, tm);
+}
+
 // ---- 2-D level sweep (ridc_sweep2d_levels.cuh): one CTA of nx / 16 threads per SM
 template <int KIND, int NT>
 cudaError_t sweep2d_levels_t(int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,

@@ -569,6 +569,8 @@ struct ridc_ctx {
     bool sweep2d = false;
     int sweep2d_nt = 256;
     Sweep2DParams s2params;
+    // 1-D level sweep (ridc_sweep_levels.cuh): the ticks of levels >= 2 on long RD lines
+    bool sweeplev1 = false;
     // 2-D level sweep (ridc_sweep2d_levels.cuh): the ticks of levels >= 2 on 2-D grids
     bool sweeplev = false;
     int sweeplev_nt = 256;
@@ -724,7 +726,9 @@ int capture_graph(ridc_ctx* c)
             const bool top_active = ttop >= 1 && ttop <= c->per;
             if (top_active) slot_free((long long)r * c->per + ttop);
             if (le != cudaSuccess) break;
-            if (c->sweeplev)   // 2-D levels: every CTA sweeps its row block for each active level
+            if (c->sweeplev1)   // 1-D levels: every SM sweeps its range for each active level
+                le = sweep_levels_k<RD_1D>(c->nsm, c->stream, ep, tp, c->sparams, c->tm_lev);
+            else if (c->sweeplev)   // 2-D levels: every CTA sweeps its row block for each active level
                 le = c->pb.kind == ADV_DIFF_2D
                          ? sweep2d_levels_k<ADV_DIFF_2D>(c->sweeplev_nt, c->nsm, c->stream, ep, tp, c->slparams,
                                                          c->tm_lev)
@@ -1012,6 +1016,7 @@ int setup_sweep(ridc_ctx* c)
     sp.hc = hc;
     sp.per = c->per;
     sp.err = c->d_err;
+    sp.g = g;
     memset(&c->tm_sweep, 0, sizeof c->tm_sweep);
     int rc = make_ring_map(&c->tm_sweep.map[0], c->d_ring[0], c->Vs, c->cap[0], c->sweep_nt, &c->err);
     if (rc) return rc;
@@ -1113,6 +1118,46 @@ int setup_sweep2d_levels(ridc_ctx* c)
     }
     c->sweeplev_nt = nt;
     c->sweeplev = true;
+    return RIDC_OK;
+}
+
+// 1-D level sweep (ridc_sweep_levels.cuh): RIDC order >= 2 on a periodic
+// reaction-diffusion line of a multiple of 16 points that the resident level
+// march cannot hold, at least 1024 points per SM, carry reach <= 512.
+int setup_sweep_levels(ridc_ctx* c)
+{
+    const DevProblem& pb = c->pb;
+    if (c->levels < 2 || c->reslev || pb.kind != RD_1D || pb.ny != 1 || (pb.nx & 15) ||
+        (c->flags & RIDC_TICK_ONLY) || c->ss.sv.nseg < 2)
+        return RIDC_OK;
+    if (getenv("RIDC_NO_SWEEP") && atoi(getenv("RIDC_NO_SWEEP")) > 0) return RIDC_OK;
+    const double lam = c->ss.sv.lam;
+    const int hc = halo_of(lam);
+    if (hc > 512 || pb.nx < 1024 * c->nsm || c->ss.lay.GW < 16) return RIDC_OK;
+    SweepParams& sp = c->sparams;
+    memset(&sp, 0, sizeof sp);
+    sp.pb = pb;
+    sp.lam = lam;
+    sp.g = c->ss.sv.g;
+    for (int e = 0; e < 16; ++e) {
+        sp.pw[e] = c->ss.sv.pw[e];
+        sp.zf[e] = c->ss.sv.zf16[e];
+    }
+    for (int i = 0; i < 10; ++i) sp.mp[i] = c->ss.sv.mp16[i];
+    sp.Vs = c->Vs;
+    sp.GW = c->ss.lay.GW;
+    sp.gpr = c->ss.lay.gpr;
+    sp.gdata = c->ss.lay.gdata;
+    sp.nx = pb.nx;
+    sp.hc = hc;
+    sp.per = c->per;
+    sp.err = c->d_err;
+    memset(&c->tm_lev, 0, sizeof c->tm_lev);
+    for (int j = 0; j < c->levels; ++j) {   // every level ring, boxes of 256 groups (4096 points)
+        int rc = make_ring_map(&c->tm_lev.map[j], c->d_ring[j], c->Vs, c->cap[j], 256, &c->err);
+        if (rc) return rc;
+    }
+    c->sweeplev1 = true;
     return RIDC_OK;
 }
 
@@ -1444,6 +1489,7 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     if ((rc = setup_sweep(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep2d(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep2d_levels(c)) != RIDC_OK) return bail(rc);
+    if ((rc = setup_sweep_levels(c)) != RIDC_OK) return bail(rc);
     if (!c->resident && !c->reslev && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
 #undef CTX_TRY
     *out = c;
@@ -1507,6 +1553,7 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
                  : (c->sweep && !c->resident) ? RIDC_PATH_SWEEP_FEBE
                  : c->sweep2d ? RIDC_PATH_SWEEP2D_FEBE
                  : c->sweeplev ? RIDC_PATH_SWEEP2D_LEVELS
+                 : c->sweeplev1 ? RIDC_PATH_SWEEP_LEVELS
                           : c->resident ? RIDC_PATH_RESIDENT_FEBE
                                         : (c->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK);
     info->fell_back = c->fell_back ? 1 : 0;

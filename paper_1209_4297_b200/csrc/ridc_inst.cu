@@ -35,6 +35,8 @@ template cudaError_t resident_k<RIDC_INST_KIND>(int, int, bool, int, cudaStream_
 template cudaError_t febe_carry_k<RIDC_INST_KIND>(bool, int, int, cudaStream_t, const CarryParams&, int*);
 template cudaError_t sweep_k<RIDC_INST_KIND>(int, int, cudaStream_t, const SweepParams&, const TmapSet&, long long,
                                              long long);
+template cudaError_t sweep_levels_k<RIDC_INST_KIND>(int, cudaStream_t, const EngineParams&, const TickParams&,
+                                                    const SweepParams&, const TmapSet&);
 #endif
 #elif RIDC_INST_PART == 2
 template cudaError_t levels_k<RIDC_INST_KIND, false>(int, int, bool, int, cudaStream_t, const LevelsParams&,

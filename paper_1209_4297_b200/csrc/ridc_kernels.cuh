@@ -358,6 +358,7 @@ constexpr int kResStages = 2;
 }  // namespace ridc
 
 #include "ridc_sweep2d_levels.cuh"
+#include "ridc_sweep_levels.cuh"
 
 namespace ridc {
 
@@ -379,6 +380,9 @@ cudaError_t sweep_k(int nt, int grid, cudaStream_t st, const SweepParams& sp, co
 template <int KIND>
 cudaError_t sweep2d_k(int nt, int grid, cudaStream_t st, const Sweep2DParams& sp, const TmapSet& tm, long long off,
                       long long target);
+template <int KIND>
+cudaError_t sweep_levels_k(int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+                           const SweepParams& sp, const TmapSet& tm);
 template <int KIND>
 cudaError_t sweep2d_levels_k(int nt, int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
                              const SweepLevParams& sp, const TmapSet& tm);

@@ -51,6 +51,7 @@ struct SweepParams {
     DevProblem pb;
     double lam;
     double aa, bb;             // RD rhs with g folded in: (aa + bb u) u
+    double g;                  // the solve's scale (the level sweep folds it into every node)
     double pw[16];             // lam^(e+1)
     double zf[16];             // forward-carry response of a chunk's backward pass
     double mp[10];             // M^(2^i), M = lam^16

@@ -131,3 +131,34 @@ def test_sweep_febe_long_lines(name, n, steps, restarts, traj):
     dt = (ivp.t_end - ivp.t_start) / steps
     ref = O.run(ivp.problem, ivp.initial_state, 1, steps, restarts, dt, pack_weight_tables(1, dt))
     assert G.normwise(a.final_state, ref["final_state"]) <= 1e-10
+
+
+LEVEL_SWEEP_CASES = [
+    # (id, n, levels, steps, restarts): r ~ 110 as C2
+    ("2^20-p2", 1 << 20, 2, 20, 1),
+    ("2^20-p4-r2", 1 << 20, 4, 48, 2),
+    ("2^21-p3", 1 << 21, 3, 20, 1),
+    ("uneven-p2", (1 << 20) + 16 * 777, 2, 16, 1),
+]
+
+
+@pytest.mark.parametrize("name,n,levels,steps,restarts", LEVEL_SWEEP_CASES, ids=[c[0] for c in LEVEL_SWEEP_CASES])
+def test_sweep_levels_long_lines(name, n, levels, steps, restarts):
+    """RIDC p >= 2 on lines the resident level march cannot hold: every SM sweeps
+    its range for each active level per tick (csrc/ridc_sweep_levels.cuh), every
+    level's final against the tick kernel (<= 1e-12) and the oracle."""
+    ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
+                 1e-4 * steps)
+    cfg = E.RidcConfig(levels=levels, steps=steps, restarts=restarts)
+    with E.Engine(ivp, cfg) as sw, E.Engine(ivp, cfg, tick_only=True) as tick:
+        assert sw.info["path_name"] == "sweep_levels", sw.info
+        a, b = sw.run(), tick.run()
+        a2 = sw.run()
+    assert np.array_equal(a.final_state, a2.final_state)
+    for j in range(levels):
+        assert G.normwise(a.level_finals[j], b.level_finals[j]) <= 1e-12, j
+    dt = (ivp.t_end - ivp.t_start) / steps
+    ref = O.run(ivp.problem, ivp.initial_state, levels, steps, restarts, dt, pack_weight_tables(levels, dt),
+                level_finals=True)
+    for j in range(levels):
+        assert G.normwise(a.level_finals[j], ref["level_finals"][j]) <= 1e-10, j
