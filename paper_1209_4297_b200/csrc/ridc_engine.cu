@@ -1133,7 +1133,11 @@ int setup_sweep_levels(ridc_ctx* c)
     if (getenv("RIDC_NO_SWEEP") && atoi(getenv("RIDC_NO_SWEEP")) > 0) return RIDC_OK;
     const double lam = c->ss.sv.lam;
     const int hc = halo_of(lam);
-    if (hc > 512 || pb.nx < 1024 * c->nsm || c->ss.lay.GW < 16) return RIDC_OK;
+    // at least three chunks per SM: shorter lines stay L2-resident and the tick
+    // kernel is faster there (C2 p = 2 / 4 / 8: 15 / 36 / 90 us per tick against
+    // 17 / 46 / 134; 2^22: 0.63-0.77 of HBM against 0.56-0.75; 2^26: 0.89-0.98
+    // against 0.60-0.74 -- profiles/r2_sweep_c5_levels.json)
+    if (hc > 512 || pb.nx < 3 * kSweepLevMaxChunk * c->nsm || c->ss.lay.GW < 16) return RIDC_OK;
     SweepParams& sp = c->sparams;
     memset(&sp, 0, sizeof sp);
     sp.pb = pb;

@@ -134,11 +134,11 @@ def test_sweep_febe_long_lines(name, n, steps, restarts, traj):
 
 
 LEVEL_SWEEP_CASES = [
-    # (id, n, levels, steps, restarts): r ~ 110 as C2
-    ("2^20-p2", 1 << 20, 2, 20, 1),
-    ("2^20-p4-r2", 1 << 20, 4, 48, 2),
-    ("2^21-p3", 1 << 21, 3, 20, 1),
-    ("uneven-p2", (1 << 20) + 16 * 777, 2, 16, 1),
+    # (id, n, levels, steps, restarts): r ~ 110 as C2; at least three chunks per SM
+    ("2^22-p2", 1 << 22, 2, 20, 1),
+    ("2^22-p4-r2", 1 << 22, 4, 48, 2),
+    ("2^22-p8", 1 << 22, 8, 40, 1),
+    ("uneven-p3", (1 << 22) + 16 * 777, 3, 16, 1),
 ]
 
 
