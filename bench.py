@@ -445,6 +445,9 @@ def run_ours(args):
                       "factored tridiagonal solve per step, tiles coupled by two tagged carries per step through L2)",
         "sweep_febe": "k_sweep_febe (one launch per step: every SM sweeps a contiguous range of the line through "
                       "TMA-staged chunks, carries along the sweep, each point read and written once)",
+        "sweep_warp_febe": "k_sweep_febe_warp (one launch per step: every warp sweeps a contiguous range of the "
+                           "line through its own TMA-staged 512-point chunks, no block barriers, each point read "
+                           "and written once)",
         "sweep2d_febe": "k_sweep2d_febe (one launch per step: every CTA sweeps a row block, each row read once and "
                         "folded into three right-hand sides, cyclic x-line solves)",
         "tick": "k_tick_chunk (fused level-step: stencils + factored tridiagonal solve)",

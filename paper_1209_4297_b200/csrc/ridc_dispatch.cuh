@@ -2,6 +2,7 @@
 // in ridc_kernels.cuh (template instantiation happens in ridc_inst.cu only).
 #pragma once
 #include "ridc_kernels.cuh"
+#include "ridc_sweep_warp.cuh"
 
 namespace ridc {
 
@@ -235,6 +236,36 @@ cudaError_t sweep_t(int grid, cudaStream_t st, const SweepParams& sp, const Tmap
     return cudaLaunchKernelEx(&cfg, kfn, sp, tm, off, target);
 }
 
+// ---- warp-sweep FEBE (ridc_sweep_warp.cuh): one 512-thread CTA per SM, every
+// warp sweeps its own range; PDL between consecutive steps
+template <int KIND>
+cudaError_t sweep_warp_t(int grid, cudaStream_t st, const SweepParams& sp, const TmapSet& tm, long long off,
+                         long long target)
+{
+    auto kfn = k_sweep_febe_warp<KIND>;
+    const size_t smem = warp_sweep_smem();
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kWarpSweepWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, sp, tm, off, target);
+}
+
 // ---- 2-D streaming FEBE sweep (ridc_sweep2d.cuh): nx = 16 NT, 512 / NT CTAs per SM
 template <int KIND, int NT>
 cudaError_t sweep2d_t(int grid, cudaStream_t st, const Sweep2DParams& sp, const TmapSet& tm, long long off,
@@ -351,7 +382,9 @@ template <int KIND>
 cudaError_t sweep_k(int nt, int grid, cudaStream_t st, const SweepParams& sp, const TmapSet& tm, long long off,
                     long long target)
 {
-    return nt == 512 ? sweep_t<KIND, 512>(grid, st, sp, tm, off, target) : cudaErrorInvalidValue;
+    return nt == 512 ? sweep_t<KIND, 512>(grid, st, sp, tm, off, target)
+           : nt == 32 ? sweep_warp_t<KIND>(grid, st, sp, tm, off, target)
+                      : cudaErrorInvalidValue;
 }
 
 }  // namespace ridc

@@ -38,6 +38,7 @@
 
 #include "../../include/ridc_b200.h"
 #include "ridc_kernels.cuh"
+#include "ridc_sweep_warp.cuh"
 
 using namespace ridc;
 
@@ -740,7 +741,7 @@ int capture_graph(ridc_ctx* c)
                          : sweep2d_k<RD_2D>(c->sweep2d_nt, c->nsm * (512 / c->sweep2d_nt), c->stream, c->s2params,
                                             c->tm_sweep, ep.off[0], tp.target[0]);
             else if (c->sweep)   // FEBE on a long periodic line: every SM sweeps its range
-                le = sweep_k<RD_1D>(c->sweep_nt, c->nsm * (512 / c->sweep_nt), c->stream, c->sparams, c->tm_sweep,
+                le = sweep_k<RD_1D>(c->sweep_nt, c->nsm, c->stream, c->sparams, c->tm_sweep,
                                     ep.off[0], tp.target[0]);
             else
                 le = launch_chunk(c->pb.kind, c->ss.ccfg,
@@ -992,8 +993,12 @@ int setup_sweep(ridc_ctx* c)
     if (getenv("RIDC_NO_SWEEP") && atoi(getenv("RIDC_NO_SWEEP")) > 0) return RIDC_OK;
     const double lam = c->ss.sv.lam;
     const int hc = halo_of(lam);
-    c->sweep_nt = 512;
-    if (hc > 512 || pb.nx < 1024 * c->nsm * (512 / c->sweep_nt)) return RIDC_OK;
+    if (hc > 512 || pb.nx < 1024 * c->nsm) return RIDC_OK;
+    // one independent sweep per warp (ridc_sweep_warp.cuh) when every warp's
+    // range holds a full 512-point chunk; else one sweep per CTA (ridc_sweep.cuh).
+    // RIDC_SWEEP_CTA=1 keeps the CTA sweep (A/B).
+    const bool cta_only = getenv("RIDC_SWEEP_CTA") && atoi(getenv("RIDC_SWEEP_CTA")) > 0;
+    c->sweep_nt = (!cta_only && (long long)pb.nx >= (long long)kWarpChunk * kWarpSweepWarps * c->nsm) ? 32 : 512;
     SweepParams& sp = c->sparams;
     memset(&sp, 0, sizeof sp);
     sp.pb = pb;
@@ -1554,7 +1559,7 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->lambda = c->ss.sv.lam;
     info->r = c->ss.r;
     info->path = c->carry ? RIDC_PATH_CARRY_FEBE
-                 : (c->sweep && !c->resident) ? RIDC_PATH_SWEEP_FEBE
+                 : (c->sweep && !c->resident) ? (c->sweep_nt == 32 ? RIDC_PATH_SWEEP_WARP_FEBE : RIDC_PATH_SWEEP_FEBE)
                  : c->sweep2d ? RIDC_PATH_SWEEP2D_FEBE
                  : c->sweeplev ? RIDC_PATH_SWEEP2D_LEVELS
                  : c->sweeplev1 ? RIDC_PATH_SWEEP_LEVELS

@@ -112,16 +112,20 @@ SWEEP_CASES = [
 ]
 
 
+@pytest.mark.parametrize("variant", ["warp", "cta"])
 @pytest.mark.parametrize("name,n,steps,restarts,traj", SWEEP_CASES, ids=[c[0] for c in SWEEP_CASES])
-def test_sweep_febe_long_lines(name, n, steps, restarts, traj):
-    """Lines too long to stay resident: the streaming sweep (one launch per step,
-    every SM sweeps a contiguous range, csrc/ridc_sweep.cuh) against the tick
-    kernel (<= 1e-13: same solve, different association) and the oracle."""
+def test_sweep_febe_long_lines(name, n, steps, restarts, traj, variant, monkeypatch):
+    """Lines too long to stay resident: the streaming sweeps (one launch per step;
+    every warp sweeps a contiguous range, csrc/ridc_sweep_warp.cuh, or every
+    SM, csrc/ridc_sweep.cuh with RIDC_SWEEP_CTA=1) against the tick kernel
+    (<= 1e-13: same solve, different association) and the oracle."""
+    if variant == "cta":
+        monkeypatch.setenv("RIDC_SWEEP_CTA", "1")
     ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
                  1e-4 * steps)
     cfg = E.RidcConfig(levels=1, steps=steps, restarts=restarts, record_trajectory=traj)
     with E.Engine(ivp, cfg) as sw, E.Engine(ivp, cfg, tick_only=True) as tick:
-        assert sw.info["path_name"] == "sweep_febe", sw.info
+        assert sw.info["path_name"] == {"warp": "sweep_warp_febe", "cta": "sweep_febe"}[variant], sw.info
         a, b = sw.run(), tick.run()
         a2 = sw.run()
     assert np.array_equal(a.final_state, a2.final_state)
