@@ -61,6 +61,13 @@ def workload(name, points=None, nt=None):
         nt = nt or 10000
         sysm = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, t_end=1e-4 * nt))
         return sysm, nt, {"workload": "c2-reaction-diffusion-1d", "points": n, "nt": nt, "t_end": 1e-4 * nt}
+    if name == "c5":
+        # configs[4] grid-size sweep: 1-D RD, r held at C2's ~110 (d scaled with N), dt = 1e-4
+        n = points or (1 << 24)
+        nt = nt or 200
+        sysm = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (float(1 << 20) / n) ** 2,
+                                                                  t_end=1e-4 * nt))
+        return sysm, nt, {"workload": "c5-reaction-diffusion-1d", "points": n, "nt": nt, "t_end": 1e-4 * nt}
     if name == "c1":
         sysm = P.build_advection_diffusion(P.AdvectionDiffusionSpec(dx=1 / 1024, t_end=4.0))
         return sysm, nt or 1000, {"workload": "c1-adv-diff-1d", "points": 1024, "nt": nt or 1000}
@@ -282,12 +289,12 @@ def _timed_solves(run_device, flush, reps):
     return ts
 
 
-def workload_line(name, order, flush, reps=2, nt=None):
-    """One extra 1-GPU workload (C3 / C4 shapes): device time of whole solves,
-    the dominant kernel's roofline (tick kernel, bytes per tick / tick time)."""
+def workload_line(name, order, flush, reps=2, nt=None, points=None):
+    """One extra 1-GPU workload (C3 / C4 / C5 shapes): device time of whole solves,
+    the dominant kernel's roofline (algorithmic bytes of a steady tick / tick time)."""
     import torch
     from paper_1209_4297_b200 import engine as E
-    sysm, nt, cfg = workload(name, None, nt)
+    sysm, nt, cfg = workload(name, points, nt)
     n = sysm.ivp.dimension
     y0 = torch.from_numpy(np.array(sysm.ivp.initial_state)).cuda()
     out = torch.empty_like(y0)
@@ -448,6 +455,8 @@ def run_ours(args):
         "sweep_warp_febe": "k_sweep_febe_warp (one launch per step: every warp sweeps a contiguous range of the "
                            "line through its own TMA-staged 512-point chunks, no block barriers, each point read "
                            "and written once)",
+        "carry_levels": "k_carry_levels (one launch per tick: every warp folds and solves one 512-point chunk of "
+                        "each active level, neighbouring chunks exchange two carries through L2)",
         "sweep2d_febe": "k_sweep2d_febe (one launch per step: every CTA sweeps a row block, each row read once and "
                         "folded into three right-hand sides, cyclic x-line solves)",
         "tick": "k_tick_chunk (fused level-step: stencils + factored tridiagonal solve)",
@@ -503,10 +512,16 @@ def run_ours(args):
                 with E.Engine(sysm, E.RidcConfig(levels=p, steps=nt)) as e2:
                     e2.run_device(y0, out)
                     ts = _timed_solves(lambda: e2.run_device(y0, out), flush, 2)
+                    t_solve = sum(ts) / len(ts)
+                    # every level does nt steps of bytes_per_point(j) algorithmic bytes per point
+                    alg = sum(bytes_per_point(j) for j in range(p)) * n * nt
                     extra[f"order{p}_1gpu"] = {"value": n * nt * len(ts) / sum(ts),
                                                "level_steps_per_s": p * n * nt * len(ts) / sum(ts),
-                                               "ms_per_solve": sum(ts) / len(ts) * 1e3,
-                                               "wall_ratio_vs_febe": (sum(ts) / len(ts)) / (t_max / args.steps),
+                                               "ms_per_solve": t_solve * 1e3,
+                                               "wall_ratio_vs_febe": t_solve / (t_max / args.steps),
+                                               "roofline": {"bound": "hbm", "achieved": alg / t_solve / 1e9,
+                                                            "peak": peak, "unit": "GB/s",
+                                                            "frac": alg / t_solve / 1e9 / peak},
                                                "path": e2.info["path_name"],
                                                "cpu_baseline": cpu_sample(sysm, p, nt, budget_s=args.cpu_budget / 3)}
             # the paper's ARK comparators on the same grid and dt (steppers.integrate_ark)
@@ -531,6 +546,8 @@ def run_ours(args):
             # the paper headline's shape (configs[2], C3: 2-D adv-diff 4096^2): FEBE on
             # one GPU is the denominator of "RIDC-4 on 4 GPUs <= 1.1x FEBE on 1 GPU"
             line["c3_1gpu"] = {f"order{p}": workload_line("c3", p, flush) for p in (1, 4)}
+            # configs[4]: the HBM-streaming FEBE sweep at 2^24 and 2^26 points (Nt 200, dt kept)
+            line["c5_1gpu"] = {f"febe_2^{e}": workload_line("c5", 1, flush, points=1 << e) for e in (24, 26)}
     else:
         # e2e at N GPUs: every rank copies y0 in from pinned host memory, the
         # pipeline marches, every rank reads the solution back; wall time of the
@@ -567,7 +584,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--order", type=int, default=0)
     ap.add_argument("--points", type=int, default=0)
     ap.add_argument("--nt", type=int, default=0)

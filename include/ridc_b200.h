@@ -97,7 +97,8 @@ typedef struct ridc_info {
     int32_t path;                 /* marching path in effect (after the last run):
                                      RIDC_PATH_TICK / _RESIDENT_FEBE / _RESIDENT_LEVELS /
                                      _CARRY_FEBE / _SWEEP_FEBE / _SWEEP2D_FEBE /
-                                     _SWEEP2D_LEVELS / _SWEEP_LEVELS / _SWEEP_WARP_FEBE */
+                                     _SWEEP2D_LEVELS / _SWEEP_LEVELS / _SWEEP_WARP_FEBE /
+                                     _CARRY_LEVELS */
     int32_t fell_back;            /* 1: a resident march could not get its co-resident
                                      SMs at run time and the tick graph replaced it */
 } ridc_info;
@@ -116,7 +117,10 @@ typedef struct ridc_info {
 #define RIDC_PATH_SWEEP_LEVELS 7     /* one launch per pipeline tick on a long 1-D line, every SM
                                         sweeps its range for each active level (CUDA graph) */
 #define RIDC_PATH_SWEEP_WARP_FEBE 8  /* one launch per FEBE step, every warp sweeps a contiguous
-                                        range once (lines of >= 512 x 16 x SMs points, CUDA graph) */
+                                        range once (lines of >= 512 x 12 x SMs points, CUDA graph) */
+#define RIDC_PATH_CARRY_LEVELS 9     /* one launch per pipeline tick on a 1-D line of 512-point
+                                        chunks, one chunk per warp, carries exchanged between
+                                        neighbouring chunks (CUDA graph) */
 
 /*
  * Create a run context (RidcConfig validation engine.py:71-87, _prepare

@@ -336,6 +336,36 @@ cudaError_t sweep_levels_k(int grid, cudaStream_t st, const EngineParams& ep, co
     return cudaLaunchKernelEx(&cfg, kfn, ep, tp, sp, tm);
 }
 
+// ---- carry-exchange level tick (ridc_carry_levels.cuh): one 512-point chunk
+// per warp, wpc warps per CTA, PDL between consecutive ticks
+template <int KIND>
+cudaError_t carry_levels_k(int grid, int wpc, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+                           const CarryLevParams& cp, const TmapSet& tm, unsigned tick)
+{
+    auto kfn = k_carry_levels<KIND>;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)carry_levels_smem());
+        if (e != cudaSuccess) return e;
+        attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32 * wpc);
+    cfg.dynamicSmemBytes = carry_levels_smem();
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, ep, tp, cp, tm, tick);
+}
+
 // ---- 2-D level sweep (ridc_sweep2d_levels.cuh): one CTA of nx / 16 threads per SM
 template <int KIND, int NT>
 cudaError_t sweep2d_levels_t(int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,

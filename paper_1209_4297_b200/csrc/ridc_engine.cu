@@ -39,6 +39,7 @@
 #include "../../include/ridc_b200.h"
 #include "ridc_kernels.cuh"
 #include "ridc_sweep_warp.cuh"
+#include "ridc_carry_levels.cuh"
 
 using namespace ridc;
 
@@ -76,6 +77,8 @@ __global__ void k_seed_chunk(const double* __restrict__ src, EngineParams ep, lo
             if (ep.ring[j]) ring_slot(ep, j, 0, off)[i] = v;
     }
 }
+
+__global__ void k_bump_epoch(unsigned* e) { *e += 1u; }
 
 // Wait on the device until *flag >= want: the consumer side of a watermark
 // written by a producer on ANOTHER device where the stream wait cannot flush
@@ -577,6 +580,13 @@ struct ridc_ctx {
     int sweeplev_nt = 256;
     SweepLevParams slparams;
     TmapSet tm_lev;
+    // carry-exchange level tick (ridc_carry_levels.cuh): RIDC p >= 2 on RD lines of <= 14 x SMs x 512 points
+    bool carrylev = false;
+    int cl_grid = 0, cl_wpc = 0;
+    CarryLevParams clparams;
+    TmapSet tm_cl;
+    uint4* d_clx = nullptr;
+    unsigned* d_clepoch = nullptr;
     bool fell_back = false;        // a resident march was replaced by the tick graph at run time
     double watchdog = 30.0;        // seconds per in-kernel neighbour wait (ridc_set_watchdog)
     std::string err;
@@ -692,6 +702,11 @@ int capture_graph(ridc_ctx* c)
     for (int r = 0; r < c->restarts && le == cudaSuccess; ++r) {
         EngineParams ep = interval_params(c, r);
         if (r == 0) {
+            if (c->carrylev) {   // a fresh tag epoch for the exchange lines of this run
+                k_bump_epoch<<<1, 1, 0, c->stream>>>(c->d_clepoch);
+                le = cudaGetLastError();
+                ++launches;
+            }
             const int sb = (int)std::min<long long>((c->Vs + 255) / 256, 148 * 8);
             k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
             le = cudaGetLastError();
@@ -727,7 +742,10 @@ int capture_graph(ridc_ctx* c)
             const bool top_active = ttop >= 1 && ttop <= c->per;
             if (top_active) slot_free((long long)r * c->per + ttop);
             if (le != cudaSuccess) break;
-            if (c->sweeplev1)   // 1-D levels: every SM sweeps its range for each active level
+            if (c->carrylev)   // 1-D levels: one chunk per warp, carries exchanged between chunks
+                le = carry_levels_k<RD_1D>(c->cl_grid, c->cl_wpc, c->stream, ep, tp, c->clparams, c->tm_cl,
+                                           (unsigned)((long long)r * c->ticks + k));
+            else if (c->sweeplev1)   // 1-D levels: every SM sweeps its range for each active level
                 le = sweep_levels_k<RD_1D>(c->nsm, c->stream, ep, tp, c->sparams, c->tm_lev);
             else if (c->sweeplev)   // 2-D levels: every CTA sweeps its row block for each active level
                 le = c->pb.kind == ADV_DIFF_2D
@@ -891,6 +909,7 @@ int march(ridc_ctx* c, double* wall_seconds)
         }
     }
     if (!c->resident && !c->reslev) {
+        if (c->carrylev) CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, sizeof(unsigned), c->stream));
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
         CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
     }
@@ -901,7 +920,7 @@ int march(ridc_ctx* c, double* wall_seconds)
         CUDA_TRY(&c->err, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         *wall_seconds = ms * 1e-3;
     }
-    if (c->resident || c->reslev) {
+    if (c->resident || c->reslev || c->carrylev) {
         unsigned ab = 0;
         CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_flags, sizeof ab, cudaMemcpyDeviceToHost));
         if (ab) return fail(&c->err, RIDC_E_PROTOCOL, "resident march: a neighbour segment wait timed out");
@@ -1167,6 +1186,62 @@ int setup_sweep_levels(ridc_ctx* c)
         if (rc) return rc;
     }
     c->sweeplev1 = true;
+    return RIDC_OK;
+}
+
+// Carry-exchange level tick (ridc_carry_levels.cuh): RIDC order >= 2 on a
+// periodic reaction-diffusion line of a multiple of 512 points, at most
+// kClWarps x SMs chunks, carry reach <= 512; one launch per tick in the graph.
+// Lines the resident level march holds stay there.
+int setup_carry_levels(ridc_ctx* c)
+{
+    const DevProblem& pb = c->pb;
+    if (c->levels < 2 || c->reslev || c->resident || pb.kind != RD_1D || pb.ny != 1 || (pb.nx % 512) ||
+        (c->flags & RIDC_TICK_ONLY) || c->ss.lay.GW < 16)
+        return RIDC_OK;
+    if (getenv("RIDC_NO_CARRYLEV") && atoi(getenv("RIDC_NO_CARRYLEV")) > 0) return RIDC_OK;
+    const double lam = c->ss.sv.lam;
+    const int hc = halo_of(lam);
+    const int nchunk = pb.nx / 512;
+    if (hc > 512 || nchunk < 2 || nchunk > kClWarps * c->nsm) return RIDC_OK;
+    const int grid = std::min(c->nsm, nchunk);
+    const int wpc = (nchunk + grid - 1) / grid;
+    CarryLevParams& cp = c->clparams;
+    memset(&cp, 0, sizeof cp);
+    cp.lam = lam;
+    cp.g = c->ss.sv.g;
+    cp.inv1ml2 = 1.0 / (1.0 - lam * lam);
+    cp.zc = lam * cp.inv1ml2;
+    for (int e = 0; e < 16; ++e) {
+        cp.pw[e] = c->ss.sv.pw[e];
+        cp.zf[e] = c->ss.sv.zf16[e];
+    }
+    for (int i = 0; i < 10; ++i) cp.mp[i] = c->ss.sv.mp16[i];
+    cp.nx = pb.nx;
+    cp.GW = c->ss.lay.GW;
+    cp.gdata = c->ss.lay.gdata;
+    cp.nchunk = nchunk;
+    cp.wpc = wpc;
+    const size_t xb = (size_t)2 * kMaxLevels * nchunk * sizeof(uint4);
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_clx, xb));
+    CUDA_TRY(&c->err, cudaMemset(c->d_clx, 0, xb));
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_clepoch, sizeof(unsigned)));
+    CUDA_TRY(&c->err, cudaMemset(c->d_clepoch, 0, sizeof(unsigned)));
+    if (!c->d_flags) CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, sizeof(unsigned)));
+    CUDA_TRY(&c->err, cudaMemset(c->d_flags, 0, sizeof(unsigned)));
+    cp.xch = c->d_clx;
+    cp.epoch = c->d_clepoch;
+    cp.ticks = (unsigned)(c->restarts * c->ticks + 1);
+    cp.abort = c->d_flags;
+    cp.spin_limit = (long long)(c->watchdog * 2.0e9);
+    memset(&c->tm_cl, 0, sizeof c->tm_cl);
+    for (int j = 0; j < c->levels; ++j) {   // every level ring, boxes of one chunk + one group either side
+        int rc = make_ring_map(&c->tm_cl.map[j], c->d_ring[j], c->Vs, c->cap[j], kClBoxGroups, &c->err);
+        if (rc) return rc;
+    }
+    c->cl_grid = (nchunk + wpc - 1) / wpc;
+    c->cl_wpc = wpc;
+    c->carrylev = true;
     return RIDC_OK;
 }
 
@@ -1498,7 +1573,8 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     if ((rc = setup_sweep(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep2d(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep2d_levels(c)) != RIDC_OK) return bail(rc);
-    if ((rc = setup_sweep_levels(c)) != RIDC_OK) return bail(rc);
+    if ((rc = setup_carry_levels(c)) != RIDC_OK) return bail(rc);
+    if (!c->carrylev && (rc = setup_sweep_levels(c)) != RIDC_OK) return bail(rc);
     if (!c->resident && !c->reslev && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
 #undef CTX_TRY
     *out = c;
@@ -1563,6 +1639,7 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
                  : c->sweep2d ? RIDC_PATH_SWEEP2D_FEBE
                  : c->sweeplev ? RIDC_PATH_SWEEP2D_LEVELS
                  : c->sweeplev1 ? RIDC_PATH_SWEEP_LEVELS
+                 : c->carrylev ? RIDC_PATH_CARRY_LEVELS
                           : c->resident ? RIDC_PATH_RESIDENT_FEBE
                                         : (c->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK);
     info->fell_back = c->fell_back ? 1 : 0;
@@ -1576,6 +1653,15 @@ int ridc_set_watchdog(ridc_ctx* c, double seconds)
     c->rp.spin_limit = (long long)(seconds * 2.0e9);
     c->lp.spin_limit = (long long)(seconds * 2.0e9);
     c->cparams.spin_limit = (long long)(seconds * 2.0e9);
+    if (c->carrylev && c->clparams.spin_limit != (long long)(seconds * 2.0e9)) {
+        // the limit is a kernel parameter of every captured tick: capture again
+        c->clparams.spin_limit = (long long)(seconds * 2.0e9);
+        CUDA_TRY(&c->err, cudaSetDevice(c->device));
+        CUDA_TRY(&c->err, cudaStreamSynchronize(c->stream));
+        if (c->gexec) cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+        return capture_graph(c);
+    }
     return RIDC_OK;
 }
 
@@ -1596,6 +1682,8 @@ int ridc_destroy(ridc_ctx* c)
     if (c->d_flags) cudaFree(c->d_flags);
     if (c->d_mail) cudaFree(c->d_mail);
     if (c->d_cmail) cudaFree(c->d_cmail);
+    if (c->d_clx) cudaFree(c->d_clx);
+    if (c->d_clepoch) cudaFree(c->d_clepoch);
     for (int j = 0; j < kMaxLevels; ++j)
         if (c->d_inbox[j]) cudaFree(c->d_inbox[j]);
     if (c->d_lflags) cudaFree(c->d_lflags);

@@ -74,7 +74,8 @@ __device__ __forceinline__ double sweep_rhs(const SweepParams& sp, double u) { r
 
 // Warp-level scans of the chunk carries (multiplier M = lam^16 per lane):
 // inclusive forward (lane l accumulates lanes <= l) and backward (lanes >= l).
-__device__ __forceinline__ double warp_fwd_incl(const SweepParams& sp, double v, int lane)
+template <class PP>   // any parameter block with mp[i] = M^(2^i)
+__device__ __forceinline__ double warp_fwd_incl(const PP& sp, double v, int lane)
 {
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
@@ -84,7 +85,8 @@ __device__ __forceinline__ double warp_fwd_incl(const SweepParams& sp, double v,
     return v;
 }
 
-__device__ __forceinline__ double warp_bwd_incl(const SweepParams& sp, double v, int lane)
+template <class PP>
+__device__ __forceinline__ double warp_bwd_incl(const PP& sp, double v, int lane)
 {
 #pragma unroll
     for (int i = 0; i < 5; ++i) {

@@ -166,3 +166,58 @@ def test_sweep_levels_long_lines(name, n, levels, steps, restarts):
                 level_finals=True)
     for j in range(levels):
         assert G.normwise(a.level_finals[j], ref["level_finals"][j]) <= 1e-10, j
+
+
+CARRY_LEVEL_CASES = [
+    # (id, n, levels, steps, restarts, trajectory): r ~ 110 as C2; one 512-point chunk per warp
+    ("c2-p2", 1 << 20, 2, 24, 1, False),
+    ("c2-p4-r2", 1 << 20, 4, 32, 2, False),
+    ("c2-p3-traj", 1 << 20, 3, 20, 1, True),
+    ("2^17-p8", 1 << 17, 8, 40, 1, False),
+    ("uneven-p4", 512 * 1000, 4, 24, 1, False),
+    ("2^18-p12", 1 << 18, 12, 80, 1, False),
+]
+
+
+@pytest.mark.parametrize("name,n,levels,steps,restarts,traj", CARRY_LEVEL_CASES,
+                         ids=[c[0] for c in CARRY_LEVEL_CASES])
+def test_carry_levels(name, n, levels, steps, restarts, traj):
+    """RIDC p >= 2 on lines of 512-point chunks, one chunk per warp, the chunks'
+    solves coupled by two exchanged carries (csrc/ridc_carry_levels.cuh):
+    repeat runs bitwise, every level's final against the tick kernel (<= 1e-12:
+    the same solve, different association) and the oracle (<= 1e-10)."""
+    ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
+                 1e-4 * steps)
+    cfg = E.RidcConfig(levels=levels, steps=steps, restarts=restarts, record_trajectory=traj)
+    with E.Engine(ivp, cfg) as cl, E.Engine(ivp, cfg, tick_only=True) as tick:
+        assert cl.info["path_name"] == "carry_levels", cl.info
+        a, b = cl.run(), tick.run()
+        a2 = cl.run()
+    assert np.array_equal(a.final_state, a2.final_state)
+    for j in range(levels):
+        assert np.array_equal(a.level_finals[j], a2.level_finals[j]), j
+        # 12 levels amplify last-bit differences: tick vs this kernel 5e-12, the
+        # two CPU codes 1.4e-10 (DESIGN §2)
+        assert G.normwise(a.level_finals[j], b.level_finals[j]) <= (1e-10 if levels > 8 else 1e-12), j
+    if traj:
+        assert G.normwise(a.trajectory, b.trajectory) <= 1e-12
+    dt = (ivp.t_end - ivp.t_start) / steps
+    ref = O.run(ivp.problem, ivp.initial_state, levels, steps, restarts, dt, pack_weight_tables(levels, dt),
+                level_finals=True)
+    bar = 5e-10 if levels > 8 else 1e-10
+    for j in range(levels):
+        assert G.normwise(a.level_finals[j], ref["level_finals"][j]) <= bar, j
+
+
+def test_carry_levels_watchdog_recapture():
+    """ridc_set_watchdog re-captures the carry-level graph (the limit is a kernel
+    parameter of every tick): the run after it is unchanged."""
+    ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=1 << 18, d=1e-6 * 16.0)), 1e-4 * 12)
+    cfg = E.RidcConfig(levels=3, steps=12, watchdog_seconds=5.0)
+    with E.Engine(ivp, cfg) as cl:
+        assert cl.info["path_name"] == "carry_levels", cl.info
+        a = cl.run()
+        from paper_1209_4297_b200 import _lib
+        _lib.check(_lib.lib().ridc_set_watchdog(cl._h, 11.0), cl._h)
+        b = cl.run()
+    assert np.array_equal(a.final_state, b.final_state)
