@@ -376,7 +376,7 @@ def run_ours(args):
         bcast = gloo_bcast if shared else None
 
         def solve_device():
-            return runner.run_device(y0, out, broadcast=bcast)
+            return runner.run_device(y0, out, broadcast=bcast, barrier=barrier)
         launches_per_step = runner.kernel_launches
         tick_launches = runner.tick_launches
         # this rank's level-step bytes per point; the producer side also writes the
@@ -562,7 +562,7 @@ def run_ours(args):
             e0.record()
             y0.copy_(y0h, non_blocking=True)
             torch.cuda.current_stream().synchronize()   # the pipeline runs on its own stream
-            runner.run_device(y0, out, broadcast=bcast)
+            runner.run_device(y0, out, broadcast=bcast, barrier=barrier)
             finh.copy_(out, non_blocking=True)
             e1.record()
             torch.cuda.synchronize()

@@ -229,6 +229,14 @@ int ridc_pipe_connect(ridc_pipe *p, const void *prev_blob, const void *next_blob
  * (bounded by the watchdog).  wall_seconds: device time of this rank. */
 int ridc_pipe_run_interval(ridc_pipe *p, int32_t interval, const double *state0_dev,
                            double *final_dev, double *wall_seconds);
+/* Zero this rank's mailbox counters (watermarks, release and progress
+ * counters).  The stream-memop protocol counts global step numbers, so
+ * before a SECOND run of the same ranks every rank resets -- after all ranks
+ * finished the previous run and before any starts the next (barrier, reset,
+ * barrier; distributed.PipelineRank.run_device / ConcurrentPipeline /
+ * GridPipeline do this).  The resident mode's flags carry a run epoch and
+ * need no reset. */
+int ridc_pipe_reset(ridc_pipe *p);
 int ridc_pipe_info(const ridc_pipe *p, ridc_info *info);
 /* Resident level march (default where the line qualifies: 1-D, one
  * co-resident CTA per segment): the rank's whole interval is ONE cooperative
@@ -241,6 +249,25 @@ int ridc_pipe_info(const ridc_pipe *p, ridc_info *info);
  * each other).  ridc_pipe_resident reports the mode in effect. */
 int ridc_pipe_set_resident(ridc_pipe *p, int32_t enable);
 int ridc_pipe_resident(const ridc_pipe *p);
+/* Levels x row shards (the layer that uses every GPU
+ * when p < #GPUs): the rank owning level `level` of row shard `shard`
+ * (global rows [ny*shard/nshards, ny*(shard+1)/nshards)), 2-D kinds, stream
+ * memops only.  Besides the pipeline's watermark / release protocol with
+ * (level-1, shard) and (level+1, shard), every step it delivers its first and
+ * last row into the ghost rows of (level, shard-+1)'s own ring and of
+ * (level+1, shard-+1)'s inbox, each with its own watermark, and releases
+ * inbox slots to all three producers; ny periodic (shard 0's upper
+ * neighbour is shard nshards-1).  run_interval takes the GLOBAL state0 and
+ * returns this shard's rows (nrows x nx) of the level's final. */
+int ridc_pipe_create_shard(const ridc_problem *problem, double t_start, double t_end,
+                           int32_t levels, int64_t steps, int32_t restarts,
+                           const double *weights, int64_t nweights, int32_t level,
+                           int32_t shard, int32_t nshards, int32_t device,
+                           int32_t inbox_capacity, double watchdog_seconds, ridc_pipe **out);
+/* blobs[8]: (level-1, shard), (level-1, shard-1), (level-1, shard+1),
+ * (level+1, shard), (level+1, shard-1), (level+1, shard+1), (level, shard-1),
+ * (level, shard+1); NULL exactly where the level does not exist. */
+int ridc_pipe_connect_shard(ridc_pipe *p, const void *const *blobs);
 int ridc_pipe_destroy(ridc_pipe *p);
 const char *ridc_pipe_last_error(const ridc_pipe *p);
 
@@ -264,6 +291,10 @@ int ridc_ark_run(ridc_ark_ctx *ctx, const double *y0_host, double *final_host,
 int ridc_ark_run_device(ridc_ark_ctx *ctx, const double *y0_dev, double *final_dev,
                         double *wall_seconds);
 int ridc_ark_info(const ridc_ark_ctx *ctx, int64_t *kernel_launches, int32_t *items_per_step);
+/* The path the stages run on: RIDC_PATH_CARRY_LEVELS (periodic RD lines of
+ * 512-point chunks: every stage one carry-exchange launch) or RIDC_PATH_TICK;
+ * -1 for a NULL context. */
+int ridc_ark_path(const ridc_ark_ctx *ctx);
 int ridc_ark_destroy(ridc_ark_ctx *ctx);
 const char *ridc_ark_last_error(const ridc_ark_ctx *ctx);
 

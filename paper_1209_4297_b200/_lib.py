@@ -65,10 +65,16 @@ SIGNATURES = {
     "ridc_pipe_create": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int32, ctypes.c_int64,
                                         ctypes.c_int32, _vp, ctypes.c_int64, ctypes.c_int32,
                                         ctypes.c_int32, ctypes.c_int32, _d, _P(_vp)]),
+    "ridc_pipe_create_shard": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int32, ctypes.c_int64,
+                                              ctypes.c_int32, _vp, ctypes.c_int64, ctypes.c_int32,
+                                              ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                              _d, _P(_vp)]),
+    "ridc_pipe_connect_shard": (ctypes.c_int, [_vp, _P(_vp)]),
     "ridc_pipe_export": (ctypes.c_int, [_vp, _vp]),
     "ridc_pipe_connect": (ctypes.c_int, [_vp, _vp, _vp]),
     "ridc_pipe_run_interval": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, _dp]),
     "ridc_pipe_info": (ctypes.c_int, [_vp, _P(RidcInfo)]),
+    "ridc_pipe_reset": (ctypes.c_int, [_vp]),
     "ridc_pipe_set_resident": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "ridc_pipe_resident": (ctypes.c_int, [_vp]),
     "ridc_pipe_destroy": (ctypes.c_int, [_vp]),
@@ -78,6 +84,7 @@ SIGNATURES = {
     "ridc_ark_run": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
     "ridc_ark_run_device": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
     "ridc_ark_info": (ctypes.c_int, [_vp, _P(ctypes.c_int64), _P(ctypes.c_int32)]),
+    "ridc_ark_path": (ctypes.c_int, [_vp]),
     "ridc_ark_destroy": (ctypes.c_int, [_vp]),
     "ridc_ark_last_error": (ctypes.c_char_p, [_vp]),
     "ridc_shards_create": (ctypes.c_int, [_P(CProblem), _d, _d, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,

@@ -125,7 +125,24 @@ __global__ void __launch_bounds__(kClWarps * 32, 1)
     // the fold tables of this tick's items (build_item's nodes, g folded into the
     // coefficients), one thread per active level (before the wait: overlaps the
     // previous tick's tail)
-    if (tid < nact) {
+    if (tp.pre) {   // precomputed items (ARK stages: nodes y_n and the earlier stages, steppers.py:122-142)
+        if (tid < nact) {
+            int nn = 0;
+            for (int b = 0; b < tid; ++b) nn += tp.pre[b].nnodes;
+            const StepItem& it = tp.pre[tid];
+            ClLevel& lv = s_lev[tid];
+            lv.level = it.level;
+            lv.target = tp.target[tid];
+            lv.node0 = nn;
+            lv.nn = it.nnodes;
+            lv.out = it.out;
+            for (int b = 0; b < it.nnodes; ++b) {
+                const NodeCoef nc = node_coef<KIND>(ep.pb, it.ca[b], it.cs[b], it.cn[b]);
+                s_node[nn + b] = ClNode{g * nc.a, g * nc.b, g * nc.cs * ep.pb.cdx, it.vslot[b], it.vlev[b]};
+            }
+            RIDC_CHECK(nn + it.nnodes <= kClMaxNodes);
+        }
+    } else if (tid < nact) {
         const int a = tid;
         int nn = 0;
         for (int b = 0; b < a; ++b) nn += tp.level[b] > 0 ? tp.level[b] + 2 : 1;

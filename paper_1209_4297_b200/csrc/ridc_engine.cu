@@ -36,6 +36,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing unless a tool attaches
+
 #include "../../include/ridc_b200.h"
 #include "ridc_kernels.cuh"
 #include "ridc_sweep_warp.cuh"
@@ -46,6 +48,15 @@ using namespace ridc;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX range over a host entry point (the phases a profiler timeline shows:
+// create / graph capture / march / pipeline interval / shards / ARK)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int env_int(const char* name, int def)
 {
@@ -675,6 +686,7 @@ cudaError_t copy_out(ridc_ctx* c, double* dst, const double* slot, cudaMemcpyKin
 // Capture the whole run: per interval one seed + one launch per tick.
 int capture_graph(ridc_ctx* c)
 {
+    NvtxRange nvtx_("ridc.capture_graph");
     const int L = c->levels;
     const int items = c->pb.ny * c->ss.sv.nseg;
     cudaGraph_t graph = nullptr;
@@ -859,6 +871,7 @@ int march_reslev(ridc_ctx* c, bool* fell_back)
 
 int march(ridc_ctx* c, double* wall_seconds)
 {
+    NvtxRange nvtx_("ridc.march");
     CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
     if (c->reslev) {
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
@@ -1189,6 +1202,22 @@ int setup_sweep_levels(ridc_ctx* c)
     return RIDC_OK;
 }
 
+// The carry-level tick's per-launch solve constants from a factored shift
+// (DevSolve: lam, g and the 16-point tables).  lam = 0, g = 1 (the identity
+// "solve" of an ARK final combination) zeroes every carry.
+void fill_carry_lev(CarryLevParams& cp, const DevSolve& sv)
+{
+    cp.lam = sv.lam;
+    cp.g = sv.g;
+    cp.inv1ml2 = 1.0 / (1.0 - sv.lam * sv.lam);
+    cp.zc = sv.lam * cp.inv1ml2;
+    for (int e = 0; e < 16; ++e) {
+        cp.pw[e] = sv.pw[e];
+        cp.zf[e] = sv.zf16[e];
+    }
+    for (int i = 0; i < 10; ++i) cp.mp[i] = sv.mp16[i];
+}
+
 // Carry-exchange level tick (ridc_carry_levels.cuh): RIDC order >= 2 on a
 // periodic reaction-diffusion line of a multiple of 512 points, at most
 // kClWarps x SMs chunks, carry reach <= 512; one launch per tick in the graph.
@@ -1208,15 +1237,7 @@ int setup_carry_levels(ridc_ctx* c)
     const int wpc = (nchunk + grid - 1) / grid;
     CarryLevParams& cp = c->clparams;
     memset(&cp, 0, sizeof cp);
-    cp.lam = lam;
-    cp.g = c->ss.sv.g;
-    cp.inv1ml2 = 1.0 / (1.0 - lam * lam);
-    cp.zc = lam * cp.inv1ml2;
-    for (int e = 0; e < 16; ++e) {
-        cp.pw[e] = c->ss.sv.pw[e];
-        cp.zf[e] = c->ss.sv.zf16[e];
-    }
-    for (int i = 0; i < 10; ++i) cp.mp[i] = c->ss.sv.mp16[i];
+    fill_carry_lev(cp, c->ss.sv);
     cp.nx = pb.nx;
     cp.GW = c->ss.lay.GW;
     cp.gdata = c->ss.lay.gdata;
@@ -1425,6 +1446,7 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
                 int64_t steps, int32_t restarts, const double* weights, int64_t nweights,
                 int32_t device, uint32_t flags, ridc_ctx** out)
 {
+    NvtxRange nvtx_("ridc.create");
     if (!out) return fail(nullptr, RIDC_E_CONFIG, "out is NULL");
     *out = nullptr;
     int rc = validate_problem(problem);
@@ -1584,6 +1606,7 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
 int ridc_run(ridc_ctx* c, const double* y0_host, double* final_host, double* level_finals_host,
              double* traj_host, double* wall_seconds)
 {
+    NvtxRange nvtx_("ridc.run");
     if (!c || !y0_host || !final_host) return fail(c ? &c->err : nullptr, RIDC_E_CONFIG, "NULL argument");
     if (traj_host && !(c->flags & RIDC_RECORD_TRAJECTORY))
         return fail(&c->err, RIDC_E_CONFIG, "trajectory requested but not recorded (flags)");
@@ -1608,6 +1631,7 @@ int ridc_run(ridc_ctx* c, const double* y0_host, double* final_host, double* lev
 
 int ridc_run_device(ridc_ctx* c, const double* y0_dev, double* final_dev, double* wall_seconds)
 {
+    NvtxRange nvtx_("ridc.run_device");
     if (!c || !y0_dev || !final_dev) return fail(c ? &c->err : nullptr, RIDC_E_CONFIG, "NULL argument");
     CUDA_TRY(&c->err, cudaSetDevice(c->device));
     const size_t vb = (size_t)c->V * sizeof(double);
@@ -1898,7 +1922,17 @@ bool device_can_flush_remote(int device)
 constexpr uint32_t kBlobMagic = 0x52494443u;   // "RIDC"
 constexpr size_t kFlagBytes = 4096;            // wm (+0), rel (+8), pub[nseg] (+256), relv[nseg] (+2048), then the inbox ring
 constexpr size_t kPubOff = 256, kRelOff = 2048;
+// levels x shards words (after relv[kPipeMaxSeg]): global step numbers
+constexpr size_t kWInUp = 3840;     // inbox ghost row 0 delivered (by level-1, shard-1)
+constexpr size_t kWInDn = 3848;     // inbox ghost row n+1 delivered (by level-1, shard+1)
+constexpr size_t kWRelUp = 3856;    // released-below of consumer (level+1, shard-1)
+constexpr size_t kWRelDn = 3864;    // released-below of consumer (level+1, shard+1)
+constexpr size_t kWGhUp = 3872;     // own ghost row 0 delivered (by level, shard-1)
+constexpr size_t kWGhDn = 3880;     // own ghost row n+1 delivered (by level, shard+1)
+constexpr size_t kWDoneUp = 3888;   // (level, shard-1) finished step g
+constexpr size_t kWDoneDn = 3896;   // (level, shard+1) finished step g
 constexpr int kPipeMaxSeg = (int)((kRelOff - kPubOff) / 8);
+static_assert(kRelOff + 8 * kPipeMaxSeg <= kWInUp && kWDoneDn + 8 <= kFlagBytes, "mailbox words overlap");
 
 struct PipeBlob {
     uint32_t magic;
@@ -1908,6 +1942,7 @@ struct PipeBlob {
     int64_t inbox_cap;
     int64_t vs;
     int32_t resident;      // resident level march (device-side flags) vs stream memops
+    int32_t shard, nshards, rows;   // row shard of a levels x shards grid (rows: local ny incl. 2 ghost rows)
 };
 
 }  // namespace
@@ -1932,7 +1967,30 @@ struct ridc_pipe {
     long long next_cap = 0;
     unsigned long long* next_wm = nullptr;
     unsigned long long* prev_rel = nullptr;
-    void* opened[2] = {nullptr, nullptr};
+    void* opened[8] = {};
+    uint64_t opened_direct[8] = {};
+    int32_t opened_pid[8] = {};
+    // levels x row shards (ridc_pipe_create_shard): this rank computes level
+    // `level` on rows [r0, r0 + nrows) of a gny-row grid, held as a local grid
+    // of nrows + 2 rows (ghost rows 0 and nrows + 1); the own ring lives in the
+    // mailbox allocation so the neighbour shards can deliver its ghost rows
+    int shard = 0, nshards = 1, r0 = 0, nrows = 0, gny = 0;
+    double* d_s0 = nullptr;                       // the interval's state0 rows r0-1 .. r0+nrows (local seed)
+    double* up_inbox = nullptr;                   // (level+1, shard-1)'s inbox ring
+    double* dn_inbox = nullptr;                   // (level+1, shard+1)'s inbox ring
+    int up_rows = 0, dn_rows = 0;                 // local rows (ghosts included) of shards s-1 / s+1
+    unsigned long long* up_in_wm = nullptr;       // its W_INDN: my first row landed in its ghost row n+1
+    unsigned long long* dn_in_wm = nullptr;       // its W_INUP: my last row landed in its ghost row 0
+    unsigned long long* prev_up_rel = nullptr;    // (level-1, shard-1)'s W_RELDN: I release my ghost-row-0 slots
+    unsigned long long* prev_dn_rel = nullptr;    // (level-1, shard+1)'s W_RELUP
+    double* side_up_own = nullptr;                // (level, shard-1)'s own ring
+    double* side_dn_own = nullptr;                // (level, shard+1)'s own ring
+    unsigned long long* side_up_gh = nullptr;     // its W_GHDN: my first row landed in its ghost row n+1
+    unsigned long long* side_dn_gh = nullptr;     // its W_GHUP
+    unsigned long long* side_up_done = nullptr;   // its W_DONEDN: I finished step g
+    unsigned long long* side_dn_done = nullptr;   // its W_DONEUP
+    bool up_remote = false, dn_remote = false;    // the up / down neighbours of the previous level sit on another device
+    bool sup_remote = false, sdn_remote = false;  // the same-level neighbours
     double* d_weights = nullptr;
     double* d_tab = nullptr;
     ChunkGeo* d_cgeo = nullptr;
@@ -2007,6 +2065,7 @@ EngineParams pipe_params(ridc_pipe* p, long long g0)
     }
     ep.lay = p->ss.lay;
     ep.cgeo = p->d_cgeo;
+    if (p->nshards > 1) ep.row0 = 1;   // rows 1..nrows; rows 0 and nrows + 1 are the neighbours' ghosts
     return ep;
 }
 
@@ -2060,21 +2119,122 @@ int pipe_enqueue(ridc_pipe* p, int interval, long long* launches)
     return RIDC_OK;
 }
 
+// One interval of a levels x shards rank (stream memops only).  Per step t
+// (global step g): wait for the window -- my inbox interior from (j-1, s) and
+// its ghost rows 0 / n+1 from (j-1, s-1) / (j-1, s+1) -- for my own ghost rows
+// of step g-1 from (j, s-1) / (j, s+1), and for ring space at my three
+// consumers; run the tick kernel on my rows (storing into (j+1, s)'s inbox);
+// then deliver: my first / last row into the same-level neighbours' own ring
+// (once they finished step g-1) and into the diagonal consumers' inbox ghost
+// rows, raise every watermark, report step g done and release the producers'
+// slots below my next window (LevelBuffer's protocol, engine.py:284-331, per
+// neighbour).
+int pipe_enqueue_shard(ridc_pipe* p, int interval, long long* launches)
+{
+    const DriverOps& ops = driver_ops();
+    const int j = p->level, top = p->levels - 1;
+    const long long g0 = (long long)interval * p->per;
+    const EngineParams ep = pipe_params(p, g0);
+    const int items = p->nrows * p->ss.sv.nseg;
+    CUstream cs = reinterpret_cast<CUstream>(p->stream);
+    const long long spin = (long long)(p->watchdog * 2.0e9);
+    const size_t P = (size_t)p->ss.lay.P, rowb = P * sizeof(double);
+    const size_t Vs = (size_t)p->Vs;
+    const size_t vs_up = (size_t)p->up_rows * P, vs_dn = (size_t)p->dn_rows * P;
+    auto word = [&](size_t off) { return reinterpret_cast<unsigned long long*>(p->mailbox + off); };
+    auto wait = [&](const unsigned long long* f, long long v, bool remote) {
+        return wait_value(p->stream, f, (unsigned long long)v, remote, p->can_flush, p->d_abort, spin) == cudaSuccess;
+    };
+    auto write = [&](unsigned long long* f, long long v) {
+        return ops.write(cs, (CUdeviceptr)f, (cuuint64_t)v, CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS;
+    };
+    auto copy_row = [&](double* dst, const double* src) {
+        return cudaMemcpyAsync(dst, src, rowb, cudaMemcpyDefault, p->stream) == cudaSuccess;
+    };
+    long long n = 0;
+    for (long long t = 1; t <= p->per; ++t) {
+        const long long g = g0 + t;
+        if (j > 0) {
+            const long long need = g0 + (t < j ? j : t);
+            if (!wait(p->wm, need, p->prev_remote) || !wait(word(kWInUp), need, p->up_remote) ||
+                !wait(word(kWInDn), need, p->dn_remote))
+                return pipe_fail(p, RIDC_E_CUDA, "watermark wait failed");
+        }
+        if (t > 1 && (!wait(word(kWGhUp), g - 1, p->sup_remote) || !wait(word(kWGhDn), g - 1, p->sdn_remote)))
+            return pipe_fail(p, RIDC_E_CUDA, "ghost-row wait failed");
+        if (j < top) {
+            const long long need_rel = g - p->next_cap + 1;
+            if (need_rel > 0 && (!wait(p->rel, need_rel, false) || !wait(word(kWRelUp), need_rel, false) ||
+                                 !wait(word(kWRelDn), need_rel, false)))
+                return pipe_fail(p, RIDC_E_CUDA, "release wait failed");
+        }
+        TickParams tp;
+        memset(&tp, 0, sizeof tp);
+        tp.sv = ep.sv;
+        tp.nact = 1;
+        tp.level[0] = j;
+        tp.target[0] = t;
+        cudaError_t le = launch_chunk(p->pb.kind, p->ss.ccfg, std::min(p->nsm * chunk_ctas_per_sm(p->ss.ccfg, 1), items),
+                                      p->stream, ep, tp, items, p->tm);
+        if (le != cudaSuccess) return pipe_fail(p, RIDC_E_CUDA, std::string("tick launch: ") + cudaGetErrorString(le));
+        ++n;
+        const double* mine = p->own + (g % 2) * Vs;
+        const double* first = mine + P, *last = mine + (size_t)p->nrows * P;
+        // my boundary rows -> the same-level neighbours' own slot of step g (their ghost rows),
+        // once each finished step g-1 (its last read of that slot's old content)
+        if (t > 1 && (!wait(word(kWDoneUp), g - 1, p->sup_remote) || !wait(word(kWDoneDn), g - 1, p->sdn_remote)))
+            return pipe_fail(p, RIDC_E_CUDA, "neighbour progress wait failed");
+        if (!copy_row(p->side_up_own + (g % 2) * vs_up + (size_t)(p->up_rows - 1) * P, first) ||
+            !copy_row(p->side_dn_own + (g % 2) * vs_dn, last) || !write(p->side_up_gh, g) || !write(p->side_dn_gh, g))
+            return pipe_fail(p, RIDC_E_CUDA, "ghost-row delivery failed");
+        if (j < top) {   // the diagonal consumers' inbox ghost rows, then every consumer's watermark
+            const long long slot = g % p->next_cap;
+            if (!copy_row(p->up_inbox + slot * vs_up + (size_t)(p->up_rows - 1) * P, first) ||
+                !copy_row(p->dn_inbox + slot * vs_dn, last) || !write(p->up_in_wm, g) || !write(p->dn_in_wm, g) ||
+                !write(p->next_wm, g))
+                return pipe_fail(p, RIDC_E_CUDA, "inbox ghost-row delivery failed");
+        }
+        if (!write(p->side_up_done, g) || !write(p->side_dn_done, g))
+            return pipe_fail(p, RIDC_E_CUDA, "progress write failed");
+        if (j > 0) {
+            const long long below = g0 + std::max(0LL, t + 1 - j);
+            if (!write(p->prev_rel, below) || !write(p->prev_up_rel, below) || !write(p->prev_dn_rel, below))
+                return pipe_fail(p, RIDC_E_CUDA, "release write failed");
+        }
+    }
+    *launches = n;
+    return RIDC_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 int64_t ridc_pipe_handle_bytes(void) { return (int64_t)sizeof(PipeBlob); }
 
-int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, int32_t levels,
-                     int64_t steps, int32_t restarts, const double* weights, int64_t nweights,
-                     int32_t level, int32_t device, int32_t inbox_capacity, double watchdog_seconds,
-                     ridc_pipe** out)
+static int pipe_create(const ridc_problem* gproblem, double t_start, double t_end, int32_t levels,
+                       int64_t steps, int32_t restarts, const double* weights, int64_t nweights,
+                       int32_t level, int32_t shard, int32_t nshards, int32_t device, int32_t inbox_capacity,
+                       double watchdog_seconds, ridc_pipe** out)
 {
     if (!out) return pipe_fail(nullptr, RIDC_E_CONFIG, "out is NULL");
     *out = nullptr;
-    int rc = validate_problem(problem);
+    int rc = validate_problem(gproblem);
     if (rc) return rc;
+    // a row shard computes its rows of the global grid as a local grid with one
+    // ghost row per side (the tiling along x depends on nx and dt only)
+    ridc_problem sub = *gproblem;
+    int r0 = 0, nrows = gproblem->ny;
+    if (nshards > 1) {
+        if (gproblem->kind != RIDC_ADV_DIFF_2D && gproblem->kind != RIDC_REACTION_DIFFUSION_2D)
+            return pipe_fail(nullptr, RIDC_E_CONFIG, "row shards need a 2-D kind (explicit in y)");
+        if (nshards > gproblem->ny) return pipe_fail(nullptr, RIDC_E_CONFIG, "need 2 <= shards <= ny");
+        if (shard < 0 || shard >= nshards) return pipe_fail(nullptr, RIDC_E_CONFIG, "shard out of range");
+        r0 = (int)((long long)gproblem->ny * shard / nshards);
+        nrows = (int)((long long)gproblem->ny * (shard + 1) / nshards) - r0;
+        sub.ny = nrows + 2;
+    }
+    const ridc_problem* problem = &sub;
     if (levels < 1 || levels > kMaxLevels) return pipe_fail(nullptr, RIDC_E_CONFIG, "levels must be in 1..12");
     if (level < 0 || level >= levels) return pipe_fail(nullptr, RIDC_E_CONFIG, "level out of range");
     if (steps < 1 || restarts < 1 || steps % restarts)
@@ -2099,6 +2259,11 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     ridc_pipe* p = new ridc_pipe();
     p->device = device;
     p->level = level;
+    p->shard = nshards > 1 ? shard : 0;
+    p->nshards = nshards > 1 ? nshards : 1;
+    p->r0 = r0;
+    p->nrows = nrows;
+    p->gny = gproblem->ny;
     p->levels = levels;
     p->restarts = restarts;
     p->steps = steps;
@@ -2157,15 +2322,23 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     P_TRY(cudaMemset(p->d_abort, 0, sizeof(unsigned)));
     p->can_flush = device_can_flush_remote(device);
     // mailbox: flags, then the inbox ring (cap slots of ny padded rows); zeroed: Dirichlet ghosts
+    // (a row shard's own 2-slot ring follows the inbox ring in the same
+    // allocation: its neighbour shards deliver the own ghost rows through it)
     const size_t ring_bytes = (size_t)p->inbox_cap * p->Vs * sizeof(double);
-    P_TRY(cudaMalloc(&p->mailbox, kFlagBytes + ring_bytes));
-    P_TRY(cudaMemset(p->mailbox, 0, kFlagBytes + ring_bytes));
+    const size_t own_bytes = p->nshards > 1 ? (size_t)2 * p->Vs * sizeof(double) : 0;
+    P_TRY(cudaMalloc(&p->mailbox, kFlagBytes + ring_bytes + own_bytes));
+    P_TRY(cudaMemset(p->mailbox, 0, kFlagBytes + ring_bytes + own_bytes));
     p->wm = reinterpret_cast<unsigned long long*>(p->mailbox);
     p->rel = reinterpret_cast<unsigned long long*>(p->mailbox + 8);
     p->inbox = reinterpret_cast<double*>(p->mailbox + kFlagBytes);
-    P_TRY(cudaMalloc(&p->own_base, ((size_t)2 * p->Vs + 2 * p->V) * sizeof(double)));
-    P_TRY(cudaMemset(p->own_base, 0, (size_t)2 * p->Vs * sizeof(double)));
-    p->own = p->own_base;
+    if (p->nshards > 1) {
+        p->own = reinterpret_cast<double*>(p->mailbox + kFlagBytes + ring_bytes);
+        P_TRY(cudaMalloc(&p->d_s0, (size_t)p->V * sizeof(double)));
+    } else {
+        P_TRY(cudaMalloc(&p->own_base, ((size_t)2 * p->Vs + 2 * p->V) * sizeof(double)));
+        P_TRY(cudaMemset(p->own_base, 0, (size_t)2 * p->Vs * sizeof(double)));
+        p->own = p->own_base;
+    }
     memset(&p->tm, 0, sizeof p->tm);
     if ((rc = make_ring_map(&p->tm.map[level], p->own, p->Vs, 2, chunk_groups(p->ss.ccfg), &p->err)) != RIDC_OK)
         return bail(rc);
@@ -2173,7 +2346,7 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
         (rc = make_ring_map(&p->tm.map[level - 1], p->inbox, p->Vs, p->inbox_cap, chunk_groups(p->ss.ccfg), &p->err)) != RIDC_OK)
         return bail(rc);
     // resident level march: 1-D lines whose segments fit one co-resident CTA each
-    if (levels >= 2 && p->ss.sv.nseg <= kPipeMaxSeg && res_geometry(p->pb, p->ss, p->rgeo) &&
+    if (levels >= 2 && p->nshards == 1 && p->ss.sv.nseg <= kPipeMaxSeg && res_geometry(p->pb, p->ss, p->rgeo) &&
         !(getenv("RIDC_NO_RESIDENT_LEVELS") && atoi(getenv("RIDC_NO_RESIDENT_LEVELS")) > 0)) {
         LevelsParams lp;
         memset(&lp, 0, sizeof lp);
@@ -2202,6 +2375,25 @@ int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, 
     return RIDC_OK;
 }
 
+int ridc_pipe_create(const ridc_problem* problem, double t_start, double t_end, int32_t levels,
+                     int64_t steps, int32_t restarts, const double* weights, int64_t nweights,
+                     int32_t level, int32_t device, int32_t inbox_capacity, double watchdog_seconds,
+                     ridc_pipe** out)
+{
+    return pipe_create(problem, t_start, t_end, levels, steps, restarts, weights, nweights, level, 0, 1, device,
+                       inbox_capacity, watchdog_seconds, out);
+}
+
+int ridc_pipe_create_shard(const ridc_problem* problem, double t_start, double t_end, int32_t levels,
+                           int64_t steps, int32_t restarts, const double* weights, int64_t nweights,
+                           int32_t level, int32_t shard, int32_t nshards, int32_t device,
+                           int32_t inbox_capacity, double watchdog_seconds, ridc_pipe** out)
+{
+    if (nshards < 2) return pipe_fail(nullptr, RIDC_E_CONFIG, "need 2 <= shards <= ny");
+    return pipe_create(problem, t_start, t_end, levels, steps, restarts, weights, nweights, level, shard, nshards,
+                       device, inbox_capacity, watchdog_seconds, out);
+}
+
 int ridc_pipe_export(ridc_pipe* p, void* blob)
 {
     if (!p || !blob) return pipe_fail(p, RIDC_E_CONFIG, "NULL argument");
@@ -2215,6 +2407,9 @@ int ridc_pipe_export(ridc_pipe* p, void* blob)
     b.inbox_cap = p->inbox_cap;
     b.vs = p->Vs;
     b.resident = p->reslev ? 1 : 0;
+    b.shard = p->shard;
+    b.nshards = p->nshards;
+    b.rows = (int32_t)p->pb.ny;
     PIPE_TRY(p, cudaSetDevice(p->device));
     PIPE_TRY(p, cudaIpcGetMemHandle(&b.handle, p->mailbox));
     memcpy(blob, &b, sizeof b);
@@ -2250,9 +2445,115 @@ static int open_blob(ridc_pipe* p, const void* blob, int want_level, char** base
     return RIDC_OK;
 }
 
+// A neighbour of a levels x shards rank: (want_level, want_shard) of the same
+// grid.  Handles already opened by this rank (the two diagonal neighbours are
+// one rank when there are two shards) are reused.
+static int open_blob_shard(ridc_pipe* p, const void* blob, int want_level, int want_shard, int slot,
+                           PipeBlob* out, char** base)
+{
+    PipeBlob b;
+    memcpy(&b, blob, sizeof b);
+    if (b.magic != kBlobMagic || b.level != want_level || b.shard != want_shard || b.nshards != p->nshards ||
+        b.resident != 0 || b.vs != (int64_t)b.rows * p->ss.lay.P)
+        return pipe_fail(p, RIDC_E_PROTOCOL, "levels x shards handle from an incompatible rank");
+    if (b.pid == (int32_t)getpid()) {
+        *base = reinterpret_cast<char*>((uintptr_t)b.direct);
+        if (b.device != p->device) {
+            cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return pipe_fail(p, RIDC_E_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+            cudaGetLastError();
+        }
+    } else {
+        for (int k = 0; k < slot; ++k)   // same handle as an earlier neighbour
+            if (p->opened[k] && p->opened_direct[k] == b.direct && p->opened_pid[k] == b.pid) {
+                *base = reinterpret_cast<char*>(p->opened[k]);
+                *out = b;
+                return RIDC_OK;
+            }
+        void* ptr = nullptr;
+        PIPE_TRY(p, cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
+        p->opened[slot] = ptr;
+        p->opened_direct[slot] = b.direct;
+        p->opened_pid[slot] = b.pid;
+        *base = reinterpret_cast<char*>(ptr);
+    }
+    *out = b;
+    return RIDC_OK;
+}
+
+int ridc_pipe_connect_shard(ridc_pipe* p, const void* const* blobs)
+{
+    if (!p || !blobs) return pipe_fail(p, RIDC_E_CONFIG, "NULL argument");
+    if (p->nshards < 2) return pipe_fail(p, RIDC_E_CONFIG, "not a row-shard rank (ridc_pipe_connect)");
+    PIPE_TRY(p, cudaSetDevice(p->device));
+    const int j = p->level, top = p->levels - 1, S = p->nshards;
+    const int su = (p->shard + S - 1) % S, sd = (p->shard + 1) % S;
+    for (int k = 0; k < 8; ++k) {
+        const bool want = k < 3 ? j > 0 : k < 6 ? j < top : true;
+        if (want != (blobs[k] != nullptr))
+            return pipe_fail(p, RIDC_E_CONFIG, "shard rank needs exactly its existing neighbours");
+    }
+    int rc;
+    PipeBlob b;
+    char* base = nullptr;
+    if (j > 0) {
+        // (j-1, s): my inbox interior; its release counter
+        if ((rc = open_blob_shard(p, blobs[0], j - 1, p->shard, 0, &b, &base)) != RIDC_OK) return rc;
+        p->prev_remote = b.device != p->device;
+        p->prev_rel = reinterpret_cast<unsigned long long*>(base + 8);
+        // (j-1, s-1) delivers my inbox ghost row 0 (its last row); I release to its W_RELDN
+        if ((rc = open_blob_shard(p, blobs[1], j - 1, su, 1, &b, &base)) != RIDC_OK) return rc;
+        p->up_remote = b.device != p->device;
+        p->prev_up_rel = reinterpret_cast<unsigned long long*>(base + kWRelDn);
+        // (j-1, s+1) delivers my inbox ghost row n+1 (its first row); I release to its W_RELUP
+        if ((rc = open_blob_shard(p, blobs[2], j - 1, sd, 2, &b, &base)) != RIDC_OK) return rc;
+        p->dn_remote = b.device != p->device;
+        p->prev_dn_rel = reinterpret_cast<unsigned long long*>(base + kWRelUp);
+    }
+    if (j < top) {
+        if ((rc = open_blob_shard(p, blobs[3], j + 1, p->shard, 3, &b, &base)) != RIDC_OK) return rc;
+        p->next_wm = reinterpret_cast<unsigned long long*>(base);
+        p->next_inbox = reinterpret_cast<double*>(base + kFlagBytes);
+        p->next_cap = b.inbox_cap;
+        if ((rc = open_blob_shard(p, blobs[4], j + 1, su, 4, &b, &base)) != RIDC_OK) return rc;
+        if (b.inbox_cap != p->next_cap) return pipe_fail(p, RIDC_E_CONFIG, "consumer shards disagree on inbox capacity");
+        p->up_inbox = reinterpret_cast<double*>(base + kFlagBytes);
+        p->up_in_wm = reinterpret_cast<unsigned long long*>(base + kWInDn);
+        if ((rc = open_blob_shard(p, blobs[5], j + 1, sd, 5, &b, &base)) != RIDC_OK) return rc;
+        if (b.inbox_cap != p->next_cap) return pipe_fail(p, RIDC_E_CONFIG, "consumer shards disagree on inbox capacity");
+        p->dn_inbox = reinterpret_cast<double*>(base + kFlagBytes);
+        p->dn_in_wm = reinterpret_cast<unsigned long long*>(base + kWInUp);
+    }
+    // (j, s-1) / (j, s+1): own ghost rows both ways, and step-done counters
+    if ((rc = open_blob_shard(p, blobs[6], j, su, 6, &b, &base)) != RIDC_OK) return rc;
+    p->sup_remote = b.device != p->device;
+    p->side_up_own = reinterpret_cast<double*>(base + kFlagBytes + (size_t)b.inbox_cap * b.vs * sizeof(double));
+    p->side_up_gh = reinterpret_cast<unsigned long long*>(base + kWGhDn);
+    p->side_up_done = reinterpret_cast<unsigned long long*>(base + kWDoneDn);
+    p->up_rows = b.rows;   // shard s-1's local rows (its ranks of every level)
+    if ((rc = open_blob_shard(p, blobs[7], j, sd, 7, &b, &base)) != RIDC_OK) return rc;
+    p->sdn_remote = b.device != p->device;
+    p->side_dn_own = reinterpret_cast<double*>(base + kFlagBytes + (size_t)b.inbox_cap * b.vs * sizeof(double));
+    p->side_dn_gh = reinterpret_cast<unsigned long long*>(base + kWGhUp);
+    p->side_dn_done = reinterpret_cast<unsigned long long*>(base + kWDoneUp);
+    p->dn_rows = b.rows;
+    return RIDC_OK;
+}
+
+int ridc_pipe_reset(ridc_pipe* p)
+{
+    if (!p) return pipe_fail(nullptr, RIDC_E_CONFIG, "NULL pipe");
+    PIPE_TRY(p, cudaSetDevice(p->device));
+    PIPE_TRY(p, cudaStreamSynchronize(p->stream));
+    PIPE_TRY(p, cudaMemset(p->mailbox, 0, kFlagBytes));
+    return RIDC_OK;
+}
+
 int ridc_pipe_connect(ridc_pipe* p, const void* prev_blob, const void* next_blob)
 {
     if (!p) return pipe_fail(nullptr, RIDC_E_CONFIG, "NULL pipe");
+    if (p->nshards > 1) return pipe_fail(p, RIDC_E_CONFIG, "row-shard rank: use ridc_pipe_connect_shard");
     PIPE_TRY(p, cudaSetDevice(p->device));
     const int j = p->level, top = p->levels - 1;
     if ((j > 0) != (prev_blob != nullptr) || (j < top) != (next_blob != nullptr))
@@ -2304,14 +2605,24 @@ int ridc_pipe_connect(ridc_pipe* p, const void* prev_blob, const void* next_blob
 int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_dev, double* final_dev,
                            double* wall_seconds)
 {
+    NvtxRange nvtx_("ridc.pipe_interval");
     if (!p || !state0_dev || !final_dev) return pipe_fail(p, RIDC_E_CONFIG, "NULL argument");
     if (interval < 0 || interval >= p->restarts) return pipe_fail(p, RIDC_E_CONFIG, "interval out of range");
     const int j = p->level, top = p->levels - 1;
-    if ((j > 0 && !p->prev_rel) || (j < top && !p->next_inbox))
+    if ((j > 0 && !p->prev_rel) || (j < top && !p->next_inbox) || (p->nshards > 1 && !p->side_up_own))
         return pipe_fail(p, RIDC_E_CONFIG, "pipeline rank not connected");
     PIPE_TRY(p, cudaSetDevice(p->device));
     const long long g0 = (long long)interval * p->per;
-    const size_t vb = (size_t)p->V * sizeof(double);
+    if (p->nshards > 1) {
+        // a row shard seeds from global rows r0-1 .. r0+nrows (periodic in y)
+        const size_t rb = (size_t)p->pb.nx * sizeof(double);
+        for (int lr = 0; lr < p->nrows + 2; ++lr) {
+            const int gr = ((p->r0 - 1 + lr) % p->gny + p->gny) % p->gny;
+            PIPE_TRY(p, cudaMemcpyAsync(p->d_s0 + (size_t)lr * p->pb.nx, state0_dev + (size_t)gr * p->pb.nx, rb,
+                                        cudaMemcpyDeviceToDevice, p->stream));
+        }
+        state0_dev = p->d_s0;
+    }
     // seed: step g0 of my own ring and of my inbox is the interval's state0
     // (plain state -> padded rows with periodic ghosts)
     EngineParams ep = pipe_params(p, g0);
@@ -2371,7 +2682,7 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
         cudaGraphExec_t exec = nullptr;
         bool captured = false;
         if (cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-            int rc = pipe_enqueue(p, interval, &launches);
+            int rc = p->nshards > 1 ? pipe_enqueue_shard(p, interval, &launches) : pipe_enqueue(p, interval, &launches);
             cudaError_t ce = cudaStreamEndCapture(p->stream, &graph);
             if (rc == RIDC_OK && ce == cudaSuccess && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess)
                 captured = true;
@@ -2382,7 +2693,8 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
             p->graphs[interval] = exec;
             PIPE_TRY(p, cudaGraphLaunch(exec, p->stream));
         } else {
-            int rc = pipe_enqueue(p, interval, &launches);   // direct enqueue fallback
+            int rc = p->nshards > 1 ? pipe_enqueue_shard(p, interval, &launches)
+                                    : pipe_enqueue(p, interval, &launches);   // direct enqueue fallback
             if (rc) return rc;
         }
     } else {
@@ -2393,9 +2705,10 @@ int ridc_pipe_run_interval(ridc_pipe* p, int32_t interval, const double* state0_
     {
         const ChunkLayout& Ly = p->ss.lay;
         const double* fin = ep.ring[j] + ((ep.off[j] + p->per) % 2) * p->Vs;
-        PIPE_TRY(p, cudaMemcpy2DAsync(final_dev, (size_t)p->pb.nx * sizeof(double), fin + Ly.GW,
+        const int r_first = p->nshards > 1 ? 1 : 0, nr = p->nshards > 1 ? p->nrows : (int)p->pb.ny;
+        PIPE_TRY(p, cudaMemcpy2DAsync(final_dev, (size_t)p->pb.nx * sizeof(double), fin + (size_t)r_first * Ly.P + Ly.GW,
                                       (size_t)Ly.P * sizeof(double), (size_t)p->pb.nx * sizeof(double),
-                                      (size_t)p->pb.ny, cudaMemcpyDeviceToDevice, p->stream));
+                                      (size_t)nr, cudaMemcpyDeviceToDevice, p->stream));
     }
     PIPE_TRY(p, cudaEventRecord(p->ev1, p->stream));
     // watchdog (engine.py:432-439): neighbours that never publish turn into an error
@@ -2469,6 +2782,7 @@ int ridc_pipe_destroy(ridc_pipe* p)
         if (o) cudaIpcCloseMemHandle(o);
     if (p->mailbox) cudaFree(p->mailbox);
     if (p->own_base) cudaFree(p->own_base);
+    if (p->d_s0) cudaFree(p->d_s0);
     if (p->d_weights) cudaFree(p->d_weights);
     if (p->d_tab) cudaFree(p->d_tab);
     if (p->d_cgeo) cudaFree(p->d_cgeo);
@@ -2546,6 +2860,15 @@ struct ridc_ark_ctx {
     cudaGraphExec_t gexec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
+    // the carry-exchange tick for every stage (periodic RD lines of 512-point chunks)
+    bool carrylev = false;
+    int cl_grid = 0, cl_wpc = 0;
+    std::vector<CarryLevParams> clp;   // per item: the stage's solve
+    TmapSet tm_cl;
+    uint4* d_clx = nullptr;
+    unsigned* d_clepoch = nullptr;
+    unsigned* d_abort = nullptr;
+    double watchdog = 30.0;
     std::string err;
 };
 
@@ -2719,15 +3042,65 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
     ARK_TRY(cudaMalloc(&a->d_items, items.size() * sizeof(StepItem)));
     ARK_TRY(cudaMemcpy(a->d_items, items.data(), items.size() * sizeof(StepItem), cudaMemcpyHostToDevice));
 
+    // ---- the carry-exchange tick (ridc_carry_levels.cuh) for every stage where
+    // the line qualifies: periodic RD, 512-point chunks, the stiffest stage's
+    // carry reach <= 512
+    {
+        const int nchunk = a->pb.nx / 512;
+        const bool off = getenv("RIDC_NO_CARRYLEV") && atoi(getenv("RIDC_NO_CARRYLEV")) > 0;
+        if (!off && a->pb.kind == RD_1D && a->pb.ny == 1 && a->pb.nx % 512 == 0 && nchunk >= 2 &&
+            nchunk <= kClWarps * a->nsm && halo_of(a->ss.sv.lam) <= 512 && a->ss.lay.GW >= 16 &&
+            (long long)steps * a->nitems < 0x7fffffffLL) {
+            const int grid = std::min(a->nsm, nchunk), wpc = (nchunk + grid - 1) / grid;
+            const size_t xb = (size_t)2 * kMaxLevels * nchunk * sizeof(uint4);
+            ARK_TRY(cudaMalloc(&a->d_clx, xb));
+            ARK_TRY(cudaMemset(a->d_clx, 0, xb));
+            ARK_TRY(cudaMalloc(&a->d_clepoch, sizeof(unsigned)));
+            ARK_TRY(cudaMemset(a->d_clepoch, 0, sizeof(unsigned)));
+            ARK_TRY(cudaMalloc(&a->d_abort, sizeof(unsigned)));
+            ARK_TRY(cudaMemset(a->d_abort, 0, sizeof(unsigned)));
+            a->clp.resize(a->nitems);
+            for (int k = 0; k < a->nitems; ++k) {
+                CarryLevParams& cp = a->clp[k];
+                memset(&cp, 0, sizeof cp);
+                fill_carry_lev(cp, a->solves[k].sv);
+                cp.nx = a->pb.nx;
+                cp.GW = a->ss.lay.GW;
+                cp.gdata = a->ss.lay.gdata;
+                cp.nchunk = nchunk;
+                cp.wpc = wpc;
+                cp.xch = a->d_clx;
+                cp.epoch = a->d_clepoch;
+                cp.ticks = (unsigned)(steps * a->nitems + 1);
+                cp.abort = a->d_abort;
+                cp.spin_limit = (long long)(a->watchdog * 2.0e9);
+            }
+            memset(&a->tm_cl, 0, sizeof a->tm_cl);
+            if ((rc = make_ring_map(&a->tm_cl.map[0], a->d_ring, a->Vs, a->cap, kClBoxGroups, &a->err)) != RIDC_OK)
+                return bail(rc);
+            a->cl_grid = (nchunk + wpc - 1) / wpc;
+            a->cl_wpc = wpc;
+            a->carrylev = true;
+        }
+    }
+
     // ---- capture: seed y_0 into slot 0, then per step one launch per item
     const int tiles = a->pb.ny * a->ss.sv.nseg;
     cudaGraph_t graph = nullptr;
     ARK_TRY(cudaStreamBeginCapture(a->stream, cudaStreamCaptureModeThreadLocal));
     cudaError_t le = cudaSuccess;
+    long long launches = 0;
+    if (a->carrylev) {   // a fresh tag epoch for the exchange lines of this run
+        k_bump_epoch<<<1, 1, 0, a->stream>>>(a->d_clepoch);
+        le = cudaGetLastError();
+        ++launches;
+    }
     const int sb = (int)std::min<long long>((a->Vs + 255) / 256, 148 * 8);
-    k_seed_chunk<<<sb, 256, 0, a->stream>>>(a->d_y0, ep, -1);
-    le = cudaGetLastError();
-    long long launches = 1;
+    if (le == cudaSuccess) {
+        k_seed_chunk<<<sb, 256, 0, a->stream>>>(a->d_y0, ep, -1);
+        le = cudaGetLastError();
+    }
+    ++launches;
     for (long long n = 0; n < steps && le == cudaSuccess; ++n) {
         const int parity = (int)(n & 1);
         for (int k = 0; k < a->nitems && le == cudaSuccess; ++k) {
@@ -2737,8 +3110,12 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
             tp.sv = a->solves[k].sv;
             tp.pre = a->d_items + parity * a->nitems + k;
             tp.target[0] = n + 1;
-            le = launch_chunk(a->pb.kind, a->ss.ccfg, std::min(a->nsm * chunk_ctas_per_sm(a->ss.ccfg, 1), tiles), a->stream,
-                              ep, tp, tiles, a->tm);
+            if (a->carrylev)
+                le = carry_levels_k<RD_1D>(a->cl_grid, a->cl_wpc, a->stream, ep, tp, a->clp[k], a->tm_cl,
+                                           (unsigned)(n * a->nitems + k + 1));
+            else
+                le = launch_chunk(a->pb.kind, a->ss.ccfg, std::min(a->nsm * chunk_ctas_per_sm(a->ss.ccfg, 1), tiles),
+                                  a->stream, ep, tp, tiles, a->tm);
             ++launches;
         }
     }
@@ -2761,6 +3138,7 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
 static int ark_march(ridc_ark_ctx* a, double* wall_seconds)
 {
     CUDA_TRY(&a->err, cudaMemsetAsync(a->d_err, 0xff, sizeof(unsigned long long), a->stream));
+    if (a->d_abort) CUDA_TRY(&a->err, cudaMemsetAsync(a->d_abort, 0, sizeof(unsigned), a->stream));
     CUDA_TRY(&a->err, cudaEventRecord(a->ev0, a->stream));
     CUDA_TRY(&a->err, cudaGraphLaunch(a->gexec, a->stream));
     CUDA_TRY(&a->err, cudaEventRecord(a->ev1, a->stream));
@@ -2769,6 +3147,11 @@ static int ark_march(ridc_ark_ctx* a, double* wall_seconds)
         float ms = 0.f;
         CUDA_TRY(&a->err, cudaEventElapsedTime(&ms, a->ev0, a->ev1));
         *wall_seconds = ms * 1e-3;
+    }
+    if (a->d_abort) {
+        unsigned ab = 0;
+        CUDA_TRY(&a->err, cudaMemcpy(&ab, a->d_abort, sizeof ab, cudaMemcpyDeviceToHost));
+        if (ab) return ark_fail(a, RIDC_E_PROTOCOL, "ARK march: a neighbour chunk's carry wait timed out");
     }
     unsigned long long w = 0;
     CUDA_TRY(&a->err, cudaMemcpy(&w, a->d_err, sizeof w, cudaMemcpyDeviceToHost));
@@ -2784,6 +3167,7 @@ static const double* ark_final(const ridc_ark_ctx* a) { return a->d_ring + (a->s
 
 int ridc_ark_run(ridc_ark_ctx* a, const double* y0_host, double* final_host, double* wall_seconds)
 {
+    NvtxRange nvtx_("ridc.ark_run");
     if (!a || !y0_host || !final_host) return ark_fail(a, RIDC_E_CONFIG, "NULL argument");
     CUDA_TRY(&a->err, cudaSetDevice(a->device));
     CUDA_TRY(&a->err, cudaMemcpyAsync(a->d_y0, y0_host, (size_t)a->V * sizeof(double), cudaMemcpyHostToDevice,
@@ -2800,6 +3184,7 @@ int ridc_ark_run(ridc_ark_ctx* a, const double* y0_host, double* final_host, dou
 
 int ridc_ark_run_device(ridc_ark_ctx* a, const double* y0_dev, double* final_dev, double* wall_seconds)
 {
+    NvtxRange nvtx_("ridc.ark_run_device");
     if (!a || !y0_dev || !final_dev) return ark_fail(a, RIDC_E_CONFIG, "NULL argument");
     CUDA_TRY(&a->err, cudaSetDevice(a->device));
     CUDA_TRY(&a->err, cudaMemcpyAsync(a->d_y0, y0_dev, (size_t)a->V * sizeof(double), cudaMemcpyDeviceToDevice,
@@ -2822,6 +3207,15 @@ int ridc_ark_info(const ridc_ark_ctx* a, int64_t* kernel_launches, int32_t* item
     return RIDC_OK;
 }
 
+int ridc_ark_path(const ridc_ark_ctx* a)
+{
+    if (!a) {
+        fail(nullptr, RIDC_E_CONFIG, "NULL argument");
+        return -1;
+    }
+    return a->carrylev ? RIDC_PATH_CARRY_LEVELS : RIDC_PATH_TICK;
+}
+
 int ridc_ark_destroy(ridc_ark_ctx* a)
 {
     if (!a) return RIDC_OK;
@@ -2833,6 +3227,9 @@ int ridc_ark_destroy(ridc_ark_ctx* a)
     if (a->d_ring) cudaFree(a->d_ring);
     if (a->d_cgeo) cudaFree(a->d_cgeo);
     if (a->d_items) cudaFree(a->d_items);
+    if (a->d_clx) cudaFree(a->d_clx);
+    if (a->d_clepoch) cudaFree(a->d_clepoch);
+    if (a->d_abort) cudaFree(a->d_abort);
     if (a->d_y0) cudaFree(a->d_y0);
     if (a->d_err) cudaFree(a->d_err);
     if (a->ev0) cudaEventDestroy(a->ev0);
@@ -3216,6 +3613,7 @@ static int shards_run_multi(ridc_shards* g, const double* y0_host, double* final
 
 int ridc_shards_run(ridc_shards* g, const double* y0_host, double* final_host, double* wall_seconds)
 {
+    NvtxRange nvtx_("ridc.shards_run");
     if (!g || !y0_host || !final_host) return shard_fail(g, RIDC_E_CONFIG, "NULL argument");
     if (g->multi) return shards_run_multi(g, y0_host, final_host, wall_seconds);
     CUDA_TRY(&g->err, cudaSetDevice(g->device));

@@ -27,7 +27,8 @@ from .errors import ConfigError
 from .problems import as_descriptor
 from .quadrature import pack_weight_tables
 
-__all__ = ["PipelineRank", "SequentialPipeline", "run_levels", "run_pipelined_distributed"]
+__all__ = ["PipelineRank", "SequentialPipeline", "ConcurrentPipeline", "ShardRank", "GridPipeline", "run_levels",
+           "run_pipelined_distributed"]
 
 
 def run_levels(runner, restarts: int, state0, broadcast: Callable, is_top: bool):
@@ -74,6 +75,7 @@ class PipelineRank:
             config.steps, config.restarts, self.weights.ctypes.data, self.weights.shape[0],
             rank, device, int(inbox_capacity), float(config.watchdog_seconds), ctypes.byref(h)))
         self._h = h
+        self._runs = 0
         # resident level march (one launch per interval, in-kernel flag waits)
         # where the line qualifies; every rank must choose the same (the blob
         # carries it and connect checks it)
@@ -122,10 +124,28 @@ class PipelineRank:
             self._h, r, state0_dev.data_ptr(), out.data_ptr(), ctypes.byref(sec)), self._h)
         return out, sec.value
 
-    def run_device(self, y0_dev, out_dev, broadcast=None) -> float:
-        """All intervals; out_dev receives the solution on every rank."""
+    def reset(self):
+        """Zero this rank's mailbox counters (ridc_pipe_reset): between runs,
+        after every rank finished and before any starts again."""
+        _lib.check_pipe(_lib.lib().ridc_pipe_reset(self._h), self._h)
+
+    def run_device(self, y0_dev, out_dev, broadcast=None, barrier=None) -> float:
+        """All intervals; out_dev receives the solution on every rank.
+
+        The stream-memop protocol counts global step numbers, so a run after
+        the first resets every rank's counters between two barriers (every
+        rank finished, every rank reset): ``barrier()`` defaults to
+        torch.distributed.barrier."""
         if broadcast is None:
             broadcast = _nccl_broadcast(self.world)
+        if self._runs and not self.resident:
+            if barrier is None:
+                import torch.distributed as dist
+                barrier = dist.barrier
+            barrier()
+            self.reset()
+            barrier()
+        self._runs += 1
         _fin, sol, sec = run_levels(self, self.config.restarts, y0_dev, broadcast,
                                     self.rank == self.world - 1)
         out_dev.copy_(sol)
@@ -169,9 +189,15 @@ class SequentialPipeline:
         for r in self.ranks:
             r.connect(blobs)
         self.ivp = self.ranks[0].ivp
+        self._runs = 0
 
     def run(self, y0=None):
         y0 = self.ivp.initial_state if y0 is None else y0
+        if self._runs:   # every rank is idle here: zero the step counters of the last run
+            for rk in self.ranks:
+                if not rk.resident:
+                    rk.reset()
+        self._runs += 1
         s0 = D.to_device(y0, self.ranks[0].device)
         finals = [None] * len(self.ranks)
         for r in range(self.config.restarts):
@@ -209,10 +235,16 @@ class ConcurrentPipeline:
         for r in self.ranks:
             r.connect(blobs)
         self.ivp = self.ranks[0].ivp
+        self._runs = 0
 
     def run(self, y0=None):
         import threading
         y0 = self.ivp.initial_state if y0 is None else y0
+        if self._runs:   # every rank is idle here: zero the step counters of the last run
+            for r in self.ranks:
+                if not r.resident:
+                    r.reset()
+        self._runs += 1
         s0 = [D.to_device(y0, r.device) for r in self.ranks]
         finals = [None] * len(self.ranks)
         secs = [0.0] * len(self.ranks)
@@ -239,6 +271,153 @@ class ConcurrentPipeline:
     def close(self):
         for r in self.ranks:
             r.close()
+
+
+def shard_rows(ny: int, shard: int, nshards: int):
+    """Global rows [r0, r1) of row shard `shard` (ridc_pipe_create_shard's split)."""
+    return ny * shard // nshards, ny * (shard + 1) // nshards
+
+
+class ShardRank:
+    """Level ``level`` of row shard ``shard`` in a levels x row-shards grid
+    (the layer that uses every GPU when p < #GPUs).
+
+    The rank computes its level on its rows of a 2-D grid; per step it takes
+    its window from (level-1, shard) plus the two ghost rows from
+    (level-1, shard-+1), its own ghost rows from (level, shard-+1), and
+    delivers its boundary rows to the same-level neighbours and to the
+    diagonal consumers (ridc_pipe_create_shard, include/ridc_b200.h).  The
+    watermark / release protocol is the reference's LevelBuffer
+    (engine.py:284-331), per neighbour."""
+
+    def __init__(self, ivp, config, level: int, shard: int, nshards: int, device: int = 0,
+                 inbox_capacity: int = 0):
+        self.ivp = as_descriptor(ivp)
+        self.config = config
+        self.level, self.shard, self.nshards, self.device = level, shard, nshards, device
+        self.problem = self.ivp.problem
+        self.dt = (self.ivp.t_end - self.ivp.t_start) / config.steps
+        self.weights = pack_weight_tables(config.levels, self.dt)
+        D.require_cuda(device)
+        cp = self.problem.to_c()
+        h = ctypes.c_void_p()
+        _lib.check_pipe(_lib.lib().ridc_pipe_create_shard(
+            ctypes.byref(cp), float(self.ivp.t_start), float(self.ivp.t_end), config.levels,
+            config.steps, config.restarts, self.weights.ctypes.data, self.weights.shape[0],
+            level, shard, nshards, device, int(inbox_capacity), float(config.watchdog_seconds),
+            ctypes.byref(h)))
+        self._h = h
+        nb = _lib.lib().ridc_pipe_handle_bytes()
+        blob = ctypes.create_string_buffer(nb)
+        _lib.check_pipe(_lib.lib().ridc_pipe_export(self._h, blob), self._h)
+        self.blob = bytes(blob.raw)
+        self.r0, self.r1 = shard_rows(self.problem.ny, shard, nshards)
+
+    def connect(self, blobs):
+        """blobs[(level, shard)] for every rank of the grid."""
+        j, s, S, L = self.level, self.shard, self.nshards, self.config.levels
+        want = [(j - 1, s), (j - 1, s - 1), (j - 1, s + 1), (j + 1, s), (j + 1, s - 1), (j + 1, s + 1),
+                (j, s - 1), (j, s + 1)]
+        keep = [blobs[(a, b % S)] if 0 <= a < L else None for a, b in want]
+        arr = (ctypes.c_void_p * 8)(*[ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p) if b is not None else None
+                                      for b in keep])
+        self._keep = keep
+        _lib.check_pipe(_lib.lib().ridc_pipe_connect_shard(self._h, arr), self._h)
+
+    def reset(self):
+        _lib.check_pipe(_lib.lib().ridc_pipe_reset(self._h), self._h)
+
+    def run_interval(self, r: int, state0_dev):
+        """state0_dev: the GLOBAL interval state; returns this shard's rows of
+        the level's final and the device seconds."""
+        nx = self.problem.nx
+        out = D.torch().empty((self.r1 - self.r0) * nx, dtype=state0_dev.dtype, device=state0_dev.device)
+        D.torch().cuda.current_stream(state0_dev.device).synchronize()
+        sec = ctypes.c_double(0.0)
+        _lib.check_pipe(_lib.lib().ridc_pipe_run_interval(
+            self._h, r, state0_dev.data_ptr(), out.data_ptr(), ctypes.byref(sec)), self._h)
+        return out, sec.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().ridc_pipe_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GridPipeline:
+    """Levels x row shards in one process: rank (j, s) on
+    ``devices[(j * nshards + s) % len(devices)]``, each driven by its own host
+    thread on its own stream (stream-memory waits only, so ranks may share a
+    device).  Per interval the top level's shards are gathered into the next
+    interval's state0 (the reference's re-seed, engine.py:506-521)."""
+
+    def __init__(self, ivp, config, nshards: int, devices=(0,), inbox_capacity: int = 0):
+        self.config = config
+        L, S = config.levels, nshards
+        self.nshards = S
+        self.ranks = {}
+        for j in range(L):
+            for s in range(S):
+                dev = devices[(j * S + s) % len(devices)]
+                self.ranks[(j, s)] = ShardRank(ivp, config, j, s, S, dev, inbox_capacity=inbox_capacity)
+        blobs = {k: r.blob for k, r in self.ranks.items()}
+        for r in self.ranks.values():
+            r.connect(blobs)
+        self.ivp = self.ranks[(0, 0)].ivp
+        self._runs = 0
+
+    def run(self, y0=None):
+        """(final_state, level_finals) as host arrays; device_seconds is the
+        slowest rank's device time."""
+        import threading
+        torch = D.torch()
+        L, S = self.config.levels, self.nshards
+        y0 = self.ivp.initial_state if y0 is None else y0
+        if self._runs:   # every rank is idle here: zero the step counters of the last run
+            for r in self.ranks.values():
+                r.reset()
+        self._runs += 1
+        state = D.to_device(y0, self.ranks[(0, 0)].device)
+        secs = {k: 0.0 for k in self.ranks}
+        finals = {}
+        for interval in range(self.config.restarts):
+            s0 = {k: state.to(f"cuda:{r.device}") for k, r in self.ranks.items()}
+            errs = []
+
+            def work(k):
+                try:
+                    finals[k], t = self.ranks[k].run_interval(interval, s0[k])
+                    secs[k] += t
+                except Exception as exc:   # surfaced below
+                    errs.append(exc)
+            th = [threading.Thread(target=work, args=(k,)) for k in self.ranks]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            if errs:
+                raise errs[0]
+            dev = state.device
+            state = torch.cat([finals[(L - 1, s)].to(dev) for s in range(S)])
+        self.device_seconds = max(secs.values())
+        levels = [torch.cat([finals[(j, s)].to(state.device) for s in range(S)]) for j in range(L)]
+        return D.to_host(state), [D.to_host(x) for x in levels]
+
+    def close(self):
+        for r in self.ranks.values():
+            r.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def run_pipelined_distributed(ivp, config, device: Optional[int] = None):

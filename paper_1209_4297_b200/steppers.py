@@ -59,7 +59,9 @@ class ArkEngine:
     def info(self) -> dict:
         nl, ni = ctypes.c_int64(0), ctypes.c_int32(0)
         _lib.check_ark(_lib.lib().ridc_ark_info(self._h, ctypes.byref(nl), ctypes.byref(ni)), self._h)
-        return {"kernel_launches": nl.value, "items_per_step": ni.value}
+        path = _lib.lib().ridc_ark_path(self._h)
+        return {"kernel_launches": nl.value, "items_per_step": ni.value, "path": path,
+                "path_name": _lib.PATH_NAMES.get(path, "?")}
 
     def run(self, y0) -> tuple:
         """March from a host state -> (final ndarray, device seconds)."""

@@ -46,10 +46,38 @@ def test_segmented_long_line_against_oracle():
     with S.ArkEngine(ivp, tab, 0.0, 0.002, 20) as eng:
         y, wall = eng.run(ivp.initial_state)
         inf = eng.info
-    assert inf["items_per_step"] == tab.stages and inf["kernel_launches"] == 1 + 20 * tab.stages
+    # the carry-exchange path adds the run's tag-epoch bump to the seed launch
+    assert inf["path_name"] == "carry_levels", inf
+    assert inf["items_per_step"] == tab.stages and inf["kernel_launches"] == 2 + 20 * tab.stages
     ref = O.ark(s.problem, tab.a_implicit, tab.a_explicit, tab.b_implicit, tab.b_explicit,
                 ivp.initial_state, 0.0, 0.002, 20)
     assert G.normwise(y, ref) <= 1e-10 and wall > 0
+
+
+@pytest.mark.parametrize("scheme", ["imex3", "imex4"])
+@pytest.mark.parametrize("exp", [16, 20])
+def test_ark_carry_levels_vs_tick(scheme, exp, monkeypatch):
+    """Periodic RD lines of 512-point chunks run every ARK stage on the
+    carry-exchange tick (csrc/ridc_carry_levels.cuh, one chunk per warp): the
+    same stage solves as the tick kernel to rounding (<= 1e-12), the oracle
+    to <= 1e-10, and repeat runs bitwise (C2's grid and dt at exp = 20)."""
+    s = P.reaction_diffusion_c2(n=1 << exp)
+    steps = 20 if exp < 20 else 8   # the numpy oracle takes ~1.5 s per imex4 step at 2^20
+    ivp = P.StructuredIVP(s.problem, 0.0, 1e-4 * steps, s.ivp.initial_state)
+    tab = _tab(scheme)
+    with S.ArkEngine(ivp, tab, 0.0, 1e-4 * steps, steps) as eng:
+        assert eng.info["path_name"] == "carry_levels", eng.info
+        a, _ = eng.run(ivp.initial_state)
+        a2, _ = eng.run(ivp.initial_state)
+    monkeypatch.setenv("RIDC_NO_CARRYLEV", "1")
+    with S.ArkEngine(ivp, tab, 0.0, 1e-4 * steps, steps) as eng:
+        assert eng.info["path_name"] == "tick", eng.info
+        b, _ = eng.run(ivp.initial_state)
+    assert np.array_equal(a, a2)
+    assert G.normwise(a, b) <= 1e-12
+    ref = O.ark(s.problem, tab.a_implicit, tab.a_explicit, tab.b_implicit, tab.b_explicit,
+                ivp.initial_state, 0.0, 1e-4 * steps, steps)
+    assert G.normwise(a, ref) <= 1e-10
 
 
 @pytest.mark.parametrize("scheme,order", [("imex3", 3), ("imex4", 4)])

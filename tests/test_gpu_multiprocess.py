@@ -77,6 +77,10 @@ def _worker(rank, world, port, name, levels, steps, restarts, outdir):
         out = torch.empty_like(y0)
         sec = rk.run_device(y0, out, broadcast=bcast)
         np.save(os.path.join(outdir, f"rank{rank}.npy"), out.cpu().numpy())
+        # a second run: every rank resets its step counters between two barriers
+        out2 = torch.empty_like(y0)
+        rk.run_device(y0, out2, broadcast=bcast)
+        np.save(os.path.join(outdir, f"rank{rank}_2.npy"), out2.cpu().numpy())
         np.save(os.path.join(outdir, f"sec{rank}.npy"), np.array([sec]))
         dist.barrier()
         rk.close()
@@ -105,5 +109,7 @@ def test_pipeline_ranks_as_processes_bitwise(name, levels, steps, restarts):
         mp.start_processes(_worker, args=(levels, _free_port(), name, levels, steps, restarts, td),
                            nprocs=levels, join=True, start_method="spawn")
         outs = [np.load(os.path.join(td, f"rank{r}.npy")) for r in range(levels)]
+        outs2 = [np.load(os.path.join(td, f"rank{r}_2.npy")) for r in range(levels)]
     for r in range(levels):   # every rank holds the solution (the re-seed broadcast of the last interval)
         assert np.array_equal(outs[r], ref), (r, np.abs(outs[r] - ref).max())
+        assert np.array_equal(outs2[r], ref), (r, "second run", np.abs(outs2[r] - ref).max())

@@ -34,9 +34,10 @@ def test_pipeline_equals_engine_bitwise(name, builder, levels, steps, restarts):
     pipe = SequentialPipeline(s, cfg)
     try:
         final, level_finals = pipe.run()
+        final2, _ = pipe.run()   # counters reset between runs
     finally:
         pipe.close()
-    assert np.array_equal(final, ref.final_state)
+    assert np.array_equal(final, ref.final_state) and np.array_equal(final2, ref.final_state)
     for j in range(levels):
         assert np.array_equal(level_finals[j], ref.level_finals[j])
 
@@ -54,8 +55,12 @@ def test_concurrent_pipeline_small_rings_bitwise(name, builder, levels, steps, r
     try:
         assert all(r.info["ring_vectors"] < steps for r in pipe.ranks[1:])
         final, level_finals = pipe.run()
+        # a second run of the same ranks: the step counters are reset between
+        # runs (ridc_pipe_reset), else the last run's watermarks would satisfy
+        # every wait at once
+        final2, _ = pipe.run()
     finally:
         pipe.close()
-    assert np.array_equal(final, ref.final_state)
+    assert np.array_equal(final, ref.final_state) and np.array_equal(final2, ref.final_state)
     for j in range(levels):
         assert np.array_equal(level_finals[j], ref.level_finals[j])
