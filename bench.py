@@ -289,7 +289,7 @@ def _timed_solves(run_device, flush, reps):
     return ts
 
 
-def workload_line(name, order, flush, reps=2, nt=None, points=None):
+def workload_line(name, order, flush, reps=2, nt=None, points=None, cpu_budget=3.0):
     """One extra 1-GPU workload (C3 / C4 / C5 shapes): device time of whole solves,
     the dominant kernel's roofline (algorithmic bytes of a steady tick / tick time)."""
     import torch
@@ -312,7 +312,9 @@ def workload_line(name, order, flush, reps=2, nt=None, points=None):
     return {"workload": cfg["workload"], "points": n, "nt": nt, "order": order, "path": info["path_name"],
             "value": n * nt / t, "unit": UNIT, "ms_per_solve": t * 1e3, "us_per_tick": t / ticks * 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "bytes_per_tick": bytes_tick}}
+                         "frac": achieved / peak, "bytes_per_tick": bytes_tick},
+            # the CPU oracle port beside it (one thread per level), a bounded sample
+            "cpu_baseline": cpu_sample(sysm, order, nt, budget_s=cpu_budget)}
 
 
 def run_ours(args):
@@ -455,6 +457,8 @@ def run_ours(args):
         "sweep_warp_febe": "k_sweep_febe_warp (one launch per step: every warp sweeps a contiguous range of the "
                            "line through its own TMA-staged 512-point chunks, no block barriers, each point read "
                            "and written once)",
+        "resident_carry_levels": "k_carry_res2 (RIDC-2: both levels' tiles in registers for a whole interval, one "
+                                 "cooperative launch, tiles coupled by carries and the predictor's end points)",
         "carry_levels": "k_carry_levels (one launch per tick: every warp folds and solves one 512-point chunk of "
                         "each active level, neighbouring chunks exchange two carries through L2)",
         "sweep2d_febe": "k_sweep2d_febe (one launch per step: every CTA sweeps a row block, each row read once and "

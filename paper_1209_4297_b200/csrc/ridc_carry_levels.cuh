@@ -81,6 +81,7 @@ struct CarryLevParams {
     unsigned ticks;               // ticks per run: tag = epoch * ticks + tick
     unsigned* abort;
     long long spin_limit;
+    int exp;                      // diagnostics (RIDC_CL_EXP): 1 = every CTA exits after the launch prologue
 };
 
 __device__ __forceinline__ double cl_poll(const uint4* p, unsigned want, const CarryLevParams& cp, bool& dead)
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(kClWarps * 32, 1)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0) s_tag = *(volatile const unsigned*)cp.epoch * cp.ticks + tick;
     __syncthreads();
-    if (!active) return;
+    if (!active || cp.exp == 1) return;
     const unsigned tag = s_tag;
     const int c0 = chunk * 512;   // data column of my chunk's first point
     const int cl = chunk == 0 ? cp.nchunk - 1 : chunk - 1, cr = chunk == cp.nchunk - 1 ? 0 : chunk + 1;

@@ -295,7 +295,7 @@ struct NodeCoef {
 };
 
 template <int KIND>
-__device__ __forceinline__ NodeCoef node_coef(const DevProblem& pb, double ca, double cs, double cn)
+__host__ __device__ __forceinline__ NodeCoef node_coef(const DevProblem& pb, double ca, double cs, double cn)
 {
     NodeCoef k;
     k.cs = cs;

@@ -336,6 +336,28 @@ cudaError_t sweep_levels_k(int grid, cudaStream_t st, const EngineParams& ep, co
     return cudaLaunchKernelEx(&cfg, kfn, ep, tp, sp, tm);
 }
 
+// ---- resident RIDC-2 (ridc_carry_res2.cuh): one cooperative launch per interval
+template <int KIND>
+cudaError_t carry_res2_k(bool launch, int grid, int nt, cudaStream_t st, const CarryRes2Params& cp, int* per_sm)
+{
+    auto kfn = k_carry_res2<KIND>;
+    const size_t smem = carry_res2_smem(nt);
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, nt, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // all tiles co-resident (neighbour carry waits)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, cp);
+}
+
 // ---- carry-exchange level tick (ridc_carry_levels.cuh): one 512-point chunk
 // per warp, wpc warps per CTA, PDL between consecutive ticks
 template <int KIND>

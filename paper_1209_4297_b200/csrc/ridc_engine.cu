@@ -591,6 +591,13 @@ struct ridc_ctx {
     int sweeplev_nt = 256;
     SweepLevParams slparams;
     TmapSet tm_lev;
+    std::vector<double> h_weights;   // the packed quadrature tables (host copy)
+    std::vector<int> h_steady_off;
+    // resident RIDC-2 (ridc_carry_res2.cuh): one cooperative launch per interval
+    bool carryres = false;
+    int cr_nt = 0;
+    CarryRes2Params crparams;
+    uint4* d_crmail = nullptr;
     // carry-exchange level tick (ridc_carry_levels.cuh): RIDC p >= 2 on RD lines of <= 14 x SMs x 512 points
     bool carrylev = false;
     int cl_grid = 0, cl_wpc = 0;
@@ -670,7 +677,7 @@ EngineParams interval_params(ridc_ctx* c, int interval)
 const double* final_slot(ridc_ctx* c, int level)
 {
     if (c->resident) return c->d_ring[0] + (c->steps % c->cap[0]) * c->Vs;   // one launch, global steps
-    if (c->reslev) return c->d_ring[level] + c->Vs;                              // slot 1: the final tile
+    if (c->reslev || c->carryres) return c->d_ring[level] + c->Vs;               // slot 1: the final tile
     EngineParams ep = interval_params(c, c->restarts - 1);
     return ep.ring[level] + ((ep.off[level] + c->per) % ep.cap[level]) * c->Vs;
 }
@@ -869,10 +876,54 @@ int march_reslev(ridc_ctx* c, bool* fell_back)
     return RIDC_OK;
 }
 
+// The resident RIDC-2 march (ridc_carry_res2.cuh): one cooperative launch per
+// restart interval from that interval's state0; the top level's final (ring
+// slot 1) becomes the next state0.  false in *fell_back: no co-residency.
+int march_carryres(ridc_ctx* c, bool* fell_back)
+{
+    *fell_back = false;
+    const int nseg = c->crparams.nseg;
+    if ((unsigned long long)c->tag_next + (unsigned long long)c->restarts * (c->per + 2) + 2 >= 0xffffffffull) {
+        CUDA_TRY(&c->err, cudaMemsetAsync(c->d_crmail, 0, (size_t)(4 * 4 + 4 * 2) * nseg * sizeof(uint4), c->stream));
+        c->tag_next = 1;
+    }
+    CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, sizeof(unsigned), c->stream));
+    for (int r = 0; r < c->restarts; ++r) {
+        const double* src = c->d_y0;
+        if (r > 0) {
+            CUDA_TRY(&c->err, copy_out(c, c->d_y0 + c->V, final_slot(c, c->levels - 1), cudaMemcpyDeviceToDevice));
+            src = c->d_y0 + c->V;
+        }
+        CarryRes2Params cp = c->crparams;
+        cp.src = src;
+        cp.tag0 = c->tag_next;
+        c->tag_next += (unsigned)c->per + 2;
+        const cudaError_t le = carry_res2_k<RD_1D>(true, nseg, c->cr_nt, c->stream, cp, nullptr);
+        if (le == cudaErrorCooperativeLaunchTooLarge && r == 0) {
+            cudaGetLastError();
+            *fell_back = true;
+            return RIDC_OK;
+        }
+        CUDA_TRY(&c->err, le);
+    }
+    return RIDC_OK;
+}
+
 int march(ridc_ctx* c, double* wall_seconds)
 {
     NvtxRange nvtx_("ridc.march");
     CUDA_TRY(&c->err, cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+    if (c->carryres) {
+        CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
+        bool fb = false;
+        int rc = march_carryres(c, &fb);
+        if (rc) return rc;
+        if (fb) {   // the SMs are shared right now: the tick kernel's graph for good
+            c->carryres = false;
+            c->fell_back = true;
+            if ((rc = capture_graph(c)) != RIDC_OK) return rc;
+        }
+    }
     if (c->reslev) {
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
         bool fb = false;
@@ -921,7 +972,7 @@ int march(ridc_ctx* c, double* wall_seconds)
             CUDA_TRY(&c->err, le);
         }
     }
-    if (!c->resident && !c->reslev) {
+    if (!c->resident && !c->reslev && !c->carryres) {
         if (c->carrylev) CUDA_TRY(&c->err, cudaMemsetAsync(c->d_flags, 0, sizeof(unsigned), c->stream));
         CUDA_TRY(&c->err, cudaEventRecord(c->ev0, c->stream));
         CUDA_TRY(&c->err, cudaGraphLaunch(c->gexec, c->stream));
@@ -933,7 +984,7 @@ int march(ridc_ctx* c, double* wall_seconds)
         CUDA_TRY(&c->err, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         *wall_seconds = ms * 1e-3;
     }
-    if (c->resident || c->reslev || c->carrylev) {
+    if (c->resident || c->reslev || c->carrylev || c->carryres) {
         unsigned ab = 0;
         CUDA_TRY(&c->err, cudaMemcpy(&ab, c->d_flags, sizeof ab, cudaMemcpyDeviceToHost));
         if (ab) return fail(&c->err, RIDC_E_PROTOCOL, "resident march: a neighbour segment wait timed out");
@@ -1202,6 +1253,81 @@ int setup_sweep_levels(ridc_ctx* c)
     return RIDC_OK;
 }
 
+// Resident RIDC-2 (ridc_carry_res2.cuh): two levels of a periodic
+// reaction-diffusion line of a multiple of 16 points held on the SMs, one
+// tile per SM (<= 16 x 448 points, >= 2 carry reaches + a warp), no
+// trajectory recording (the top level's states never leave the SMs).
+int setup_carry_res2(ridc_ctx* c)
+{
+    const DevProblem& pb = c->pb;
+    if (c->levels != 2 || pb.kind != RD_1D || pb.ny != 1 || (pb.nx & 15) ||
+        (c->flags & (RIDC_TICK_ONLY | RIDC_RECORD_TRAJECTORY)) || c->traj_stream)
+        return RIDC_OK;
+    if (getenv("RIDC_NO_CARRYRES") && atoi(getenv("RIDC_NO_CARRYRES")) > 0) return RIDC_OK;
+    const double lam = c->ss.sv.lam;
+    const int hc = halo_of(lam), nx = pb.nx;
+    int nseg = 0, T = 0;
+    for (int n = c->nsm; n >= 2; --n) {   // the carry march's tiling, 448 threads at most
+        const int t = 16 * ((nx + 16 * n - 1) / (16 * n));
+        const int ns = (nx + t - 1) / t;
+        const int tlast = nx - (ns - 1) * t;
+        if (t > 16 * kRes2MaxNT) break;
+        if (ns >= 2 && t >= 2 * hc + 512 && tlast >= 2 * hc + 512) { nseg = ns; T = t; break; }
+    }
+    if (nseg < 2) return RIDC_OK;
+    const int nt = 32 * ((T / 16 + 31) / 32);
+    int per_sm = 0;
+    CarryRes2Params& cp = c->crparams;
+    memset(&cp, 0, sizeof cp);
+    if (carry_res2_k<RD_1D>(false, 0, nt, c->stream, cp, &per_sm) != cudaSuccess || per_sm * c->nsm < nseg) {
+        cudaGetLastError();
+        return RIDC_OK;
+    }
+    const size_t mb = (size_t)(4 * 4 + 4 * 2) * nseg * sizeof(uint4);
+    CUDA_TRY(&c->err, cudaMalloc(&c->d_crmail, mb));
+    CUDA_TRY(&c->err, cudaMemset(c->d_crmail, 0, mb));
+    if (!c->d_flags) CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, sizeof(unsigned)));
+    const double g = c->ss.sv.g, dt = c->dt;
+    cp.lam = lam;
+    cp.inv1ml2 = 1.0 / (1.0 - lam * lam);
+    cp.aa = g * (1.0 + dt * pb.rho);   // the predictor: g (u + dt rho u (1 - u))
+    cp.bb = -(g * dt * pb.rho);
+    // the corrector's nodes at steady steps (j = 1: window t, t-1; i_new 0, i_old 1), build_item's coefficients
+    const double* w = c->h_weights.data() + c->h_steady_off[1];
+    const NodeCoef n0 = node_coef<RD_1D>(pb, 1.0, 0.0, dt);
+    const NodeCoef nn = node_coef<RD_1D>(pb, 0.0, w[0] - dt, w[0]);
+    const NodeCoef no = node_coef<RD_1D>(pb, 0.0, w[1], w[1] - dt);
+    cp.a1 = g * n0.a;
+    cp.b1 = g * n0.b;
+    cp.an = g * nn.a;
+    cp.bn = g * nn.b;
+    cp.sn = g * nn.cs * pb.cdx;
+    cp.ao = g * no.a;
+    cp.bo = g * no.b;
+    cp.so = g * no.cs * pb.cdx;
+    for (int e = 0; e < 16; ++e) {
+        cp.pw[e] = c->ss.sv.pw[e];
+        cp.zf[e] = c->ss.sv.zf16[e];
+    }
+    for (int i = 0; i < 10; ++i) cp.mp[i] = c->ss.sv.mp16[i];
+    cp.fin0 = c->d_ring[0] + c->Vs + c->ss.lay.GW;   // slot 1 of each level (final_slot)
+    cp.fin1 = c->d_ring[1] + c->Vs + c->ss.lay.GW;
+    cp.T = T;
+    cp.nx = nx;
+    cp.nseg = nseg;
+    cp.hc = hc;
+    cp.mail = c->d_crmail;
+    cp.edge = c->d_crmail + 16 * nseg;
+    cp.per = c->per;
+    cp.err = c->d_err;
+    cp.abort = c->d_flags;
+    cp.spin_limit = (long long)(c->watchdog * 2.0e9);
+    c->cr_nt = nt;
+    c->carryres = true;
+    c->launches = c->restarts;
+    return RIDC_OK;
+}
+
 // The carry-level tick's per-launch solve constants from a factored shift
 // (DevSolve: lam, g and the 16-point tables).  lam = 0, g = 1 (the identity
 // "solve" of an ARK final combination) zeroes every carry.
@@ -1255,6 +1381,7 @@ int setup_carry_levels(ridc_ctx* c)
     cp.ticks = (unsigned)(c->restarts * c->ticks + 1);
     cp.abort = c->d_flags;
     cp.spin_limit = (long long)(c->watchdog * 2.0e9);
+    cp.exp = env_int("RIDC_CL_EXP", 0);   // diagnostics: WRONG states, timing only
     memset(&c->tm_cl, 0, sizeof c->tm_cl);
     for (int j = 0; j < c->levels; ++j) {   // every level ring, boxes of one chunk + one group either side
         int rc = make_ring_map(&c->tm_cl.map[j], c->d_ring[j], c->Vs, c->cap[j], kClBoxGroups, &c->err);
@@ -1515,6 +1642,8 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     CTX_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CTX_TRY(cudaEventCreate(&c->ev0));
     CTX_TRY(cudaEventCreate(&c->ev1));
+    if (wtotal > 0) c->h_weights.assign(weights, weights + wtotal);
+    c->h_steady_off = st;
     CTX_TRY(cudaMalloc(&c->d_weights, std::max<long long>(wtotal, 1) * sizeof(double)));
     if (wtotal > 0)
         CTX_TRY(cudaMemcpy(c->d_weights, weights, wtotal * sizeof(double), cudaMemcpyHostToDevice));
@@ -1591,13 +1720,14 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     ep.lay = c->ss.lay;
     ep.cgeo = c->d_cgeo;
     if ((rc = setup_resident(c)) != RIDC_OK) return bail(rc);
-    if (!c->resident && (rc = setup_reslev(c)) != RIDC_OK) return bail(rc);
+    if (!c->resident && (rc = setup_carry_res2(c)) != RIDC_OK) return bail(rc);
+    if (!c->resident && !c->carryres && (rc = setup_reslev(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep2d(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep2d_levels(c)) != RIDC_OK) return bail(rc);
-    if ((rc = setup_carry_levels(c)) != RIDC_OK) return bail(rc);
+    if (!c->carryres && (rc = setup_carry_levels(c)) != RIDC_OK) return bail(rc);
     if (!c->carrylev && (rc = setup_sweep_levels(c)) != RIDC_OK) return bail(rc);
-    if (!c->resident && !c->reslev && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
+    if (!c->resident && !c->reslev && !c->carryres && (rc = capture_graph(c)) != RIDC_OK) return bail(rc);
 #undef CTX_TRY
     *out = c;
     return RIDC_OK;
@@ -1664,6 +1794,7 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
                  : c->sweeplev ? RIDC_PATH_SWEEP2D_LEVELS
                  : c->sweeplev1 ? RIDC_PATH_SWEEP_LEVELS
                  : c->carrylev ? RIDC_PATH_CARRY_LEVELS
+                 : c->carryres ? RIDC_PATH_RESIDENT_CARRY_LEVELS
                           : c->resident ? RIDC_PATH_RESIDENT_FEBE
                                         : (c->reslev ? RIDC_PATH_RESIDENT_LEVELS : RIDC_PATH_TICK);
     info->fell_back = c->fell_back ? 1 : 0;
@@ -1677,6 +1808,7 @@ int ridc_set_watchdog(ridc_ctx* c, double seconds)
     c->rp.spin_limit = (long long)(seconds * 2.0e9);
     c->lp.spin_limit = (long long)(seconds * 2.0e9);
     c->cparams.spin_limit = (long long)(seconds * 2.0e9);
+    c->crparams.spin_limit = (long long)(seconds * 2.0e9);
     if (c->carrylev && c->clparams.spin_limit != (long long)(seconds * 2.0e9)) {
         // the limit is a kernel parameter of every captured tick: capture again
         c->clparams.spin_limit = (long long)(seconds * 2.0e9);
@@ -1707,6 +1839,7 @@ int ridc_destroy(ridc_ctx* c)
     if (c->d_mail) cudaFree(c->d_mail);
     if (c->d_cmail) cudaFree(c->d_cmail);
     if (c->d_clx) cudaFree(c->d_clx);
+    if (c->d_crmail) cudaFree(c->d_crmail);
     if (c->d_clepoch) cudaFree(c->d_clepoch);
     for (int j = 0; j < kMaxLevels; ++j)
         if (c->d_inbox[j]) cudaFree(c->d_inbox[j]);

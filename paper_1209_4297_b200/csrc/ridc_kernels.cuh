@@ -360,6 +360,7 @@ constexpr int kResStages = 2;
 #include "ridc_sweep2d_levels.cuh"
 #include "ridc_sweep_levels.cuh"
 #include "ridc_carry_levels.cuh"
+#include "ridc_carry_res2.cuh"
 
 namespace ridc {
 
@@ -384,6 +385,8 @@ cudaError_t sweep2d_k(int nt, int grid, cudaStream_t st, const Sweep2DParams& sp
 template <int KIND>
 cudaError_t sweep_levels_k(int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
                            const SweepParams& sp, const TmapSet& tm);
+template <int KIND>
+cudaError_t carry_res2_k(bool launch, int grid, int nt, cudaStream_t st, const CarryRes2Params& cp, int* per_sm);
 template <int KIND>
 cudaError_t carry_levels_k(int grid, int wpc, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
                            const CarryLevParams& cp, const TmapSet& tm, unsigned tick);

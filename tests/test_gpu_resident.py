@@ -21,6 +21,7 @@ if not torch.cuda.is_available():
 
 from oracle import oracle as O  # noqa: E402
 from paper_1209_4297_b200 import engine as E, problems as P  # noqa: E402
+from paper_1209_4297_b200.errors import NonFiniteStateError  # noqa: E402
 from paper_1209_4297_b200.quadrature import pack_weight_tables  # noqa: E402
 
 
@@ -190,7 +191,9 @@ def test_carry_levels(name, n, levels, steps, restarts, traj):
                  1e-4 * steps)
     cfg = E.RidcConfig(levels=levels, steps=steps, restarts=restarts, record_trajectory=traj)
     with E.Engine(ivp, cfg) as cl, E.Engine(ivp, cfg, tick_only=True) as tick:
-        assert cl.info["path_name"] == "carry_levels", cl.info
+        # RIDC-2 without a recorded trajectory holds both levels on the SMs (ridc_carry_res2.cuh)
+        want = "resident_carry_levels" if levels == 2 and not traj else "carry_levels"
+        assert cl.info["path_name"] == want, cl.info
         a, b = cl.run(), tick.run()
         a2 = cl.run()
     assert np.array_equal(a.final_state, a2.final_state)
@@ -221,3 +224,55 @@ def test_carry_levels_watchdog_recapture():
         _lib.check(_lib.lib().ridc_set_watchdog(cl._h, 11.0), cl._h)
         b = cl.run()
     assert np.array_equal(a.final_state, b.final_state)
+
+
+RES2_CASES = [
+    # (id, n, steps, restarts): r ~ 110 as C2
+    ("c2", 1 << 20, 40, 1),
+    ("c2-r4", 1 << 20, 48, 4),
+    ("2^18", 1 << 18, 30, 1),
+    ("uneven-tiles", (1 << 20) - 16 * 999, 30, 2),
+]
+
+
+@pytest.mark.parametrize("name,n,steps,restarts", RES2_CASES, ids=[c[0] for c in RES2_CASES])
+def test_resident_carry_res2(name, n, steps, restarts):
+    """RIDC-2 with both levels held on the SMs for a whole interval, one tile
+    per SM, the tiles coupled by carries and the predictor's end points
+    (csrc/ridc_carry_res2.cuh): repeat runs bitwise, both level finals against
+    the tick kernel (<= 1e-12) and the oracle (<= 1e-10)."""
+    ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
+                 1e-4 * steps)
+    cfg = E.RidcConfig(levels=2, steps=steps, restarts=restarts)
+    with E.Engine(ivp, cfg) as cr, E.Engine(ivp, cfg, tick_only=True) as tick:
+        assert cr.info["path_name"] == "resident_carry_levels", cr.info
+        a, b = cr.run(), tick.run()
+        a2 = cr.run()
+    for j in range(2):
+        assert np.array_equal(a.level_finals[j], a2.level_finals[j]), j
+        assert G.normwise(a.level_finals[j], b.level_finals[j]) <= 1e-12, j
+    assert np.array_equal(a.final_state, a.level_finals[1])
+    dt = (ivp.t_end - ivp.t_start) / steps
+    ref = O.run(ivp.problem, ivp.initial_state, 2, steps, restarts, dt, pack_weight_tables(2, dt),
+                level_finals=True)
+    for j in range(2):
+        assert G.normwise(a.level_finals[j], ref["level_finals"][j]) <= 1e-10, j
+
+
+def test_resident_carry_res2_nonfinite_message():
+    """A blow-up inside the resident RIDC-2 march reports the reference's
+    message with the first non-finite (step, level), the same as the tick
+    kernel's (engine.py:160-164)."""
+    n = 1 << 18
+    spec = P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)
+    sysm = P.build_reaction_diffusion(spec)
+    y0 = np.array(sysm.ivp.initial_state) * 1e150   # the logistic term overflows within a few steps
+    ivp = P.StructuredIVP(sysm.ivp.problem, 0.0, 1e-4 * 20, y0)
+    msgs = []
+    for tick_only in (False, True):   # the same first (step, level) as the tick kernel reports
+        with E.Engine(ivp, E.RidcConfig(levels=2, steps=20), tick_only=tick_only) as eng:
+            assert (eng.info["path_name"] == "resident_carry_levels") != tick_only, eng.info
+            with pytest.raises(NonFiniteStateError, match=r"level \d produced non-finite entries at step \d+") as ei:
+                eng.run()
+            msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1], msgs
