@@ -2,9 +2,10 @@
 // reaction-diffusion line held on the SMs for a whole restart interval.
 //
 // The lagged pipeline (engine.py:349-459) with p = 2: at tick k the predictor
-// computes step k and the corrector step k - 1 (startup_delay, engine.py:50-54),
-// the corrector reading the predictor's steps k - 1 and k - 2 (its window,
-// _window_span / _orient, engine.py:124-140; _correct_core, :179-187).
+// computes step k and the corrector step k - 2 (one more than startup_delay,
+// engine.py:50-54: see the tick below), the corrector reading the predictor's
+// steps k - 2 and k - 3 (its window, _window_span / _orient, engine.py:124-140;
+// _correct_core, :179-187).
 // Like the carry-exchange FEBE march (ridc_febe_carry.cuh), the line is one
 // tile per SM and every tile solves its own points only; here each thread
 // holds 16 points of BOTH levels in registers, so a tick is the FEBE step on
@@ -75,14 +76,14 @@ __device__ __forceinline__ double res2_poll(const uint4* p, unsigned want, const
 }
 
 constexpr int kRes2NP = kRes2MaxNT + 2;   // ring row stride (compile-time: the addressing is constant offsets)
-inline size_t carry_res2_smem(int) { return (size_t)2 * 16 * kRes2NP * sizeof(double); }
+inline size_t carry_res2_smem(int) { return (size_t)3 * 16 * kRes2NP * sizeof(double); }
 
 template <int KIND>
 __global__ void __launch_bounds__(kRes2MaxNT, 1) k_carry_res2(const __grid_constant__ CarryRes2Params cp)
 {
     static_assert(KIND == RD_1D, "resident RIDC-2: periodic reaction-diffusion lines");
     constexpr int K = 16;
-    extern __shared__ double ring[];               // [2 slots][16][NT + 2]: predictor steps, [e][thread + 1]
+    extern __shared__ double ring[];               // [3 slots][16][NP]: predictor steps, [e][thread + 1]
     __shared__ double sx[4 * (kRes2MaxNT / 32)];   // block-scan warp totals: fwd 0, fwd 1, bwd 0, bwd 1
     __shared__ double s_yend[2];
     const unsigned FULL = 0xffffffffu;
@@ -137,27 +138,31 @@ __global__ void __launch_bounds__(kRes2MaxNT, 1) k_carry_res2(const __grid_const
     if (last) R(0, 0, nch + 1) = __ldcg(cp.src + (c0 + Tk == cp.nx ? 0 : c0 + Tk));
     bool dead = false;
 
-    // one tick: A0 -- the predictor computes step kk, A1 -- the corrector step kk - 1
-    auto tick = [&](long long kk, auto a0c, auto a1c) {
+    // one tick: A0 -- the predictor computes step kk, A1 -- the corrector step kk - 2
+    // (a lag of two instead of the tick engine's one: the newest predictor step a
+    // fold reads was stored before the LAST tick's barriers, so a tick needs no
+    // barrier of its own before the fold; the same level-steps, computed alike).
+    // Ring slot of predictor step s: s % 3 (r3 = kk % 3).
+    auto tick = [&](long long kk, int r3, auto a0c, auto a1c) {
         constexpr bool A0 = decltype(a0c)::value, A1 = decltype(a1c)::value;
         const unsigned tag = cp.tag0 + (unsigned)kk;
         uint4* box = cp.mail + (size_t)(kk & 3) * 4 * nseg;
-        uint4* ebox = cp.edge + (size_t)((kk - 1) & 3) * 2 * nseg;
-        const int sn = (int)((kk - 1) & 1), so = (int)(kk & 1);   // ring slots: predictor steps kk-1, kk-2
-        // the neighbour tiles' end points of predictor step kk-1 (published at tick kk-1)
-        if (A1 && kk >= 2) {
-            if (tid == 0) R(sn, K - 1, 0) = res2_poll(ebox + 2 * kl + 1, cp.tag0 + (unsigned)(kk - 1), cp, dead);
-            if (last) R(sn, 0, nch + 1) = res2_poll(ebox + 2 * kr, cp.tag0 + (unsigned)(kk - 1), cp, dead);
+        uint4* ebox = cp.edge + (size_t)((kk - 2) & 3) * 2 * nseg;
+        const int sn = r3 == 2 ? 0 : r3 + 1, so = r3;   // ring slots: predictor steps kk-2, kk-3 (then kk)
+        // the neighbour tiles' end points of predictor step kk-2 (published two ticks ago),
+        // kept in the ring's end cells that only threads 0 and nch-1 read
+        if (A1) {
+            if (tid == 0) R(sn, K - 1, 0) = res2_poll(ebox + 2 * kl + 1, cp.tag0 + (unsigned)(kk - 2), cp, dead);
+            if (last) R(sn, 0, nch + 1) = res2_poll(ebox + 2 * kr, cp.tag0 + (unsigned)(kk - 2), cp, dead);
         }
-        __syncthreads();   // the ring's step kk-1 (stored at the end of the last tick) and its ends
         // ---- right-hand sides (g folded in)
         if (A0) {
 #pragma unroll
             for (int e = 0; e < K; ++e) u0[e] = fma(cp.bb, u0[e], cp.aa) * u0[e];
         }
         if (A1) {
-            const double* Pn = ring + sn * K * NP + tid + 1;   // point (tid, e) of step kk-1 at Pn[e NP]
-            const double* Po = ring + so * K * NP + tid + 1;   // step kk-2
+            const double* Pn = ring + sn * K * NP + tid + 1;   // point (tid, e) of step kk-2 at Pn[e NP]
+            const double* Po = ring + so * K * NP + tid + 1;   // step kk-3
             double nl = Pn[(K - 1) * NP - 1], nc = Pn[0], ol = Po[(K - 1) * NP - 1], oc = Po[0];
 #pragma unroll
             for (int e = 0; e < K; ++e) {
@@ -297,8 +302,8 @@ __global__ void __launch_bounds__(kRes2MaxNT, 1) k_carry_res2(const __grid_const
             for (int e = 0; e < K; ++e) { u0[e] = 0.0; u1[e] = 0.0; }
         } else {
             if (A0 && !chunk_finite(u0)) atomicMin(cp.err, err_code(kk, 0));
-            if (A1 && !chunk_finite(u1)) atomicMin(cp.err, err_code(kk - 1, 1));
-            if (A0) {   // step kk over step kk-2
+            if (A1 && !chunk_finite(u1)) atomicMin(cp.err, err_code(kk - 2, 1));
+            if (A0) {   // step kk over step kk-3 (read above, before this tick's barriers)
                 double* Pw = ring + so * K * NP + tid + 1;
 #pragma unroll
                 for (int e = 0; e < K; ++e) Pw[e * NP] = u0[e];
@@ -313,9 +318,16 @@ __global__ void __launch_bounds__(kRes2MaxNT, 1) k_carry_res2(const __grid_const
 
     const std::true_type on;
     const std::false_type off;
-    tick(1, on, off);
-    for (long long kk = 2; kk <= cp.per; ++kk) tick(kk, on, on);
-    tick(cp.per + 1, off, on);
+#pragma unroll 1
+    for (int kk = 1; kk <= 2; ++kk) tick(kk, kk, on, off);
+    int r3 = 0;
+#pragma unroll 1
+    for (long long kk = 3; kk <= cp.per; ++kk) {
+        tick(kk, r3, on, on);
+        r3 = r3 == 2 ? 0 : r3 + 1;
+    }
+#pragma unroll 1
+    for (long long kk = cp.per + 1; kk <= cp.per + 2; ++kk) tick(kk, (int)(kk % 3), off, on);
     if (mine) {
 #pragma unroll
         for (int e = 0; e < K; e += 2) {

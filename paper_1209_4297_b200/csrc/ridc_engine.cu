@@ -883,7 +883,7 @@ int march_carryres(ridc_ctx* c, bool* fell_back)
 {
     *fell_back = false;
     const int nseg = c->crparams.nseg;
-    if ((unsigned long long)c->tag_next + (unsigned long long)c->restarts * (c->per + 2) + 2 >= 0xffffffffull) {
+    if ((unsigned long long)c->tag_next + (unsigned long long)c->restarts * (c->per + 3) + 2 >= 0xffffffffull) {
         CUDA_TRY(&c->err, cudaMemsetAsync(c->d_crmail, 0, (size_t)(4 * 4 + 4 * 2) * nseg * sizeof(uint4), c->stream));
         c->tag_next = 1;
     }
@@ -897,7 +897,7 @@ int march_carryres(ridc_ctx* c, bool* fell_back)
         CarryRes2Params cp = c->crparams;
         cp.src = src;
         cp.tag0 = c->tag_next;
-        c->tag_next += (unsigned)c->per + 2;
+        c->tag_next += (unsigned)c->per + 3;   // ticks 1 .. per + 2
         const cudaError_t le = carry_res2_k<RD_1D>(true, nseg, c->cr_nt, c->stream, cp, nullptr);
         if (le == cudaErrorCooperativeLaunchTooLarge && r == 0) {
             cudaGetLastError();
@@ -1720,6 +1720,9 @@ int ridc_create(const ridc_problem* problem, double t_start, double t_end, int32
     ep.lay = c->ss.lay;
     ep.cgeo = c->d_cgeo;
     if ((rc = setup_resident(c)) != RIDC_OK) return bail(rc);
+    // RIDC-2 on RD lines: both levels per tile (ridc_carry_res2.cuh; 3.1 us per
+    // tick at 2^16-2^18 against the resident level march's 5.9-10); other
+    // orders: the resident level march where levels x segments fit the SMs
     if (!c->resident && (rc = setup_carry_res2(c)) != RIDC_OK) return bail(rc);
     if (!c->resident && !c->carryres && (rc = setup_reslev(c)) != RIDC_OK) return bail(rc);
     if ((rc = setup_sweep(c)) != RIDC_OK) return bail(rc);

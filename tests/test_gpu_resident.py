@@ -80,16 +80,19 @@ def test_resident_equals_tick_kernel_bitwise(name, builder, steps, restarts, tra
 
 def test_default_selection():
     """Single-level runs on 1-D lines march resident (whole lines and segmented
-    lines); multi-level runs on 1-D lines use the resident level march (two
-    seeds + one launch per interval, tests/test_gpu_reslevels.py)."""
+    lines); RIDC-2 on RD lines holds both levels per tile (one launch per
+    interval); other multi-level runs on short 1-D lines use the resident
+    level march (two seeds + one launch per interval, tests/test_gpu_reslevels.py)."""
     whole = _short(P.reaction_diffusion_c2(n=8192), 0.002)
     seg = _short(P.reaction_diffusion_c2(n=1 << 16), 0.002)
     with E.Engine(whole, E.RidcConfig(levels=1, steps=20)) as a, \
             E.Engine(seg, E.RidcConfig(levels=1, steps=20)) as b, \
-            E.Engine(whole, E.RidcConfig(levels=2, steps=20)) as c:
+            E.Engine(whole, E.RidcConfig(levels=2, steps=20)) as c, \
+            E.Engine(whole, E.RidcConfig(levels=3, steps=20)) as d:
         assert a.info["kernel_launches"] == 2
         assert b.info["kernel_launches"] == 2
-        assert c.info["kernel_launches"] == 3
+        assert c.info["path_name"] == "resident_carry_levels" and c.info["kernel_launches"] == 1
+        assert d.info["path_name"] == "resident_levels" and d.info["kernel_launches"] == 3
 
 
 def test_resident_device_run_and_wall():

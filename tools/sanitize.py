@@ -1,7 +1,8 @@
 """Small marches of every kernel family against the CPU oracle: the tick
 kernel (1-D segmented, whole-line, 2-D x-lines), the resident marches (FEBE:
-halo exchange and carry exchange; all levels), the streaming sweeps (1-D
-FEBE, 2-D FEBE, 2-D levels), the pipeline ranks and the ARK comparator.
+halo exchange and carry exchange; all levels; the resident RIDC-2), the
+streaming sweeps (1-D FEBE per warp, 2-D FEBE, 2-D levels), the carry-level
+tick, the pipeline ranks, levels x row shards and the ARK comparators.
 
 Run it under compute-sanitizer where that is available, or -- on the GPU pool,
 where compute-sanitizer is closed -- against the checked build, whose kernels
@@ -54,6 +55,10 @@ CASES = {
     "tick-2d-p2": (lambda: P.build_advection_diffusion_2d(P.AdvectionDiffusion2DSpec(nx=256, ny=16,
                                                                                      t_end=1e-4)).ivp, 2, 8, {}),
     "burgers-p3": (lambda: _short(P.burgers_paper(), 0.02), 3, 20, {}),
+    # round 2 (end): the warp sweep, the carry-level tick, the resident RIDC-2
+    "febe-sweep-warp": (lambda: seg(1 << 22, 6), 1, 6, {}),
+    "carry-levels-p4": (lambda: seg(1 << 19, 24), 4, 24, {}),
+    "resident-res2": (lambda: seg(1 << 18, 24), 2, 24, {}),
 }
 
 
@@ -99,15 +104,46 @@ def ark():
     assert err <= 1e-10
 
 
+def ark_carry():
+    """imex4 stages on the carry-exchange tick (periodic RD, 512-point chunks)."""
+    from paper_1209_4297_b200.steppers import ArkEngine
+    from paper_1209_4297_b200.tableaus import imex4_tableau
+    ivp = seg(1 << 17, 6)
+    tab = imex4_tableau()
+    with ArkEngine(ivp, tab, 0.0, ivp.t_end, 6) as eng:
+        y, _ = eng.run(ivp.initial_state)
+        path = eng.info["path_name"]
+    ref = O.ark(ivp.problem, tab.a_implicit, tab.a_explicit, tab.b_implicit, tab.b_explicit,
+                ivp.initial_state, 0.0, ivp.t_end, 6)
+    err = np.abs(y - ref).max() / np.abs(ref).max()
+    print(f"ark-imex4-carry: path {path}, normwise err {err:.2e}", flush=True)
+    assert err <= 1e-10
+
+
+def grid():
+    """Levels x row shards (ridc_pipe_create_shard): 3 levels x 2 shards on one device."""
+    s = P.build_advection_diffusion_2d(P.AdvectionDiffusion2DSpec(nx=256, ny=20, t_end=0.002))
+    cfg = E.RidcConfig(levels=3, steps=12)
+    with PD.GridPipeline(s, cfg, 2, devices=[0]) as g:
+        fin, _ = g.run()
+    ref = E.run_serial(s, cfg).final_state
+    print(f"grid-3x2: bitwise {np.array_equal(fin, ref)}", flush=True)
+    assert np.array_equal(fin, ref)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cases", default=",".join(list(CASES) + ["pipe", "ark"]))
+    ap.add_argument("--cases", default=",".join(list(CASES) + ["pipe", "ark", "ark-carry", "grid"]))
     a = ap.parse_args()
     for name in a.cases.split(","):
         if name == "pipe":
             pipe("pipe-resident-p2", True)
         elif name == "ark":
             ark()
+        elif name == "ark-carry":
+            ark_carry()
+        elif name == "grid":
+            grid()
         else:
             b, levels, steps, kw = CASES[name]
             check(name, b(), levels, steps, kw)
