@@ -278,6 +278,17 @@ def shard_rows(ny: int, shard: int, nshards: int):
     return ny * shard // nshards, ny * (shard + 1) // nshards
 
 
+def shard_neighbours(level: int, shard: int, nshards: int, levels: int):
+    """The eight (level, shard) neighbours ridc_pipe_connect_shard takes, in its
+    order -- (j-1, s), (j-1, s-1), (j-1, s+1), (j+1, s), (j+1, s-1), (j+1, s+1),
+    (j, s-1), (j, s+1) -- shards wrapping around (y is periodic), None where
+    the level does not exist."""
+    j, s, S = level, shard, nshards
+    want = [(j - 1, s), (j - 1, s - 1), (j - 1, s + 1), (j + 1, s), (j + 1, s - 1), (j + 1, s + 1),
+            (j, s - 1), (j, s + 1)]
+    return [(a, b % S) if 0 <= a < levels else None for a, b in want]
+
+
 class ShardRank:
     """Level ``level`` of row shard ``shard`` in a levels x row-shards grid
     (the layer that uses every GPU when p < #GPUs).
@@ -315,10 +326,8 @@ class ShardRank:
 
     def connect(self, blobs):
         """blobs[(level, shard)] for every rank of the grid."""
-        j, s, S, L = self.level, self.shard, self.nshards, self.config.levels
-        want = [(j - 1, s), (j - 1, s - 1), (j - 1, s + 1), (j + 1, s), (j + 1, s - 1), (j + 1, s + 1),
-                (j, s - 1), (j, s + 1)]
-        keep = [blobs[(a, b % S)] if 0 <= a < L else None for a, b in want]
+        keep = [blobs[k] if k is not None else None
+                for k in shard_neighbours(self.level, self.shard, self.nshards, self.config.levels)]
         arr = (ctypes.c_void_p * 8)(*[ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p) if b is not None else None
                                       for b in keep])
         self._keep = keep
