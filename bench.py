@@ -450,6 +450,9 @@ def run_ours(args):
                             "over NVLink)") if world > 1 else
                            ("k_resident_levels (all levels on this GPU in one launch: a co-resident CTA group "
                             "per level, registers-resident chunks, TMA-staged windows, per-segment flags)"),
+        "warp_carry_febe": "k_febe_wcarry (whole FEBE march in one launch: one 512-point chunk per warp in "
+                           "registers, rhs + factored tridiagonal solve per step, chunks coupled by two carries per "
+                           "step -- shared memory within a CTA, L2 between CTAs -- no block barriers)",
         "carry_febe": "k_febe_carry (whole FEBE march in one launch: one tile per SM in registers, rhs + "
                       "factored tridiagonal solve per step, tiles coupled by two tagged carries per step through L2)",
         "sweep_febe": "k_sweep_febe (one launch per step: every SM sweeps a contiguous range of the line through "

@@ -98,7 +98,8 @@ typedef struct ridc_info {
                                      RIDC_PATH_TICK / _RESIDENT_FEBE / _RESIDENT_LEVELS /
                                      _CARRY_FEBE / _SWEEP_FEBE / _SWEEP2D_FEBE /
                                      _SWEEP2D_LEVELS / _SWEEP_LEVELS / _SWEEP_WARP_FEBE /
-                                     _CARRY_LEVELS / _RESIDENT_CARRY_LEVELS */
+                                     _CARRY_LEVELS / _RESIDENT_CARRY_LEVELS /
+                                     _WARP_CARRY_FEBE */
     int32_t fell_back;            /* 1: a resident march could not get its co-resident
                                      SMs at run time and the tick graph replaced it */
 } ridc_info;
@@ -124,6 +125,9 @@ typedef struct ridc_info {
 #define RIDC_PATH_RESIDENT_CARRY_LEVELS 10  /* RIDC-2 on a periodic RD line: one cooperative launch per
                                         interval, both levels' tiles held on the SMs, carries
                                         exchanged between tiles */
+#define RIDC_PATH_WARP_CARRY_FEBE 11 /* one cooperative launch marches every FEBE step, one
+                                        512-point chunk per warp, chunks exchange two carries per
+                                        step (shared memory within a CTA, L2 between CTAs) */
 
 /*
  * Create a run context (RidcConfig validation engine.py:71-87, _prepare

@@ -34,12 +34,12 @@ class RidcInfo(ctypes.Structure):
 
 (PATH_TICK, PATH_RESIDENT_FEBE, PATH_RESIDENT_LEVELS, PATH_CARRY_FEBE, PATH_SWEEP_FEBE, PATH_SWEEP2D_FEBE,
  PATH_SWEEP2D_LEVELS, PATH_SWEEP_LEVELS, PATH_SWEEP_WARP_FEBE, PATH_CARRY_LEVELS,
- PATH_RESIDENT_CARRY_LEVELS) = range(11)
+ PATH_RESIDENT_CARRY_LEVELS, PATH_WARP_CARRY_FEBE) = range(12)
 PATH_NAMES = {PATH_TICK: "tick", PATH_RESIDENT_FEBE: "resident_febe", PATH_RESIDENT_LEVELS: "resident_levels",
               PATH_CARRY_FEBE: "carry_febe", PATH_SWEEP_FEBE: "sweep_febe", PATH_SWEEP2D_FEBE: "sweep2d_febe",
               PATH_SWEEP2D_LEVELS: "sweep2d_levels", PATH_SWEEP_LEVELS: "sweep_levels",
               PATH_SWEEP_WARP_FEBE: "sweep_warp_febe", PATH_CARRY_LEVELS: "carry_levels",
-              PATH_RESIDENT_CARRY_LEVELS: "resident_carry_levels"}
+              PATH_RESIDENT_CARRY_LEVELS: "resident_carry_levels", PATH_WARP_CARRY_FEBE: "warp_carry_febe"}
 
 
 # name -> (restype, argtypes); every symbol include/ridc_b200.h declares

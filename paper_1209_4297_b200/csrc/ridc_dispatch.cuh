@@ -206,6 +206,26 @@ cudaError_t febe_carry_k(bool launch, int grid, int nt, cudaStream_t st, const C
     return cudaLaunchKernelEx(&cfg, kfn, cp);
 }
 
+// ---- warp-chunk carry FEBE march (ridc_febe_carry.cuh k_febe_wcarry): one
+// cooperative launch, wpc warps (512-point chunks) per CTA
+template <int KIND>
+cudaError_t febe_wcarry_k(bool launch, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm)
+{
+    auto kfn = k_febe_wcarry<KIND>;
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, nt, 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // all chunks co-resident (neighbour carry waits)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, cp);
+}
+
 // ---- streaming FEBE sweep (ridc_sweep.cuh): one persistent CTA per SM, PDL
 // between consecutive steps
 template <int KIND, int NT>

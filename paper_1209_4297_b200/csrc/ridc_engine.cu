@@ -572,6 +572,7 @@ struct ridc_ctx {
     unsigned long long lepoch = 0;
     // carry-exchange FEBE march (ridc_febe_carry.cuh): periodic RD lines, one tile per SM
     bool carry = false;
+    bool carry_warp = false;   // k_febe_wcarry: 512-point chunks, one per warp (cparams.T = warps per CTA)
     int carry_nt = 0;
     CarryParams cparams;
     uint4* d_cmail = nullptr;
@@ -956,7 +957,9 @@ int march(ridc_ctx* c, double* wall_seconds)
         k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
         CUDA_TRY(&c->err, cudaGetLastError());
         const cudaError_t le =
-            c->carry ? febe_carry_k<RD_1D>(true, c->cparams.nseg, c->carry_nt, c->stream, c->cparams, nullptr)
+            c->carry_warp ? febe_wcarry_k<RD_1D>(true, (c->cparams.nseg + c->cparams.T - 1) / c->cparams.T,
+                                                 c->carry_nt, c->stream, c->cparams, nullptr)
+            : c->carry ? febe_carry_k<RD_1D>(true, c->cparams.nseg, c->carry_nt, c->stream, c->cparams, nullptr)
                      : resident_dispatch(c->pb.kind, c->ss.ccfg.nt, c->res_mode, true, nseg, c->stream, c->rp,
                                          nullptr);
         if (le == cudaErrorCooperativeLaunchTooLarge) {
@@ -965,6 +968,7 @@ int march(ridc_ctx* c, double* wall_seconds)
             cudaGetLastError();
             c->resident = false;
             c->carry = false;
+            c->carry_warp = false;
             c->fell_back = true;
             int rc = capture_graph(c);
             if (rc) return rc;
@@ -1024,7 +1028,28 @@ int setup_carry(ridc_ctx* c, bool* ok)
     }
     if (nseg < 2) return RIDC_OK;
     const int nch = T / 16;
-    const int nt = 32 * ((nch + 31) / 32);
+    int nt = 32 * ((nch + 31) / 32);
+    // lines of 512-point chunks: one chunk per warp, warps coupled through
+    // shared memory within a CTA (k_febe_wcarry: no block barriers);
+    // RIDC_NO_WCARRY=1 keeps the tile march (A/B)
+    bool warp_chunks = false;
+    {
+        const int nchunk = nx / 512;
+        const bool off = getenv("RIDC_NO_WCARRY") && atoi(getenv("RIDC_NO_WCARRY")) > 0;
+        int wps = 0;
+        if (!off && nx % 512 == 0 && nchunk >= 2 && nchunk <= kWCarryMaxWarps * c->nsm && hc <= 512) {
+            const int grid = std::min(c->nsm, nchunk);
+            const int wpc = (nchunk + grid - 1) / grid;
+            if (febe_wcarry_k<RD_1D>(false, 0, 32 * wpc, c->stream, cp, &wps) == cudaSuccess &&
+                wps * c->nsm >= (nchunk + wpc - 1) / wpc) {
+                warp_chunks = true;
+                T = wpc;              // the warp march reads T as warps per CTA ...
+                nseg = nchunk;        // ... and nseg as the line's chunks
+                nt = 32 * wpc;
+            }
+            cudaGetLastError();
+        }
+    }
     CUDA_TRY(&c->err, cudaMalloc(&c->d_cmail, (size_t)2 * 2 * nseg * sizeof(uint4)));
     CUDA_TRY(&c->err, cudaMemset(c->d_cmail, 0, (size_t)2 * 2 * nseg * sizeof(uint4)));
     if (!c->d_flags) CUDA_TRY(&c->err, cudaMalloc(&c->d_flags, sizeof(unsigned)));
@@ -1056,6 +1081,7 @@ int setup_carry(ridc_ctx* c, bool* ok)
     cp.spin_limit = (long long)(c->watchdog * 2.0e9);
     c->cparams = cp;
     c->carry = true;
+    c->carry_warp = warp_chunks;
     c->carry_nt = nt;
     c->resident = true;   // the resident FEBE path (final state in ring slot steps % cap)
     c->launches = 2;
@@ -1784,14 +1810,15 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->steps = c->steps;
     info->ticks_per_interval = c->ticks;
     info->kernel_launches = c->launches;
-    info->tile = c->carry ? c->cparams.T : c->ss.sv.tile;
+    info->tile = c->carry_warp ? 512 : c->carry ? c->cparams.T : c->ss.sv.tile;
     info->halo = c->carry ? 0 : c->ss.sv.halo;   // the carry march exchanges carries, not halos
     info->items_per_level = c->carry ? c->cparams.nseg : c->pb.ny * c->ss.sv.nseg;
     info->threads = c->carry ? c->carry_nt : c->ss.ccfg.nt;
     info->ring_vectors = c->ring_vectors;
     info->lambda = c->ss.sv.lam;
     info->r = c->ss.r;
-    info->path = c->carry ? RIDC_PATH_CARRY_FEBE
+    info->path = c->carry_warp ? RIDC_PATH_WARP_CARRY_FEBE
+                 : c->carry ? RIDC_PATH_CARRY_FEBE
                  : (c->sweep && !c->resident) ? (c->sweep_nt == 32 ? RIDC_PATH_SWEEP_WARP_FEBE : RIDC_PATH_SWEEP_FEBE)
                  : c->sweep2d ? RIDC_PATH_SWEEP2D_FEBE
                  : c->sweeplev ? RIDC_PATH_SWEEP2D_LEVELS

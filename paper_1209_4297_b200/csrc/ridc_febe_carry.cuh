@@ -267,4 +267,140 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-chunk variant (k_febe_wcarry): the same march with every WARP owning a
+// 512-point chunk (16 points per lane) and the chunks coupled exactly as the
+// tiles above, by two carries per step -- but between the warps of a CTA the
+// carries travel through shared memory (the same tagged 16-byte lines), so a
+// step has no block barrier and no block scan: each warp's only waits are its
+// two neighbours' lines of the same step, one hop each (L2 only where the
+// neighbour sits in another CTA).  Lines of 512-point chunks (C2: 2048 chunks,
+// 14 warps on each of 147 SMs); dropped terms below lam^512 <= 2^-60 (hc <= 512).
+
+__device__ __forceinline__ void st_line_gen(uint4* p, double v, unsigned tag)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    asm volatile("st.volatile.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)b), "r"(tag),
+                 "r"((unsigned)(b >> 32)), "r"(tag)
+                 : "memory");
+}
+
+__device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, const CarryParams& cp, bool& dead)
+{
+    uint4 v;
+    asm volatile("ld.volatile.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    if (v.y == want && v.w == want) return line_value(v);
+    const long long t0 = clock64();
+    while (!dead) {
+        asm volatile("ld.volatile.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+        if (v.y == want && v.w == want) return line_value(v);
+        if (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort) {
+            atomicExch(cp.abort, 1u);
+            dead = true;
+        }
+    }
+    return 0.0;
+}
+
+constexpr int kWCarryMaxWarps = 14;   // 448 threads: C2's 2048 chunks on 147 SMs
+
+template <int KIND>
+__global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const __grid_constant__ CarryParams cp)
+{
+    static_assert(KIND == RD_1D, "carry-exchange FEBE: periodic reaction-diffusion lines");
+    constexpr int K = 16;
+    __shared__ uint4 s_line[2][kWCarryMaxWarps][2];   // [parity][warp]: 0 = y_end, 1 = local first x
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wpc = cp.T;                                  // warps (chunks) per CTA
+    const int nch = cp.nseg;                               // chunks of the line
+    const int chunk = blockIdx.x * wpc + warp;
+    if (threadIdx.x < 2 * kWCarryMaxWarps * 2)             // no stale tag from an earlier kernel's shared memory
+        reinterpret_cast<uint4*>(s_line)[threadIdx.x] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    if (warp >= wpc || chunk >= nch) return;               // no block barrier follows
+    const int cl = chunk == 0 ? nch - 1 : chunk - 1, cr = chunk == nch - 1 ? 0 : chunk + 1;
+    const bool left_local = warp > 0;                      // chunk - 1 is this CTA's previous warp
+    const bool right_local = warp + 1 < wpc && chunk + 1 < nch;
+    const int c0 = chunk * 512 + lane * K;                 // data column of my first point
+    RIDC_CHECK(c0 + K <= cp.nx && cp.hc <= 512 && wpc <= kWCarryMaxWarps);
+    const double lam = cp.lam;
+
+    double ml = 1.0, mr = 1.0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if (lane & (1 << i)) ml *= cp.mp[i];
+        if ((31 - lane) & (1 << i)) mr *= cp.mp[i];
+    }
+    const double hmul = cp.inv1ml2 * ml, zc = lam * cp.inv1ml2;
+    double mf[5], mb[5];   // lane-masked scan multipliers (no selects in the scans)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        mf[i] = lane >= (1 << i) ? cp.mp[i] : 0.0;
+        mb[i] = lane + (1 << i) < 32 ? cp.mp[i] : 0.0;
+    }
+    double* const fin = cp.ring + cp.GW + c0;   // + slot * Vs
+    long long slot = 0;
+    double u[K];
+    load_chunk_cg(fin, u);   // slot 0: the seeded initial state
+    bool dead = false;
+
+    for (long long s = 1; s <= cp.steps; ++s) {
+        const unsigned tag = cp.tag0 + (unsigned)s;
+        const int par = (int)(s & 1);
+        uint4* box = cp.mail + (size_t)par * 2 * nch;
+        // ---- rhs (g folded in) and the local forward recurrence
+        double y = 0.0;
+#pragma unroll
+        for (int e = 0; e < K; ++e) {
+            y = fma(lam, y, fma(cp.bb, u[e], cp.aa) * u[e]);
+            u[e] = y;
+        }
+        double inc = y;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) inc = fma(mf[i], __shfl_up_sync(FULL, inc, 1 << i), inc);
+        double cf = __shfl_up_sync(FULL, inc, 1);
+        if (lane == 0) cf = 0.0;
+        const double yend = __shfl_sync(FULL, inc, 31);   // y at my chunk's last point (zero carry in)
+        // 1. publish y_end for the right neighbour
+        if (lane == 31 && !dead) st_line_gen(right_local ? &s_line[par][warp][0] : box + 2 * chunk, yend, tag);
+        // ---- local backward recurrence (zero carry at the chunk end) and its warp scan
+        double x = 0.0;
+#pragma unroll
+        for (int e = K - 1; e >= 0; --e) {
+            x = fma(lam, x, u[e]);
+            u[e] = x;
+        }
+        double rinc = fma(cf, cp.zf[0], x);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) rinc = fma(mb[i], __shfl_down_sync(FULL, rinc, 1 << i), rinc);
+        double exr = __shfl_down_sync(FULL, rinc, 1);
+        if (lane == 31) exr = 0.0;
+#pragma unroll
+        for (int e = 0; e < K; ++e) u[e] = fma(exr, cp.pw[K - 1 - e], fma(cf, cp.zf[e], u[e]));
+        // 2. publish my first point's local x for the left neighbour
+        if (lane == 0 && !dead) st_line_gen(left_local ? &s_line[par][warp][1] : box + 2 * chunk + 1, u[0], tag);
+        // ---- the neighbours' carries: left y_end (lane 0), right local first x (lane 31)
+        double cv = 0.0, dv = 0.0;
+        if (lane == 0) cv = poll_line_gen(left_local ? &s_line[par][warp - 1][0] : box + 2 * cl, tag, cp, dead);
+        if (lane == 31) dv = poll_line_gen(right_local ? &s_line[par][warp + 1][1] : box + 2 * cr + 1, tag, cp, dead);
+        const double hm = __shfl_sync(FULL, cv, 0) * hmul;
+        const double tm = fma(yend, zc, __shfl_sync(FULL, dv, 31)) * mr;   // + the head correction my y_end causes there
+#pragma unroll
+        for (int e = 0; e < K; ++e) u[e] = fma(tm, cp.pw[K - 1 - e], fma(hm, cp.pw[e], u[e]));
+        if (!chunk_finite(u)) atomicMin(cp.err, err_code((s - 1) % cp.per + 1, 0));
+        if (cp.full_every) {   // trajectory: every step to its slot (cap = steps + 1)
+            slot = slot + 1 == cp.cap ? 0 : slot + 1;
+            double* out = fin + slot * cp.Vs;
+#pragma unroll
+            for (int e = 0; e < K; e += 2) *reinterpret_cast<double2*>(out + e) = make_double2(u[e], u[e + 1]);
+        }
+    }
+    if (!cp.full_every) {   // the final state to ring slot steps % cap
+        double* out = fin + (cp.steps % cp.cap) * cp.Vs;
+#pragma unroll
+        for (int e = 0; e < K; e += 2) *reinterpret_cast<double2*>(out + e) = make_double2(u[e], u[e + 1]);
+    }
+}
+
 }  // namespace ridc

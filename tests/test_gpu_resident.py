@@ -56,11 +56,13 @@ def test_resident_equals_tick_kernel_bitwise(name, builder, steps, restarts, tra
         a, b = res.run(), tick.run()
         a2 = res.run()
         path = res.info["path_name"]
-        assert path in ("resident_febe", "carry_febe") and tick.info["path_name"] == "tick"
+        assert path in ("resident_febe", "carry_febe", "warp_carry_febe") and tick.info["path_name"] == "tick"
         if ivp.problem.kind == P.KIND_REACTION_DIFFUSION_1D and res.info["items_per_level"] > 1:
-            assert path == "carry_febe", res.info
+            # lines of 512-point chunks: one chunk per warp; other RD lines: one tile per SM
+            want = "warp_carry_febe" if ivp.dimension % 512 == 0 else "carry_febe"
+            assert path == want, res.info
     assert np.array_equal(a.final_state, a2.final_state)
-    if path == "carry_febe":
+    if path in ("carry_febe", "warp_carry_febe"):
         # periodic RD lines: tiles exchange carries instead of halos -- the same
         # solve to rounding (the tick kernel truncates at lam^H <= 2^-60)
         assert G.normwise(a.final_state, b.final_state) <= 1e-13
@@ -279,3 +281,28 @@ def test_resident_carry_res2_nonfinite_message():
                 eng.run()
             msgs.append(str(ei.value))
     assert msgs[0] == msgs[1], msgs
+
+
+@pytest.mark.parametrize("n,steps,restarts,traj", [(1 << 20, 200, 1, False), (1 << 18, 40, 2, True),
+                                                    (512 * 1000, 60, 1, False), (1 << 16, 100, 1, False)])
+def test_warp_carry_vs_tile_carry(n, steps, restarts, traj, monkeypatch):
+    """The warp-chunk march (k_febe_wcarry: a 512-point chunk per warp, carries
+    through shared memory inside a CTA) against the tile march (k_febe_carry,
+    RIDC_NO_WCARRY=1) and the oracle: the same solve to rounding."""
+    ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
+                 1e-4 * steps)
+    cfg = E.RidcConfig(levels=1, steps=steps, restarts=restarts, record_trajectory=traj)
+    with E.Engine(ivp, cfg) as w:
+        assert w.info["path_name"] == "warp_carry_febe", w.info
+        a, a2 = w.run(), w.run()
+    monkeypatch.setenv("RIDC_NO_WCARRY", "1")
+    with E.Engine(ivp, cfg) as t:
+        assert t.info["path_name"] == "carry_febe", t.info
+        b = t.run()
+    assert np.array_equal(a.final_state, a2.final_state)
+    assert G.normwise(a.final_state, b.final_state) <= 1e-13
+    if traj:
+        assert G.normwise(a.trajectory, b.trajectory) <= 1e-13
+    dt = (ivp.t_end - ivp.t_start) / steps
+    ref = O.run(ivp.problem, ivp.initial_state, 1, steps, restarts, dt, pack_weight_tables(1, dt))
+    assert G.normwise(a.final_state, ref["final_state"]) <= 1e-10
