@@ -89,10 +89,10 @@ __device__ __forceinline__ double cl_poll(const uint4* p, unsigned want, const C
     uint4 v = ld_line(p);
     if (v.y == want && v.w == want) return line_value(v);
     const long long t0 = clock64();
-    while (!dead) {
+    for (unsigned it = 1; !dead; ++it) {   // the watchdog only every 64 polls
         v = ld_line(p);
         if (v.y == want && v.w == want) return line_value(v);
-        if (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort) {
+        if ((it & 63u) == 0u && (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort)) {
             atomicExch(cp.abort, 1u);
             dead = true;
         }

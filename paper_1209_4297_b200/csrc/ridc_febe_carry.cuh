@@ -83,10 +83,10 @@ __device__ __forceinline__ double poll_line(const uint4* p, unsigned want, const
     uint4 v = ld_line(p);
     if (v.y == want && v.w == want) return line_value(v);
     const long long t0 = clock64();
-    while (!dead) {
+    for (unsigned it = 1; !dead; ++it) {   // the watchdog only every 64 polls
         v = ld_line(p);
         if (v.y == want && v.w == want) return line_value(v);
-        if (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort) {
+        if ((it & 63u) == 0u && (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort)) {
             atomicExch(cp.abort, 1u);
             dead = true;
         }
@@ -291,10 +291,12 @@ __device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, c
     asm volatile("ld.volatile.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
     if (v.y == want && v.w == want) return line_value(v);
     const long long t0 = clock64();
-    while (!dead) {
+    // the watchdog (clock and the global abort word) only every 64 polls: the
+    // common wait is a few hundred cycles and every poll is one load
+    for (unsigned it = 1; !dead; ++it) {
         asm volatile("ld.volatile.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
         if (v.y == want && v.w == want) return line_value(v);
-        if (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort) {
+        if ((it & 63u) == 0u && (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort)) {
             atomicExch(cp.abort, 1u);
             dead = true;
         }
