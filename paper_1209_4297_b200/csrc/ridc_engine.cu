@@ -584,6 +584,7 @@ struct ridc_ctx {
     // 2-D streaming FEBE sweep (ridc_sweep2d.cuh): every row read once per step
     bool sweep2d = false;
     int sweep2d_nt = 256;
+    int sweep2d_grid = 0;
     Sweep2DParams s2params;
     // 1-D level sweep (ridc_sweep_levels.cuh): the ticks of levels >= 2 on long RD lines
     bool sweeplev1 = false;
@@ -774,9 +775,9 @@ int capture_graph(ridc_ctx* c)
                          : sweep2d_levels_k<RD_2D>(c->sweeplev_nt, c->nsm, c->stream, ep, tp, c->slparams, c->tm_lev);
             else if (c->sweep2d)   // 2-D FEBE: every CTA sweeps its row block, each row read once
                 le = c->pb.kind == ADV_DIFF_2D
-                         ? sweep2d_k<ADV_DIFF_2D>(c->sweep2d_nt, c->nsm * (512 / c->sweep2d_nt), c->stream,
+                         ? sweep2d_k<ADV_DIFF_2D>(c->sweep2d_nt, c->sweep2d_grid, c->stream,
                                                   c->s2params, c->tm_sweep, ep.off[0], tp.target[0])
-                         : sweep2d_k<RD_2D>(c->sweep2d_nt, c->nsm * (512 / c->sweep2d_nt), c->stream, c->s2params,
+                         : sweep2d_k<RD_2D>(c->sweep2d_nt, c->sweep2d_grid, c->stream, c->s2params,
                                             c->tm_sweep, ep.off[0], tp.target[0]);
             else if (c->sweep)   // FEBE on a long periodic line: every SM sweeps its range
                 le = sweep_k<RD_1D>(c->sweep_nt, c->nsm, c->stream, c->sparams, c->tm_sweep,
@@ -1192,6 +1193,8 @@ int setup_sweep2d(ridc_ctx* c)
     int rc = make_ring_map(&c->tm_sweep.map[0], c->d_ring[0], c->Vs, c->cap[0], nt, &c->err);
     if (rc) return rc;
     c->sweep2d_nt = nt;
+    // 512 / nt CTAs per SM (RIDC_S2D_CPS overrides: diagnostics)
+    c->sweep2d_grid = c->nsm * std::max(1, std::min(512 / nt, env_int("RIDC_S2D_CPS", 512 / nt)));
     c->sweep2d = true;
     return RIDC_OK;
 }

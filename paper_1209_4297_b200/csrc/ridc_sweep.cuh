@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)NS * L::STAGE);
     uint64_t* empty = full + NS;
     __shared__ double sx[2 * NW];
+    __shared__ unsigned s_cnt[NS];   // warps done with each stage (refill when all are)
     __shared__ double s_bc[2];   // broadcasts: [0] forward carry into the next chunk, [1] x at its first point
     // tail threads park their chunk here one iteration (transposed: [e][slot], conflict-free)
     __shared__ double s_pend[16 * kSweepPend];
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], NW);
+            s_cnt[i] = 0u;
         }
         mbar_fence_init();
     }
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         if (tid & (1 << i)) mt *= sp.mp[i];
     }
     __syncthreads();
-    auto issue = [&](int i) {   // thread 0: chunk i of my range into stage i % NS
+    auto issue = [&](int i) {   // one lane: chunk i of my range into stage i % NS
         const int s = i % NS;
         constexpr int NBOX = NT / L::BR;
         mbar_arrive_expect_tx(&full[s], (uint32_t)(NBOX * L::BR * 128));
@@ -233,10 +235,13 @@ __global__ void __launch_bounds__(NT, 512 / NT)
             v[e] = y;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (tid == 0 && i + NS < nch) {
-            mbar_wait(&empty[s], (uint32_t)((i / NS) & 1));
-            issue(i + NS);
+        if (lane == 0) {   // the last warp done with the stage refills it (no warp blocks on the slowest)
+            __threadfence_block();
+            if (atomicAdd(&s_cnt[s], 1u) == (unsigned)(NW - 1)) {
+                s_cnt[s] = 0u;
+                __threadfence_block();
+                if (i + NS < nch) issue(i + NS);
+            }
         }
         const double bf = mine ? y : 0.0;
         double inc = warp_fwd_incl(sp, bf, lane);

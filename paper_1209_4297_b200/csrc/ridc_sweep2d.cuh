@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)NS * L::STAGE);
     uint64_t* empty = full + NS;
     __shared__ double sx[2 * NW];
+    __shared__ unsigned s_cnt[NS];   // warps done with each stage (refill when all are)
     const unsigned FULL = 0xffffffffu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], NW);
+            s_cnt[i] = 0u;
         }
         mbar_fence_init();
     }
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     }
     const double mlc = ml * mwf * sp.cyc, mrc = mr * mwb * sp.cyc;
     __syncthreads();
-    auto issue = [&](int k) {   // thread 0: loaded row k (grid row r0 - 1 + k) into stage k % NS
+    auto issue = [&](int k) {   // one lane: loaded row k (grid row r0 - 1 + k) into stage k % NS
         const int s = k % NS;
         int q = r0 - 1 + k;
         q = q < 0 ? q + ny : (q >= ny ? q - ny : q);
@@ -217,11 +219,17 @@ __global__ void __launch_bounds__(NT, 512 / NT)
                 }
             }
         }
+        // the stage goes back to the TMA once every warp consumed it: the LAST
+        // warp to finish issues the refill (a shared counter), so no warp ever
+        // blocks waiting for the slowest one (thread 0 used to, holding warp 0)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (tid == 0 && k + NS < nl) {
-            mbar_wait(&empty[s], (uint32_t)((k / NS) & 1));
-            issue(k + NS);
+        if (lane == 0) {
+            __threadfence_block();   // my warp's reads of the stage before the count
+            if (atomicAdd(&s_cnt[s], 1u) == (unsigned)(NW - 1)) {
+                s_cnt[s] = 0u;
+                __threadfence_block();
+                if (k + NS < nl) issue(k + NS);
+            }
         }
     };
     double A[K], B[K];
