@@ -591,6 +591,7 @@ struct ridc_ctx {
     // 2-D level sweep (ridc_sweep2d_levels.cuh): the ticks of levels >= 2 on 2-D grids
     bool sweeplev = false;
     int sweeplev_nt = 256;
+    int sweeplev_grid = 0;
     SweepLevParams slparams;
     TmapSet tm_lev;
     std::vector<double> h_weights;   // the packed quadrature tables (host copy)
@@ -770,9 +771,10 @@ int capture_graph(ridc_ctx* c)
                 le = sweep_levels_k<RD_1D>(c->nsm, c->stream, ep, tp, c->sparams, c->tm_lev);
             else if (c->sweeplev)   // 2-D levels: every CTA sweeps its row block for each active level
                 le = c->pb.kind == ADV_DIFF_2D
-                         ? sweep2d_levels_k<ADV_DIFF_2D>(c->sweeplev_nt, c->nsm, c->stream, ep, tp, c->slparams,
-                                                         c->tm_lev)
-                         : sweep2d_levels_k<RD_2D>(c->sweeplev_nt, c->nsm, c->stream, ep, tp, c->slparams, c->tm_lev);
+                         ? sweep2d_levels_k<ADV_DIFF_2D>(c->sweeplev_nt, c->sweeplev_grid, c->stream, ep, tp,
+                                                         c->slparams, c->tm_lev)
+                         : sweep2d_levels_k<RD_2D>(c->sweeplev_nt, c->sweeplev_grid, c->stream, ep, tp, c->slparams,
+                                                   c->tm_lev);
             else if (c->sweep2d)   // 2-D FEBE: every CTA sweeps its row block, each row read once
                 le = c->pb.kind == ADV_DIFF_2D
                          ? sweep2d_k<ADV_DIFF_2D>(c->sweep2d_nt, c->sweep2d_grid, c->stream,
@@ -1234,6 +1236,9 @@ int setup_sweep2d_levels(ridc_ctx* c)
         if (rc) return rc;
     }
     c->sweeplev_nt = nt;
+    // 4096-point rows (256 threads): two CTAs per SM (two row chains per SM
+    // hide each other's scan latency; 2 stages each); 8192: one
+    c->sweeplev_grid = c->nsm * (nt == 256 && pb.ny >= 4 * c->nsm ? std::max(1, std::min(2, env_int("RIDC_S2L_CPS", 2))) : 1);
     c->sweeplev = true;
     return RIDC_OK;
 }

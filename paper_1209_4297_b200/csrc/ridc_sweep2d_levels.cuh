@@ -37,7 +37,7 @@ namespace ridc {
 // accumulator row + the active levels' item descriptors
 template <int NT>
 struct SweepLevSmem {
-    static constexpr int NS = NT <= 256 ? 5 : 2;
+    static constexpr int NS = 2;   // (experiment: 2 stages so that two 256-thread CTAs fit an SM)
     static constexpr int ROWB = NT * 128;
     static constexpr size_t OFF_C = (size_t)NS * ROWB;
     static constexpr size_t OFF_BAR = OFF_C + ROWB;
@@ -53,7 +53,7 @@ struct SweepLevParams {
 };
 
 template <int KIND, int NT>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
     k_sweep2d_levels(EngineParams ep, TickParams tp, const __grid_constant__ SweepLevParams sp,
                      const __grid_constant__ TmapSet tm)
 {
