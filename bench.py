@@ -475,6 +475,13 @@ def run_ours(args):
                 "steps_per_launch": nt // max(tick_launches, 1)}
     if traffic_note:
         roofline["traffic_source"] = traffic_note
+    if path_name in ("warp_carry_febe", "carry_febe", "resident_febe", "resident_levels", "resident_carry_levels"):
+        # the state stays on the SMs for the whole launch: `achieved` is the
+        # equivalent bandwidth of the algorithmic bytes (frac may exceed 1);
+        # the kernel is bound by its per-step dependency chain, not by HBM
+        roofline["note"] = ("SM-resident march: DRAM traffic is one read and one write of the state per launch "
+                            "(traffic); achieved/frac are the algorithmic 16 B/pt/step as equivalent bandwidth, "
+                            "the bound is the per-step carry exchange and scan latency")
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             # level-steps/s = p N Nt / wall (work done by all levels)

@@ -59,6 +59,7 @@ CASES = {
     "febe-sweep-warp": (lambda: seg(1 << 22, 6), 1, 6, {}),
     "carry-levels-p4": (lambda: seg(1 << 19, 24), 4, 24, {}),
     "resident-res2": (lambda: seg(1 << 18, 24), 2, 24, {}),
+    "febe-warp-carry": (lambda: seg(1 << 18, 20), 1, 20, {}),
 }
 
 
