@@ -297,10 +297,9 @@ __global__ void __launch_bounds__(kRes2MaxNT, 1) k_carry_res2(const __grid_const
             }
         }
         // ---- finite checks (engine.py:160-164); the predictor's new step into the ring
-        if (!mine) {
-#pragma unroll
-            for (int e = 0; e < K; ++e) { u0[e] = 0.0; u1[e] = 0.0; }
-        } else {
+        // (threads past the tile carry garbage that never leaves them: their scan
+        // inputs are masked to zero, they store nothing and publish nothing)
+        if (mine) {
             if (A0 && !chunk_finite(u0)) atomicMin(cp.err, err_code(kk, 0));
             if (A1 && !chunk_finite(u1)) atomicMin(cp.err, err_code(kk - 2, 1));
             if (A0) {   // step kk over step kk-3 (read above, before this tick's barriers)
