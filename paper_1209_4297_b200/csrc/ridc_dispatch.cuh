@@ -209,9 +209,9 @@ cudaError_t febe_carry_k(bool launch, int grid, int nt, cudaStream_t st, const C
 // ---- warp-chunk carry FEBE march (ridc_febe_carry.cuh k_febe_wcarry): one
 // cooperative launch, wpc warps (512-point chunks) per CTA
 template <int KIND>
-cudaError_t febe_wcarry_k(bool launch, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm)
+cudaError_t febe_wcarry_k(bool launch, int k, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm)
 {
-    auto kfn = k_febe_wcarry<KIND>;
+    auto kfn = k == 32 ? k_febe_wcarry<KIND, 32> : k_febe_wcarry<KIND, 16>;
     if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, nt, 0);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

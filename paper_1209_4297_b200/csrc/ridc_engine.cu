@@ -573,6 +573,7 @@ struct ridc_ctx {
     // carry-exchange FEBE march (ridc_febe_carry.cuh): periodic RD lines, one tile per SM
     bool carry = false;
     bool carry_warp = false;   // k_febe_wcarry: 512-point chunks, one per warp (cparams.T = warps per CTA)
+    int carry_wk = 16;         // its points per lane (16 or 32)
     int carry_nt = 0;
     CarryParams cparams;
     uint4* d_cmail = nullptr;
@@ -960,7 +961,7 @@ int march(ridc_ctx* c, double* wall_seconds)
         k_seed_chunk<<<sb, 256, 0, c->stream>>>(c->d_y0, ep, -1);
         CUDA_TRY(&c->err, cudaGetLastError());
         const cudaError_t le =
-            c->carry_warp ? febe_wcarry_k<RD_1D>(true, (c->cparams.nseg + c->cparams.T - 1) / c->cparams.T,
+            c->carry_warp ? febe_wcarry_k<RD_1D>(true, c->carry_wk, (c->cparams.nseg + c->cparams.T - 1) / c->cparams.T,
                                                  c->carry_nt, c->stream, c->cparams, nullptr)
             : c->carry ? febe_carry_k<RD_1D>(true, c->cparams.nseg, c->carry_nt, c->stream, c->cparams, nullptr)
                      : resident_dispatch(c->pb.kind, c->ss.ccfg.nt, c->res_mode, true, nseg, c->stream, c->rp,
@@ -1019,39 +1020,46 @@ int setup_carry(ridc_ctx* c, bool* ok)
         cudaGetLastError();
         return RIDC_OK;
     }
-    // as many tiles as SMs (each tile a multiple of 16 points), fewer if a tile
-    // would be shorter than two carry reaches + one warp of chunks
-    int nseg = 0, T = 0;
-    for (int n = c->nsm; n >= 2; --n) {
-        const int t = 16 * ((nx + 16 * n - 1) / (16 * n));
-        const int ns = (nx + t - 1) / t;
-        const int tlast = nx - (ns - 1) * t;
-        if (t > 16 * kCarryMaxNT) break;                     // longer tiles than a CTA holds
-        if (ns >= 2 && t >= 2 * hc + 512 && tlast >= 2 * hc + 512) { nseg = ns; T = t; break; }
-    }
-    if (nseg < 2) return RIDC_OK;
-    const int nch = T / 16;
-    int nt = 32 * ((nch + 31) / 32);
-    // lines of 512-point chunks: one chunk per warp, warps coupled through
-    // shared memory within a CTA (k_febe_wcarry: no block barriers);
-    // RIDC_NO_WCARRY=1 keeps the tile march (A/B)
+    int nseg = 0, T = 0, nt = 0;
+    // lines of 512-point (or 1024-point) chunks: one chunk per warp, warps
+    // coupled through shared memory within a CTA (k_febe_wcarry: no block
+    // barriers); RIDC_NO_WCARRY=1 keeps the tile march (A/B)
     bool warp_chunks = false;
+    int wk = 0;   // points per lane of the warp march
     {
-        const int nchunk = nx / 512;
         const bool off = getenv("RIDC_NO_WCARRY") && atoi(getenv("RIDC_NO_WCARRY")) > 0;
-        int wps = 0;
-        if (!off && nx % 512 == 0 && nchunk >= 2 && nchunk <= kWCarryMaxWarps * c->nsm && hc <= 512) {
+        const int kmin = env_int("RIDC_WCARRY_K", 16) >= 32 ? 32 : 16;   // RIDC_WCARRY_K=32: A/B
+        for (int k : {16, 32}) {
+            if (k < kmin) continue;
+            const int ch = 32 * k, nchunk = nx / ch;
+            int wps = 0;
+            if (off || nx % ch || nchunk < 2 || nchunk > kWCarryMaxWarps * c->nsm || hc > ch) continue;
             const int grid = std::min(c->nsm, nchunk);
             const int wpc = (nchunk + grid - 1) / grid;
-            if (febe_wcarry_k<RD_1D>(false, 0, 32 * wpc, c->stream, cp, &wps) == cudaSuccess &&
+            if (febe_wcarry_k<RD_1D>(false, k, 0, 32 * wpc, c->stream, cp, &wps) == cudaSuccess &&
                 wps * c->nsm >= (nchunk + wpc - 1) / wpc) {
                 warp_chunks = true;
+                wk = k;
                 T = wpc;              // the warp march reads T as warps per CTA ...
                 nseg = nchunk;        // ... and nseg as the line's chunks
                 nt = 32 * wpc;
             }
             cudaGetLastError();
+            if (warp_chunks) break;
         }
+    }
+    if (!warp_chunks) {
+        // as many tiles as SMs (each tile a multiple of 16 points), fewer if a tile
+        // would be shorter than two carry reaches + one warp of chunks
+        for (int n = c->nsm; n >= 2; --n) {
+            const int t = 16 * ((nx + 16 * n - 1) / (16 * n));
+            const int ns = (nx + t - 1) / t;
+            const int tlast = nx - (ns - 1) * t;
+            if (t > 16 * kCarryMaxNT) break;                     // longer tiles than a CTA holds
+            if (ns >= 2 && t >= 2 * hc + 512 && tlast >= 2 * hc + 512) { nseg = ns; T = t; break; }
+        }
+        if (nseg < 2) return RIDC_OK;
+        nt = 32 * ((T / 16 + 31) / 32);
     }
     CUDA_TRY(&c->err, cudaMalloc(&c->d_cmail, (size_t)2 * 2 * nseg * sizeof(uint4)));
     CUDA_TRY(&c->err, cudaMemset(c->d_cmail, 0, (size_t)2 * 2 * nseg * sizeof(uint4)));
@@ -1067,6 +1075,16 @@ int setup_carry(ridc_ctx* c, bool* ok)
         cp.zf[e] = c->ss.sv.zf16[e];
     }
     for (int i = 0; i < 10; ++i) cp.mp[i] = c->ss.sv.mp16[i];
+    if (wk == 32) {   // the 32-point tables (fill_zf / fill_mp of make_factors for K = 32)
+        for (int e = 0; e < 32; ++e) cp.pw[e] = c->ss.sv.pw[e];
+        for (int e = 0; e < 32; ++e) {
+            double acc = 0.0;
+            for (int k = 31; k >= e; --k) acc = acc * lam + cp.pw[k];
+            cp.zf[e] = acc;
+        }
+        cp.mp[0] = cp.pw[31];
+        for (int i = 1; i < 10; ++i) cp.mp[i] = cp.mp[i - 1] * cp.mp[i - 1];
+    }
     cp.ring = c->d_ring[0];
     cp.cap = c->cap[0];
     cp.Vs = c->Vs;
@@ -1085,6 +1103,7 @@ int setup_carry(ridc_ctx* c, bool* ok)
     c->cparams = cp;
     c->carry = true;
     c->carry_warp = warp_chunks;
+    c->carry_wk = wk;
     c->carry_nt = nt;
     c->resident = true;   // the resident FEBE path (final state in ring slot steps % cap)
     c->launches = 2;
@@ -1818,7 +1837,7 @@ int ridc_info_get(const ridc_ctx* c, ridc_info* info)
     info->steps = c->steps;
     info->ticks_per_interval = c->ticks;
     info->kernel_launches = c->launches;
-    info->tile = c->carry_warp ? 512 : c->carry ? c->cparams.T : c->ss.sv.tile;
+    info->tile = c->carry_warp ? 32 * c->carry_wk : c->carry ? c->cparams.T : c->ss.sv.tile;
     info->halo = c->carry ? 0 : c->ss.sv.halo;   // the carry march exchanges carries, not halos
     info->items_per_level = c->carry ? c->cparams.nseg : c->pb.ny * c->ss.sv.nseg;
     info->threads = c->carry ? c->carry_nt : c->ss.ccfg.nt;

@@ -53,9 +53,9 @@ struct CarryParams {
     double lam;                // decay factor of the shifted operator's factors
     double aa, bb;             // RD rhs with g folded in: g (u + dt rho u (1 - u)) = (aa + bb u) u
     double inv1ml2;            // 1 / (1 - lam^2)
-    double pw[16];             // lam^(e+1)
-    double zf[16];             // forward-carry response of a chunk's backward pass (DevSolve::zf16)
-    double mp[10];             // M^(2^i), M = lam^16
+    double pw[32];             // lam^(e+1) (16 entries; 32 for the 32-point-per-lane warp march)
+    double zf[32];             // forward-carry response of a K-point backward pass (DevSolve::zf16 for K = 16)
+    double mp[10];             // M^(2^i), M = lam^K (K = 16; 32 for the 32-point warp march)
     double* ring;              // level-0 ring, padded layout (data column c at GW + c)
     long long cap, Vs;
     int GW;
@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
 // step has no block barrier and no block scan: each warp's only waits are its
 // two neighbours' lines of the same step, one hop each (L2 only where the
 // neighbour sits in another CTA).  Lines of 512-point chunks (C2: 2048 chunks,
-// 14 warps on each of 147 SMs); dropped terms below lam^512 <= 2^-60 (hc <= 512).
+// 14 warps on each of 147 SMs; K = 16 points per lane) or 1024-point chunks
+// (2^21: K = 32); dropped terms below lam^(32 K) <= 2^-60 (hc <= 32 K).
 
 __device__ __forceinline__ void st_line_gen(uint4* p, double v, unsigned tag)
 {
@@ -306,11 +307,15 @@ __device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, c
 
 constexpr int kWCarryMaxWarps = 14;   // 448 threads: C2's 2048 chunks on 147 SMs
 
-template <int KIND>
+// K points per lane: 16 (512-point chunks) or 32 (1024-point chunks: lines of
+// up to 14 x 148 x 1024 points, carry reach <= 1024); cp.pw / zf / mp hold the
+// K-point tables
+template <int KIND, int K>
 __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const __grid_constant__ CarryParams cp)
 {
     static_assert(KIND == RD_1D, "carry-exchange FEBE: periodic reaction-diffusion lines");
-    constexpr int K = 16;
+    static_assert(K == 16 || K == 32, "16 or 32 points per lane");
+    constexpr int CH = 32 * K;   // points per chunk
     __shared__ uint4 s_line[2][kWCarryMaxWarps][2];   // [parity][warp]: 0 = y_end, 1 = local first x
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -324,8 +329,8 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
     const int cl = chunk == 0 ? nch - 1 : chunk - 1, cr = chunk == nch - 1 ? 0 : chunk + 1;
     const bool left_local = warp > 0;                      // chunk - 1 is this CTA's previous warp
     const bool right_local = warp + 1 < wpc && chunk + 1 < nch;
-    const int c0 = chunk * 512 + lane * K;                 // data column of my first point
-    RIDC_CHECK(c0 + K <= cp.nx && cp.hc <= 512 && wpc <= kWCarryMaxWarps);
+    const int c0 = chunk * CH + lane * K;                  // data column of my first point
+    RIDC_CHECK(c0 + K <= cp.nx && cp.hc <= CH && wpc <= kWCarryMaxWarps);
     const double lam = cp.lam;
 
     double ml = 1.0, mr = 1.0;
@@ -344,8 +349,25 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
     double* const fin = cp.ring + cp.GW + c0;   // + slot * Vs
     long long slot = 0;
     double u[K];
-    load_chunk_cg(fin, u);   // slot 0: the seeded initial state
+#pragma unroll
+    for (int e = 0; e < K; e += 2) {   // slot 0: the seeded initial state
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(fin + e));
+        u[e] = v.x;
+        u[e + 1] = v.y;
+    }
     bool dead = false;
+    auto finite = [&]() {   // chunk_finite over K points
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+#pragma unroll
+        for (int e = 0; e < K; e += 4) {
+            c0 = fma(u[e], 0.0, c0);
+            c1 = fma(u[e + 1], 0.0, c1);
+            c2 = fma(u[e + 2], 0.0, c2);
+            c3 = fma(u[e + 3], 0.0, c3);
+        }
+        const double c = (c0 + c1) + (c2 + c3);
+        return c == c;
+    };
 
     for (long long s = 1; s <= cp.steps; ++s) {
         const unsigned tag = cp.tag0 + (unsigned)s;
@@ -390,7 +412,7 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
         const double tm = fma(yend, zc, __shfl_sync(FULL, dv, 31)) * mr;   // + the head correction my y_end causes there
 #pragma unroll
         for (int e = 0; e < K; ++e) u[e] = fma(tm, cp.pw[K - 1 - e], fma(hm, cp.pw[e], u[e]));
-        if (!chunk_finite(u)) atomicMin(cp.err, err_code((s - 1) % cp.per + 1, 0));
+        if (!finite()) atomicMin(cp.err, err_code((s - 1) % cp.per + 1, 0));
         if (cp.full_every) {   // trajectory: every step to its slot (cap = steps + 1)
             slot = slot + 1 == cp.cap ? 0 : slot + 1;
             double* out = fin + slot * cp.Vs;

@@ -33,7 +33,7 @@ template cudaError_t launch_item_k<RIDC_INST_KIND>(const LaunchCfg&, int, cudaSt
 template cudaError_t resident_k<RIDC_INST_KIND>(int, int, bool, int, cudaStream_t, const ResidentParams&, int*);
 #if RIDC_INST_KIND == 3
 template cudaError_t febe_carry_k<RIDC_INST_KIND>(bool, int, int, cudaStream_t, const CarryParams&, int*);
-template cudaError_t febe_wcarry_k<RIDC_INST_KIND>(bool, int, int, cudaStream_t, const CarryParams&, int*);
+template cudaError_t febe_wcarry_k<RIDC_INST_KIND>(bool, int, int, int, cudaStream_t, const CarryParams&, int*);
 template cudaError_t sweep_k<RIDC_INST_KIND>(int, int, cudaStream_t, const SweepParams&, const TmapSet&, long long,
                                              long long);
 template cudaError_t sweep_levels_k<RIDC_INST_KIND>(int, cudaStream_t, const EngineParams&, const TickParams&,

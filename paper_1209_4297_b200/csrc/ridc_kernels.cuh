@@ -377,7 +377,7 @@ cudaError_t resident_k(int nt, int mode, bool launch, int grid, cudaStream_t st,
 template <int KIND>
 cudaError_t febe_carry_k(bool launch, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm);
 template <int KIND>
-cudaError_t febe_wcarry_k(bool launch, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm);
+cudaError_t febe_wcarry_k(bool launch, int k, int grid, int nt, cudaStream_t st, const CarryParams& cp, int* per_sm);
 template <int KIND>
 cudaError_t sweep_k(int nt, int grid, cudaStream_t st, const SweepParams& sp, const TmapSet& tm, long long off,
                     long long target);

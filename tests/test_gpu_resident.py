@@ -284,20 +284,24 @@ def test_resident_carry_res2_nonfinite_message():
 
 
 @pytest.mark.parametrize("n,steps,restarts,traj", [(1 << 20, 200, 1, False), (1 << 18, 40, 2, True),
-                                                    (512 * 1000, 60, 1, False), (1 << 16, 100, 1, False)])
+                                                    (512 * 1000, 60, 1, False), (1 << 16, 100, 1, False),
+                                                    (1 << 21, 60, 1, False), (1024 * 1500, 40, 2, True)])
 def test_warp_carry_vs_tile_carry(n, steps, restarts, traj, monkeypatch):
-    """The warp-chunk march (k_febe_wcarry: a 512-point chunk per warp, carries
-    through shared memory inside a CTA) against the tile march (k_febe_carry,
-    RIDC_NO_WCARRY=1) and the oracle: the same solve to rounding."""
+    """The warp-chunk march (k_febe_wcarry: a 512- or 1024-point chunk per warp,
+    carries through shared memory inside a CTA) against the tile march
+    (k_febe_carry, RIDC_NO_WCARRY=1; the tick kernel beyond its lines) and the
+    oracle: the same solve to rounding."""
     ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
                  1e-4 * steps)
     cfg = E.RidcConfig(levels=1, steps=steps, restarts=restarts, record_trajectory=traj)
     with E.Engine(ivp, cfg) as w:
         assert w.info["path_name"] == "warp_carry_febe", w.info
+        # 16 points per lane where 512-point chunks fit 14 warps per SM, else 32
+        assert w.info["tile"] == (512 if n <= 14 * 148 * 512 else 1024), w.info
         a, a2 = w.run(), w.run()
     monkeypatch.setenv("RIDC_NO_WCARRY", "1")
-    with E.Engine(ivp, cfg) as t:
-        assert t.info["path_name"] == "carry_febe", t.info
+    with E.Engine(ivp, cfg, tick_only=n > 148 * 8192) as t:   # longer lines than the tile march holds: the tick kernel
+        assert t.info["path_name"] in ("carry_febe", "tick"), t.info
         b = t.run()
     assert np.array_equal(a.final_state, a2.final_state)
     assert G.normwise(a.final_state, b.final_state) <= 1e-13
