@@ -1,6 +1,7 @@
 // ridc_carry_levels.cuh -- the tick of the lagged level pipeline on 1-D
 // periodic reaction-diffusion lines of up to 14 x SMs x 512 points (C2:
-// 2^20 at p = 2..4), one 512-point chunk per warp, no truncation halos.
+// 2^20 at p = 2..4; or 7 x SMs x 1024 points for shifts whose carry reach
+// exceeds 512), one chunk per warp, no truncation halos.
 //
 // One launch per pipeline tick (the tick kernel's schedule, engine.py:363-371;
 // every level of a tick reads only data published in earlier ticks).  The
@@ -43,10 +44,17 @@
 
 namespace ridc {
 
-constexpr int kClWarps = 14;          // warps (chunks) per CTA at most: 448 threads, <= 146 registers
+// K points per lane: 16 (512-point chunks, carry reach <= 512) or 32
+// (1024-point chunks, reach <= 1024: stiffer shifts, e.g. imex3's a_ii = 2
+// stage at C2)
+template <int K> struct ClGeom {
+    static constexpr int WARPS = K == 16 ? 14 : 7;   // warps (chunks) per CTA at most (shared memory)
+    static constexpr int BOX = 2 * K + 2;            // staged groups per node chunk: 2K + one either side
+    static constexpr int STAGE = (BOX * 128 + 1023) / 1024 * 1024;   // bytes, the 1024-byte swizzle atom
+};
+constexpr int kClWarps = 14;          // warps per CTA at most (K = 16)
 constexpr int kClStages = 3;          // TMA stages per warp
-constexpr int kClBoxGroups = 34;      // staged groups per node chunk: 32 + one either side
-constexpr int kClStage = 5 * 1024;    // bytes per stage (34 x 128 rounded up to the 1024-byte swizzle atom)
+constexpr int kClBoxGroups = 34;      // the tensor maps' box (K = 16); K = 32 issues two boxes
 
 struct ClNode {   // one node of one level's fold, coefficients with g folded in
     double ga, gb, gs;
@@ -63,18 +71,19 @@ struct ClLevel {
 
 constexpr int kClMaxNodes = kMaxLevels * (kMaxLevels + 3) / 2 + 1;   // sum over levels of (j + 2)
 
+template <int K>
 inline size_t carry_levels_smem()
 {
-    return (size_t)kClWarps * kClStages * kClStage + 1024;
+    return (size_t)ClGeom<K>::WARPS * kClStages * ClGeom<K>::STAGE + 1024;
 }
 
 struct CarryLevParams {
     double lam, g, inv1ml2, zc;   // zc = lam / (1 - lam^2)
-    double pw[16];                // lam^(e+1)
-    double zf[16];                // forward-carry response of a 16-point backward pass
-    double mp[10];                // M^(2^i), M = lam^16
+    double pw[32];                // lam^(e+1), e < K
+    double zf[32];                // forward-carry response of a K-point backward pass
+    double mp[10];                // M^(2^i), M = lam^K
     int nx, GW, gdata;
-    int nchunk;                   // nx / 512
+    int nchunk;                   // nx / (32 K)
     int wpc;                      // chunks (warps) per CTA
     uint4* xch;                   // [2][kMaxLevels][nchunk] LL lines: 0 = y_end, 1 = first x
     const unsigned* epoch;        // bumped once per run (the graph's first node)
@@ -100,16 +109,18 @@ __device__ __forceinline__ double cl_poll(const uint4* p, unsigned want, const C
     return 0.0;
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(kClWarps * 32, 1)
+template <int KIND, int K>
+__global__ void __launch_bounds__(ClGeom<K>::WARPS * 32, 1)
     k_carry_levels(EngineParams ep, TickParams tp, const __grid_constant__ CarryLevParams cp,
                    const __grid_constant__ TmapSet tm, unsigned tick)
 {
     static_assert(KIND == RD_1D, "carry-exchange level tick: periodic reaction-diffusion lines");
-    constexpr int K = 16, NS = kClStages;
+    static_assert(K == 16 || K == 32, "16 or 32 points per lane");
+    constexpr int NS = kClStages, GL = K / 16, CH = 32 * K;   // groups per lane, points per chunk
+    constexpr int kClStage = ClGeom<K>::STAGE;
     extern __shared__ __align__(1024) char smraw[];
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t s_full[kClWarps * NS];
+    __shared__ uint64_t s_full[ClGeom<K>::WARPS * NS];
     __shared__ ClLevel s_lev[kMaxLevels];
     __shared__ ClNode s_node[kClMaxNodes];
     __shared__ unsigned s_tag;
@@ -181,9 +192,9 @@ __global__ void __launch_bounds__(kClWarps * 32, 1)
     __syncthreads();
     if (!active || cp.exp == 1) return;
     const unsigned tag = s_tag;
-    const int c0 = chunk * 512;   // data column of my chunk's first point
+    const int c0 = chunk * CH;   // data column of my chunk's first point
     const int cl = chunk == 0 ? cp.nchunk - 1 : chunk - 1, cr = chunk == cp.nchunk - 1 ? 0 : chunk + 1;
-    RIDC_CHECK(cl >= 0 && cl < cp.nchunk && cr >= 0 && cr < cp.nchunk && c0 + 512 <= cp.nx);
+    RIDC_CHECK(cl >= 0 && cl < cp.nchunk && cr >= 0 && cr < cp.nchunk && c0 + CH <= cp.nx);
 
     // node loads in fold order (level a, node n), NS stages ahead; lane 0 issues
     const int ntot = s_lev[nact - 1].node0 + s_lev[nact - 1].nn;
@@ -191,8 +202,10 @@ __global__ void __launch_bounds__(kClWarps * 32, 1)
         const int s = m % NS;
         const ClNode& nd = s_node[m];
         RIDC_CHECK(nd.slot >= 0 && nd.slot < ep.cap[nd.lev]);
-        mbar_arrive_expect_tx(&full[s], (uint32_t)(kClBoxGroups * 128));
-        tma_load_3d(stage + (size_t)s * kClStage, &tm.map[nd.lev], 0, cp.gdata + c0 / 16 - 1, (int)nd.slot, &full[s]);
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(GL * kClBoxGroups * 128));
+        for (int b = 0; b < GL; ++b)   // GL boxes of 34 groups: the chunk + one group either side (+ 2 spare)
+            tma_load_3d(stage + (size_t)s * kClStage + b * (32 * 128), &tm.map[nd.lev], 0,
+                        cp.gdata + c0 / 16 - 1 + 32 * b, (int)nd.slot, &full[s]);
     };
     if (lane == 0)
         for (int m = 0; m < NS && m < ntot; ++m) issue(m);
@@ -224,13 +237,15 @@ __global__ void __launch_bounds__(kClWarps * 32, 1)
                 mbar_wait(&full[s], (uint32_t)((m / NS) & 1));
                 const char* st = stage + (size_t)s * kClStage;
                 const ClNode nd = s_node[m];
-                // my points: staged group lane + 1; neighbours: group lane element 15, group lane + 2 element 0
-                double wl = lds128(swz(st, lane, 7)).y;
-                double2 w2 = lds128(swz(st, lane + 1, 0));
+                // my points: staged groups GL lane + 1 ...; neighbours: group GL lane
+                // element 15, group GL (lane + 1) + 1 element 0
+                const int g0 = GL * lane + 1;
+                double wl = lds128(swz(st, g0 - 1, 7)).y;
+                double2 w2 = lds128(swz(st, g0, 0));
 #pragma unroll
                 for (int q = 0; q < K / 2; ++q) {
-                    const double2 wn = q + 1 < K / 2 ? lds128(swz(st, lane + 1, q + 1))
-                                                     : make_double2(lds128(swz(st, lane + 2, 0)).x, 0.0);
+                    const double2 wn = q + 1 < K / 2 ? lds128(swz(st, g0 + (q + 1) / 8, (q + 1) % 8))
+                                                     : make_double2(lds128(swz(st, g0 + GL, 0)).x, 0.0);
                     v[2 * q] = fma(nd.gs, (wl - 2.0 * w2.x) + w2.y, fma(fma(nd.gb, w2.x, nd.ga), w2.x, v[2 * q]));
                     v[2 * q + 1] =
                         fma(nd.gs, (w2.x - 2.0 * w2.y) + wn.x, fma(fma(nd.gb, w2.y, nd.ga), w2.y, v[2 * q + 1]));
@@ -281,17 +296,23 @@ __global__ void __launch_bounds__(kClWarps * 32, 1)
             const double hm = c * cp.inv1ml2 * ml, tmul = d * mr;
 #pragma unroll
             for (int e = 0; e < K; ++e) vp[e] = fma(tmul, cp.pw[K - 1 - e], fma(hm, cp.pw[e], vp[e]));
-            const bool bad = !chunk_finite(vp);
+            double fc0 = 0.0, fc1 = 0.0;   // finite check over K points (chunk_finite)
+#pragma unroll
+            for (int e = 0; e < K; e += 2) {
+                fc0 = fma(vp[e], 0.0, fc0);
+                fc1 = fma(vp[e + 1], 0.0, fc1);
+            }
+            const bool bad = (fc0 + fc1) != (fc0 + fc1);
             // ---- store (+ the periodic ghost copies of the line's end groups)
             double* o = lv.out + cp.GW + c0 + lane * K;
 #pragma unroll
             for (int e = 0; e < K; e += 4) stg256(o + e, vp[e], vp[e + 1], vp[e + 2], vp[e + 3]);
-            if (chunk == 0 && lane == 0)
+            if (chunk == 0 && lane == 0)   // the line's first group -> the right ghost group
 #pragma unroll
-                for (int e = 0; e < K; e += 4) stg256(o + cp.nx + e, vp[e], vp[e + 1], vp[e + 2], vp[e + 3]);
-            if (chunk == cp.nchunk - 1 && lane == 31)
+                for (int e = 0; e < 16; e += 4) stg256(o + cp.nx + e, vp[e], vp[e + 1], vp[e + 2], vp[e + 3]);
+            if (chunk == cp.nchunk - 1 && lane == 31)   // its last group -> the left ghost group
 #pragma unroll
-                for (int e = 0; e < K; e += 4) stg256(o - cp.nx + e, vp[e], vp[e + 1], vp[e + 2], vp[e + 3]);
+                for (int e = K - 16; e < K; e += 4) stg256(o - cp.nx + e, vp[e], vp[e + 1], vp[e + 2], vp[e + 3]);
             if (bad) atomicMin(ep.err, err_code(lv.target, lv.level));
         }
         if (a < nact) {

@@ -378,27 +378,25 @@ cudaError_t carry_res2_k(bool launch, int grid, int nt, cudaStream_t st, const C
     return cudaLaunchKernelEx(&cfg, kfn, cp);
 }
 
-// ---- carry-exchange level tick (ridc_carry_levels.cuh): one 512-point chunk
-// per warp, wpc warps per CTA, PDL between consecutive ticks
-template <int KIND>
-cudaError_t carry_levels_k(int grid, int wpc, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+template <int KIND, int K>
+cudaError_t carry_levels_t(int grid, int wpc, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
                            const CarryLevParams& cp, const TmapSet& tm, unsigned tick)
 {
-    auto kfn = k_carry_levels<KIND>;
+    auto kfn = k_carry_levels<KIND, K>;
     static bool attr[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     if (!attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)carry_levels_smem());
+                                             (int)carry_levels_smem<K>());
         if (e != cudaSuccess) return e;
         attr[dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(32 * wpc);
-    cfg.dynamicSmemBytes = carry_levels_smem();
+    cfg.dynamicSmemBytes = carry_levels_smem<K>();
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -406,6 +404,16 @@ cudaError_t carry_levels_k(int grid, int wpc, cudaStream_t st, const EngineParam
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kfn, ep, tp, cp, tm, tick);
+}
+
+// ---- carry-exchange level tick (ridc_carry_levels.cuh): one chunk of 32 k
+// points per warp (k = 16 or 32), wpc warps per CTA, PDL between ticks
+template <int KIND>
+cudaError_t carry_levels_k(int grid, int wpc, int k, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+                           const CarryLevParams& cp, const TmapSet& tm, unsigned tick)
+{
+    return k == 32 ? carry_levels_t<KIND, 32>(grid, wpc, st, ep, tp, cp, tm, tick)
+                   : carry_levels_t<KIND, 16>(grid, wpc, st, ep, tp, cp, tm, tick);
 }
 
 // ---- 2-D level sweep (ridc_sweep2d_levels.cuh): one CTA of nx / 16 threads per SM

@@ -604,7 +604,7 @@ struct ridc_ctx {
     uint4* d_crmail = nullptr;
     // carry-exchange level tick (ridc_carry_levels.cuh): RIDC p >= 2 on RD lines of <= 14 x SMs x 512 points
     bool carrylev = false;
-    int cl_grid = 0, cl_wpc = 0;
+    int cl_grid = 0, cl_wpc = 0, cl_k = 16;
     CarryLevParams clparams;
     TmapSet tm_cl;
     uint4* d_clx = nullptr;
@@ -766,7 +766,7 @@ int capture_graph(ridc_ctx* c)
             if (top_active) slot_free((long long)r * c->per + ttop);
             if (le != cudaSuccess) break;
             if (c->carrylev)   // 1-D levels: one chunk per warp, carries exchanged between chunks
-                le = carry_levels_k<RD_1D>(c->cl_grid, c->cl_wpc, c->stream, ep, tp, c->clparams, c->tm_cl,
+                le = carry_levels_k<RD_1D>(c->cl_grid, c->cl_wpc, c->cl_k, c->stream, ep, tp, c->clparams, c->tm_cl,
                                            (unsigned)((long long)r * c->ticks + k));
             else if (c->sweeplev1)   // 1-D levels: every SM sweeps its range for each active level
                 le = sweep_levels_k<RD_1D>(c->nsm, c->stream, ep, tp, c->sparams, c->tm_lev);
@@ -1384,7 +1384,7 @@ int setup_carry_res2(ridc_ctx* c)
 // The carry-level tick's per-launch solve constants from a factored shift
 // (DevSolve: lam, g and the 16-point tables).  lam = 0, g = 1 (the identity
 // "solve" of an ARK final combination) zeroes every carry.
-void fill_carry_lev(CarryLevParams& cp, const DevSolve& sv)
+void fill_carry_lev(CarryLevParams& cp, const DevSolve& sv, int k = 16)
 {
     cp.lam = sv.lam;
     cp.g = sv.g;
@@ -1395,6 +1395,26 @@ void fill_carry_lev(CarryLevParams& cp, const DevSolve& sv)
         cp.zf[e] = sv.zf16[e];
     }
     for (int i = 0; i < 10; ++i) cp.mp[i] = sv.mp16[i];
+    if (k == 32) {   // the 32-point tables (make_factors' fill_zf / fill_mp for K = 32)
+        for (int e = 0; e < 32; ++e) cp.pw[e] = sv.pw[e];
+        for (int e = 0; e < 32; ++e) {
+            double acc = 0.0;
+            for (int j = 31; j >= e; --j) acc = acc * sv.lam + cp.pw[j];
+            cp.zf[e] = acc;
+        }
+        cp.mp[0] = cp.pw[31];
+        for (int i = 1; i < 10; ++i) cp.mp[i] = cp.mp[i - 1] * cp.mp[i - 1];
+    }
+}
+
+// Points per lane of the carry-level tick for a line of nx points whose
+// stiffest shift has carry reach hc: 16 (512-point chunks, <= 14 per CTA) where
+// it fits, else 32 (1024-point chunks, <= 7 per CTA); 0: neither.
+int carry_lev_k(int nx, int hc, int nsm)
+{
+    if (nx % 512 == 0 && hc <= 512 && nx / 512 >= 2 && nx / 512 <= ClGeom<16>::WARPS * nsm) return 16;
+    if (nx % 1024 == 0 && hc <= 1024 && nx / 1024 >= 2 && nx / 1024 <= ClGeom<32>::WARPS * nsm) return 32;
+    return 0;
 }
 
 // Carry-exchange level tick (ridc_carry_levels.cuh): RIDC order >= 2 on a
@@ -1410,13 +1430,14 @@ int setup_carry_levels(ridc_ctx* c)
     if (getenv("RIDC_NO_CARRYLEV") && atoi(getenv("RIDC_NO_CARRYLEV")) > 0) return RIDC_OK;
     const double lam = c->ss.sv.lam;
     const int hc = halo_of(lam);
-    const int nchunk = pb.nx / 512;
-    if (hc > 512 || nchunk < 2 || nchunk > kClWarps * c->nsm) return RIDC_OK;
+    const int k = carry_lev_k(pb.nx, hc, c->nsm);
+    if (!k) return RIDC_OK;
+    const int nchunk = pb.nx / (32 * k);
     const int grid = std::min(c->nsm, nchunk);
     const int wpc = (nchunk + grid - 1) / grid;
     CarryLevParams& cp = c->clparams;
     memset(&cp, 0, sizeof cp);
-    fill_carry_lev(cp, c->ss.sv);
+    fill_carry_lev(cp, c->ss.sv, k);
     cp.nx = pb.nx;
     cp.GW = c->ss.lay.GW;
     cp.gdata = c->ss.lay.gdata;
@@ -1442,6 +1463,7 @@ int setup_carry_levels(ridc_ctx* c)
     }
     c->cl_grid = (nchunk + wpc - 1) / wpc;
     c->cl_wpc = wpc;
+    c->cl_k = k;
     c->carrylev = true;
     return RIDC_OK;
 }
@@ -3052,7 +3074,7 @@ struct ridc_ark_ctx {
     long long launches = 0;
     // the carry-exchange tick for every stage (periodic RD lines of 512-point chunks)
     bool carrylev = false;
-    int cl_grid = 0, cl_wpc = 0;
+    int cl_grid = 0, cl_wpc = 0, cl_k = 16;
     std::vector<CarryLevParams> clp;   // per item: the stage's solve
     TmapSet tm_cl;
     uint4* d_clx = nullptr;
@@ -3236,11 +3258,11 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
     // the line qualifies: periodic RD, 512-point chunks, the stiffest stage's
     // carry reach <= 512
     {
-        const int nchunk = a->pb.nx / 512;
         const bool off = getenv("RIDC_NO_CARRYLEV") && atoi(getenv("RIDC_NO_CARRYLEV")) > 0;
-        if (!off && a->pb.kind == RD_1D && a->pb.ny == 1 && a->pb.nx % 512 == 0 && nchunk >= 2 &&
-            nchunk <= kClWarps * a->nsm && halo_of(a->ss.sv.lam) <= 512 && a->ss.lay.GW >= 16 &&
-            (long long)steps * a->nitems < 0x7fffffffLL) {
+        const int kp = (a->pb.kind == RD_1D && a->pb.ny == 1) ? carry_lev_k(a->pb.nx, halo_of(a->ss.sv.lam), a->nsm) : 0;
+        const int nchunk = kp ? a->pb.nx / (32 * kp) : 0;
+        if (!off && kp && a->ss.lay.GW >= 16 && (long long)steps * a->nitems < 0x7fffffffLL) {
+            a->cl_k = kp;
             const int grid = std::min(a->nsm, nchunk), wpc = (nchunk + grid - 1) / grid;
             const size_t xb = (size_t)2 * kMaxLevels * nchunk * sizeof(uint4);
             ARK_TRY(cudaMalloc(&a->d_clx, xb));
@@ -3253,7 +3275,7 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
             for (int k = 0; k < a->nitems; ++k) {
                 CarryLevParams& cp = a->clp[k];
                 memset(&cp, 0, sizeof cp);
-                fill_carry_lev(cp, a->solves[k].sv);
+                fill_carry_lev(cp, a->solves[k].sv, a->cl_k);
                 cp.nx = a->pb.nx;
                 cp.GW = a->ss.lay.GW;
                 cp.gdata = a->ss.lay.gdata;
@@ -3301,7 +3323,7 @@ int ridc_ark_create(const ridc_problem* problem, double t_start, double t_end, i
             tp.pre = a->d_items + parity * a->nitems + k;
             tp.target[0] = n + 1;
             if (a->carrylev)
-                le = carry_levels_k<RD_1D>(a->cl_grid, a->cl_wpc, a->stream, ep, tp, a->clp[k], a->tm_cl,
+                le = carry_levels_k<RD_1D>(a->cl_grid, a->cl_wpc, a->cl_k, a->stream, ep, tp, a->clp[k], a->tm_cl,
                                            (unsigned)(n * a->nitems + k + 1));
             else
                 le = launch_chunk(a->pb.kind, a->ss.ccfg, std::min(a->nsm * chunk_ctas_per_sm(a->ss.ccfg, 1), tiles),

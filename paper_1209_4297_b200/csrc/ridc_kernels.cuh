@@ -390,7 +390,7 @@ cudaError_t sweep_levels_k(int grid, cudaStream_t st, const EngineParams& ep, co
 template <int KIND>
 cudaError_t carry_res2_k(bool launch, int grid, int nt, cudaStream_t st, const CarryRes2Params& cp, int* per_sm);
 template <int KIND>
-cudaError_t carry_levels_k(int grid, int wpc, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
+cudaError_t carry_levels_k(int grid, int wpc, int k, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
                            const CarryLevParams& cp, const TmapSet& tm, unsigned tick);
 template <int KIND>
 cudaError_t sweep2d_levels_k(int nt, int grid, cudaStream_t st, const EngineParams& ep, const TickParams& tp,

@@ -66,10 +66,9 @@ def test_ark_carry_levels_vs_tick(scheme, exp, monkeypatch):
     ivp = P.StructuredIVP(s.problem, 0.0, 1e-4 * steps, s.ivp.initial_state)
     tab = _tab(scheme)
     # imex3's stiffest stage (a_ii = 2) at C2's r ~ 110 has a carry reach of 618
-    # points > the 512-point chunks: that march stays on the tick kernel
-    want = "tick" if (scheme == "imex3" and exp == 20) else "carry_levels"
+    # points: 1024-point chunks (32 points per lane) there
     with S.ArkEngine(ivp, tab, 0.0, 1e-4 * steps, steps) as eng:
-        assert eng.info["path_name"] == want, eng.info
+        assert eng.info["path_name"] == "carry_levels", eng.info
         a, _ = eng.run(ivp.initial_state)
         a2, _ = eng.run(ivp.initial_state)
     monkeypatch.setenv("RIDC_NO_CARRYLEV", "1")

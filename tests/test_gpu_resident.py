@@ -127,6 +127,8 @@ def test_sweep_febe_long_lines(name, n, steps, restarts, traj, variant, monkeypa
     (<= 1e-13: same solve, different association) and the oracle."""
     if variant == "cta":
         monkeypatch.setenv("RIDC_SWEEP_CTA", "1")
+    # lines the warp-chunk march holds (up to 14 x 148 x 1024 points) would take it
+    monkeypatch.setenv("RIDC_NO_WCARRY", "1")
     ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
                  1e-4 * steps)
     cfg = E.RidcConfig(levels=1, steps=steps, restarts=restarts, record_trajectory=traj)
@@ -310,3 +312,26 @@ def test_warp_carry_vs_tile_carry(n, steps, restarts, traj, monkeypatch):
     dt = (ivp.t_end - ivp.t_start) / steps
     ref = O.run(ivp.problem, ivp.initial_state, 1, steps, restarts, dt, pack_weight_tables(1, dt))
     assert G.normwise(a.final_state, ref["final_state"]) <= 1e-10
+
+
+@pytest.mark.parametrize("levels,steps", [(3, 24), (4, 30)])
+def test_carry_levels_1024_point_chunks(levels, steps):
+    """A stiffer C2 line (r ~ 220: carry reach 618 > 512) runs the carry-level
+    tick with 1024-point chunks (32 points per lane, csrc/ridc_carry_levels.cuh):
+    against the tick kernel (<= 1e-12) and the oracle (<= 1e-10)."""
+    n = 1 << 20
+    ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=2e-6)), 1e-4 * steps)
+    cfg = E.RidcConfig(levels=levels, steps=steps)
+    with E.Engine(ivp, cfg) as cl, E.Engine(ivp, cfg, tick_only=True) as tick:
+        assert cl.info["path_name"] == "carry_levels", cl.info
+        assert cl.info["r"] > 200, cl.info
+        a, b = cl.run(), tick.run()
+        a2 = cl.run()
+    for j in range(levels):
+        assert np.array_equal(a.level_finals[j], a2.level_finals[j]), j
+        assert G.normwise(a.level_finals[j], b.level_finals[j]) <= 1e-12, j
+    dt = (ivp.t_end - ivp.t_start) / steps
+    ref = O.run(ivp.problem, ivp.initial_state, levels, steps, 1, dt, pack_weight_tables(levels, dt),
+                level_finals=True)
+    for j in range(levels):
+        assert G.normwise(a.level_finals[j], ref["level_finals"][j]) <= 1e-10, j
