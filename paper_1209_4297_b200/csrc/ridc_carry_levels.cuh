@@ -288,8 +288,12 @@ __global__ void __launch_bounds__(ClGeom<K>::WARPS * 32, 1)
             const int b = a - 1;
             const ClLevel lv = s_lev[b];
             double cv = 0.0, dv = 0.0;
-            if (lane == 0) cv = cl_poll(cp.xch + (size_t)b * cp.nchunk + cl, tag, cp, dead);
-            if (lane == 31) dv = cl_poll(cp.xch + (size_t)(kMaxLevels + b) * cp.nchunk + cr, tag, cp, dead);
+            if (lane == 0 || lane == 31) {   // one loop for both lanes: the two L2 round trips overlap
+                const double v = cl_poll(lane == 0 ? cp.xch + (size_t)b * cp.nchunk + cl
+                                                   : cp.xch + (size_t)(kMaxLevels + b) * cp.nchunk + cr,
+                                         tag, cp, dead);
+                if (lane == 0) cv = v; else dv = v;
+            }
             const double c = __shfl_sync(FULL, cv, 0);
             // + the head correction my own y_end causes at the right chunk's first point
             const double d = fma(yend_p, cp.zc, __shfl_sync(FULL, dv, 31));

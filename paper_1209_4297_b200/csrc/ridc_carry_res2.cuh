@@ -263,13 +263,11 @@ __global__ void __launch_bounds__(kRes2MaxNT, 1) k_carry_res2(const __grid_const
         }
         // ---- head: the left neighbour's forward carries
         if (head_warp) {
-            double ca = 0.0, cb = 0.0;
-            if (lane == 0) {
-                if (A0) ca = res2_poll(box + 4 * kl + 0, tag, cp, dead);
-                if (A1) cb = res2_poll(box + 4 * kl + 1, tag, cp, dead);
-            }
-            ca = __shfl_sync(FULL, ca, 0) * Mh;
-            cb = __shfl_sync(FULL, cb, 0) * Mh;
+            // lane 0 waits for level 0's line, lane 1 for level 1's, in one loop
+            double cv = 0.0;
+            if ((A0 && lane == 0) || (A1 && lane == 1)) cv = res2_poll(box + 4 * kl + lane, tag, cp, dead);
+            const double ca = __shfl_sync(FULL, cv, 0) * Mh;
+            const double cb = __shfl_sync(FULL, cv, 1) * Mh;
             if (head) {
 #pragma unroll
                 for (int e = 0; e < K; ++e) {
@@ -281,13 +279,11 @@ __global__ void __launch_bounds__(kRes2MaxNT, 1) k_carry_res2(const __grid_const
         // ---- tail: the right neighbour's backward carries (its local first x + the
         // head correction my own y_end causes there)
         if (tail_warp) {
-            double da = 0.0, db = 0.0;
-            if (lane == 0) {
-                if (A0) da = fma(s_yend[0] * cp.inv1ml2, cp.pw[0], res2_poll(box + 4 * kr + 2, tag, cp, dead));
-                if (A1) db = fma(s_yend[1] * cp.inv1ml2, cp.pw[0], res2_poll(box + 4 * kr + 3, tag, cp, dead));
-            }
-            da = __shfl_sync(FULL, da, 0) * Mt;
-            db = __shfl_sync(FULL, db, 0) * Mt;
+            double dv = 0.0;
+            if ((A0 && lane == 0) || (A1 && lane == 1))
+                dv = fma(s_yend[lane] * cp.inv1ml2, cp.pw[0], res2_poll(box + 4 * kr + 2 + lane, tag, cp, dead));
+            const double da = __shfl_sync(FULL, dv, 0) * Mt;
+            const double db = __shfl_sync(FULL, dv, 1) * Mt;
             if (tail) {
 #pragma unroll
                 for (int e = 0; e < K; ++e) {

@@ -1100,6 +1100,7 @@ int setup_carry(ridc_ctx* c, bool* ok)
     cp.err = c->d_err;
     cp.abort = c->d_flags;
     cp.spin_limit = (long long)(c->watchdog * 2.0e9);
+    cp.exp = env_int("RIDC_WC_EXP", 0);   // diagnostics: WRONG states, timing only
     c->cparams = cp;
     c->carry = true;
     c->carry_warp = warp_chunks;

@@ -69,6 +69,7 @@ struct CarryParams {
     unsigned long long* err;
     unsigned* abort;
     long long spin_limit;
+    int exp;                   // diagnostics (RIDC_WC_EXP, k_febe_wcarry): 1 = no exchange (WRONG states), 2, 4 = A/B
 };
 
 __device__ __forceinline__ void csync_n(int n)
@@ -286,10 +287,17 @@ __device__ __forceinline__ void st_line_gen(uint4* p, double v, unsigned tag)
                  : "memory");
 }
 
-__device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, const CarryParams& cp, bool& dead)
+__device__ __forceinline__ uint4 ld_line_gen(const uint4* p)
 {
     uint4 v;
     asm volatile("ld.volatile.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+}
+
+// v: a first observation of the line (issued earlier, its latency hidden)
+__device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, const CarryParams& cp, bool& dead,
+                                                uint4 v)
+{
     if (v.y == want && v.w == want) return line_value(v);
     const long long t0 = clock64();
     // the watchdog (clock and the global abort word) only every 64 polls: the
@@ -303,6 +311,11 @@ __device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, c
         }
     }
     return 0.0;
+}
+
+__device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, const CarryParams& cp, bool& dead)
+{
+    return poll_line_gen(p, want, cp, dead, ld_line_gen(p));
 }
 
 constexpr int kWCarryMaxWarps = 14;   // 448 threads: C2's 2048 chunks on 147 SMs
@@ -339,7 +352,12 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
         if (lane & (1 << i)) ml *= cp.mp[i];
         if ((31 - lane) & (1 << i)) mr *= cp.mp[i];
     }
-    const double hmul = cp.inv1ml2 * ml, zc = lam * cp.inv1ml2;
+    const double zc = lam * cp.inv1ml2, zk = lam * cp.pw[K - 1];   // lam^(K+1)
+    // diagnostics (RIDC_WC_EXP): 1 = no exchange (WRONG states), 2 = the first x
+    // published after the backward scan, no early loads; 4 = see zdot below
+    const bool late = cp.exp & 2, zdot = cp.exp & 4, chainscan = cp.exp & 8;
+    const double ilam = 1.0 / lam;
+    const double xw = ml * cp.inv1ml2 * ilam;   // first-x weight of my points: M^lane lam^e / (1 - lam^2)
     double mf[5], mb[5];   // lane-masked scan multipliers (no selects in the scans)
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
@@ -373,45 +391,110 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
         const unsigned tag = cp.tag0 + (unsigned)s;
         const int par = (int)(s & 1);
         uint4* box = cp.mail + (size_t)par * 2 * nch;
-        // ---- rhs (g folded in) and the local forward recurrence
-        double y = 0.0;
+        const bool pub = !dead && !(cp.exp & 1);
+        // ---- rhs (g folded in)
 #pragma unroll
-        for (int e = 0; e < K; ++e) {
-            y = fma(lam, y, fma(cp.bb, u[e], cp.aa) * u[e]);
-            u[e] = y;
+        for (int e = 0; e < K; ++e) u[e] = fma(cp.bb, u[e], cp.aa) * u[e];
+        // Per lane, dot products of the rhs with pw[e] and pw[K-1-e]:
+        //   sb = lam * (y at my last point, zero carry in): the forward scan's input,
+        //        so the scan (and y_end) does not wait for the recurrence;
+        //   sa gives my chunk's local first x for the left neighbour,
+        //        x_0 = sum_j lam^j (1 - lam^(2 (CH - j))) / (1 - lam^2) r_j over the
+        //        chunk's points j = K lane + e, the lam^(2 CH - j) part below
+        //        lam^CH <= 2^-60 (the march's truncation) dropped: one butterfly.
+        // Both carries leave before any recurrence: the L2 hop overlaps my two
+        // recurrences and scans instead of following them
+        // (profiles/r2_wcarry_early.json).  RIDC_WC_EXP=4 also takes the backward
+        // scan's input from a third dot product (with zf[e]: lam * the lane's x
+        // at its first point), A/B only.
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, z0 = 0.0, z1 = 0.0;
+#pragma unroll
+        for (int e = 0; e < K; e += 2) {
+            a0 = fma(u[e], cp.pw[e], a0);
+            a1 = fma(u[e + 1], cp.pw[e + 1], a1);
+            if (!chainscan) {
+                b0 = fma(u[e], cp.pw[K - 1 - e], b0);
+                b1 = fma(u[e + 1], cp.pw[K - 2 - e], b1);
+            }
+            if (zdot) {
+                z0 = fma(u[e], cp.zf[e], z0);
+                z1 = fma(u[e + 1], cp.zf[e + 1], z1);
+            }
         }
-        double inc = y;
+        if (!late) {
+            double cx = (a0 + a1) * xw;
+#pragma unroll
+            for (int i = 16; i >= 1; i >>= 1) cx += __shfl_xor_sync(FULL, cx, i);
+            if (lane == 0 && pub) st_line_gen(left_local ? &s_line[par][warp][1] : box + 2 * chunk + 1, cx, tag);
+        }
+        // ---- forward carries: the warp scan of the lanes' last y
+        double inc = (b0 + b1) * ilam;
+        double y = 0.0;
+        if (chainscan) {   // A/B: the scan's input from the recurrence
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+                y = fma(lam, y, u[e]);
+                u[e] = y;
+            }
+            inc = y;
+        }
 #pragma unroll
         for (int i = 0; i < 5; ++i) inc = fma(mf[i], __shfl_up_sync(FULL, inc, 1 << i), inc);
         double cf = __shfl_up_sync(FULL, inc, 1);
         if (lane == 0) cf = 0.0;
         const double yend = __shfl_sync(FULL, inc, 31);   // y at my chunk's last point (zero carry in)
         // 1. publish y_end for the right neighbour
-        if (lane == 31 && !dead) st_line_gen(right_local ? &s_line[par][warp][0] : box + 2 * chunk, yend, tag);
-        // ---- local backward recurrence (zero carry at the chunk end) and its warp scan
+        if (lane == 31 && pub) st_line_gen(right_local ? &s_line[par][warp][0] : box + 2 * chunk, yend, tag);
+        // ---- the local forward and backward recurrences (zero carries)
+        if (!chainscan) {
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+                y = fma(lam, y, u[e]);
+                u[e] = y;
+            }
+        }
         double x = 0.0;
 #pragma unroll
         for (int e = K - 1; e >= 0; --e) {
             x = fma(lam, x, u[e]);
             u[e] = x;
         }
+        if (zdot) x = (z0 + z1) * ilam;
+        // the neighbours' lines, loaded now and checked after the backward scan
+        // (published early, they are usually there: the load's L2 round trip
+        // overlaps the scan)
+        const uint4* lsrc = left_local ? &s_line[par][warp - 1][0] : box + 2 * cl;
+        const uint4* rsrc = right_local ? &s_line[par][warp + 1][1] : box + 2 * cr + 1;
+        uint4 lv = make_uint4(0u, 0u, 0u, 0u);
+        if (!late && (lane == 0 || lane == 31)) lv = ld_line_gen(lane == 0 ? lsrc : rsrc);
         double rinc = fma(cf, cp.zf[0], x);
 #pragma unroll
         for (int i = 0; i < 5; ++i) rinc = fma(mb[i], __shfl_down_sync(FULL, rinc, 1 << i), rinc);
         double exr = __shfl_down_sync(FULL, rinc, 1);
         if (lane == 31) exr = 0.0;
-#pragma unroll
-        for (int e = 0; e < K; ++e) u[e] = fma(exr, cp.pw[K - 1 - e], fma(cf, cp.zf[e], u[e]));
-        // 2. publish my first point's local x for the left neighbour
-        if (lane == 0 && !dead) st_line_gen(left_local ? &s_line[par][warp][1] : box + 2 * chunk + 1, u[0], tag);
-        // ---- the neighbours' carries: left y_end (lane 0), right local first x (lane 31)
+        if (late && lane == 0 && pub)   // lane 0: no forward carry inside the warp, only the backward one
+            st_line_gen(left_local ? &s_line[par][warp][1] : box + 2 * chunk + 1, fma(exr, cp.pw[K - 1], u[0]), tag);
+        // ---- the neighbours' carries: left y_end (lane 0), right local first x
+        // (lane 31), both lanes in ONE wait loop (two divergent branches would
+        // run their waits back to back: a second L2 round trip)
         double cv = 0.0, dv = 0.0;
-        if (lane == 0) cv = poll_line_gen(left_local ? &s_line[par][warp - 1][0] : box + 2 * cl, tag, cp, dead);
-        if (lane == 31) dv = poll_line_gen(right_local ? &s_line[par][warp + 1][1] : box + 2 * cr + 1, tag, cp, dead);
-        const double hm = __shfl_sync(FULL, cv, 0) * hmul;
-        const double tm = fma(yend, zc, __shfl_sync(FULL, dv, 31)) * mr;   // + the head correction my y_end causes there
+        if (!(cp.exp & 1) && (lane == 0 || lane == 31)) {
+            const uint4* src = lane == 0 ? lsrc : rsrc;
+            const double v = poll_line_gen(src, tag, cp, dead, late ? ld_line_gen(src) : lv);
+            if (lane == 0) cv = v; else dv = v;
+        }
+        // ---- every correction at once.  The warp's own carries move x_e by
+        // cf zf[e] + exr pw[K-1-e] with zf[e] = (pw[e] - lam^(K+1) pw[K-1-e]) /
+        // (1 - lam^2); the left neighbour's y_end by cv M^lane pw[e] / (1 - lam^2)
+        // (head), the right neighbour's first x (+ the head correction my y_end
+        // causes there) by tm pw[K-1-e] (tail): one rank-2 update in the basis
+        // pw[e], pw[K-1-e]
+        const double fw = cf * cp.inv1ml2;
+        const double fc = fma(__shfl_sync(FULL, cv, 0) * ml, cp.inv1ml2, fw);
+        const double tm = fma(yend, zc, __shfl_sync(FULL, dv, 31)) * mr;
+        const double bc = fma(-fw, zk, exr + tm);
 #pragma unroll
-        for (int e = 0; e < K; ++e) u[e] = fma(tm, cp.pw[K - 1 - e], fma(hm, cp.pw[e], u[e]));
+        for (int e = 0; e < K; ++e) u[e] = fma(bc, cp.pw[K - 1 - e], fma(fc, cp.pw[e], u[e]));
         if (!finite()) atomicMin(cp.err, err_code((s - 1) % cp.per + 1, 0));
         if (cp.full_every) {   // trajectory: every step to its slot (cap = steps + 1)
             slot = slot + 1 == cp.cap ? 0 : slot + 1;
