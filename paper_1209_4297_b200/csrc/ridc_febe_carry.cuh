@@ -69,7 +69,7 @@ struct CarryParams {
     unsigned long long* err;
     unsigned* abort;
     long long spin_limit;
-    int exp;                   // diagnostics (RIDC_WC_EXP, k_febe_wcarry): 1 = no exchange (WRONG states), 2, 4 = A/B
+    int exp;                   // diagnostics (RIDC_WC_EXP, k_febe_wcarry): 1 = no exchange (WRONG states), 2 = late first x
 };
 
 __device__ __forceinline__ void csync_n(int n)
@@ -279,12 +279,25 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
 // 14 warps on each of 147 SMs; K = 16 points per lane) or 1024-point chunks
 // (2^21: K = 32); dropped terms below lam^(32 K) <= 2^-60 (hc <= 32 K).
 
-__device__ __forceinline__ void st_line_gen(uint4* p, double v, unsigned tag)
+// Predicated forms (no branch around a one-lane store / load: the warp's basic
+// block stays whole, so the scheduler interleaves the recurrences with the
+// scans' shuffles and no convergence check precedes the next shuffle)
+__device__ __forceinline__ void st_line_if(bool pred, uint4* p, double v, unsigned tag)
 {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-    asm volatile("st.volatile.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)b), "r"(tag),
-                 "r"((unsigned)(b >> 32)), "r"(tag)
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.volatile.v4.u32 [%0], {%1, %2, %3, %4};\n\t}"
+                 ::"l"(p), "r"((unsigned)b), "r"(tag), "r"((unsigned)(b >> 32)), "r"(tag), "r"((int)pred)
                  : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_line_if(bool pred, const uint4* p)
+{
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.volatile.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+                 : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+                 : "l"(p), "r"((int)pred)
+                 : "memory");
+    return v;
 }
 
 __device__ __forceinline__ uint4 ld_line_gen(const uint4* p)
@@ -292,30 +305,6 @@ __device__ __forceinline__ uint4 ld_line_gen(const uint4* p)
     uint4 v;
     asm volatile("ld.volatile.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
     return v;
-}
-
-// v: a first observation of the line (issued earlier, its latency hidden)
-__device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, const CarryParams& cp, bool& dead,
-                                                uint4 v)
-{
-    if (v.y == want && v.w == want) return line_value(v);
-    const long long t0 = clock64();
-    // the watchdog (clock and the global abort word) only every 64 polls: the
-    // common wait is a few hundred cycles and every poll is one load
-    for (unsigned it = 1; !dead; ++it) {
-        asm volatile("ld.volatile.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-        if (v.y == want && v.w == want) return line_value(v);
-        if ((it & 63u) == 0u && (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort)) {
-            atomicExch(cp.abort, 1u);
-            dead = true;
-        }
-    }
-    return 0.0;
-}
-
-__device__ __forceinline__ double poll_line_gen(const uint4* p, unsigned want, const CarryParams& cp, bool& dead)
-{
-    return poll_line_gen(p, want, cp, dead, ld_line_gen(p));
 }
 
 constexpr int kWCarryMaxWarps = 14;   // 448 threads: C2's 2048 chunks on 147 SMs
@@ -354,8 +343,8 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
     }
     const double zc = lam * cp.inv1ml2, zk = lam * cp.pw[K - 1];   // lam^(K+1)
     // diagnostics (RIDC_WC_EXP): 1 = no exchange (WRONG states), 2 = the first x
-    // published after the backward scan, no early loads; 4 = see zdot below
-    const bool late = cp.exp & 2, zdot = cp.exp & 4, chainscan = cp.exp & 8;
+    // published after the backward scan, no early loads
+    const bool late = cp.exp & 2;
     const double ilam = 1.0 / lam;
     const double xw = ml * cp.inv1ml2 * ilam;   // first-x weight of my points: M^lane lam^e / (1 - lam^2)
     double mf[5], mb[5];   // lane-masked scan multipliers (no selects in the scans)
@@ -404,54 +393,37 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
         //        lam^CH <= 2^-60 (the march's truncation) dropped: one butterfly.
         // Both carries leave before any recurrence: the L2 hop overlaps my two
         // recurrences and scans instead of following them
-        // (profiles/r2_wcarry_early.json).  RIDC_WC_EXP=4 also takes the backward
-        // scan's input from a third dot product (with zf[e]: lam * the lane's x
-        // at its first point), A/B only.
-        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, z0 = 0.0, z1 = 0.0;
+        // (profiles/r2_wcarry_early.json: also the A/Bs not kept -- the scan fed
+        // by the recurrence, a third dot product for the backward scan, K = 32).
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
         for (int e = 0; e < K; e += 2) {
             a0 = fma(u[e], cp.pw[e], a0);
             a1 = fma(u[e + 1], cp.pw[e + 1], a1);
-            if (!chainscan) {
-                b0 = fma(u[e], cp.pw[K - 1 - e], b0);
-                b1 = fma(u[e + 1], cp.pw[K - 2 - e], b1);
-            }
-            if (zdot) {
-                z0 = fma(u[e], cp.zf[e], z0);
-                z1 = fma(u[e + 1], cp.zf[e + 1], z1);
-            }
+            b0 = fma(u[e], cp.pw[K - 1 - e], b0);
+            b1 = fma(u[e + 1], cp.pw[K - 2 - e], b1);
         }
         if (!late) {
             double cx = (a0 + a1) * xw;
 #pragma unroll
             for (int i = 16; i >= 1; i >>= 1) cx += __shfl_xor_sync(FULL, cx, i);
-            if (lane == 0 && pub) st_line_gen(left_local ? &s_line[par][warp][1] : box + 2 * chunk + 1, cx, tag);
+            st_line_if(lane == 0 && pub, left_local ? &s_line[par][warp][1] : box + 2 * chunk + 1, cx, tag);
         }
         // ---- forward carries: the warp scan of the lanes' last y
         double inc = (b0 + b1) * ilam;
-        double y = 0.0;
-        if (chainscan) {   // A/B: the scan's input from the recurrence
-#pragma unroll
-            for (int e = 0; e < K; ++e) {
-                y = fma(lam, y, u[e]);
-                u[e] = y;
-            }
-            inc = y;
-        }
 #pragma unroll
         for (int i = 0; i < 5; ++i) inc = fma(mf[i], __shfl_up_sync(FULL, inc, 1 << i), inc);
         double cf = __shfl_up_sync(FULL, inc, 1);
         if (lane == 0) cf = 0.0;
         const double yend = __shfl_sync(FULL, inc, 31);   // y at my chunk's last point (zero carry in)
         // 1. publish y_end for the right neighbour
-        if (lane == 31 && pub) st_line_gen(right_local ? &s_line[par][warp][0] : box + 2 * chunk, yend, tag);
+        st_line_if(lane == 31 && pub, right_local ? &s_line[par][warp][0] : box + 2 * chunk, yend, tag);
         // ---- the local forward and backward recurrences (zero carries)
-        if (!chainscan) {
+        double y = 0.0;
 #pragma unroll
-            for (int e = 0; e < K; ++e) {
-                y = fma(lam, y, u[e]);
-                u[e] = y;
-            }
+        for (int e = 0; e < K; ++e) {
+            y = fma(lam, y, u[e]);
+            u[e] = y;
         }
         double x = 0.0;
 #pragma unroll
@@ -459,30 +431,43 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
             x = fma(lam, x, u[e]);
             u[e] = x;
         }
-        if (zdot) x = (z0 + z1) * ilam;
         // the neighbours' lines, loaded now and checked after the backward scan
         // (published early, they are usually there: the load's L2 round trip
         // overlaps the scan)
-        const uint4* lsrc = left_local ? &s_line[par][warp - 1][0] : box + 2 * cl;
-        const uint4* rsrc = right_local ? &s_line[par][warp + 1][1] : box + 2 * cr + 1;
-        uint4 lv = make_uint4(0u, 0u, 0u, 0u);
-        if (!late && (lane == 0 || lane == 31)) lv = ld_line_gen(lane == 0 ? lsrc : rsrc);
+        // lane 0 reads the left neighbour's y_end, lane 31 the right one's first x
+        const bool need = (lane == 0 || lane == 31) && !(cp.exp & 1);
+        const uint4* src = lane == 0 ? (left_local ? &s_line[par][warp - 1][0] : box + 2 * cl)
+                                     : (right_local ? &s_line[par][warp + 1][1] : box + 2 * cr + 1);
+        uint4 lv = ld_line_if(need && !late, src);
         double rinc = fma(cf, cp.zf[0], x);
 #pragma unroll
         for (int i = 0; i < 5; ++i) rinc = fma(mb[i], __shfl_down_sync(FULL, rinc, 1 << i), rinc);
         double exr = __shfl_down_sync(FULL, rinc, 1);
         if (lane == 31) exr = 0.0;
-        if (late && lane == 0 && pub)   // lane 0: no forward carry inside the warp, only the backward one
-            st_line_gen(left_local ? &s_line[par][warp][1] : box + 2 * chunk + 1, fma(exr, cp.pw[K - 1], u[0]), tag);
-        // ---- the neighbours' carries: left y_end (lane 0), right local first x
-        // (lane 31), both lanes in ONE wait loop (two divergent branches would
-        // run their waits back to back: a second L2 round trip)
-        double cv = 0.0, dv = 0.0;
-        if (!(cp.exp & 1) && (lane == 0 || lane == 31)) {
-            const uint4* src = lane == 0 ? lsrc : rsrc;
-            const double v = poll_line_gen(src, tag, cp, dead, late ? ld_line_gen(src) : lv);
-            if (lane == 0) cv = v; else dv = v;
+        // lane 0: no forward carry inside the warp, only the backward one
+        st_line_if(late && lane == 0 && pub, left_local ? &s_line[par][warp][1] : box + 2 * chunk + 1,
+                   fma(exr, cp.pw[K - 1], u[0]), tag);
+        if (late) lv = ld_line_if(need, src);
+        // ---- the neighbours' carries: one vote over lanes 0 and 31; the rare
+        // re-poll is a warp-uniform loop (both lanes wait together, one L2 round
+        // trip per round, the watchdog every 64 rounds)
+        bool ok = !need || dead || (lv.y == tag && lv.w == tag);
+        if (!__all_sync(FULL, ok)) {
+            const long long t0 = clock64();
+            for (unsigned it = 1; !__all_sync(FULL, ok); ++it) {
+                if (!ok) {
+                    lv = ld_line_gen(src);
+                    ok = lv.y == tag && lv.w == tag;
+                    if (!ok && (it & 63u) == 0u && (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort)) {
+                        atomicExch(cp.abort, 1u);
+                        dead = true;
+                        ok = true;
+                    }
+                }
+            }
         }
+        const double lvv = need && !dead ? line_value(lv) : 0.0;
+        const double cv = lane == 0 ? lvv : 0.0, dv = lane == 31 ? lvv : 0.0;
         // ---- every correction at once.  The warp's own carries move x_e by
         // cf zf[e] + exr pw[K-1-e] with zf[e] = (pw[e] - lam^(K+1) pw[K-1-e]) /
         // (1 - lam^2); the left neighbour's y_end by cv M^lane pw[e] / (1 - lam^2)
@@ -495,7 +480,10 @@ __global__ void __launch_bounds__(kWCarryMaxWarps * 32, 1) k_febe_wcarry(const _
         const double bc = fma(-fw, zk, exr + tm);
 #pragma unroll
         for (int e = 0; e < K; ++e) u[e] = fma(bc, cp.pw[K - 1 - e], fma(fc, cp.pw[e], u[e]));
-        if (!finite()) atomicMin(cp.err, err_code((s - 1) % cp.per + 1, 0));
+        {
+            const bool bad = !finite();
+            if (__any_sync(FULL, bad) && bad) atomicMin(cp.err, err_code((s - 1) % cp.per + 1, 0));   // uniform test first
+        }
         if (cp.full_every) {   // trajectory: every step to its slot (cap = steps + 1)
             slot = slot + 1 == cp.cap ? 0 : slot + 1;
             double* out = fin + slot * cp.Vs;
