@@ -378,6 +378,28 @@ cudaError_t carry_res2_k(bool launch, int grid, int nt, cudaStream_t st, const C
     return cudaLaunchKernelEx(&cfg, kfn, cp);
 }
 
+// ---- resident RIDC-2, one chunk per warp (ridc_carry_res2w.cuh): two CTAs per SM
+template <int KIND>
+cudaError_t carry_res2w_k(bool launch, int grid, cudaStream_t st, const CarryRes2Params& cp, int* per_sm)
+{
+    auto kfn = k_carry_res2w<KIND>;
+    const size_t smem = carry_res2w_smem();
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, kR2wNT, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kR2wNT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // all chunks co-resident (neighbour carry waits)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, cp);
+}
+
 template <int KIND, int K>
 cudaError_t carry_levels_t(int grid, int wpc, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
                            const CarryLevParams& cp, const TmapSet& tm, unsigned tick)

@@ -599,6 +599,7 @@ struct ridc_ctx {
     std::vector<int> h_steady_off;
     // resident RIDC-2 (ridc_carry_res2.cuh): one cooperative launch per interval
     bool carryres = false;
+    bool cr_warp = false;   // k_carry_res2w: 512-point chunks, one per warp (cr_nt: the grid)
     int cr_nt = 0;
     CarryRes2Params crparams;
     uint4* d_crmail = nullptr;
@@ -903,7 +904,8 @@ int march_carryres(ridc_ctx* c, bool* fell_back)
         cp.src = src;
         cp.tag0 = c->tag_next;
         c->tag_next += (unsigned)c->per + 3;   // ticks 1 .. per + 2
-        const cudaError_t le = carry_res2_k<RD_1D>(true, nseg, c->cr_nt, c->stream, cp, nullptr);
+        const cudaError_t le = c->cr_warp ? carry_res2w_k<RD_1D>(true, c->cr_nt, c->stream, cp, nullptr)
+                                          : carry_res2_k<RD_1D>(true, nseg, c->cr_nt, c->stream, cp, nullptr);
         if (le == cudaErrorCooperativeLaunchTooLarge && r == 0) {
             cudaGetLastError();
             *fell_back = true;
@@ -1320,22 +1322,39 @@ int setup_carry_res2(ridc_ctx* c)
     if (getenv("RIDC_NO_CARRYRES") && atoi(getenv("RIDC_NO_CARRYRES")) > 0) return RIDC_OK;
     const double lam = c->ss.sv.lam;
     const int hc = halo_of(lam), nx = pb.nx;
-    int nseg = 0, T = 0;
-    for (int n = c->nsm; n >= 2; --n) {   // the carry march's tiling, 448 threads at most
-        const int t = 16 * ((nx + 16 * n - 1) / (16 * n));
-        const int ns = (nx + t - 1) / t;
-        const int tlast = nx - (ns - 1) * t;
-        if (t > 16 * kRes2MaxNT) break;
-        if (ns >= 2 && t >= 2 * hc + 512 && tlast >= 2 * hc + 512) { nseg = ns; T = t; break; }
-    }
-    if (nseg < 2) return RIDC_OK;
-    const int nt = 32 * ((T / 16 + 31) / 32);
-    int per_sm = 0;
+    int nseg = 0, T = 0, nt = 0;
     CarryRes2Params& cp = c->crparams;
     memset(&cp, 0, sizeof cp);
-    if (carry_res2_k<RD_1D>(false, 0, nt, c->stream, cp, &per_sm) != cudaSuccess || per_sm * c->nsm < nseg) {
+    // one 512-point chunk per warp (k_carry_res2w: no block barriers) where the
+    // line divides and 7-warp CTAs fit two per SM; RIDC_RES2_TILE=1 keeps the
+    // tile march (A/B)
+    bool warp_chunks = false;
+    if (nx % 512 == 0 && hc <= 512 && nx / 512 >= 2 && env_int("RIDC_RES2_TILE", 0) == 0) {
+        const int nch = nx / 512, grid = (nch + kR2wWarps - 1) / kR2wWarps;
+        int per_sm = 0;
+        if (carry_res2w_k<RD_1D>(false, 0, c->stream, cp, &per_sm) == cudaSuccess && per_sm * c->nsm >= grid) {
+            warp_chunks = true;
+            nseg = nch;           // the warp march reads nseg as the line's chunks ...
+            T = kR2wWarps;        // ... and T as warps per CTA
+            nt = grid;            // cr_nt: its grid
+        }
         cudaGetLastError();
-        return RIDC_OK;
+    }
+    if (!warp_chunks) {
+        for (int n = c->nsm; n >= 2; --n) {   // the carry march's tiling, 448 threads at most
+            const int t = 16 * ((nx + 16 * n - 1) / (16 * n));
+            const int ns = (nx + t - 1) / t;
+            const int tlast = nx - (ns - 1) * t;
+            if (t > 16 * kRes2MaxNT) break;
+            if (ns >= 2 && t >= 2 * hc + 512 && tlast >= 2 * hc + 512) { nseg = ns; T = t; break; }
+        }
+        if (nseg < 2) return RIDC_OK;
+        nt = 32 * ((T / 16 + 31) / 32);
+        int per_sm = 0;
+        if (carry_res2_k<RD_1D>(false, 0, nt, c->stream, cp, &per_sm) != cudaSuccess || per_sm * c->nsm < nseg) {
+            cudaGetLastError();
+            return RIDC_OK;
+        }
     }
     const size_t mb = (size_t)(4 * 4 + 4 * 2) * nseg * sizeof(uint4);
     CUDA_TRY(&c->err, cudaMalloc(&c->d_crmail, mb));
@@ -1377,6 +1396,7 @@ int setup_carry_res2(ridc_ctx* c)
     cp.abort = c->d_flags;
     cp.spin_limit = (long long)(c->watchdog * 2.0e9);
     c->cr_nt = nt;
+    c->cr_warp = warp_chunks;
     c->carryres = true;
     c->launches = c->restarts;
     return RIDC_OK;

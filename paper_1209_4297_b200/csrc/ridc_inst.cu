@@ -39,6 +39,7 @@ template cudaError_t sweep_k<RIDC_INST_KIND>(int, int, cudaStream_t, const Sweep
 template cudaError_t sweep_levels_k<RIDC_INST_KIND>(int, cudaStream_t, const EngineParams&, const TickParams&,
                                                     const SweepParams&, const TmapSet&);
 template cudaError_t carry_res2_k<RIDC_INST_KIND>(bool, int, int, cudaStream_t, const CarryRes2Params&, int*);
+template cudaError_t carry_res2w_k<RIDC_INST_KIND>(bool, int, cudaStream_t, const CarryRes2Params&, int*);
 template cudaError_t carry_levels_k<RIDC_INST_KIND>(int, int, int, cudaStream_t, const EngineParams&,
                                                     const TickParams&, const CarryLevParams&, const TmapSet&, unsigned);
 #endif

@@ -361,6 +361,7 @@ constexpr int kResStages = 2;
 #include "ridc_sweep_levels.cuh"
 #include "ridc_carry_levels.cuh"
 #include "ridc_carry_res2.cuh"
+#include "ridc_carry_res2w.cuh"
 
 namespace ridc {
 
@@ -389,6 +390,8 @@ cudaError_t sweep_levels_k(int grid, cudaStream_t st, const EngineParams& ep, co
                            const SweepParams& sp, const TmapSet& tm);
 template <int KIND>
 cudaError_t carry_res2_k(bool launch, int grid, int nt, cudaStream_t st, const CarryRes2Params& cp, int* per_sm);
+template <int KIND>
+cudaError_t carry_res2w_k(bool launch, int grid, cudaStream_t st, const CarryRes2Params& cp, int* per_sm);
 template <int KIND>
 cudaError_t carry_levels_k(int grid, int wpc, int k, cudaStream_t st, const EngineParams& ep, const TickParams& tp,
                            const CarryLevParams& cp, const TmapSet& tm, unsigned tick);

@@ -238,16 +238,18 @@ RES2_CASES = [
     ("c2", 1 << 20, 40, 1),
     ("c2-r4", 1 << 20, 48, 4),
     ("2^18", 1 << 18, 30, 1),
-    ("uneven-tiles", (1 << 20) - 16 * 999, 30, 2),
+    ("uneven-tiles", (1 << 20) - 16 * 999, 30, 2),   # not whole 512-point chunks: the tile kernel
+    ("two-ctas", 512 * 9, 30, 1),                     # warp chunks: a full and a 2-warp CTA
 ]
 
 
 @pytest.mark.parametrize("name,n,steps,restarts", RES2_CASES, ids=[c[0] for c in RES2_CASES])
 def test_resident_carry_res2(name, n, steps, restarts):
-    """RIDC-2 with both levels held on the SMs for a whole interval, one tile
-    per SM, the tiles coupled by carries and the predictor's end points
-    (csrc/ridc_carry_res2.cuh): repeat runs bitwise, both level finals against
-    the tick kernel (<= 1e-12) and the oracle (<= 1e-10)."""
+    """RIDC-2 with both levels held on the SMs for a whole interval: one
+    512-point chunk per warp where the line divides (csrc/ridc_carry_res2w.cuh),
+    else one tile per SM (ridc_carry_res2.cuh), coupled by carries and the
+    predictor's end points: repeat runs bitwise, both level finals against the
+    tick kernel (<= 1e-12) and the oracle (<= 1e-10)."""
     ivp = _short(P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=n, d=1e-6 * (2.0 ** 20 / n) ** 2)),
                  1e-4 * steps)
     cfg = E.RidcConfig(levels=2, steps=steps, restarts=restarts)
