@@ -452,7 +452,8 @@ def run_ours(args):
                             "per level, registers-resident chunks, TMA-staged windows, per-segment flags)"),
         "warp_carry_febe": "k_febe_wcarry (whole FEBE march in one launch: one 512-point chunk per warp in "
                            "registers, rhs + factored tridiagonal solve per step, chunks coupled by two carries per "
-                           "step -- shared memory within a CTA, L2 between CTAs -- no block barriers)",
+                           "step -- shared memory within a CTA, L2 between CTAs -- computed from the rhs and "
+                           "published before the recurrences, no block barriers)",
         "carry_febe": "k_febe_carry (whole FEBE march in one launch: one tile per SM in registers, rhs + "
                       "factored tridiagonal solve per step, tiles coupled by two tagged carries per step through L2)",
         "sweep_febe": "k_sweep_febe (one launch per step: every SM sweeps a contiguous range of the line through "
@@ -460,8 +461,9 @@ def run_ours(args):
         "sweep_warp_febe": "k_sweep_febe_warp (one launch per step: every warp sweeps a contiguous range of the "
                            "line through its own TMA-staged 512-point chunks, no block barriers, each point read "
                            "and written once)",
-        "resident_carry_levels": "k_carry_res2 (RIDC-2: both levels' tiles in registers for a whole interval, one "
-                                 "cooperative launch, tiles coupled by carries and the predictor's end points)",
+        "resident_carry_levels": "k_carry_res2w / k_carry_res2 (RIDC-2: both levels in registers for a whole "
+                                 "interval, one cooperative launch; one 512-point chunk per warp (or one tile per "
+                                 "SM) coupled by carries and the predictor's end points)",
         "carry_levels": "k_carry_levels (one launch per tick: every warp folds and solves one 512-point chunk of "
                         "each active level, neighbouring chunks exchange two carries through L2)",
         "sweep2d_febe": "k_sweep2d_febe (one launch per step: every CTA sweeps a row block, each row read once and "
@@ -481,7 +483,8 @@ def run_ours(args):
         # the kernel is bound by its per-step dependency chain, not by HBM
         roofline["note"] = ("SM-resident march: DRAM traffic is one read and one write of the state per launch "
                             "(traffic); achieved/frac are the algorithmic 16 B/pt/step as equivalent bandwidth, "
-                            "the bound is the per-step carry exchange and scan latency")
+                            "the bound is the per-step dependency chain (recurrences, warp scans, the neighbour "
+                            "carries' L2 hop) and FP64 instruction issue")
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             # level-steps/s = p N Nt / wall (work done by all levels)
