@@ -15,6 +15,7 @@ ap.add_argument("--n", type=int, default=1 << 23)
 ap.add_argument("--steps", type=int, default=12)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--kind", default="rd1")
+ap.add_argument("--levels", type=int, default=1)
 a = ap.parse_args()
 if a.kind == "rd1":
     ivp = P.build_reaction_diffusion(P.ReactionDiffusionSpec(n=a.n, d=1e-6 * (2.0 ** 20 / a.n) ** 2,
@@ -23,7 +24,7 @@ elif a.kind == "ad2":
     ivp = P.build_advection_diffusion_2d(P.AdvectionDiffusion2DSpec(nx=a.n, ny=a.n, t_end=0.02 * a.steps / 1000)).ivp
 else:
     ivp = P.build_reaction_diffusion_2d(P.ReactionDiffusion2DSpec(nx=a.n, ny=a.n, t_end=0.05 * a.steps / 1000)).ivp
-with E.Engine(ivp, E.RidcConfig(levels=1, steps=a.steps)) as eng:
+with E.Engine(ivp, E.RidcConfig(levels=a.levels, steps=a.steps)) as eng:
     print("path", eng.info["path_name"], flush=True)
     outs = [eng.run().final_state for _ in range(a.reps)]
 for r in range(1, a.reps):
