@@ -45,6 +45,7 @@ struct CarryRes2Params {
     double a1, b1;                 // corrector own node (ca 1, cs 0, cn dt), g folded
     double an, bn, sn;             // node "new" (predictor step t: cs w0 - dt, cn w0), g folded, sn = g cs cdx
     double ao, bo, so;             // node "old" (predictor step t - 1: cs w1, cn w1 - dt)
+    double an2, ao2;               // an - 2 sn, ao - 2 so: the f^S stencil's centre folded into the node's linear term
     double pw[16], zf[16], mp[10];
     const double* src;             // the interval's state0 (plain layout, nx doubles)
     double* fin0;                  // level finals: padded slot + GW (data column 0)
@@ -169,8 +170,8 @@ __global__ void __launch_bounds__(kRes2MaxNT, 1) k_carry_res2(const __grid_const
                 const double nr = e == K - 1 ? Pn[1] : Pn[(e + 1) * NP];
                 const double orr = e == K - 1 ? Po[1] : Po[(e + 1) * NP];
                 double r = fma(cp.b1, u1[e], cp.a1) * u1[e];
-                r = fma(cp.sn, (nl - 2.0 * nc) + nr, fma(fma(cp.bn, nc, cp.an), nc, r));
-                r = fma(cp.so, (ol - 2.0 * oc) + orr, fma(fma(cp.bo, oc, cp.ao), oc, r));
+                r = fma(cp.sn, nl + nr, fma(fma(cp.bn, nc, cp.an2), nc, r));   // an2 = an - 2 sn
+                r = fma(cp.so, ol + orr, fma(fma(cp.bo, oc, cp.ao2), oc, r));
                 u1[e] = r;
                 nl = nc; nc = nr; ol = oc; oc = orr;
             }

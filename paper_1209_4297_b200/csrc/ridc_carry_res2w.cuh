@@ -27,7 +27,7 @@
 // reader's tick-k line, which the reader publishes after its tick-k fold.
 // Across a CTA edge the end points travel as tagged edge lines
 // (k_carry_res2's, two ticks old when read).
-// Two 7-warp CTAs per SM (<= 144 registers a thread); states agree with the
+// One CTA per SM of 7 or 14 warps (128 registers); states agree with the
 // tick kernel to rounding and with k_carry_res2 (tests/test_gpu_resident.py).
 #pragma once
 #include <cuda_runtime.h>
@@ -40,10 +40,9 @@
 
 namespace ridc {
 
-constexpr int kR2wWarps = 7;
-constexpr int kR2wNT = kR2wWarps * 32;
-constexpr int kR2wNP = kR2wNT + 2;   // ring row stride
-inline size_t carry_res2w_smem() { return (size_t)3 * 16 * kR2wNP * sizeof(double); }
+constexpr int kR2wWarps = 7;   // warps per CTA while one CTA per SM holds the line; else 14
+__host__ __device__ constexpr int r2w_np(int w) { return w * 32 + 2; }   // ring row stride
+inline size_t carry_res2w_smem(int w) { return (size_t)3 * 16 * r2w_np(w) * sizeof(double); }
 
 // Wait (one lane or none per call site, every lane of the warp calls it) for a
 // tagged line: the first load predicated, then one vote; the re-poll loop is
@@ -70,21 +69,21 @@ __device__ __forceinline__ double r2w_wait(bool need, const uint4* p, unsigned w
     return need && !dead ? line_value(v) : 0.0;
 }
 
-// cp.T: warps per CTA (<= kR2wWarps); cp.nseg: chunks of the line (512 points);
+// W: warps per CTA (cp.T); cp.nseg: chunks of the line (512 points);
 // cp.mail: [2 parities][nseg][4] lines (y_end level 0, level 1, first x level 0,
 // level 1); cp.edge: [4 parities][CTAs][2] (a CTA's first / last predictor point)
-template <int KIND>
-__global__ void __launch_bounds__(kR2wNT, 2) k_carry_res2w(const __grid_constant__ CarryRes2Params cp)
+template <int KIND, int W>
+__global__ void __launch_bounds__(W * 32, W <= 7 ? 2 : 1) k_carry_res2w(const __grid_constant__ CarryRes2Params cp)
 {
     static_assert(KIND == RD_1D, "resident RIDC-2: periodic reaction-diffusion lines");
-    constexpr int K = 16, CH = 32 * K, NP = kR2wNP;
+    constexpr int K = 16, CH = 32 * K, NP = r2w_np(W);
     extern __shared__ double ring[];   // [3 slots][16][NP]
-    __shared__ uint4 s_line[2][kR2wWarps][4];
+    __shared__ uint4 s_line[2][W][4];
     const unsigned FULL = 0xffffffffu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wpc = cp.T, nch = cp.nseg, ncta = gridDim.x, k = blockIdx.x;
     const int nwk = min(wpc, nch - k * wpc);   // my CTA's warps (chunks)
-    if (tid < 2 * kR2wWarps * 4) reinterpret_cast<uint4*>(s_line)[tid] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid < 2 * W * 4) reinterpret_cast<uint4*>(s_line)[tid] = make_uint4(0u, 0u, 0u, 0u);
     const int chunk = k * wpc + warp;
     const bool active = warp < nwk;
     const int c0 = chunk * CH + lane * K;   // data column of my first point
@@ -93,7 +92,7 @@ __global__ void __launch_bounds__(kR2wNT, 2) k_carry_res2w(const __grid_constant
     const int cl = chunk == 0 ? nch - 1 : chunk - 1, cr = chunk == nch - 1 ? 0 : chunk + 1;
     const bool left_local = warp > 0, right_local = warp + 1 < nwk;
     const double lam = cp.lam, ilam = 1.0 / lam;
-    RIDC_CHECK(nwk >= 1 && wpc <= kR2wWarps && cp.hc <= CH && nch * CH == cp.nx);
+    RIDC_CHECK(nwk >= 1 && wpc == W && cp.hc <= CH && nch * CH == cp.nx);
     auto R = [&](int slot, int e, int col) -> double& { return ring[(slot * K + e) * NP + col]; };
 
     double ml = 1.0, mr = 1.0;
@@ -175,8 +174,8 @@ __global__ void __launch_bounds__(kR2wNT, 2) k_carry_res2w(const __grid_constant
                 const double nr = e == K - 1 ? Pn[1] : Pn[(e + 1) * NP];
                 const double orr = e == K - 1 ? Po[1] : Po[(e + 1) * NP];
                 double r = fma(cp.b1, u1[e], cp.a1) * u1[e];
-                r = fma(cp.sn, (nl - 2.0 * nc) + nr, fma(fma(cp.bn, nc, cp.an), nc, r));
-                r = fma(cp.so, (ol - 2.0 * oc) + orr, fma(fma(cp.bo, oc, cp.ao), oc, r));
+                r = fma(cp.sn, nl + nr, fma(fma(cp.bn, nc, cp.an2), nc, r));   // an2 = an - 2 sn
+                r = fma(cp.so, ol + orr, fma(fma(cp.bo, oc, cp.ao2), oc, r));
                 u1[e] = r;
                 nl = nc; nc = nr; ol = oc; oc = orr;
             }

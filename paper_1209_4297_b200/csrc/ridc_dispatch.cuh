@@ -382,14 +382,15 @@ cudaError_t carry_res2_k(bool launch, int grid, int nt, cudaStream_t st, const C
 template <int KIND>
 cudaError_t carry_res2w_k(bool launch, int grid, cudaStream_t st, const CarryRes2Params& cp, int* per_sm)
 {
-    auto kfn = k_carry_res2w<KIND>;
-    const size_t smem = carry_res2w_smem();
+    auto kfn = cp.T == 14 ? k_carry_res2w<KIND, 14> : k_carry_res2w<KIND, 7>;
+    const int nt = 32 * cp.T;
+    const size_t smem = carry_res2w_smem(cp.T);
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, kR2wNT, smem);
+    if (!launch) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, nt, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kR2wNT);
+    cfg.blockDim = dim3(nt);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];

@@ -1330,12 +1330,19 @@ int setup_carry_res2(ridc_ctx* c)
     // tile march (A/B)
     bool warp_chunks = false;
     if (nx % 512 == 0 && hc <= 512 && nx / 512 >= 2 && env_int("RIDC_RES2_TILE", 0) == 0) {
-        const int nch = nx / 512, grid = (nch + kR2wWarps - 1) / kR2wWarps;
+        // 7-warp CTAs while one per SM holds the line, else one 14-warp CTA per SM
+        // (two 7-warp CTAs per SM measured 7% slower at C2, profiles/r2_res2w.json);
+        // RIDC_RES2W_WARPS=7 / 14 forces it (A/B)
+        const int nch = nx / 512;
+        const int fw = env_int("RIDC_RES2W_WARPS", 0);
+        const int wpc = fw == 7 || fw == 14 ? fw : ((nch + kR2wWarps - 1) / kR2wWarps > c->nsm ? 14 : kR2wWarps);
+        const int grid = (nch + wpc - 1) / wpc;
+        cp.T = wpc;
         int per_sm = 0;
         if (carry_res2w_k<RD_1D>(false, 0, c->stream, cp, &per_sm) == cudaSuccess && per_sm * c->nsm >= grid) {
             warp_chunks = true;
             nseg = nch;           // the warp march reads nseg as the line's chunks ...
-            T = kR2wWarps;        // ... and T as warps per CTA
+            T = wpc;              // ... and T as warps per CTA
             nt = grid;            // cr_nt: its grid
         }
         cudaGetLastError();
@@ -1378,6 +1385,8 @@ int setup_carry_res2(ridc_ctx* c)
     cp.ao = g * no.a;
     cp.bo = g * no.b;
     cp.so = g * no.cs * pb.cdx;
+    cp.an2 = cp.an - 2.0 * cp.sn;
+    cp.ao2 = cp.ao - 2.0 * cp.so;
     for (int e = 0; e < 16; ++e) {
         cp.pw[e] = c->ss.sv.pw[e];
         cp.zf[e] = c->ss.sv.zf16[e];
