@@ -278,6 +278,10 @@ __global__ void __launch_bounds__(kCarryMaxNT, 1) k_febe_carry(const __grid_cons
 // neighbour sits in another CTA).  Lines of 512-point chunks (C2: 2048 chunks,
 // 14 warps on each of 147 SMs; K = 16 points per lane) or 1024-point chunks
 // (2^21: K = 32); dropped terms below lam^(32 K) <= 2^-60 (hc <= 32 K).
+// Both outgoing carries are computed from the step's right-hand side (dot
+// products with the pw tables) and published before the recurrences, so the
+// L2 hop overlaps the solve; every one-lane store / load is predicated and the
+// neighbour wait is a warp vote ("Early carries").
 
 // Predicated forms (no branch around a one-lane store / load: the warp's basic
 // block stays whole, so the scheduler interleaves the recurrences with the
