@@ -37,6 +37,7 @@
 
 #include "ridc_chunk.cuh"
 #include "ridc_device.cuh"
+#include "ridc_febe_carry.cuh"
 #include "ridc_resident.cuh"
 #include "ridc_sweep.cuh"
 #include "ridc_tma.cuh"
@@ -92,22 +93,6 @@ struct CarryLevParams {
     long long spin_limit;
     int exp;                      // diagnostics (RIDC_CL_EXP): 1 = every CTA exits after the launch prologue
 };
-
-__device__ __forceinline__ double cl_poll(const uint4* p, unsigned want, const CarryLevParams& cp, bool& dead)
-{
-    uint4 v = ld_line(p);
-    if (v.y == want && v.w == want) return line_value(v);
-    const long long t0 = clock64();
-    for (unsigned it = 1; !dead; ++it) {   // the watchdog only every 64 polls
-        v = ld_line(p);
-        if (v.y == want && v.w == want) return line_value(v);
-        if ((it & 63u) == 0u && (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort)) {
-            atomicExch(cp.abort, 1u);
-            dead = true;
-        }
-    }
-    return 0.0;
-}
 
 template <int KIND, int K>
 __global__ void __launch_bounds__(ClGeom<K>::WARPS * 32, 1)
@@ -266,7 +251,7 @@ __global__ void __launch_bounds__(ClGeom<K>::WARPS * 32, 1)
             double cf = __shfl_up_sync(FULL, inc, 1);
             if (lane == 0) cf = 0.0;
             yend = __shfl_sync(FULL, inc, 31);   // y at my last point (zero carry in)
-            if (lane == 31) st_line(cp.xch + (size_t)a * cp.nchunk + chunk, yend, tag);
+            st_line_if(lane == 31, cp.xch + (size_t)a * cp.nchunk + chunk, yend, tag);
             // ---- backward with a zero carry at the chunk end
             double x = 0.0;
 #pragma unroll
@@ -280,20 +265,38 @@ __global__ void __launch_bounds__(ClGeom<K>::WARPS * 32, 1)
 #pragma unroll
             for (int e = 0; e < K; ++e) v[e] = fma(exr, cp.pw[K - 1 - e], fma(cf, cp.zf[e], v[e]));
             // my first x (zero carries at both ends)
-            if (lane == 0) st_line(cp.xch + (size_t)(kMaxLevels + a) * cp.nchunk + chunk, v[0], tag);
+            st_line_if(lane == 0, cp.xch + (size_t)(kMaxLevels + a) * cp.nchunk + chunk, v[0], tag);
         }
         if (a > 0) {
             // ---- level a - 1: the neighbours' carries (the left chunk's y_end, the
             // right chunk's first x), the corrections, the store
             const int b = a - 1;
             const ClLevel lv = s_lev[b];
-            double cv = 0.0, dv = 0.0;
-            if (lane == 0 || lane == 31) {   // one loop for both lanes: the two L2 round trips overlap
-                const double v = cl_poll(lane == 0 ? cp.xch + (size_t)b * cp.nchunk + cl
-                                                   : cp.xch + (size_t)(kMaxLevels + b) * cp.nchunk + cr,
-                                         tag, cp, dead);
-                if (lane == 0) cv = v; else dv = v;
+            // lane 0 reads the left chunk's y_end, lane 31 the right one's first x:
+            // one predicated load each, one vote, a warp-uniform re-poll loop (no
+            // divergent branch around the wait, as the warp FEBE march)
+            const bool need = lane == 0 || lane == 31;
+            const uint4* src = lane == 0 ? cp.xch + (size_t)b * cp.nchunk + cl
+                                         : cp.xch + (size_t)(kMaxLevels + b) * cp.nchunk + cr;
+            uint4 lw = ld_line_if(need && !dead, src);
+            bool ok = !need || dead || (lw.y == tag && lw.w == tag);
+            if (!__all_sync(FULL, ok)) {
+                const long long t0 = clock64();
+                for (unsigned it = 1; !__all_sync(FULL, ok); ++it) {
+                    if (!ok) {
+                        lw = ld_line_gen(src);
+                        ok = lw.y == tag && lw.w == tag;
+                        if (!ok && (it & 63u) == 0u &&
+                            (clock64() - t0 > cp.spin_limit || *(volatile unsigned*)cp.abort)) {
+                            atomicExch(cp.abort, 1u);
+                            dead = true;
+                            ok = true;
+                        }
+                    }
+                }
             }
+            const double lwv = need && !dead ? line_value(lw) : 0.0;
+            const double cv = lane == 0 ? lwv : 0.0, dv = lane == 31 ? lwv : 0.0;
             const double c = __shfl_sync(FULL, cv, 0);
             // + the head correction my own y_end causes at the right chunk's first point
             const double d = fma(yend_p, cp.zc, __shfl_sync(FULL, dv, 31));
